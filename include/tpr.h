@@ -1,0 +1,188 @@
+/*
+ * tpr.h — C ABI of libtpr.so, the B200 (sm_100a) TP-reconfiguration data path.
+ *
+ * The reference (arxiv 2605.05467 artifact, `tpsim`) exposes this path as a pure
+ * Python API in pkg/src/tpsim/migration.py; it has no FFI. Every entry point
+ * below is what a binding for that API would call underneath, and each cites the
+ * reference function it replaces or executes:
+ *
+ *   tpr_plan_heads        -> migration.py:101-134 head_transfers (run coalescing)
+ *                            and migration.py:168-188 plan_repartition (plan order)
+ *   tpr_kv_remap    (K3)  -> migration.py:192-207 apply_plan (placement replay),
+ *                            executed on device: block-table remap + free-ring
+ *                            allocation by warp-level prefix sums
+ *   tpr_kv_migrate  (K1)  -> the Transfer list (migration.py:50-57) executed:
+ *                            paged-KV head-shard movement, 16-B vectorised
+ *                            loads/stores straight into the destination pool
+ *                            (a peer mapping when the destination is another GPU)
+ *   tpr_weight_reshard (K2)-> migration.py:295-306 weight_memory("sharded", tp)
+ *                            volumes realised: fetch only missing shard slices
+ *
+ * Conventions: every call returns 0 on success and a negative tpr_status code on
+ * failure; tpr_last_error() returns a thread-local message. Device pointers are
+ * plain uint64 virtual addresses (local, or peer mappings opened with
+ * tpr_ipc_open). Every device call is stream-ordered on the caller's
+ * cudaStream_t (passed as void*) and launches on the caller's current device.
+ * No torch types cross this boundary.
+ */
+#ifndef TPR_H_
+#define TPR_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPR_ABI_VERSION 1
+#define TPR_MAX_GPUS 16
+
+enum tpr_status {
+  TPR_OK = 0,
+  TPR_EINVAL = -1,     /* bad argument                                   */
+  TPR_ECUDA = -2,      /* CUDA runtime error                             */
+  TPR_ECAPACITY = -3,  /* output buffer too small                        */
+};
+
+/* Device-side status bits written by the K3 remap kernel (status word). */
+#define TPR_STATUS_WRONG_SOURCE 1 /* head not on src_gpu (migration.py:201-205) */
+#define TPR_STATUS_DST_OCCUPIED 2 /* destination block-table slot already set   */
+
+/* Paged KV pool geometry. One pool unit = one KV head x one page of
+ * `block_tokens` tokens x all layers x {K,V}, laid out [layer][kv][token][dim].
+ * The pool shape is independent of the TP degree (KvLayout, migration.py:25-47,
+ * only changes which GPU owns a head). */
+typedef struct tpr_kv_geometry {
+  int32_t layers;        /* L                                          */
+  int32_t head_dim;      /* D                                          */
+  int32_t dtype_bytes;   /* 2 for bf16                                 */
+  int32_t block_tokens;  /* tokens per page                            */
+  int32_t total_heads;   /* H (KV heads), KvLayout.total_heads         */
+  int32_t max_blocks;    /* pages per (request slot, head) table row   */
+  int32_t n_req_slots;   /* request slots per block table              */
+  int32_t n_units;       /* units per pool == free-ring capacity       */
+} tpr_kv_geometry_t;
+
+/* The set of pools a plan touches, indexed by GPU slot (dense 0..n_gpus-1).
+ * ring_head / ring_tail are monotonically increasing counters owned by the
+ * host: the next allocation takes ring[ring_head % n_units], the next release
+ * is stored at ring[ring_tail % n_units]. */
+typedef struct tpr_kv_cluster {
+  int32_t n_gpus;
+  int32_t _pad;
+  uint64_t pool[TPR_MAX_GPUS];        /* uint8 [n_units][unit_bytes]          */
+  uint64_t block_table[TPR_MAX_GPUS]; /* int32 [n_req_slots][H][max_blocks]   */
+  uint64_t free_ring[TPR_MAX_GPUS];   /* int32 [n_units]                      */
+  int64_t ring_head[TPR_MAX_GPUS];
+  int64_t ring_tail[TPR_MAX_GPUS];
+} tpr_kv_cluster_t;
+
+/* One transfer record on device, int32 x 6:
+ *   {src_slot, dst_slot, req_slot, head_lo, head_hi (excl.), context_len}
+ * src_slot == -1 means "allocate only" (admission of a new request).      */
+#define TPR_XFER_FIELDS 6
+
+/* Per-transfer scan output of K3 (int64 x 4): {mine_off, alloc_off, rel_off, units} */
+#define TPR_META_FIELDS 4
+
+/* totals output of K3 (int64): [0] units processed by this caller,
+ * [1+g] units allocated on slot g, [1+TPR_MAX_GPUS+g] units released on g. */
+#define TPR_TOTALS_LEN (1 + 2 * TPR_MAX_GPUS)
+
+/* ---- host utilities -------------------------------------------------- */
+int tpr_version(void);
+const char* tpr_last_error(void);
+int tpr_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* ---- planner (host) --------------------------------------------------- */
+/* Coalesced head-range transfers for n_req requests, in the given request
+ * order. Request i moves from group gpu_ids[old_off[i] .. +old_tp[i]) to group
+ * gpu_ids[new_off[i] .. +new_tp[i]); rank r of a tp-N group owns heads
+ * [r*H/N, (r+1)*H/N). out is int64 [capacity][6] =
+ * {src_gpu, dst_gpu, request_id, head_lo, head_hi, bytes}. Replaces
+ * migration.py:101-134 (and the per-request loop of migration.py:168-188). */
+int tpr_plan_heads(int32_t n_req, const int64_t* req_ids, const int64_t* ctx,
+                   const int32_t* old_off, const int32_t* old_tp,
+                   const int32_t* new_off, const int32_t* new_tp,
+                   const int64_t* gpu_ids, int32_t total_heads, int64_t kvb,
+                   int64_t capacity, int64_t* out, int64_t* n_out);
+
+/* ---- K3: block-table remap + free-ring allocation (device) ------------- */
+/* d_xfers: int32 [n][6] transfer records (device). d_meta: int64 [n][4]
+ * scratch, d_totals: int64 [TPR_TOTALS_LEN] (device). filter_src = -1
+ * processes every transfer (single-process, all pools visible); filter_src =
+ * g processes only transfers leaving slot g (one process per GPU, push
+ * model) while allocation offsets still follow the whole plan.
+ * d_work: int32x4 [n_units] {src_unit, dst_unit, src|dst<<16, ntok};
+ * d_work_ext (nullable): int32x4 {req_slot, head, block, xfer}.
+ * n_units_hint: host-computed number of units this caller processes (the
+ * expand grid is sized from it). d_status: int32 (device), OR-ed status bits. */
+int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                 const int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
+                 int64_t* d_meta, int64_t* d_totals, int64_t n_units_hint,
+                 int32_t* d_work, int32_t* d_work_ext, int32_t* d_status,
+                 void* stream);
+
+/* ---- K1: paged-KV head-shard migration (device) ------------------------ */
+/* Copies the valid tokens of every work unit from pool[src] to pool[dst]. */
+int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                   const int32_t* d_work, int64_t n_units, void* stream);
+
+/* ---- K2: weight reshard = batched 2-D strided copy (device) ------------ */
+typedef struct tpr_copy_seg {
+  uint64_t src;       /* device VA (local or peer)        */
+  uint64_t dst;       /* device VA (local or peer)        */
+  int64_t rows;
+  int64_t row_bytes;
+  int64_t src_pitch;
+  int64_t dst_pitch;
+  int64_t flags;      /* set by tpr_copy_prepare          */
+  int64_t _pad;
+} tpr_copy_seg_t;
+
+/* Host: normalise segments in place (collapse contiguous ones, flag
+ * unaligned ones) and fill prefix[n+1] with per-segment work-item counts for
+ * the given chunk size. Returns the number of items in *n_items. */
+int tpr_copy_prepare(tpr_copy_seg_t* segs, int32_t n, int64_t chunk_bytes,
+                     int64_t* prefix, int64_t* n_items);
+int tpr_weight_reshard(const tpr_copy_seg_t* d_segs, const int64_t* d_prefix,
+                       int32_t n_segs, int64_t n_items, int64_t chunk_bytes,
+                       void* stream);
+
+/* ---- synthetic data + full-size property checks (device) --------------- */
+/* Pattern fill of every work unit's valid tokens in its destination pool
+ * (typically the work list of an admission remap); the pattern is a function
+ * of (seed, req_slot, head, block, offset) only, so it is placement-invariant. */
+int tpr_kv_fill(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                const int32_t* d_work, const int32_t* d_work_ext, int64_t n_units,
+                uint64_t seed, void* stream);
+/* Whole-pool "garbage" fill keyed by (seed, slot, unit, offset). */
+int tpr_pool_fill(const tpr_kv_geometry_t* geo, uint64_t pool, int32_t slot,
+                  uint64_t seed, void* stream);
+/* Checks one GPU's block table + pool: every (req, head, block) that
+ * `owner[req][head] == slot` expects is present and carries the pattern, and
+ * nothing else is present. d_ctx: int32 [n_req_slots] (-1 = empty slot).
+ * d_counts: int64 [3] += {placement errors, word mismatches, units checked}. */
+int tpr_kv_verify(const tpr_kv_geometry_t* geo, uint64_t pool, const int32_t* d_bt,
+                  const int32_t* d_ctx, const int32_t* d_owner, int32_t slot,
+                  uint64_t seed, int64_t* d_counts, void* stream);
+/* 2-D weight slice fill/verify: element (i, j) of the buffer is element
+ * (row0 + i, col0 + j) of the full matrix identified by key. */
+int tpr_matrix_fill(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch_elems,
+                    int64_t row0, int64_t col0, int64_t full_cols, uint64_t key,
+                    int32_t elem_bytes, void* stream);
+int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch_elems,
+                      int64_t row0, int64_t col0, int64_t full_cols, uint64_t key,
+                      int32_t elem_bytes, int64_t* d_mismatch, void* stream);
+
+/* ---- peer memory (one process per GPU) -------------------------------- */
+int tpr_enable_peer(int32_t peer_device);
+int tpr_ipc_get_handle(uint64_t dptr, uint8_t* handle64);
+int tpr_ipc_open(const uint8_t* handle64, uint64_t* dptr);
+int tpr_ipc_close(uint64_t dptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPR_H_ */

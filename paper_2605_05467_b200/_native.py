@@ -1,0 +1,135 @@
+"""ctypes binding of libtpr.so (the C ABI declared in include/tpr.h).
+
+This is the only way the package reaches the device: there is no eager /
+PyTorch fallback for the data path. If the library is missing or fails to
+load, every device entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, Structure, c_char_p, c_int32, c_int64, c_uint8, c_uint64, c_void_p
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libtpr.so"
+
+TPR_ABI_VERSION = 1
+TPR_MAX_GPUS = 16
+TPR_XFER_FIELDS = 6
+TPR_META_FIELDS = 4
+TPR_TOTALS_LEN = 1 + 2 * TPR_MAX_GPUS
+TPR_STATUS_WRONG_SOURCE = 1
+TPR_STATUS_DST_OCCUPIED = 2
+
+# Every exported symbol of include/tpr.h; tests check the library exports all.
+EXPORTS = (
+    "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads",
+    "tpr_kv_remap", "tpr_kv_migrate", "tpr_copy_prepare", "tpr_weight_reshard",
+    "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
+    "tpr_matrix_verify", "tpr_enable_peer", "tpr_ipc_get_handle", "tpr_ipc_open",
+    "tpr_ipc_close",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class KvGeometryC(Structure):
+    _fields_ = [
+        ("layers", c_int32), ("head_dim", c_int32), ("dtype_bytes", c_int32),
+        ("block_tokens", c_int32), ("total_heads", c_int32), ("max_blocks", c_int32),
+        ("n_req_slots", c_int32), ("n_units", c_int32),
+    ]
+
+
+class KvClusterC(Structure):
+    _fields_ = [
+        ("n_gpus", c_int32), ("_pad", c_int32),
+        ("pool", c_uint64 * TPR_MAX_GPUS),
+        ("block_table", c_uint64 * TPR_MAX_GPUS),
+        ("free_ring", c_uint64 * TPR_MAX_GPUS),
+        ("ring_head", c_int64 * TPR_MAX_GPUS),
+        ("ring_tail", c_int64 * TPR_MAX_GPUS),
+    ]
+
+
+class CopySegC(Structure):
+    _fields_ = [
+        ("src", c_uint64), ("dst", c_uint64), ("rows", c_int64), ("row_bytes", c_int64),
+        ("src_pitch", c_int64), ("dst_pitch", c_int64), ("flags", c_int64), ("_pad", c_int64),
+    ]
+
+
+_P64 = POINTER(c_int64)
+_P32 = POINTER(c_int32)
+
+_SIGNATURES = {
+    "tpr_version": (c_int32, []),
+    "tpr_last_error": (c_char_p, []),
+    "tpr_device_info": (c_int32, [_P32, _P32, _P32]),
+    "tpr_plan_heads": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p, _P64]),
+    "tpr_kv_remap": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int32,
+                               c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                               c_void_p, c_void_p]),
+    "tpr_kv_migrate": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int64,
+                                 c_void_p]),
+    "tpr_copy_prepare": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, _P64]),
+    "tpr_weight_reshard": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p]),
+    "tpr_kv_fill": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
+                              c_int64, c_uint64, c_void_p]),
+    "tpr_pool_fill": (c_int32, [POINTER(KvGeometryC), c_uint64, c_int32, c_uint64, c_void_p]),
+    "tpr_kv_verify": (c_int32, [POINTER(KvGeometryC), c_uint64, c_void_p, c_void_p, c_void_p,
+                                c_int32, c_uint64, c_void_p, c_void_p]),
+    "tpr_matrix_fill": (c_int32, [c_uint64, c_int64, c_int64, c_int64, c_int64, c_int64,
+                                  c_int64, c_uint64, c_int32, c_void_p]),
+    "tpr_matrix_verify": (c_int32, [c_uint64, c_int64, c_int64, c_int64, c_int64, c_int64,
+                                    c_int64, c_uint64, c_int32, c_void_p, c_void_p]),
+    "tpr_enable_peer": (c_int32, [c_int32]),
+    "tpr_ipc_get_handle": (c_int32, [c_uint64, POINTER(c_uint8)]),
+    "tpr_ipc_open": (c_int32, [POINTER(c_uint8), POINTER(c_uint64)]),
+    "tpr_ipc_close": (c_int32, [c_uint64]),
+}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libtpr.so once; raise NativeUnavailable when it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeUnavailable(
+            f"{LIB_PATH} is missing: run `python -m paper_2605_05467_b200.build` "
+            "(there is no CPU fallback for the TP-reconfiguration data path)"
+        )
+    try:
+        lib = ctypes.CDLL(str(LIB_PATH))
+    except OSError as exc:
+        raise NativeUnavailable(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.tpr_version() != TPR_ABI_VERSION:
+        raise NativeUnavailable(
+            f"libtpr ABI {lib.tpr_version()} != expected {TPR_ABI_VERSION}; rebuild"
+        )
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().tpr_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,118 @@
+"""Reconfiguration controller execution hook.
+
+In the reference the controller's hook ``Simulator._apply_config``
+(pkg/src/tpsim/engine.py:500-621) builds per-request ``KvLayout``s
+(engine.py:571-582), calls ``head_transfers`` (engine.py:583-589), prices the
+resulting ``MigrationPlan`` with ``switch_cost`` (+ ``planning_delay_ms``,
+engine.py:590-597) and pauses the destination groups for that long
+(engine.py:607-609). ``ReconfigurationExecutor.switch`` is the executed form
+of steps d-g: handshake, plan, K3 block-table remap, K1 KV migration on one
+stream in parallel with K2 weight reshard on another, barrier, resume. It
+returns the measured pause, which replaces ``switch_cost`` in the engine
+(see INTEGRATION.md).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from .kvcache import MigrationStats, PagedKvCluster
+from .migration import KvLayout, MigrationPlan, plan_repartition
+from .weights import ReshardStats, ShardedWeightStore
+
+
+@dataclass
+class SwitchResult:
+    plan: MigrationPlan
+    kv: MigrationStats
+    weights: ReshardStats | None
+    host_ms: float = 0.0        # pause -> resume wall time (only when synced)
+    device_ms: float = 0.0      # CUDA-event time of the whole switch (only when synced)
+    status: int = 0             # K3 status bits (0 = every head was where the plan said)
+    events: dict = field(default_factory=dict)
+
+    @property
+    def bytes(self) -> int:
+        return self.kv.bytes + (self.weights.bytes if self.weights else 0)
+
+
+class ReconfigurationExecutor:
+    """Executes TP switches on a PagedKvCluster (+ optional ShardedWeightStore)."""
+
+    def __init__(self, kv: PagedKvCluster, weights: ShardedWeightStore | None = None,
+                 handshake=None, time_kernels: bool = False):
+        self.kv = kv
+        self.weights = weights
+        self.handshake = handshake  # callable(plan) for multi-process metadata exchange
+        dev = kv.home
+        self.device = dev
+        self.kv_stream = torch.cuda.Stream(device=dev)
+        self.w_stream = torch.cuda.Stream(device=dev)
+        self.time_kernels = time_kernels
+        self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+
+    def switch(self, old_layouts: list[KvLayout], new_layouts: list[KvLayout],
+               new_weight_groups=None, parked=(), sync: bool = True,
+               validate: bool = True) -> SwitchResult:
+        """Stop-and-migrate TP switch. With ``sync`` the call returns after the
+        switch completed on the device and reports measured latencies; without
+        it, work is only enqueued (the caller's current stream is joined)."""
+        t0 = time.perf_counter()
+        main = torch.cuda.current_stream(self.device)
+        ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
+        if self.time_kernels:
+            for k in ("k1_start", "k1_end", "k2_start", "k2_end"):
+                ev[k] = torch.cuda.Event(enable_timing=True)
+        ev["start"].record(main)
+        plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
+        if self.handshake is not None:
+            self.handshake(plan)
+        self.kv_stream.wait_event(ev["start"])
+        kv_stats = self.kv.migrate(plan, stream=self.kv_stream, validate=validate,
+                                   k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
+        w_stats = None
+        if self.weights is not None and new_weight_groups is not None:
+            self.w_stream.wait_event(ev["start"])
+            w_stats = self.weights.reshard(
+                new_weight_groups, stream=self.w_stream, parked=parked,
+                events=(ev["k2_start"], ev["k2_end"]) if self.time_kernels else None)
+            main.wait_stream(self.w_stream)
+        main.wait_stream(self.kv_stream)
+        ev["end"].record(main)
+        res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev)
+        if sync:
+            # the step's result: K3's status word, read back D2H
+            self._status_host.copy_(self.kv.status, non_blocking=True)
+            ev["end"].synchronize()
+            res.status = int(self._status_host.item())
+            res.host_ms = (time.perf_counter() - t0) * 1e3
+            res.device_ms = ev["start"].elapsed_time(ev["end"])
+        return res
+
+
+def measured_switch_cost(executor: ReconfigurationExecutor):
+    """Adapter with the signature of ``migration.switch_cost(mode, plan, params)``
+    that executes ``plan`` (already in this cluster's placement) and returns the
+    measured pause in ms, for wiring into the reference engine."""
+
+    def cost(mode, plan: MigrationPlan, params) -> float:
+        t0 = time.perf_counter()
+        executor.kv.migrate(plan, stream=executor.kv_stream)
+        executor.kv_stream.synchronize()
+        return (time.perf_counter() - t0) * 1e3
+
+    return cost
+
+
+def host_to_device_bytes(plan: MigrationPlan, w: ReshardStats | None) -> int:
+    """Bytes a switch uploads: transfer records + weight copy segments/prefix."""
+    n = len(plan)
+    segs = w.segments if w else 0
+    return n * 6 * 4 + (segs * 64 + (segs + 1) * 8 if segs else 0)
+
+
+__all__ = ["ReconfigurationExecutor", "SwitchResult", "measured_switch_cost",
+           "host_to_device_bytes"]

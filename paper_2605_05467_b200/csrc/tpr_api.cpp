@@ -1,0 +1,354 @@
+// libtpr C ABI (see include/tpr.h). Host-side validation, the native head
+// planner, segment preparation for K2, and thin launch wrappers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tpr.h"
+#include "tpr_common.cuh"
+#include "tpr_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(TPR_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int check_geometry(const tpr_kv_geometry_t* g) {
+  if (!g) return fail(TPR_EINVAL, "null geometry");
+  if (g->layers <= 0 || g->head_dim <= 0 || g->dtype_bytes <= 0 || g->block_tokens <= 0 ||
+      g->total_heads <= 0 || g->max_blocks <= 0 || g->n_req_slots <= 0 || g->n_units <= 0)
+    return fail(TPR_EINVAL, "geometry fields must be positive");
+  if ((g->head_dim * g->dtype_bytes) % 16 != 0)
+    return fail(TPR_EINVAL, "head_dim*dtype_bytes=%d is not a multiple of 16 bytes",
+                g->head_dim * g->dtype_bytes);
+  return TPR_OK;
+}
+
+tpr::KvCopyParams copy_params(const tpr_kv_geometry_t* g) {
+  tpr::KvCopyParams p;
+  p.tok_bytes = g->head_dim * g->dtype_bytes;
+  p.pitch = (int64_t)g->block_tokens * p.tok_bytes;
+  p.rows = 2 * g->layers;
+  p.unit_bytes = p.pitch * p.rows;
+  int64_t rpi = tpr::kRowsPerItemTarget / p.pitch;
+  if (rpi < 1) rpi = 1;
+  if (rpi > p.rows) rpi = p.rows;
+  p.rows_per_item = (int32_t)rpi;
+  p.items_per_unit = (p.rows + p.rows_per_item - 1) / p.rows_per_item;
+  return p;
+}
+
+int cluster_params(const tpr_kv_cluster_t* cl, tpr::KvClusterParams* out) {
+  if (!cl) return fail(TPR_EINVAL, "null cluster");
+  if (cl->n_gpus <= 0 || cl->n_gpus > TPR_MAX_GPUS)
+    return fail(TPR_EINVAL, "n_gpus=%d outside [1, %d]", cl->n_gpus, TPR_MAX_GPUS);
+  std::memset(out, 0, sizeof(*out));
+  for (int g = 0; g < cl->n_gpus; ++g) {
+    out->pool[g] = cl->pool[g];
+    out->block_table[g] = cl->block_table[g];
+    out->free_ring[g] = cl->free_ring[g];
+    out->ring_head[g] = cl->ring_head[g];
+    out->ring_tail[g] = cl->ring_tail[g];
+  }
+  return TPR_OK;
+}
+
+}  // namespace
+
+namespace tpr {
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+}  // namespace tpr
+
+extern "C" {
+
+int tpr_version(void) { return TPR_ABI_VERSION; }
+
+const char* tpr_last_error(void) { return g_err.c_str(); }
+
+int tpr_device_info(int32_t* sm, int32_t* major, int32_t* minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int a = 0, b = 0, c = 0;
+  cudaDeviceGetAttribute(&a, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&b, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&c, cudaDevAttrComputeCapabilityMinor, dev);
+  if (sm) *sm = a;
+  if (major) *major = b;
+  if (minor) *minor = c;
+  return TPR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Native head planner. Ownership follows KvLayout (migration.py:25-47): rank r
+// of a tp-N group owns heads [r*H/N, (r+1)*H/N). Ownership of both layouts is
+// piecewise constant between multiples of H/N_old and H/N_new, so the planner
+// walks those breakpoints instead of single heads and merges neighbouring
+// pieces that share a (src, dst) pair. Pieces whose owner does not change are
+// skipped and break runs, as in migration.py:112-133.
+// ---------------------------------------------------------------------------
+int tpr_plan_heads(int32_t n_req, const int64_t* req_ids, const int64_t* ctx,
+                   const int32_t* old_off, const int32_t* old_tp, const int32_t* new_off,
+                   const int32_t* new_tp, const int64_t* gpu_ids, int32_t total_heads,
+                   int64_t kvb, int64_t capacity, int64_t* out, int64_t* n_out) {
+  if (n_req < 0 || total_heads <= 0 || !n_out) return fail(TPR_EINVAL, "bad planner arguments");
+  int64_t n = 0;
+  for (int32_t i = 0; i < n_req; ++i) {
+    const int32_t to = old_tp[i], tn = new_tp[i];
+    if (to <= 0 || tn <= 0 || total_heads % to || total_heads % tn)
+      return fail(TPR_EINVAL, "request %lld: total_heads=%d not divisible by tp",
+                  (long long)req_ids[i], total_heads);
+    const int32_t ho = total_heads / to, hn = total_heads / tn;
+    const int64_t* go = gpu_ids + old_off[i];
+    const int64_t* gn = gpu_ids + new_off[i];
+    const int64_t per_head = ctx[i] * kvb;
+    bool open = false;
+    int64_t run_src = 0, run_dst = 0;
+    int32_t run_lo = 0;
+    int32_t p = 0;
+    while (p <= total_heads) {
+      int32_t next;
+      bool moving = false;
+      int64_t s = 0, d = 0;
+      if (p < total_heads) {
+        next = std::min((p / ho + 1) * ho, (p / hn + 1) * hn);
+        s = go[p / ho];
+        d = gn[p / hn];
+        moving = s != d;
+      } else {
+        next = total_heads + 1;
+      }
+      const bool extends = open && moving && s == run_src && d == run_dst;
+      if (open && !extends) {
+        if (n >= capacity) return fail(TPR_ECAPACITY, "planner output capacity exhausted");
+        int64_t* o = out + n * 6;
+        o[0] = run_src;
+        o[1] = run_dst;
+        o[2] = req_ids[i];
+        o[3] = run_lo;
+        o[4] = p;
+        o[5] = (int64_t)(p - run_lo) * per_head;
+        ++n;
+        open = false;
+      }
+      if (moving && !open) {
+        open = true;
+        run_src = s;
+        run_dst = d;
+        run_lo = p;
+      }
+      p = next;
+    }
+  }
+  *n_out = n;
+  return TPR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K3 / K1 / K2 wrappers
+// ---------------------------------------------------------------------------
+int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const int32_t* d_xfers,
+                 int32_t n_xfers, int32_t filter_src, int64_t* d_meta, int64_t* d_totals,
+                 int64_t n_units_hint, int32_t* d_work, int32_t* d_work_ext, int32_t* d_status,
+                 void* stream) {
+  int rc = check_geometry(geo);
+  if (rc) return rc;
+  tpr::KvClusterParams cp;
+  if ((rc = cluster_params(cl, &cp))) return rc;
+  if (n_xfers < 0) return fail(TPR_EINVAL, "n_xfers < 0");
+  if (n_xfers == 0) return TPR_OK;
+  if (!d_xfers || !d_meta || !d_totals || !d_work || !d_status)
+    return fail(TPR_EINVAL, "null device buffer");
+  cudaError_t e = tpr::launch_k3(*geo, cp, d_xfers, n_xfers, filter_src, d_meta, d_totals,
+                                 n_units_hint, reinterpret_cast<int4*>(d_work),
+                                 reinterpret_cast<int4*>(d_work_ext), d_status,
+                                 static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_remap launch");
+}
+
+int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const int32_t* d_work,
+                   int64_t n_units, void* stream) {
+  int rc = check_geometry(geo);
+  if (rc) return rc;
+  tpr::KvClusterParams cp;
+  if ((rc = cluster_params(cl, &cp))) return rc;
+  if (n_units < 0) return fail(TPR_EINVAL, "n_units < 0");
+  if (n_units > 0 && !d_work) return fail(TPR_EINVAL, "null work list");
+  cudaError_t e = tpr::launch_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
+                                 n_units, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_migrate launch");
+}
+
+int tpr_copy_prepare(tpr_copy_seg_t* segs, int32_t n, int64_t chunk, int64_t* prefix,
+                     int64_t* n_items) {
+  if (n < 0 || !prefix || !n_items) return fail(TPR_EINVAL, "bad copy_prepare arguments");
+  if (chunk <= 0 || chunk % 16) return fail(TPR_EINVAL, "chunk_bytes must be a positive multiple of 16");
+  int64_t total = 0;
+  prefix[0] = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    tpr_copy_seg_t& s = segs[i];
+    int64_t items = 0;
+    if (s.rows > 0 && s.row_bytes > 0) {
+      if (s.rows > 1 && s.src_pitch == s.row_bytes && s.dst_pitch == s.row_bytes) {
+        s.row_bytes *= s.rows;
+        s.rows = 1;
+        s.src_pitch = s.dst_pitch = s.row_bytes;
+      }
+      if (s.rows == 1) s.src_pitch = s.dst_pitch = s.row_bytes;
+      const bool aligned = ((s.src | s.dst) % 16 == 0) && s.row_bytes % 16 == 0 &&
+                           s.src_pitch % 16 == 0 && s.dst_pitch % 16 == 0;
+      s.flags = aligned ? TPR_SEG_ALIGNED16 : 0;
+      if (s.row_bytes <= chunk) {
+        const int64_t rpi = chunk / s.row_bytes;
+        items = (s.rows + rpi - 1) / rpi;
+      } else {
+        items = s.rows * ((s.row_bytes + chunk - 1) / chunk);
+      }
+    } else {
+      s.flags = 0;
+    }
+    total += items;
+    prefix[i + 1] = total;
+  }
+  *n_items = total;
+  return TPR_OK;
+}
+
+int tpr_weight_reshard(const tpr_copy_seg_t* d_segs, const int64_t* d_prefix, int32_t n_segs,
+                       int64_t n_items, int64_t chunk, void* stream) {
+  if (n_segs < 0 || n_items < 0 || chunk <= 0) return fail(TPR_EINVAL, "bad reshard arguments");
+  if (n_items == 0) return TPR_OK;
+  if (!d_segs || !d_prefix) return fail(TPR_EINVAL, "null segment buffers");
+  cudaError_t e = tpr::launch_k2(d_segs, d_prefix, n_segs, n_items, chunk,
+                                 static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_weight_reshard launch");
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic data and checks
+// ---------------------------------------------------------------------------
+int tpr_kv_fill(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const int32_t* d_work,
+                const int32_t* d_work_ext, int64_t n_units, uint64_t seed, void* stream) {
+  int rc = check_geometry(geo);
+  if (rc) return rc;
+  tpr::KvClusterParams cp;
+  if ((rc = cluster_params(cl, &cp))) return rc;
+  if (n_units > 0 && (!d_work || !d_work_ext)) return fail(TPR_EINVAL, "null buffer");
+  cudaError_t e = tpr::launch_kv_fill(copy_params(geo), cp,
+                                      reinterpret_cast<const int4*>(d_work),
+                                      reinterpret_cast<const int4*>(d_work_ext), n_units, seed,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_fill launch");
+}
+
+int tpr_pool_fill(const tpr_kv_geometry_t* geo, uint64_t pool, int32_t slot, uint64_t seed,
+                  void* stream) {
+  int rc = check_geometry(geo);
+  if (rc) return rc;
+  if (!pool) return fail(TPR_EINVAL, "null pool");
+  cudaError_t e = tpr::launch_pool_fill(copy_params(geo), geo->n_units,
+                                        reinterpret_cast<char*>(pool), slot, seed,
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_pool_fill launch");
+}
+
+int tpr_kv_verify(const tpr_kv_geometry_t* geo, uint64_t pool, const int32_t* d_bt,
+                  const int32_t* d_ctx, const int32_t* d_owner, int32_t slot, uint64_t seed,
+                  int64_t* d_counts, void* stream) {
+  int rc = check_geometry(geo);
+  if (rc) return rc;
+  if (!pool || !d_bt || !d_ctx || !d_owner || !d_counts) return fail(TPR_EINVAL, "null buffer");
+  cudaError_t e = tpr::launch_kv_verify(*geo, copy_params(geo), reinterpret_cast<const char*>(pool),
+                                        d_bt, d_ctx, d_owner, slot, seed,
+                                        reinterpret_cast<unsigned long long*>(d_counts),
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_verify launch");
+}
+
+int tpr_matrix_fill(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch, int64_t row0,
+                    int64_t col0, int64_t full_cols, uint64_t key, int32_t elem_bytes,
+                    void* stream) {
+  if (!buf && rows > 0 && cols > 0) return fail(TPR_EINVAL, "null buffer");
+  cudaError_t e = tpr::launch_matrix(reinterpret_cast<char*>(buf), rows, cols, pitch, row0, col0,
+                                     full_cols, key, elem_bytes, false, nullptr,
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_matrix_fill launch");
+}
+
+int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch, int64_t row0,
+                      int64_t col0, int64_t full_cols, uint64_t key, int32_t elem_bytes,
+                      int64_t* d_mismatch, void* stream) {
+  if ((!buf && rows > 0 && cols > 0) || !d_mismatch) return fail(TPR_EINVAL, "null buffer");
+  cudaError_t e = tpr::launch_matrix(reinterpret_cast<char*>(buf), rows, cols, pitch, row0, col0,
+                                     full_cols, key, elem_bytes, true,
+                                     reinterpret_cast<unsigned long long*>(d_mismatch),
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_matrix_verify launch");
+}
+
+// ---------------------------------------------------------------------------
+// Peer memory
+// ---------------------------------------------------------------------------
+int tpr_enable_peer(int32_t peer) {
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return TPR_OK;
+  }
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
+}
+
+int tpr_ipc_get_handle(uint64_t dptr, uint8_t* handle64) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(dptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, 64);
+  return TPR_OK;
+}
+
+int tpr_ipc_open(const uint8_t* handle64, uint64_t* dptr) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  *dptr = reinterpret_cast<uint64_t>(p);
+  return TPR_OK;
+}
+
+int tpr_ipc_close(uint64_t dptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(dptr));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+}  // extern "C"

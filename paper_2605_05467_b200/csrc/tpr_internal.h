@@ -1,0 +1,57 @@
+// Internal interfaces between the C-ABI layer (tpr_api.cpp) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tpr.h"
+
+namespace tpr {
+
+constexpr int kCopyThreads = 256;  // 8 warps per CTA, warp-independent items
+constexpr int kCopyUnroll = 8;     // 8 x 16 B x 32 lanes = 4 KiB in flight per warp
+constexpr int kRowsPerItemTarget = 32 * 1024;  // bytes of one K1 work item
+
+// Pointer tables passed by value as kernel parameters (<= 4 KiB).
+struct KvClusterParams {
+  uint64_t pool[TPR_MAX_GPUS];
+  uint64_t block_table[TPR_MAX_GPUS];
+  uint64_t free_ring[TPR_MAX_GPUS];
+  int64_t ring_head[TPR_MAX_GPUS];
+  int64_t ring_tail[TPR_MAX_GPUS];
+};
+
+// Derived page geometry for the copy/fill kernels.
+struct KvCopyParams {
+  int64_t unit_bytes;     // bytes of one pool unit
+  int64_t pitch;          // bytes of one (layer, K|V) plane = block_tokens * tok_bytes
+  int32_t tok_bytes;      // head_dim * dtype_bytes
+  int32_t rows;           // planes per unit = 2 * layers
+  int32_t rows_per_item;  // planes per K1 work item
+  int32_t items_per_unit;
+};
+
+int sm_count();
+
+cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
+                      const int32_t* xf, int32_t n, int32_t filter, int64_t* meta,
+                      int64_t* totals, int64_t n_hint, int4* work, int4* work_ext,
+                      int32_t* status, cudaStream_t st);
+cudaError_t launch_k1(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
+                      int64_t n_units, cudaStream_t st);
+cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
+                      int64_t n_items, int64_t chunk, cudaStream_t st);
+cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
+                           const int4* work_ext, int64_t n_units, uint64_t seed,
+                           cudaStream_t st);
+cudaError_t launch_pool_fill(const KvCopyParams& p, int64_t n_units, char* pool, int32_t slot,
+                             uint64_t seed, cudaStream_t st);
+cudaError_t launch_kv_verify(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
+                             const char* pool, const int32_t* bt, const int32_t* ctx,
+                             const int32_t* owner, int32_t slot, uint64_t seed,
+                             unsigned long long* counts, cudaStream_t st);
+cudaError_t launch_matrix(char* buf, int64_t rows, int64_t cols, int64_t pitch, int64_t row0,
+                          int64_t col0, int64_t full_cols, uint64_t key, int32_t elem_bytes,
+                          bool verify, unsigned long long* mismatch, cudaStream_t st);
+
+}  // namespace tpr

@@ -1,0 +1,353 @@
+"""Paged KV block manager + migration engine on B200.
+
+The reference has no KV memory at all: a TP switch is priced, not executed
+(pkg/src/tpsim/engine.py:567-597 builds per-request ``KvLayout``s, calls
+``head_transfers`` and charges ``switch_cost``). This module is the executed
+counterpart. Its placement semantics are the reference's: after ``migrate``
+every (request, KV head) sits on ``layout_placement(new)`` (migration.py:210-218),
+and it moves exactly ``plan.total_bytes`` bytes (migration.py:128-130).
+
+Memory model (per GPU slot):
+
+* pool         uint8  [n_units, unit_bytes]; a unit is one KV head x one page
+                      of ``block_tokens`` tokens x all layers x {K, V}. The pool
+                      shape does not depend on the TP degree.
+* block table  int32  [max_requests, H, max_blocks]; entry = unit id or -1.
+                      Indexed by the GLOBAL head id, so a TP-N rank r reads rows
+                      [r*H/N, (r+1)*H/N) -- shard selection at execution time.
+* free ring    int32  [n_units] + host-owned monotonic (head, tail) counters.
+                      Allocation pops at head, release pushes at tail.
+
+A migration is two device steps: K3 (``tpr_kv_remap``) allocates destination
+units and rewrites both block tables in the plan's sequential order, then K1
+(``tpr_kv_migrate``) copies the valid tokens. All GPU slots may live on one
+device ("logical ranks", one B200) or on their own devices.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+from .geometry import KvGeometry
+from .migration import BYTES, DST, HI, LO, REQ, SRC, KvLayout, MigrationError, MigrationPlan
+
+
+@dataclass
+class MigrationStats:
+    transfers: int
+    units: int
+    bytes: int            # plan.total_bytes: valid KV bytes moved
+    in_units: dict        # gpu id -> units allocated there
+    out_units: dict       # gpu id -> units released there
+
+
+class _PinnedStaging:
+    """Double-buffered pinned host staging for H2D metadata uploads."""
+
+    def __init__(self, nbytes: int = 1 << 16):
+        self._bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self._events: list[torch.cuda.Event | None] = [None, None]
+        self._i = 0
+
+    def upload(self, arr: np.ndarray, dst: torch.Tensor, stream: torch.cuda.Stream) -> int:
+        raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+        n = raw.nbytes
+        i = self._i
+        self._i ^= 1
+        if self._events[i] is not None:
+            self._events[i].synchronize()
+        if self._bufs[i].numel() < n:
+            self._bufs[i] = torch.empty(max(n, 2 * self._bufs[i].numel()), dtype=torch.uint8,
+                                        pin_memory=True)
+        host = self._bufs[i][:n]
+        host.numpy()[:] = raw
+        with torch.cuda.stream(stream):
+            dst.view(torch.uint8).reshape(-1)[:n].copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self._events[i] = ev
+        return n
+
+
+class PagedKvCluster:
+    """KV pools, block tables and free rings of a set of GPUs."""
+
+    def __init__(self, kv: KvGeometry, gpu_ids: Sequence[int], units_per_gpu: int,
+                 max_requests: int, max_blocks: int, device: str | torch.device = "cuda",
+                 devices: dict | None = None, fragmented: bool = False, seed: int = 0):
+        if not 1 <= len(gpu_ids) <= _native.TPR_MAX_GPUS:
+            raise MigrationError(f"1..{_native.TPR_MAX_GPUS} GPUs per cluster")
+        if len(set(gpu_ids)) != len(gpu_ids):
+            raise MigrationError("duplicate gpu ids")
+        _native.load()
+        self.kv = kv
+        self.gpu_ids = tuple(gpu_ids)
+        self.slot_of = {g: i for i, g in enumerate(self.gpu_ids)}
+        self.n_units = int(units_per_gpu)
+        self.max_requests = int(max_requests)
+        self.max_blocks = int(max_blocks)
+        default = torch.device(device)
+        self.devices = [torch.device(devices[g]) if devices else default for g in self.gpu_ids]
+        self.home = self.devices[0]
+        self._single_device = len(set(self.devices)) == 1
+        H = kv.total_heads
+        self.pools, self.block_tables, self.rings = [], [], []
+        gen = np.random.default_rng(seed)
+        for dev in self.devices:
+            self.pools.append(torch.empty(self.n_units * kv.unit_bytes, dtype=torch.uint8, device=dev))
+            self.block_tables.append(torch.full((self.max_requests, H, self.max_blocks), -1,
+                                                dtype=torch.int32, device=dev))
+            order = gen.permutation(self.n_units) if fragmented else np.arange(self.n_units)
+            self.rings.append(torch.from_numpy(order.astype(np.int32)).to(dev))
+        self.ring_head = [0] * len(self.gpu_ids)
+        self.ring_tail = [self.n_units] * len(self.gpu_ids)
+        # request bookkeeping (host is authoritative; device copies for checks)
+        self.req_slot: dict[int, int] = {}
+        self.ctx_of: dict[int, int] = {}
+        self._free_req_slots = list(range(self.max_requests - 1, -1, -1))
+        self.owner = np.full((self.max_requests, H), -1, dtype=np.int32)  # gpu slot per head
+        self.slot_ctx = np.full(self.max_requests, -1, dtype=np.int32)
+        # scratch
+        self._staging = _PinnedStaging()
+        self._xf = torch.empty(0, dtype=torch.int32, device=self.home)
+        self._meta = torch.empty(0, dtype=torch.int64, device=self.home)
+        self._totals = torch.zeros(_native.TPR_TOTALS_LEN, dtype=torch.int64, device=self.home)
+        self._work = torch.empty(0, dtype=torch.int32, device=self.home)
+        self._work_ext = torch.empty(0, dtype=torch.int32, device=self.home)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.home)
+        self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
+                                        H, self.max_blocks, self.max_requests, self.n_units)
+
+    # ------------------------------------------------------------------ utils
+    @property
+    def n_gpus(self) -> int:
+        return len(self.gpu_ids)
+
+    def free_units(self, gpu: int) -> int:
+        s = self.slot_of[gpu]
+        return self.ring_tail[s] - self.ring_head[s]
+
+    def _cluster_c(self) -> _native.KvClusterC:
+        c = _native.KvClusterC()
+        c.n_gpus = self.n_gpus
+        for s in range(self.n_gpus):
+            c.pool[s] = self.pools[s].data_ptr()
+            c.block_table[s] = self.block_tables[s].data_ptr()
+            c.free_ring[s] = self.rings[s].data_ptr()
+            c.ring_head[s] = self.ring_head[s]
+            c.ring_tail[s] = self.ring_tail[s]
+        return c
+
+    @staticmethod
+    def _grow(t: torch.Tensor, n: int) -> torch.Tensor:
+        if t.numel() >= n:
+            return t
+        return torch.empty(max(n, 2 * t.numel()), dtype=t.dtype, device=t.device)
+
+    def _units_per_record(self, xf: np.ndarray) -> np.ndarray:
+        B = self.kv.block_tokens
+        nblk = (xf[:, 5].astype(np.int64) + B - 1) // B
+        return (xf[:, 4] - xf[:, 3]).astype(np.int64) * nblk
+
+    # -------------------------------------------------------------- K3 driver
+    def _remap(self, xf: np.ndarray, stream: torch.cuda.Stream, want_ext: bool) -> int:
+        """Upload records, run K3, advance host ring counters; returns #units."""
+        n = len(xf)
+        units = self._units_per_record(xf)
+        total = int(units.sum())
+        in_u = np.bincount(xf[:, 1], weights=units, minlength=self.n_gpus).astype(np.int64)
+        has_src = xf[:, 0] >= 0
+        out_u = np.bincount(xf[has_src, 0], weights=units[has_src],
+                            minlength=self.n_gpus).astype(np.int64)
+        for s in range(self.n_gpus):
+            free = self.ring_tail[s] - self.ring_head[s]
+            if in_u[s] > free:
+                raise MigrationError(
+                    f"gpu {self.gpu_ids[s]}: {in_u[s]} KV units needed, {free} free")
+        with torch.cuda.stream(stream):  # scratch lives on the stream that uses it
+            self._xf = self._grow(self._xf, n * 6)
+            self._meta = self._grow(self._meta, n * 4)
+            self._work = self._grow(self._work, total * 4)
+            if want_ext:
+                self._work_ext = self._grow(self._work_ext, total * 4)
+            self._staging.upload(xf.astype(np.int32, copy=False), self._xf, stream)
+        cl = self._cluster_c()
+        _native.call(
+            "tpr_kv_remap", ctypes.byref(self._geo), ctypes.byref(cl), self._xf.data_ptr(), n,
+            -1, self._meta.data_ptr(), self._totals.data_ptr(), total, self._work.data_ptr(),
+            self._work_ext.data_ptr() if want_ext else None, self.status.data_ptr(),
+            stream.cuda_stream,
+        )
+        for s in range(self.n_gpus):
+            self.ring_head[s] += int(in_u[s])
+            self.ring_tail[s] += int(out_u[s])
+        self._last_in, self._last_out = in_u, out_u
+        return total
+
+    # -------------------------------------------------------------- admission
+    def admit(self, layouts: Iterable[KvLayout], seed: int = 1,
+              stream: torch.cuda.Stream | None = None) -> int:
+        """Allocate pages for new requests in their canonical layout and fill
+        them with the placement-invariant synthetic pattern. Returns #units."""
+        stream = stream or torch.cuda.current_stream(self.home)
+        H = self.kv.total_heads
+        recs = []
+        for lay in layouts:
+            if lay.total_heads != H:
+                raise MigrationError("all layouts must share total_heads")
+            hpr = lay.heads_per_rank
+            slots = [self.slot_of[g] for g in lay.group]
+            for rid, ctx in lay.requests:
+                if rid in self.req_slot:
+                    raise MigrationError(f"request {rid} already resident")
+                if self.kv.blocks(ctx) > self.max_blocks:
+                    raise MigrationError(f"request {rid}: {ctx} tokens exceed max_blocks")
+                if not self._free_req_slots:
+                    raise MigrationError("no free request slots")
+                rs = self._free_req_slots.pop()
+                self.req_slot[rid] = rs
+                self.ctx_of[rid] = int(ctx)
+                self.slot_ctx[rs] = int(ctx)
+                for r, s in enumerate(slots):
+                    self.owner[rs, r * hpr:(r + 1) * hpr] = s
+                    recs.append((-1, s, rs, r * hpr, (r + 1) * hpr, int(ctx)))
+        if not recs:
+            return 0
+        xf = np.asarray(recs, dtype=np.int64)
+        total = self._remap(xf, stream, want_ext=True)
+        cl = self._cluster_c()
+        with torch.cuda.device(self.home):
+            _native.call("tpr_kv_fill", ctypes.byref(self._geo), ctypes.byref(cl),
+                         self._work.data_ptr(), self._work_ext.data_ptr(), total, seed,
+                         stream.cuda_stream)
+        self.pattern_seed = seed
+        return total
+
+    def fill_garbage(self, seed: int = 99, stream: torch.cuda.Stream | None = None) -> None:
+        """Fill whole pools with per-unit garbage (so stale bytes are visible)."""
+        stream = stream or torch.cuda.current_stream(self.home)
+        for s in range(self.n_gpus):
+            _native.call("tpr_pool_fill", ctypes.byref(self._geo), self.pools[s].data_ptr(), s,
+                         seed, stream.cuda_stream)
+
+    # -------------------------------------------------------------- migration
+    def records(self, plan: MigrationPlan, validate: bool = True) -> np.ndarray:
+        """Plan -> int64 [n, 6] device records (slots), with reference checks."""
+        arr = plan.as_array()
+        n = len(arr)
+        if n == 0:
+            return np.zeros((0, 6), dtype=np.int64)
+        try:
+            src = np.fromiter((self.slot_of[g] for g in arr[:, SRC].tolist()), np.int64, n)
+            dst = np.fromiter((self.slot_of[g] for g in arr[:, DST].tolist()), np.int64, n)
+        except KeyError as exc:
+            raise MigrationError(f"gpu {exc.args[0]} is not part of this cluster") from None
+        try:
+            req = np.fromiter((self.req_slot[r] for r in arr[:, REQ].tolist()), np.int64, n)
+        except KeyError as exc:
+            raise MigrationError(f"request {exc.args[0]} is not resident") from None
+        ctx = self.slot_ctx[req].astype(np.int64)
+        lo, hi = arr[:, LO], arr[:, HI]
+        if ((lo < 0) | (hi > self.kv.total_heads) | (lo >= hi)).any():
+            raise MigrationError("head range outside [0, total_heads)")
+        if validate:
+            if (arr[:, BYTES] != (hi - lo) * ctx * self.kv.kv_bytes_per_token_per_head).any():
+                raise MigrationError(
+                    "transfer bytes disagree with (head_hi-head_lo)*context_len*kv_bytes_per_token_per_head")
+            heads = np.arange(self.kv.total_heads)
+            mask = (heads >= lo[:, None]) & (heads < hi[:, None])
+            # each (request, head) may move once per plan
+            cover = np.zeros_like(self.owner, dtype=np.int32)
+            np.add.at(cover, (np.repeat(req, self.kv.total_heads)[mask.ravel()],
+                              np.tile(heads, n)[mask.ravel()]), 1)
+            if (cover > 1).any():
+                raise MigrationError("a (request, head) is moved twice in one plan")
+            wrong = mask & (self.owner[req] != src[:, None])
+            if wrong.any():
+                t, h = map(int, np.argwhere(wrong)[0])
+                rid = int(arr[t, REQ])
+                here = self.owner[req[t], h]
+                raise MigrationError(
+                    f"transfer of request {rid} head {h} from gpu {int(arr[t, SRC])}, "
+                    f"but it is on {self.gpu_ids[here] if here >= 0 else None}")
+        return np.stack([src, dst, req, lo, hi, ctx], axis=1)
+
+    def migrate(self, plan: MigrationPlan, stream: torch.cuda.Stream | None = None,
+                validate: bool = True, k1_events: tuple | None = None) -> MigrationStats:
+        """Execute ``plan``: K3 remap + K1 page copy, stream-ordered, no host sync.
+
+        ``k1_events`` = (start, end) CUDA events recorded around K1.
+        """
+        stream = stream or torch.cuda.current_stream(self.home)
+        xf = self.records(plan, validate)
+        if len(xf) == 0:
+            return MigrationStats(0, 0, 0, {}, {})
+        if not self._single_device:
+            raise MigrationError("multi-device clusters migrate through kvcache_dist")
+        units = self._remap(xf, stream, want_ext=False)
+        if k1_events:
+            k1_events[0].record(stream)
+        cl = self._cluster_c()
+        _native.call("tpr_kv_migrate", ctypes.byref(self._geo), ctypes.byref(cl),
+                     self._work.data_ptr(), units, stream.cuda_stream)
+        if k1_events:
+            k1_events[1].record(stream)
+        # host placement bookkeeping (apply_plan semantics)
+        heads = np.arange(self.kv.total_heads)
+        mask = (heads >= xf[:, 3:4]) & (heads < xf[:, 4:5])
+        rows = np.repeat(xf[:, 2], self.kv.total_heads).reshape(-1, self.kv.total_heads)
+        self.owner[rows[mask], np.broadcast_to(heads, mask.shape)[mask]] = \
+            np.broadcast_to(xf[:, 1:2], mask.shape)[mask]
+        return MigrationStats(
+            transfers=len(xf), units=units, bytes=int(plan.as_array()[:, BYTES].sum()),
+            in_units={self.gpu_ids[s]: int(v) for s, v in enumerate(self._last_in) if v},
+            out_units={self.gpu_ids[s]: int(v) for s, v in enumerate(self._last_out) if v},
+        )
+
+    # ------------------------------------------------------------ inspection
+    def placement(self) -> dict:
+        """{(request, head): gpu} as recorded by the host (layout_placement form)."""
+        out = {}
+        for rid, rs in self.req_slot.items():
+            for h in range(self.kv.total_heads):
+                out[(rid, h)] = self.gpu_ids[self.owner[rs, h]]
+        return out
+
+    def verify(self, seed: int | None = None, stream: torch.cuda.Stream | None = None) -> dict:
+        """Full-size device check: block tables realise the host placement and
+        every owned page carries its pattern. Returns counts (host sync)."""
+        stream = stream or torch.cuda.current_stream(self.home)
+        seed = self.pattern_seed if seed is None else seed
+        out = {"placement_errors": 0, "word_mismatches": 0, "pages_checked": 0}
+        for s in range(self.n_gpus):
+            dev = self.devices[s]
+            ctx = torch.from_numpy(self.slot_ctx).to(dev)
+            owner = torch.from_numpy(self.owner).to(dev)
+            counts = torch.zeros(3, dtype=torch.int64, device=dev)
+            with torch.cuda.device(dev):
+                _native.call("tpr_kv_verify", ctypes.byref(self._geo), self.pools[s].data_ptr(),
+                             self.block_tables[s].data_ptr(), ctx.data_ptr(), owner.data_ptr(), s,
+                             seed, counts.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+            c = counts.cpu().tolist()
+            out["placement_errors"] += c[0]
+            out["word_mismatches"] += c[1]
+            out["pages_checked"] += c[2]
+        out["status"] = int(self.status.item())
+        return out
+
+    def snapshot(self) -> dict:
+        """Host copies of pools, block tables, rings and ring counters."""
+        torch.cuda.synchronize()
+        return {
+            "pools": [p.cpu().numpy() for p in self.pools],
+            "block_tables": [b.cpu().numpy() for b in self.block_tables],
+            "rings": [r.cpu().numpy() for r in self.rings],
+            "ring_head": list(self.ring_head),
+            "ring_tail": list(self.ring_tail),
+        }

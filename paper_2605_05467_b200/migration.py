@@ -1,0 +1,402 @@
+"""Drop-in replacement for ``tpsim.migration`` (reference pkg/src/tpsim/migration.py).
+
+Same names, fields, argument meaning, return values and error messages as the
+reference API, so the reference's scheduler / controller / CLI / tests can
+import this module instead. Differences are underneath:
+
+* head-range planning runs in the native planner of libtpr (``tpr_plan_heads``)
+  and a plan keeps its transfers as an int64 SoA array, materialising
+  ``Transfer`` objects only when ``plan.transfers`` is read; the execution path
+  (``paper_2605_05467_b200.kvcache``) consumes the array directly;
+* a plan can be executed on B200 pools (see ``kvcache.PagedKvCluster.migrate``).
+
+The cost models are restated formula-for-formula (migration.py:221-292) so the
+reference's exact-equality event-oracle test holds bit for bit.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Iterable
+
+import numpy as np
+
+from . import _native
+
+WARM = "warm"
+NAIVE_RELOAD = "naive_reload"
+NAIVE_KERNEL_INIT = "naive_kernel_init"
+
+# columns of the transfer SoA array
+SRC, DST, REQ, LO, HI, BYTES = range(6)
+
+
+class MigrationError(ValueError):
+    """Invalid layout / plan / parameter (reference: migration.py:21-22)."""
+
+
+@dataclass(frozen=True)
+class KvLayout:
+    """KV placement of one TP group (reference: migration.py:25-47).
+
+    Rank r of ``group`` owns KV heads [r*H/N, (r+1)*H/N) of every request in
+    ``requests`` (tuples of (request id, context length in tokens)).
+    """
+
+    group: tuple[int, ...]
+    tp: int
+    total_heads: int
+    requests: tuple[tuple[int, int], ...]
+
+    def __post_init__(self):
+        if self.tp != len(self.group):
+            raise MigrationError("group size must equal tp")
+        if self.total_heads % self.tp:
+            raise MigrationError(
+                f"total_heads={self.total_heads} not divisible by tp={self.tp}"
+            )
+
+    @property
+    def heads_per_rank(self) -> int:
+        return self.total_heads // self.tp
+
+    def gpu_for_head(self, head: int) -> int:
+        return self.group[head // self.heads_per_rank]
+
+    def owners(self) -> tuple[int, ...]:
+        """GPU id owning each head 0..H-1."""
+        per = self.heads_per_rank
+        return tuple(g for g in self.group for _ in range(per))
+
+
+@dataclass(frozen=True)
+class Transfer:
+    """One coalesced head-range move (reference: migration.py:50-57)."""
+
+    src_gpu: int
+    dst_gpu: int
+    request_id: int
+    head_lo: int
+    head_hi: int  # exclusive
+    bytes: int
+
+
+class MigrationPlan:
+    """Transfer list + handshake + predicted latencies (migration.py:60-74).
+
+    Accepts a list of ``Transfer`` like the reference dataclass. Plans built by
+    the native planner hold an int64 [n, 6] array
+    (src, dst, request, head_lo, head_hi, bytes) and build ``Transfer`` objects
+    lazily, so the execution path never pays for Python objects.
+    """
+
+    def __init__(self, transfers: Iterable[Transfer] | None = None, handshake_ms: float = 0.0,
+                 predicted_latency_ms: dict | None = None):
+        self._list: list[Transfer] | None = list(transfers) if transfers is not None else []
+        self._arr: np.ndarray | None = None
+        self.handshake_ms = handshake_ms
+        self.predicted_latency_ms = {} if predicted_latency_ms is None else predicted_latency_ms
+
+    @classmethod
+    def from_array(cls, arr: np.ndarray, handshake_ms: float = 0.0) -> "MigrationPlan":
+        plan = cls(handshake_ms=handshake_ms)
+        plan._list = None
+        plan._arr = np.ascontiguousarray(arr, dtype=np.int64).reshape(-1, 6)
+        return plan
+
+    @property
+    def transfers(self) -> list[Transfer]:
+        if self._list is None:
+            self._list = [Transfer(*map(int, row)) for row in self._arr]
+        # the caller may mutate the list; the array view is rebuilt on demand
+        self._arr = None
+        return self._list
+
+    @transfers.setter
+    def transfers(self, value):
+        self._list = list(value)
+        self._arr = None
+
+    def as_array(self) -> np.ndarray:
+        """Transfers as int64 [n, 6] (src, dst, request, head_lo, head_hi, bytes)."""
+        if self._arr is None:
+            rows = [(t.src_gpu, t.dst_gpu, t.request_id, t.head_lo, t.head_hi, t.bytes)
+                    for t in self._list]
+            self._arr = np.asarray(rows, dtype=np.int64).reshape(-1, 6)
+        return self._arr
+
+    def __len__(self) -> int:
+        return len(self._list) if self._list is not None else len(self._arr)
+
+    @property
+    def total_bytes(self) -> int:
+        if self._list is not None:
+            return sum(t.bytes for t in self._list)
+        return int(self._arr[:, BYTES].sum())
+
+    def bytes_by_source(self) -> dict[int, int]:
+        out: dict[int, int] = {}
+        if self._list is not None:
+            for t in self._list:
+                out[t.src_gpu] = out.get(t.src_gpu, 0) + t.bytes
+            return out
+        arr = self._arr
+        for src in dict.fromkeys(arr[:, SRC].tolist()):  # first-appearance order
+            out[int(src)] = int(arr[arr[:, SRC] == src, BYTES].sum())
+        return out
+
+    def __eq__(self, other):
+        if not isinstance(other, MigrationPlan):
+            return NotImplemented
+        return (self.transfers == other.transfers and self.handshake_ms == other.handshake_ms
+                and self.predicted_latency_ms == other.predicted_latency_ms)
+
+    def __repr__(self):
+        return (f"MigrationPlan(transfers=<{len(self)}>, handshake_ms={self.handshake_ms}, "
+                f"predicted_latency_ms={self.predicted_latency_ms})")
+
+
+@dataclass(frozen=True)
+class CostModelParams:
+    """Latency-model constants (reference: migration.py:77-98)."""
+
+    copy_bw_gbps: float = 900.0
+    link_bw_gbps: float = 200.0
+    per_transfer_overhead_us: float = 100.0
+    page_bytes: int = 65536
+    chunk_bytes: int = 128 * 1024 * 1024
+    handshake_ms: float = 0.5
+    reload_ms: float = 30000.0
+    kernel_init_ms: float = 10000.0
+
+    def __post_init__(self):
+        for name in ("copy_bw_gbps", "link_bw_gbps", "per_transfer_overhead_us",
+                     "page_bytes", "chunk_bytes", "handshake_ms"):
+            if not getattr(self, name) > 0:
+                raise MigrationError(f"{name} must be positive")
+
+
+# ---------------------------------------------------------------------------
+# planning (native)
+# ---------------------------------------------------------------------------
+
+class _GroupTable:
+    """Concatenated GPU-id groups for the native planner."""
+
+    def __init__(self):
+        self.ids: list[int] = []
+        self._off: dict[tuple[int, ...], int] = {}
+
+    def offset(self, group: tuple[int, ...]) -> int:
+        off = self._off.get(group)
+        if off is None:
+            off = self._off[group] = len(self.ids)
+            self.ids.extend(group)
+        return off
+
+
+def _plan_native(rows: list[tuple[int, int, tuple, int, tuple, int]], total_heads: int,
+                 kvb: int) -> np.ndarray:
+    """rows: (request id, ctx, old group, old tp, new group, new tp) in plan order."""
+    n = len(rows)
+    if n == 0:
+        return np.zeros((0, 6), dtype=np.int64)
+    table = _GroupTable()
+    req = np.empty(n, np.int64)
+    ctx = np.empty(n, np.int64)
+    oo = np.empty(n, np.int32)
+    ot = np.empty(n, np.int32)
+    no = np.empty(n, np.int32)
+    nt = np.empty(n, np.int32)
+    for i, (r, c, og, otp, ng, ntp) in enumerate(rows):
+        req[i] = r
+        ctx[i] = c
+        oo[i] = table.offset(og)
+        ot[i] = otp
+        no[i] = table.offset(ng)
+        nt[i] = ntp
+    ids = np.asarray(table.ids, dtype=np.int64)
+    cap = n * total_heads
+    out = np.empty((cap, 6), dtype=np.int64)
+    n_out = _native.c_int64(0)
+    _native.call(
+        "tpr_plan_heads", n, req.ctypes.data, ctx.ctypes.data, oo.ctypes.data, ot.ctypes.data,
+        no.ctypes.data, nt.ctypes.data, ids.ctypes.data, total_heads, int(kvb), cap,
+        out.ctypes.data, _native.ctypes.byref(n_out),
+    )
+    return out[: n_out.value].copy()
+
+
+def head_transfers(old: KvLayout, new: KvLayout, kv_bytes_per_token_per_head: int) -> list[Transfer]:
+    """Coalesced head-range moves taking ``old``'s requests to ``new``'s placement.
+
+    Reference: migration.py:101-134 (GPU sets are not checked, so the engine
+    may use it for disjoint groups, engine.py:571-589).
+    """
+    return head_transfers_array(old, new, kv_bytes_per_token_per_head).transfers
+
+
+def head_transfers_array(old: KvLayout, new: KvLayout, kvb: int) -> MigrationPlan:
+    if old.total_heads != new.total_heads:
+        raise MigrationError("head counts differ between layouts")
+    rows = [(r, c, old.group, old.tp, new.group, new.tp) for r, c in old.requests]
+    return MigrationPlan.from_array(_plan_native(rows, old.total_heads, kvb))
+
+
+def plan_repartition(old_layouts: list[KvLayout], new_layouts, kv_bytes_per_token_per_head: int,
+                     handshake_ms: float = 0.0) -> MigrationPlan:
+    """Transfers converting old TP groups into the new layout(s) (migration.py:137-189).
+
+    Validation and transfer order follow the reference: new layouts in list
+    order, each layout's requests in order, head runs ascending.
+    """
+    if isinstance(new_layouts, KvLayout):
+        new_layouts = [new_layouts]
+    old_gpus = {g for lay in old_layouts for g in lay.group}
+    new_gpus = {g for lay in new_layouts for g in lay.group}
+    if old_gpus != new_gpus:
+        raise MigrationError(f"GPU sets differ: old={sorted(old_gpus)} new={sorted(new_gpus)}")
+    if len({lay.total_heads for lay in [*old_layouts, *new_layouts]}) != 1:
+        raise MigrationError("all layouts must share total_heads")
+    source: dict[int, tuple[KvLayout, int]] = {}
+    for lay in old_layouts:
+        for rid, ctx in lay.requests:
+            source[rid] = (lay, ctx)  # a duplicated request: the last one wins
+    carried = [rid for lay in new_layouts for rid, _ in lay.requests]
+    if sorted(carried) != sorted(source):
+        raise MigrationError("new layouts must carry exactly the old requests")
+    rows = []
+    for lay in new_layouts:
+        for rid, ctx in lay.requests:
+            old, old_ctx = source[rid]
+            if old_ctx != ctx:
+                raise MigrationError(f"request {rid}: context length changed")
+            rows.append((rid, ctx, old.group, old.tp, lay.group, lay.tp))
+    total_heads = new_layouts[0].total_heads if new_layouts else (
+        old_layouts[0].total_heads if old_layouts else 1)
+    arr = _plan_native(rows, total_heads, kv_bytes_per_token_per_head)
+    return MigrationPlan.from_array(arr, handshake_ms=handshake_ms)
+
+
+def layout_placement(layouts) -> dict:
+    """{(request, head): gpu} of canonical layouts (migration.py:210-218)."""
+    if isinstance(layouts, KvLayout):
+        layouts = [layouts]
+    placement = {}
+    for lay in layouts:
+        owners = lay.owners()
+        for rid, _ in lay.requests:
+            for h, g in enumerate(owners):
+                placement[(rid, h)] = g
+    return placement
+
+
+def apply_plan(old_layouts: list[KvLayout], plan: MigrationPlan) -> dict:
+    """Replay ``plan`` on the old placement (migration.py:192-207)."""
+    placement = layout_placement(list(old_layouts))
+    for src, dst, rid, lo, hi, _ in plan.as_array().tolist():
+        for h in range(lo, hi):
+            here = placement.get((rid, h))
+            if here != src:
+                raise MigrationError(
+                    f"transfer of request {rid} head {h} from gpu {src}, but it is on {here}"
+                )
+            placement[(rid, h)] = dst
+    return placement
+
+
+# ---------------------------------------------------------------------------
+# cost models (migration.py:221-292), kept operation-for-operation
+# ---------------------------------------------------------------------------
+
+def _send_ms(nbytes: float, params: CostModelParams) -> float:
+    return params.per_transfer_overhead_us / 1000.0 + nbytes / (params.link_bw_gbps * 1e9) * 1000.0
+
+
+def _copy_ms(nbytes: float, params: CostModelParams) -> float:
+    return nbytes / (params.copy_bw_gbps * 1e9) * 1000.0
+
+
+def latency_per_page(plan: MigrationPlan, params: CostModelParams) -> float:
+    """Page-at-a-time sends, serial per source, parallel across sources."""
+    page_ms = _send_ms(params.page_bytes, params)
+    per_source: dict[int, float] = {}
+    for src, _dst, _r, _lo, _hi, nbytes in _rows(plan):
+        per_source[src] = per_source.get(src, 0.0) + math.ceil(nbytes / params.page_bytes) * page_ms
+    ms = max(per_source.values(), default=0.0)
+    plan.predicted_latency_ms["per_page"] = ms
+    return ms
+
+
+def latency_aggregate(plan: MigrationPlan, params: CostModelParams) -> float:
+    """Pack each source's fragments into one buffer, then one send."""
+    ms = 0.0
+    for nbytes in plan.bytes_by_source().values():
+        ms = max(ms, _copy_ms(nbytes, params) + _send_ms(nbytes, params))
+    plan.predicted_latency_ms["aggregate"] = ms
+    return ms
+
+
+def _pipelined_source_ms(total_bytes: int, params: CostModelParams) -> float:
+    """Two-buffer schedule walked chunk by chunk (migration.py:252-272).
+
+    copy i starts after copy i-1 and after send i-2 freed its buffer; send i
+    starts after copy i and send i-1.
+    """
+    chunk = params.chunk_bytes
+    n = math.ceil(total_bytes / chunk)
+    copy_done = 0.0
+    send_done = 0.0        # send i-1
+    send_done_prev = 0.0   # send i-2
+    for i in range(n):
+        size = min(chunk, total_bytes - i * chunk)
+        start = copy_done if i >= 1 else 0.0
+        if i >= 2:
+            start = max(start, send_done_prev)
+        copy_done = start + _copy_ms(size, params)
+        go = copy_done
+        if i >= 1:
+            go = max(go, send_done)
+        send_done_prev, send_done = send_done, go + _send_ms(size, params)
+    return send_done if n else 0.0
+
+
+def latency_pipelined(plan: MigrationPlan, params: CostModelParams) -> float:
+    ms = max((_pipelined_source_ms(b, params) for b in plan.bytes_by_source().values()),
+             default=0.0)
+    plan.predicted_latency_ms["pipelined"] = ms
+    return ms
+
+
+def switch_cost(mode: str, plan: MigrationPlan, params: CostModelParams) -> float:
+    """Pause of a TP switch under a weight-handling regime (migration.py:284-292)."""
+    if mode == WARM:
+        return params.handshake_ms + latency_pipelined(plan, params)
+    if mode == NAIVE_RELOAD:
+        return params.reload_ms + latency_per_page(plan, params)
+    if mode == NAIVE_KERNEL_INIT:
+        return params.kernel_init_ms + latency_per_page(plan, params)
+    raise MigrationError(f"unknown switch mode {mode!r}")
+
+
+def weight_memory(mode: str, profile, tp: int | None = None) -> float:
+    """GB of weights per GPU under a storage scheme (migration.py:295-306)."""
+    full = profile.weight_full_copy_gb
+    if mode == "full_copy_per_gpu":
+        return full
+    if mode == "per_tp_copies":
+        return sum(full / level for level in profile.tp_levels)
+    if mode == "sharded":
+        if tp is None:
+            raise MigrationError("sharded mode needs a tp level")
+        return full / tp
+    raise MigrationError(f"unknown weight memory mode {mode!r}")
+
+
+def _rows(plan: MigrationPlan):
+    if plan._list is not None:
+        for t in plan._list:
+            yield t.src_gpu, t.dst_gpu, t.request_id, t.head_lo, t.head_hi, t.bytes
+    else:
+        yield from plan._arr.tolist()

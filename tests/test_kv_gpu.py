@@ -1,0 +1,169 @@
+"""K3 + K1 on B200 vs the oracle (oracle/kvmove.c): pools, block tables and
+free rings must be bit-exact after every migration, at oracle-friendly sizes;
+at BASELINE sizes through the size-independent property check (every owned
+page still carries its placement-invariant pattern, block tables realise
+layout_placement)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import check, kvmove
+from paper_2605_05467_b200 import geometry, migration as M, workloads
+from paper_2605_05467_b200.kvcache import PagedKvCluster
+
+pytestmark = pytest.mark.gpu
+
+TINY = geometry.KvGeometry(layers=2, head_dim=32, total_heads=8)
+
+
+def make(kv, gpus, units=512, reqs=8, blocks=16, fragmented=True, seed=0):
+    c = PagedKvCluster(kv, gpus, units_per_gpu=units, max_requests=reqs, max_blocks=blocks,
+                       fragmented=fragmented, seed=seed)
+    c.fill_garbage(seed=seed + 100)
+    return c
+
+
+def migrate_and_compare(cluster, plan):
+    before = cluster.snapshot()
+    rec = cluster.records(plan, validate=False)
+    stats = cluster.migrate(plan)
+    after = cluster.snapshot()
+    want = check.expected_after(cluster, before, rec)
+    diff = check.compare(after, want)
+    assert want["status"] == 0
+    assert int(cluster.status.item()) == 0
+    assert not any(diff.values()), diff
+    assert stats.units == want["pages"]
+    return stats
+
+
+@pytest.mark.parametrize("tp_old,tp_new", [(a, b) for a in (1, 2, 4, 8) for b in (1, 2, 4, 8) if a != b])
+@pytest.mark.parametrize("fragmented", [False, True])
+def test_all_transitions_bit_exact(tp_old, tp_new, fragmented):
+    gpus = tuple(range(8))
+    rng = np.random.default_rng(tp_old * 10 + tp_new)
+    reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 200, size=12))]
+    old = workloads.round_robin(workloads.tp_groups(gpus, tp_old), reqs, 8)
+    new = workloads.round_robin(workloads.tp_groups(gpus, tp_new), reqs, 8)
+    c = make(TINY, gpus, units=256, reqs=16, blocks=16, fragmented=fragmented, seed=tp_new)
+    c.admit(old, seed=5)
+    plan = M.plan_repartition(old, new, TINY.kv_bytes_per_token_per_head)
+    stats = migrate_and_compare(c, plan)
+    assert stats.bytes == plan.total_bytes
+    assert c.placement() == M.layout_placement(new)
+    v = c.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
+def test_chain_of_switches_and_back():
+    gpus = (0, 1, 2, 3)
+    reqs = [(i, 1 + 37 * i) for i in range(10)]  # ragged, incl. 1-token request
+    c = make(TINY, gpus, units=512, reqs=16, blocks=32)
+    layouts = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2, 4)}
+    c.admit(layouts[1], seed=9)
+    seq = [1, 2, 4, 2, 1, 4, 1]
+    for a, b in zip(seq, seq[1:]):
+        plan = M.plan_repartition(layouts[a], layouts[b], TINY.kv_bytes_per_token_per_head)
+        migrate_and_compare(c, plan)
+    v = c.verify(seed=9)
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+    assert v["pages_checked"] == sum(8 * TINY.blocks(ctx) for _, ctx in reqs)
+
+
+def test_engine_path_disjoint_groups():
+    # prefill->decode handoff style: head_transfers between disjoint groups
+    gpus = (0, 1, 2, 3, 4, 5)
+    c = make(TINY, gpus)
+    old = M.KvLayout((0, 1), 2, 8, ((3, 70), (4, 16)))
+    c.admit([old], seed=2)
+    new = M.KvLayout((2, 3, 4, 5), 4, 8, ((3, 70), (4, 16)))
+    plan = M.head_transfers_array(old, new, TINY.kv_bytes_per_token_per_head)
+    migrate_and_compare(c, plan)
+    assert c.placement() == M.layout_placement(new)
+
+
+def test_c_oracle_matches_python_oracle():
+    gpus = (0, 1)
+    c = make(TINY, gpus, units=128, reqs=4, blocks=8)
+    old = workloads.round_robin([(0,), (1,)], [(0, 33), (1, 17), (2, 64)], 8)
+    new = workloads.round_robin([(0, 1)], [(0, 33), (1, 17), (2, 64)], 8)
+    c.admit(old, seed=1)
+    before = c.snapshot()
+    rec = c.records(M.plan_repartition(old, new, TINY.kv_bytes_per_token_per_head))
+    a = check.expected_after(c, before, rec, impl="c")
+    b = check.expected_after(c, before, rec, impl="py")
+    assert not any(check.compare(a, b).values())
+
+
+def test_wrong_source_rejected_on_host():
+    c = make(TINY, (0, 1))
+    c.admit([M.KvLayout((0,), 1, 8, ((0, 10),))], seed=1)
+    bad = M.MigrationPlan(transfers=[M.Transfer(1, 0, 0, 0, 4, 4 * 10 * TINY.kv_bytes_per_token_per_head)])
+    with pytest.raises(M.MigrationError, match="but it is on 0"):
+        c.migrate(bad)
+
+
+def test_wrong_source_flagged_on_device_without_host_validation():
+    c = make(TINY, (0, 1))
+    c.admit([M.KvLayout((0,), 1, 8, ((0, 10),))], seed=1)
+    bad = M.MigrationPlan(transfers=[M.Transfer(1, 0, 0, 0, 4, 4 * 10 * TINY.kv_bytes_per_token_per_head)])
+    c.migrate(bad, validate=False)
+    torch.cuda.synchronize()
+    assert int(c.status.item()) & 1
+
+
+def test_capacity_error():
+    c = make(TINY, (0, 1), units=16, reqs=4, blocks=8)
+    c.admit([M.KvLayout((0,), 1, 8, ((0, 16),))], seed=1)  # 8 units on gpu 0
+    c.admit([M.KvLayout((1,), 1, 8, ((1, 16),))], seed=1)  # 8 units on gpu 1
+    with pytest.raises(M.MigrationError, match="units needed"):
+        c.admit([M.KvLayout((1,), 1, 8, ((2, 160),))], seed=1)
+
+
+def test_empty_plan_is_a_noop():
+    c = make(TINY, (0, 1))
+    lay = M.KvLayout((0, 1), 2, 8, ((0, 5),))
+    c.admit([lay], seed=1)
+    s = c.migrate(M.plan_repartition([lay], lay, TINY.kv_bytes_per_token_per_head))
+    assert s.units == 0 and s.bytes == 0
+
+
+def test_zero_context_request_moves_nothing():
+    c = make(TINY, (0, 1))
+    old = [M.KvLayout((0,), 1, 8, ((5, 0),)), M.KvLayout((1,), 1, 8, ())]
+    new = M.KvLayout((0, 1), 2, 8, ((5, 0),))
+    c.admit(old, seed=1)
+    plan = M.plan_repartition(old, new, TINY.kv_bytes_per_token_per_head)
+    assert len(plan) == 1 and plan.total_bytes == 0
+    migrate_and_compare(c, plan)
+
+
+@pytest.mark.slow
+def test_cfg1_full_size_bit_exact():
+    w = workloads.config(0)
+    kv = w.model.kv
+    c = make(kv, w.gpus, units=1024, reqs=4, blocks=32)
+    c.admit(w.old, seed=3)
+    plan = M.plan_repartition(w.old, w.new, kv.kv_bytes_per_token_per_head)
+    assert plan.total_bytes == 128 * 2**20
+    migrate_and_compare(c, plan)
+    v = c.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_property():
+    w = workloads.config(1, weights=False)
+    kv = w.model.kv
+    c = PagedKvCluster(kv, w.gpus, units_per_gpu=60000, max_requests=64, max_blocks=256,
+                       fragmented=True, seed=1)
+    c.admit(w.old, seed=4)
+    plan = M.plan_repartition(w.old, w.new, kv.kv_bytes_per_token_per_head)
+    assert plan.total_bytes == 24 * 2**30
+    s = c.migrate(plan)
+    assert s.bytes == plan.total_bytes
+    v = c.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
+    assert v["pages_checked"] == 64 * 8 * 256
+    assert c.placement() == M.layout_placement(w.new)

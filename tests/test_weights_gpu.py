@@ -1,0 +1,125 @@
+"""K2 weight reshard on B200 vs the narrow/concatenate oracle (oracle/weights.py).
+
+Every TP shard a GPU computes with after a reshard must equal the matching
+rows/columns of the full matrix reassembled from the OLD shards on the host,
+bit for bit; and the fetched volume must equal what weight_memory("sharded")
+implies."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import weights as W
+from paper_2605_05467_b200 import geometry, migration as M, workloads
+from paper_2605_05467_b200.weights import ShardedWeightStore
+
+pytestmark = pytest.mark.gpu
+
+MODEL = geometry.tiny_geometry()
+
+
+def host_pieces(store):
+    """{matrix index: [(row0, col0, ndarray)]} from every GPU's resident slices."""
+    out = {}
+    for g in store.gpu_ids:
+        a, b = store.resident[g]
+        saved = store.active[g]
+        store.active[g] = (a, b)
+        for i, m in enumerate(store.split):
+            v = store.shard(g, m.name, m.layer).cpu().view(torch.int16).numpy().view(np.uint16)
+            r0 = a * (m.rows // 8) if m.split == "col" else 0
+            c0 = a * (m.cols // 8) if m.split == "row" else 0
+            out.setdefault(i, []).append((r0, c0, v.copy()))
+        store.active[g] = saved
+    return out
+
+
+def check_against_oracle(store, pieces, groups):
+    for grp in groups:
+        tp = len(grp)
+        for rank, g in enumerate(grp):
+            for i, m in enumerate(store.split):
+                full, seen = W.assemble_full(pieces[i], m.rows, m.cols)
+                want = W.expected_shard(full, m.split, tp, rank)
+                (r0, r1), (c0, c1) = W.shard_bounds(m.split, m.rows, m.cols, tp, rank)
+                assert seen[r0:r1, c0:c1].all()
+                got = store.shard(g, m.name, m.layer).cpu().view(torch.int16).numpy().view(np.uint16)
+                assert np.array_equal(got, want), (m.name, m.layer, g)
+
+
+@pytest.mark.parametrize("tp_old,tp_new", [(a, b) for a in (1, 2, 4, 8) for b in (1, 2, 4, 8) if a != b])
+def test_all_transitions_bit_exact(tp_old, tp_new):
+    gpus = tuple(range(8))
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load(workloads.tp_groups(gpus, tp_old))
+    pieces = host_pieces(store)
+    new_groups = workloads.tp_groups(gpus, tp_new)
+    stats = store.reshard(new_groups)
+    torch.cuda.synchronize()
+    check_against_oracle(store, pieces, new_groups)
+    assert store.verify() == 0
+    # volume: a GPU whose new shard is resident moves nothing; otherwise it
+    # keeps its 1/tp_old and fetches the rest of its 1/tp_new (the difference
+    # of weight_memory("sharded") at the two levels, split matrices only)
+    split = store.bytes_per_slice * 8
+    if tp_new > tp_old:
+        assert stats.bytes == 0 and stats.views == 8
+    else:
+        assert stats.remote_bytes == 8 * (split // tp_new - split // tp_old)
+        assert stats.local_bytes == 8 * (split // tp_old)
+        gb = M.weight_memory("sharded", MODEL, tp=tp_new) - M.weight_memory("sharded", MODEL, tp=tp_old)
+        rep = sum(m.rows * m.cols for m in store.replicated) * MODEL.dtype_bytes
+        assert stats.remote_bytes / 8 == pytest.approx(gb * 1e9 - rep * (1 / tp_new - 1 / tp_old))
+    store.finish()
+
+
+def test_sequence_reuses_resident_slices():
+    gpus = (0, 1, 2, 3)
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load(workloads.tp_groups(gpus, 2))
+    fwd = store.reshard(workloads.tp_groups(gpus, 4))   # GPU1, GPU2 fetch a quarter each
+    assert fwd.remote_bytes == 2 * store.bytes_per_slice * 2 and fwd.local_bytes == 0
+    assert fwd.views == 2
+    pieces = host_pieces(store)
+    back = store.reshard(workloads.tp_groups(gpus, 2))  # GPU0, GPU3 still resident on halves
+    assert back.views == 2
+    torch.cuda.synchronize()
+    check_against_oracle(store, pieces, workloads.tp_groups(gpus, 2))
+    assert store.verify() == 0
+    store.finish()
+
+
+def test_full_copy_mode_moves_nothing():
+    gpus = (0, 1, 2, 3)
+    store = ShardedWeightStore(MODEL, gpus, mode="full_copy_per_gpu")
+    store.load(workloads.tp_groups(gpus, 4))
+    for tp in (1, 2, 4, 2, 1):
+        s = store.reshard(workloads.tp_groups(gpus, tp))
+        assert s.bytes == 0 and s.views == 4
+        assert store.verify() == 0
+
+
+def test_scale_in_parks_gpus():
+    gpus = tuple(range(8))
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load([gpus])
+    s = store.reshard([(0,)], parked=gpus[1:])
+    torch.cuda.synchronize()
+    split_bytes = sum(m.rows * m.cols for m in store.split) * MODEL.dtype_bytes
+    assert s.remote_bytes == 7 * split_bytes // 8 and s.local_bytes == split_bytes // 8
+    assert store.verify() == 0
+    # egress balanced: every parked GPU serves exactly its own slice
+    assert sorted(v for g, v in s.egress.items() if g) == [split_bytes // 8] * 7
+
+
+@pytest.mark.slow
+def test_llama8b_tp2_tp4_full_size():
+    gpus = (0, 1, 2, 3)
+    store = ShardedWeightStore(geometry.LLAMA_3_1_8B, gpus)
+    store.load(workloads.tp_groups(gpus, 2))
+    s = store.reshard(workloads.tp_groups(gpus, 4))
+    torch.cuda.synchronize()
+    split = sum(m.rows * m.cols for m in store.split) * 2
+    assert s.remote_bytes == 2 * split // 4 and s.views == 2
+    assert store.verify() == 0
+    store.finish()
