@@ -1,0 +1,487 @@
+"""TP-switch benchmark (BASELINE.json metric: TP-switch latency (ms) and
+KV+weight reshard GB/s vs the NVLink/HBM roofline).
+
+One step = one complete stop-and-migrate TP switch of the workload: plan
+(native planner), K3 block-table remap, K1 paged-KV migration on one stream in
+parallel with K2 weight reshard on another, joined. Steps alternate A->B and
+B->A so every step is a real switch of the same workload (the reverse moves
+the same KV bytes, test_migration.py:146-155).
+
+Default workload (N=1): BASELINE configs[1], Llama-3.1-8B TP2<->TP4, 64 seqs x
+4096 tokens of bf16 KV + sharded weights, on 4 logical GPUs whose pools all
+live in one B200's HBM (the 1-GPU mode: every byte is an HBM read + write).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N>1) every rank runs the same workload on its own GPU
+(replicas: the cross-GPU P2P path is not exercised by this harness yet) and
+rank 0 prints value = bytes moved by all ranks / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TP-switch latency (ms) and KV+weight reshard GB/s vs NVLink/HBM roofline"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int, interval_ms: int = 10):
+        self.index = index
+        self.interval_ms = interval_ms
+        self.proc = None
+        self.samples: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            if line.strip():
+                self.samples.append((time.time(), line))
+
+    def __enter__(self):
+        import threading
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
+            self.thread = threading.Thread(target=self._reader, daemon=True)
+            self.thread.start()
+            deadline = time.time() + 3.0
+            while not self.samples and time.time() < deadline:
+                time.sleep(0.01)
+        except OSError:
+            self.proc = None
+        return self
+
+    def start(self):
+        self.t0 = time.time()
+
+    def stop(self):
+        self.t1 = time.time()
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0, t1 = self.t0 or 0.0, self.t1 or float("inf")
+        window = [l for t, l in self.samples if t0 <= t <= t1]
+        if not window and self.samples:  # region shorter than one interval
+            mid = (t0 + t1) / 2
+            window = [min(self.samples, key=lambda s: abs(s[0] - mid))[1]]
+        for line in window:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# setup
+# ---------------------------------------------------------------------------
+
+def build_workload(cfg: int, seqs: int | None):
+    from paper_2605_05467_b200 import workloads
+    kw = {}
+    if seqs:
+        kw["seqs"] = seqs
+    return workloads.config(cfg, **kw)
+
+
+def capacity_units(w, kv) -> int:
+    """Units per logical GPU: resident KV of the larger layout + incoming."""
+    from paper_2605_05467_b200 import migration as M
+    need = {g: 0 for g in w.gpus}
+    for lays in (w.old, w.new):
+        for lay in lays:
+            for rid, ctx in lay.requests:
+                for g in lay.owners():
+                    need[g] += kv.blocks(ctx)
+    peak = max(need.values())
+    return int(peak * 1.05) + 64
+
+
+def setup_ours(w, device):
+    import torch
+    from paper_2605_05467_b200.controller import ReconfigurationExecutor
+    from paper_2605_05467_b200.kvcache import PagedKvCluster
+    from paper_2605_05467_b200.weights import ShardedWeightStore
+
+    kv = w.model.kv
+    max_ctx = max(c for _, c in w.requests)
+    cluster = PagedKvCluster(kv, w.gpus, units_per_gpu=capacity_units(w, kv),
+                             max_requests=len(w.requests), max_blocks=kv.blocks(max_ctx),
+                             device=device, fragmented=True, seed=0)
+    cluster.admit(w.old, seed=1234)
+    store = None
+    if w.old_weight_groups is not None:
+        store = ShardedWeightStore(w.model, w.gpus, device=device)
+        store.load(w.old_weight_groups)
+    torch.cuda.synchronize()
+    return ReconfigurationExecutor(cluster, store, time_kernels=True)
+
+
+def one_switch(ex, w, forward: bool, sync: bool):
+    if forward:
+        return ex.switch(w.old, w.new, new_weight_groups=w.new_weight_groups,
+                         parked=w.parked, sync=sync, validate=False)
+    return ex.switch(w.new, w.old, new_weight_groups=w.old_weight_groups, parked=(),
+                     sync=sync, validate=False)
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle restatement; test infrastructure)
+# ---------------------------------------------------------------------------
+
+class CpuReference:
+    """The reference's CPU path restated: pure-Python planner (as the
+    reference's plan_repartition) + C restatement of page movement and weight
+    slicing on host memory, all host threads. Bounded sample of the workload."""
+
+    def __init__(self, w, sample_seqs: int, threads: int):
+        from oracle import kvmove, plan_oracle
+        from paper_2605_05467_b200 import workloads
+        self.kvmove, self.po = kvmove, plan_oracle
+        kvmove.build()
+        self.threads = threads
+        reqs = w.requests[:sample_seqs]
+        groups_old = [lay.group for lay in w.old]
+        groups_new = [lay.group for lay in w.new]
+        H = w.model.n_kv_heads
+        self.old = [(g, H, r) for g, r in zip(groups_old, _rr(groups_old, reqs))]
+        self.new = [(g, H, r) for g, r in zip(groups_new, _rr(groups_new, reqs))]
+        kv = w.model.kv
+        self.kv = kv
+        self.kvb = kv.kv_bytes_per_token_per_head
+        self.slot = {g: i for i, g in enumerate(w.gpus)}
+        self.rslot = {rid: i for i, (rid, _) in enumerate(reqs)}
+        self.ctx = dict(reqs)
+        max_blocks = max(kv.blocks(c) for _, c in reqs)
+        need = {g: 0 for g in w.gpus}
+        for lays in (self.old, self.new):
+            for grp, _, rr in lays:
+                per = H // len(grp)
+                for _, c in rr:
+                    for gg in grp:
+                        need[gg] += per * kv.blocks(c)
+        units = max(need.values()) + 16
+        self.geo = dict(layers=kv.layers, head_dim=kv.head_dim, dtype_bytes=kv.dtype_bytes,
+                        block_tokens=kv.block_tokens, total_heads=H, max_blocks=max_blocks,
+                        n_req_slots=len(reqs), n_units=units)
+        n = len(w.gpus)
+        self.pools = [np.ones(units * kv.unit_bytes, np.uint8) for _ in range(n)]
+        self.tables = [np.full(len(reqs) * H * max_blocks, -1, np.int32) for _ in range(n)]
+        rng = np.random.default_rng(0)
+        self.rings = [rng.permutation(units).astype(np.int32) for _ in range(n)]
+        self.head = [0] * n
+        self.tail = [units] * n
+        adm = []
+        for grp, _, rr in self.old:
+            per = H // len(grp)
+            for rid, c in rr:
+                for r, g in enumerate(grp):
+                    adm.append((-1, self.slot[g], self.rslot[rid], r * per, (r + 1) * per, c))
+        self._exec(np.asarray(adm, np.int64))
+        # weights: the same 1/`frac` share of every slice copy as the GPU arm
+        self.frac = sample_seqs / len(w.requests)
+        self.w = w
+        self.wbytes_slice = None
+        if w.old_weight_groups is not None:
+            from paper_2605_05467_b200.weights import groups_ranges
+            split = [m for m in w.model.matrices if m.split != "rep"]
+            per_slice = sum((m.rows * m.cols) // 8 for m in split) * w.model.dtype_bytes
+            self.wbytes_slice = max(int(per_slice * self.frac) // 64 * 64, 64)
+            self.ranges = {True: groups_ranges(w.new_weight_groups), False: groups_ranges(w.old_weight_groups)}
+            self.res = dict(groups_ranges(w.old_weight_groups))
+            self.arena = {g: np.ones((b - a) * self.wbytes_slice, np.uint8) for g, (a, b) in self.res.items()}
+        self.fwd = True
+
+    def _exec(self, rec):
+        n, status, self.head, self.tail = self.kvmove.kv_migrate(
+            self.geo, self.pools, self.tables, self.rings, self.head, self.tail, rec, self.threads)
+        assert status == 0
+        return n
+
+    def step(self) -> int:
+        """One switch of the sample; returns bytes moved."""
+        src, dst = (self.old, self.new) if self.fwd else (self.new, self.old)
+        moves = self.po.plan(src, dst, self.kvb)
+        rec = np.array([(self.slot[s], self.slot[d], self.rslot[r], lo, hi, self.ctx[r])
+                        for s, d, r, lo, hi, _ in moves], np.int64).reshape(-1, 6)
+        self._exec(rec)
+        moved = sum(m[5] for m in moves)
+        if self.wbytes_slice:
+            moved += self._weights(self.ranges[self.fwd])
+        self.fwd = not self.fwd
+        return moved
+
+    def _weights(self, act) -> int:
+        blocks, moved, new_arena = [], 0, {}
+        for g, (x, y) in act.items():
+            a, b = self.res[g]
+            if a <= x and y <= b:
+                continue
+            buf = np.empty((y - x) * self.wbytes_slice, np.uint8)
+            for s in range(x, y):
+                if a <= s < b:
+                    h, ha = g, a
+                else:
+                    h = next(k for k, (p, q) in self.res.items() if p <= s < q and k != g)
+                    ha = self.res[h][0]
+                blocks.append((buf, (s - x) * self.wbytes_slice, self.arena[h],
+                               (s - ha) * self.wbytes_slice, 1, self.wbytes_slice,
+                               self.wbytes_slice, self.wbytes_slice))
+                moved += self.wbytes_slice
+            new_arena[g] = (buf, (x, y))
+        if blocks:
+            self.kvmove.copy_blocks(blocks, self.threads)
+        for g, (buf, r) in new_arena.items():
+            self.arena[g] = buf
+            self.res[g] = r
+        return moved
+
+
+def _rr(groups, reqs):
+    per = [[] for _ in groups]
+    for i, r in enumerate(reqs):
+        per[i % len(groups)].append(r)
+    return per
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_cpu_reference(w, steps: int, warmup: int, sample_seqs: int):
+    threads = cpu_threads()
+    ref = CpuReference(w, sample_seqs, threads)
+    for _ in range(warmup):
+        ref.step()
+    t0 = time.perf_counter()
+    moved = 0
+    for _ in range(steps):
+        moved += ref.step()
+    dt = time.perf_counter() - t0
+    return {"value": moved / dt / 1e9, "ms_per_step": dt / steps * 1e3, "bytes": moved,
+            "threads": threads, "sample": f"{sample_seqs} of {len(w.requests)} seqs "
+            f"(+ the same share of every weight slice copy), alternating switches"}
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=1, help="BASELINE configs[] index (0-based)")
+    ap.add_argument("--seqs", type=int, default=None)
+    ap.add_argument("--cpu-sample-seqs", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    w = build_workload(args.config, args.seqs)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = run_cpu_reference(w, args.steps, args.warmup, min(args.cpu_sample_seqs, len(w.requests)))
+        line = {
+            "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": w.name, "cpu_sample": r["sample"]},
+            "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["threads"],
+                             "kind": "port", "sample": r["sample"], "cpu": cpu_model()},
+            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(device)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    ex = setup_ours(w, device)
+    fwd = True
+    for _ in range(max(args.warmup, 1)):
+        one_switch(ex, w, fwd, sync=True)
+        fwd = not fwd
+
+    # ---- device-timed region: K switches enqueued back to back --------------
+    main_stream = torch.cuda.current_stream(device)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(device.index if device.index is not None else 0) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        clk.start()
+        start.record(main_stream)
+        for _ in range(args.steps):
+            results.append(one_switch(ex, w, fwd, sync=False))
+            fwd = not fwd
+        end.record(main_stream)
+        torch.cuda.synchronize()
+        clk.stop()
+        barrier()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kv_bytes = sum(r.kv.bytes for r in results)
+    w_bytes = sum(r.weights.bytes for r in results if r.weights)
+    total_bytes = kv_bytes + w_bytes
+    k1_ms = [r.events["k1_start"].elapsed_time(r.events["k1_end"]) for r in results]
+    k2_ms = [r.events["k2_start"].elapsed_time(r.events["k2_end"]) for r in results
+             if r.weights is not None and r.weights.segments]
+    launches = sum(3 + (1 if r.weights is not None and r.weights.segments else 0) for r in results)
+    status = int(ex.kv.status.item())
+
+    # ---- end to end through the public API (host layouts -> device -> status) --
+    e2e = None
+    if not args.no_e2e:
+        from paper_2605_05467_b200.controller import host_to_device_bytes
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eb, h2d = 0, 0
+        for _ in range(args.steps):
+            r = one_switch(ex, w, fwd, sync=True)
+            fwd = not fwd
+            eb += r.bytes
+            h2d += host_to_device_bytes(r.plan, r.weights)
+            status |= r.status
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device=device, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": eb * world / e2e_s / 1e9, "unit": "GB/s",
+               "ms_per_step": e2e_s / args.steps * 1e3,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": 4}
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+
+    hbm, hbm_src = peaks()
+    k1_avg = float(np.mean(k1_ms))
+    kv_per_step = kv_bytes / args.steps
+    achieved = 2 * kv_per_step / (k1_avg * 1e-3) / 1e9  # HBM read + write GB/s
+    traffic = None
+    prof = ROOT / "profiles" / "k1_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    cpu = None
+    if not args.no_cpu:
+        r = run_cpu_reference(w, 2, 1, min(args.cpu_sample_seqs, len(w.requests)))
+        cpu = {"value": r["value"], "unit": "GB/s", "cores": r["threads"], "kind": "port",
+               "sample": r["sample"], "cpu": cpu_model()}
+    value = total_bytes * world / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {
+            "workload": w.name, "model": w.model.name, "logical_gpus_per_device": len(w.gpus),
+            "seqs": len(w.requests), "ctx": w.requests[0][1],
+            "switch": "alternating forward/reverse, full stop-and-migrate (plan+K3+K1||K2)",
+            "kv_bytes_per_step": kv_per_step, "weight_bytes_per_step": w_bytes / args.steps,
+            "l2": "inputs larger than L2 (>= 24 GiB moved per step)",
+            "parallelism": "replicas" if world > 1 else "1 GPU, logical ranks",
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "kernel": "tpr_k1_kv_migrate",
+                     "k1_ms": k1_avg, "k2_ms": float(np.mean(k2_ms)) if k2_ms else None,
+                     "peak_source": hbm_src},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "status": status,
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -170,13 +170,16 @@ class PagedKvCluster:
             if in_u[s] > free:
                 raise MigrationError(
                     f"gpu {self.gpu_ids[s]}: {in_u[s]} KV units needed, {free} free")
+        self._last_in, self._last_out = in_u, out_u
+        if total == 0:  # e.g. zero-length contexts: nothing to allocate or move
+            return 0
         with torch.cuda.stream(stream):  # scratch lives on the stream that uses it
             self._xf = self._grow(self._xf, n * 6)
             self._meta = self._grow(self._meta, n * 4)
             self._work = self._grow(self._work, total * 4)
             if want_ext:
                 self._work_ext = self._grow(self._work_ext, total * 4)
-            self._staging.upload(xf.astype(np.int32, copy=False), self._xf, stream)
+            self._staging.upload(xf.astype(np.int32), self._xf, stream)
         cl = self._cluster_c()
         _native.call(
             "tpr_kv_remap", ctypes.byref(self._geo), ctypes.byref(cl), self._xf.data_ptr(), n,
@@ -187,7 +190,6 @@ class PagedKvCluster:
         for s in range(self.n_gpus):
             self.ring_head[s] += int(in_u[s])
             self.ring_tail[s] += int(out_u[s])
-        self._last_in, self._last_out = in_u, out_u
         return total
 
     # -------------------------------------------------------------- admission

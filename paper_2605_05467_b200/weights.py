@@ -100,7 +100,6 @@ class ShardedWeightStore:
         self.active: dict[int, tuple[int, int]] = {}
         self.arena: dict[int, torch.Tensor] = {}
         self.rep_arena: dict[int, torch.Tensor] = {}
-        self._retired: list[tuple[torch.cuda.Event, list[torch.Tensor]]] = []
         self._segs_dev = {}
         self._prefix_dev = {}
 
@@ -252,8 +251,10 @@ class ShardedWeightStore:
     def reshard(self, new_groups: Sequence[Sequence[int]], stream: torch.cuda.Stream | None = None,
                 events: tuple | None = None, parked: Sequence[int] = ()) -> ReshardStats:
         """Move to ``new_groups``: K2 copies for every GPU whose new shard is not
-        resident; views for the rest. Stream-ordered, no host sync."""
-        self._reap()
+        resident; views for the rest. Stream-ordered, no host sync: new arenas
+        are allocated and old ones released on ``stream`` (the caching
+        allocator reuses a block on the same stream only after the K2 that
+        last touched it), so the host may run ahead without holding memory."""
         act, new_res, moves = self.plan(new_groups, parked)
         for g in parked:
             act[g] = new_res[g]
@@ -269,7 +270,9 @@ class ShardedWeightStore:
                 stats.views += 1
                 continue
             x, y = new_res[g]
-            new_arena[g] = torch.empty((y - x) * self.bytes_per_slice, dtype=torch.uint8, device=dev)
+            with torch.cuda.stream(stream):
+                new_arena[g] = torch.empty((y - x) * self.bytes_per_slice, dtype=torch.uint8,
+                                           device=dev)
             segs.append(self._segments(g, new_res, moves, new_arena[g]))
             for src, lo, hi in moves[g]:
                 nb = (hi - lo) * self.bytes_per_slice
@@ -287,15 +290,13 @@ class ShardedWeightStore:
             self._launch(seg, dev, stream)
         if events:
             events[1].record(stream)
-        retired = [self.arena[g] for g in new_arena]
         for g, t in new_arena.items():
+            if self.arena[g].device == dev:
+                self.arena[g].record_stream(stream)
             self.arena[g] = t
         self.resident = new_res
         self.active = act
-        if retired:
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            self._retired.append((ev, retired))
+        self._stream = stream
         return stats
 
     def _launch(self, seg: np.ndarray, dev: torch.device, stream: torch.cuda.Stream) -> None:
@@ -315,17 +316,10 @@ class ShardedWeightStore:
                          n_items.value, CHUNK_BYTES, stream.cuda_stream)
         self._segs_dev[dev] = d
 
-    def _reap(self) -> None:
-        keep = []
-        for ev, tensors in self._retired:
-            if not ev.query():
-                keep.append((ev, tensors))
-        self._retired = keep
-
     def finish(self) -> None:
-        for ev, _ in self._retired:
-            ev.synchronize()
-        self._retired = []
+        """Wait for the last reshard's copies."""
+        if getattr(self, "_stream", None) is not None:
+            self._stream.synchronize()
 
     # ------------------------------------------------------------- checking
     def verify(self, stream: torch.cuda.Stream | None = None) -> int:

@@ -46,7 +46,7 @@ def test_all_transitions_bit_exact(tp_old, tp_new, fragmented):
     reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 200, size=12))]
     old = workloads.round_robin(workloads.tp_groups(gpus, tp_old), reqs, 8)
     new = workloads.round_robin(workloads.tp_groups(gpus, tp_new), reqs, 8)
-    c = make(TINY, gpus, units=256, reqs=16, blocks=16, fragmented=fragmented, seed=tp_new)
+    c = make(TINY, gpus, units=1024, reqs=16, blocks=16, fragmented=fragmented, seed=tp_new)
     c.admit(old, seed=5)
     plan = M.plan_repartition(old, new, TINY.kv_bytes_per_token_per_head)
     stats = migrate_and_compare(c, plan)
@@ -118,7 +118,7 @@ def test_capacity_error():
     c.admit([M.KvLayout((0,), 1, 8, ((0, 16),))], seed=1)  # 8 units on gpu 0
     c.admit([M.KvLayout((1,), 1, 8, ((1, 16),))], seed=1)  # 8 units on gpu 1
     with pytest.raises(M.MigrationError, match="units needed"):
-        c.admit([M.KvLayout((1,), 1, 8, ((2, 160),))], seed=1)
+        c.admit([M.KvLayout((1,), 1, 8, ((2, 64),))], seed=1)  # 32 more units
 
 
 def test_empty_plan_is_a_noop():
@@ -156,7 +156,9 @@ def test_cfg1_full_size_bit_exact():
 def test_cfg2_full_size_property():
     w = workloads.config(1, weights=False)
     kv = w.model.kv
-    c = PagedKvCluster(kv, w.gpus, units_per_gpu=60000, max_requests=64, max_blocks=256,
+    # GPU1 keeps 4 heads x 32 requests and receives heads 2-3 of all 64 before
+    # releasing: 2 x 32768 pages at peak
+    c = PagedKvCluster(kv, w.gpus, units_per_gpu=65536 + 64, max_requests=64, max_blocks=256,
                        fragmented=True, seed=1)
     c.admit(w.old, seed=4)
     plan = M.plan_repartition(w.old, w.new, kv.kv_bytes_per_token_per_head)

@@ -11,7 +11,7 @@ import torch
 
 from oracle import weights as W
 from paper_2605_05467_b200 import geometry, migration as M, workloads
-from paper_2605_05467_b200.weights import ShardedWeightStore
+from paper_2605_05467_b200.weights import ShardedWeightStore, groups_ranges
 
 pytestmark = pytest.mark.gpu
 
@@ -58,19 +58,31 @@ def test_all_transitions_bit_exact(tp_old, tp_new):
     torch.cuda.synchronize()
     check_against_oracle(store, pieces, new_groups)
     assert store.verify() == 0
-    # volume: a GPU whose new shard is resident moves nothing; otherwise it
-    # keeps its 1/tp_old and fetches the rest of its 1/tp_new (the difference
-    # of weight_memory("sharded") at the two levels, split matrices only)
-    split = store.bytes_per_slice * 8
-    if tp_new > tp_old:
-        assert stats.bytes == 0 and stats.views == 8
-    else:
-        assert stats.remote_bytes == 8 * (split // tp_new - split // tp_old)
-        assert stats.local_bytes == 8 * (split // tp_old)
-        gb = M.weight_memory("sharded", MODEL, tp=tp_new) - M.weight_memory("sharded", MODEL, tp=tp_old)
-        rep = sum(m.rows * m.cols for m in store.replicated) * MODEL.dtype_bytes
-        assert stats.remote_bytes / 8 == pytest.approx(gb * 1e9 - rep * (1 / tp_new - 1 / tp_old))
+    local, remote, views = expected_volume(workloads.tp_groups(gpus, tp_old), new_groups,
+                                           store.bytes_per_slice)
+    assert (stats.local_bytes, stats.remote_bytes, stats.views) == (local, remote, views)
+    # every rebuilt shard is exactly weight_memory("sharded", tp_new) of the
+    # split matrices (replicated norms never move)
+    rep = sum(m.rows * m.cols for m in store.replicated) * MODEL.dtype_bytes
+    per_gpu = M.weight_memory("sharded", MODEL, tp=tp_new) * 1e9 - rep / tp_new
+    assert (stats.local_bytes + stats.remote_bytes) == pytest.approx((8 - views) * per_gpu)
     store.finish()
+
+
+def expected_volume(old_groups, new_groups, per_slice):
+    """Independent count: a GPU whose new slice range lies inside its old one
+    is a view; otherwise it copies the overlap locally and fetches the rest."""
+    old, new = groups_ranges(old_groups), groups_ranges(new_groups)
+    local = remote = views = 0
+    for g, (x, y) in new.items():
+        a, b = old[g]
+        if a <= x and y <= b:
+            views += 1
+            continue
+        inter = max(0, min(b, y) - max(a, x))
+        local += inter
+        remote += (y - x) - inter
+    return local * per_slice, remote * per_slice, views
 
 
 def test_sequence_reuses_resident_slices():
