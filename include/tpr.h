@@ -177,6 +177,10 @@ int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch_el
                       int32_t elem_bytes, int64_t* d_mismatch, void* stream);
 
 /* ---- peer memory (one process per GPU) -------------------------------- */
+/* Whole-allocation device memory (cudaMalloc): the pointer is the allocation
+ * base, so its IPC handle maps exactly this buffer in a peer process. */
+int tpr_device_alloc(uint64_t bytes, uint64_t* dptr);
+int tpr_device_free(uint64_t dptr);
 int tpr_enable_peer(int32_t peer_device);
 int tpr_ipc_get_handle(uint64_t dptr, uint8_t* handle64);
 int tpr_ipc_open(const uint8_t* handle64, uint64_t* dptr);

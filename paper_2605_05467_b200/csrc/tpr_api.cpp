@@ -318,6 +318,20 @@ int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch, i
 // ---------------------------------------------------------------------------
 // Peer memory
 // ---------------------------------------------------------------------------
+int tpr_device_alloc(uint64_t bytes, uint64_t* dptr) {
+  if (!dptr) return fail(TPR_EINVAL, "null output pointer");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  *dptr = reinterpret_cast<uint64_t>(p);
+  return TPR_OK;
+}
+
+int tpr_device_free(uint64_t dptr) {
+  cudaError_t e = cudaFree(reinterpret_cast<void*>(dptr));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "cudaFree");
+}
+
 int tpr_enable_peer(int32_t peer) {
   cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
   if (e == cudaErrorPeerAccessAlreadyEnabled) {

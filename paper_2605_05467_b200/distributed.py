@@ -1,0 +1,334 @@
+"""One process per GPU: push-model KV migration over CUDA-IPC peer pools.
+
+Each rank owns the pool, block table and free ring of one GPU slot. The
+buffers come from ``tpr_device_alloc`` (whole cudaMalloc allocations). Their
+IPC handles are exchanged once with ``all_gather_object``, and every rank maps
+its peers' buffers (``tpr_ipc_open``). A switch then runs like this:
+
+1. handshake (modeled as ``handshake_ms``, migration.py:84): an
+   all-gather of the plan digest and the ring counters, which every rank also
+   tracks itself. It proves all ranks execute the same plan from the same
+   state. It is the only exchange step.
+2. K3 with ``filter_src = my slot``: allocation offsets follow the WHOLE plan,
+   so a source rank computes the destination pages by itself, reading the
+   peer's free ring and writing the peer's block table remotely.
+3. K1 pushes the pages straight into peer pools (NVLink stores between GPUs).
+4. stream sync + barrier: after it, every destination sees complete pages.
+
+No data-path collective is involved; transfers leaving different ranks are
+independent (migration.py:275-281 takes the max over sources).
+The same code runs several ranks on ONE GPU (IPC between processes on one
+device), which is how it is tested here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native
+from .geometry import KvGeometry
+from .kvcache import MigrationStats, _PinnedStaging
+from .migration import BYTES, KvLayout, MigrationError, MigrationPlan
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device allocation (zero copy)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class DeviceBuffer:
+    """A whole cudaMalloc allocation, viewed as a uint8 torch tensor."""
+
+    def __init__(self, nbytes: int, device: torch.device):
+        self.nbytes = int(nbytes)
+        ptr = ctypes.c_uint64()
+        with torch.cuda.device(device):
+            _native.call("tpr_device_alloc", self.nbytes, ctypes.byref(ptr))
+        self.ptr = ptr.value
+        self.device = device
+        self.tensor = torch.as_tensor(_CudaArray(self.ptr, self.nbytes), device=device)
+
+    def handle(self) -> bytes:
+        buf = (ctypes.c_uint8 * 64)()
+        _native.call("tpr_ipc_get_handle", self.ptr, buf)
+        return bytes(buf)
+
+    def free(self):
+        if self.ptr:
+            self.tensor = None
+            _native.call("tpr_device_free", self.ptr)
+            self.ptr = 0
+
+
+def open_peer(handle: bytes) -> int:
+    buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    ptr = ctypes.c_uint64()
+    _native.call("tpr_ipc_open", buf, ctypes.byref(ptr))
+    return ptr.value
+
+
+# ---------------------------------------------------------------------------
+# host logic (CPU-testable)
+# ---------------------------------------------------------------------------
+
+def units_per_record(rec: np.ndarray, block_tokens: int) -> np.ndarray:
+    nblk = (rec[:, 5].astype(np.int64) + block_tokens - 1) // block_tokens
+    return (rec[:, 4] - rec[:, 3]).astype(np.int64) * nblk
+
+
+def ring_deltas(rec: np.ndarray, n_slots: int, block_tokens: int):
+    """Units allocated on / released by every slot for a record list."""
+    u = units_per_record(rec, block_tokens)
+    in_u = np.bincount(rec[:, 1], weights=u, minlength=n_slots).astype(np.int64)
+    src = rec[:, 0] >= 0
+    out_u = np.bincount(rec[src, 0], weights=u[src], minlength=n_slots).astype(np.int64)
+    return in_u, out_u
+
+
+def my_units(rec: np.ndarray, slot: int, block_tokens: int) -> int:
+    """Pages the rank owning ``slot`` pushes (transfers leaving it)."""
+    return int(units_per_record(rec[rec[:, 0] == slot], block_tokens).sum())
+
+
+def plan_digest(rec: np.ndarray) -> int:
+    return int.from_bytes(hashlib.blake2b(np.ascontiguousarray(rec, np.int64).tobytes(),
+                                          digest_size=8).digest(), "little", signed=True)
+
+
+@dataclass
+class HandshakeResult:
+    digest: int
+    heads: np.ndarray
+    tails: np.ndarray
+
+
+def handshake(rec: np.ndarray, heads, tails, group=None) -> HandshakeResult:
+    """All-gather of (plan digest, ring counters); raises if ranks disagree."""
+    mine = np.concatenate([[plan_digest(rec)], np.asarray(heads, np.int64),
+                           np.asarray(tails, np.int64)]).astype(np.int64)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(mine).to(dev)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    rows = np.stack([o.cpu().numpy() for o in out])
+    if not (rows == rows[0]).all():
+        raise MigrationError("handshake: ranks disagree on the plan or on ring state")
+    n = len(heads)
+    return HandshakeResult(int(rows[0, 0]), rows[0, 1:1 + n], rows[0, 1 + n:])
+
+
+# ---------------------------------------------------------------------------
+# the per-rank cluster
+# ---------------------------------------------------------------------------
+
+class DistributedKvCluster:
+    """The KV pool of ONE GPU slot (this rank) plus IPC views of its peers."""
+
+    def __init__(self, kv: KvGeometry, gpu_ids, units_per_gpu: int, max_requests: int,
+                 max_blocks: int, device: torch.device, group=None, fragmented: bool = False,
+                 seed: int = 0):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if len(gpu_ids) != self.world:
+            raise MigrationError("one GPU slot per rank")
+        _native.load()
+        self.kv = kv
+        self.gpu_ids = tuple(gpu_ids)
+        self.slot_of = {g: i for i, g in enumerate(self.gpu_ids)}
+        self.slot = self.rank
+        self.n_units = int(units_per_gpu)
+        self.max_requests = int(max_requests)
+        self.max_blocks = int(max_blocks)
+        self.device = torch.device(device)
+        H = kv.total_heads
+        self.pool = DeviceBuffer(self.n_units * kv.unit_bytes, self.device)
+        self.bt = DeviceBuffer(self.max_requests * H * self.max_blocks * 4, self.device)
+        self.ring = DeviceBuffer(self.n_units * 4, self.device)
+        self.bt.tensor.view(torch.int32).fill_(-1)
+        order = (np.random.default_rng(seed + self.slot).permutation(self.n_units) if fragmented
+                 else np.arange(self.n_units))
+        self.ring.tensor.view(torch.int32).copy_(torch.from_numpy(order.astype(np.int32)))
+        torch.cuda.synchronize(self.device)
+        handles = (self.pool.handle(), self.bt.handle(), self.ring.handle())
+        allh = [None] * self.world
+        dist.all_gather_object(allh, handles, group=group)
+        self.peer_ptrs = []
+        for r, hs in enumerate(allh):
+            if r == self.rank:
+                self.peer_ptrs.append((self.pool.ptr, self.bt.ptr, self.ring.ptr))
+            else:
+                self.peer_ptrs.append(tuple(open_peer(h) for h in hs))
+        self.ring_head = [0] * self.world
+        self.ring_tail = [self.n_units] * self.world
+        self.req_slot: dict[int, int] = {}
+        self.slot_ctx = np.full(self.max_requests, -1, np.int32)
+        self.owner = np.full((self.max_requests, H), -1, np.int32)
+        self._free_req_slots = list(range(self.max_requests - 1, -1, -1))
+        self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
+                                        H, self.max_blocks, self.max_requests, self.n_units)
+        self._staging = _PinnedStaging()
+        self._xf = torch.empty(0, dtype=torch.int32, device=self.device)
+        self._meta = torch.empty(0, dtype=torch.int64, device=self.device)
+        self._totals = torch.zeros(_native.TPR_TOTALS_LEN, dtype=torch.int64, device=self.device)
+        self._work = torch.empty(0, dtype=torch.int32, device=self.device)
+        self._work_ext = torch.empty(0, dtype=torch.int32, device=self.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.stream = torch.cuda.Stream(device=self.device)
+        dist.barrier(group=group)
+
+    def _cluster_c(self) -> _native.KvClusterC:
+        c = _native.KvClusterC()
+        c.n_gpus = self.world
+        for s, (pool, bt, ring) in enumerate(self.peer_ptrs):
+            c.pool[s], c.block_table[s], c.free_ring[s] = pool, bt, ring
+            c.ring_head[s] = self.ring_head[s]
+            c.ring_tail[s] = self.ring_tail[s]
+        return c
+
+    def _run_k3(self, rec: np.ndarray, filter_src: int, n_mine: int, want_ext: bool):
+        st = self.stream
+        grow = lambda t, n: t if t.numel() >= n else torch.empty(max(n, 2 * t.numel()), dtype=t.dtype,
+                                                                 device=self.device)
+        with torch.cuda.stream(st):
+            self._xf = grow(self._xf, len(rec) * 6)
+            self._meta = grow(self._meta, len(rec) * 4)
+            self._work = grow(self._work, max(n_mine, 1) * 4)
+            if want_ext:
+                self._work_ext = grow(self._work_ext, max(n_mine, 1) * 4)
+            self._staging.upload(rec.astype(np.int32), self._xf, st)
+        cl = self._cluster_c()
+        with torch.cuda.device(self.device):
+            _native.call("tpr_kv_remap", ctypes.byref(self._geo), ctypes.byref(cl), self._xf.data_ptr(),
+                         len(rec), filter_src, self._meta.data_ptr(), self._totals.data_ptr(), n_mine,
+                         self._work.data_ptr(), self._work_ext.data_ptr() if want_ext else None,
+                         self.status.data_ptr(), st.cuda_stream)
+        return cl
+
+    def _advance(self, rec: np.ndarray):
+        in_u, out_u = ring_deltas(rec, self.world, self.kv.block_tokens)
+        for s in range(self.world):
+            free = self.ring_tail[s] - self.ring_head[s]
+            if in_u[s] > free:
+                raise MigrationError(f"gpu {self.gpu_ids[s]}: {in_u[s]} KV units needed, {free} free")
+        return in_u, out_u
+
+    def _commit(self, in_u, out_u):
+        for s in range(self.world):
+            self.ring_head[s] += int(in_u[s])
+            self.ring_tail[s] += int(out_u[s])
+
+    def admit(self, layouts, seed: int = 1) -> int:
+        """Every rank calls with the same layouts; each allocates + fills its pages."""
+        H = self.kv.total_heads
+        recs = []
+        for lay in layouts:
+            hpr = lay.heads_per_rank
+            for rid, ctx in lay.requests:
+                if rid in self.req_slot:
+                    raise MigrationError(f"request {rid} already resident")
+                rs = self._free_req_slots.pop()
+                self.req_slot[rid] = rs
+                self.slot_ctx[rs] = int(ctx)
+                for r, g in enumerate(lay.group):
+                    s = self.slot_of[g]
+                    self.owner[rs, r * hpr:(r + 1) * hpr] = s
+                    recs.append((-1, s, rs, r * hpr, (r + 1) * hpr, int(ctx)))
+        rec = np.asarray(recs, np.int64).reshape(-1, 6)
+        in_u, out_u = self._advance(rec)
+        mine = rec[rec[:, 1] == self.slot]
+        n = int(units_per_record(mine, self.kv.block_tokens).sum())
+        if n:
+            cl = self._run_k3(mine, -1, n, want_ext=True)
+            with torch.cuda.device(self.device):
+                _native.call("tpr_kv_fill", ctypes.byref(self._geo), ctypes.byref(cl),
+                             self._work.data_ptr(), self._work_ext.data_ptr(), n, seed,
+                             self.stream.cuda_stream)
+        self._commit(in_u, out_u)
+        self.pattern_seed = seed
+        self.stream.synchronize()
+        dist.barrier(group=self.group)
+        return n
+
+    def records(self, plan: MigrationPlan) -> np.ndarray:
+        arr = plan.as_array()
+        if len(arr) == 0:
+            return np.zeros((0, 6), np.int64)
+        src = np.array([self.slot_of[g] for g in arr[:, 0].tolist()], np.int64)
+        dst = np.array([self.slot_of[g] for g in arr[:, 1].tolist()], np.int64)
+        req = np.array([self.req_slot[r] for r in arr[:, 2].tolist()], np.int64)
+        ctx = self.slot_ctx[req].astype(np.int64)
+        if (arr[:, BYTES] != (arr[:, 4] - arr[:, 3]) * ctx * self.kv.kv_bytes_per_token_per_head).any():
+            raise MigrationError("transfer bytes disagree with context length")
+        return np.stack([src, dst, req, arr[:, 3], arr[:, 4], ctx], axis=1)
+
+    def migrate(self, plan: MigrationPlan, k1_events=None) -> MigrationStats:
+        """Collective over the group: every rank passes the same plan."""
+        rec = self.records(plan)
+        in_u, out_u = self._advance(rec)
+        handshake(rec, self.ring_head, self.ring_tail, self.group)  # also the start barrier
+        n = my_units(rec, self.slot, self.kv.block_tokens)
+        if n:
+            cl = self._run_k3(rec, self.slot, n, want_ext=False)
+            if k1_events:
+                k1_events[0].record(self.stream)
+            with torch.cuda.device(self.device):
+                _native.call("tpr_kv_migrate", ctypes.byref(self._geo), ctypes.byref(cl),
+                             self._work.data_ptr(), n, self.stream.cuda_stream)
+            if k1_events:
+                k1_events[1].record(self.stream)
+        self.stream.synchronize()
+        dist.barrier(group=self.group)  # every page has landed everywhere
+        self._commit(in_u, out_u)
+        heads = np.arange(self.kv.total_heads)
+        mask = (heads >= rec[:, 3:4]) & (heads < rec[:, 4:5])
+        rows = np.broadcast_to(rec[:, 2:3], mask.shape)
+        self.owner[rows[mask], np.broadcast_to(heads, mask.shape)[mask]] = \
+            np.broadcast_to(rec[:, 1:2], mask.shape)[mask]
+        return MigrationStats(len(rec), n, int(plan.as_array()[:, BYTES].sum()) if len(rec) else 0,
+                              {self.gpu_ids[s]: int(v) for s, v in enumerate(in_u) if v},
+                              {self.gpu_ids[s]: int(v) for s, v in enumerate(out_u) if v})
+
+    def verify(self) -> dict:
+        ctx = torch.from_numpy(self.slot_ctx).to(self.device)
+        owner = torch.from_numpy(self.owner).to(self.device)
+        counts = torch.zeros(3, dtype=torch.int64, device=self.device)
+        with torch.cuda.device(self.device):
+            _native.call("tpr_kv_verify", ctypes.byref(self._geo), self.pool.ptr, self.bt.ptr,
+                         ctx.data_ptr(), owner.data_ptr(), self.slot, self.pattern_seed,
+                         counts.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        c = counts.cpu().tolist()
+        return {"placement_errors": c[0], "word_mismatches": c[1], "pages_checked": c[2],
+                "status": int(self.status.item())}
+
+    def snapshot(self) -> dict:
+        torch.cuda.synchronize(self.device)
+        return {"pool": self.pool.tensor.cpu().numpy(),
+                "block_table": self.bt.tensor.view(torch.int32).cpu().numpy(),
+                "ring": self.ring.tensor.view(torch.int32).cpu().numpy(),
+                "ring_head": list(self.ring_head), "ring_tail": list(self.ring_tail)}
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        for r, ptrs in enumerate(self.peer_ptrs):
+            if r != self.rank:
+                for p in ptrs:
+                    _native.call("tpr_ipc_close", p)
+        dist.barrier(group=self.group)
+        for b in (self.pool, self.bt, self.ring):
+            b.free()
+
+
+__all__ = ["DistributedKvCluster", "DeviceBuffer", "handshake", "ring_deltas", "my_units",
+           "plan_digest", "units_per_record", "KvLayout"]

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from oracle import check, kvmove
-from paper_2605_05467_b200 import geometry, migration as M, workloads
+from paper_2605_05467_b200 import geometry, migration as M, pattern, workloads
 from paper_2605_05467_b200.kvcache import PagedKvCluster
 
 pytestmark = pytest.mark.gpu
@@ -94,6 +94,27 @@ def test_c_oracle_matches_python_oracle():
     a = check.expected_after(c, before, rec, impl="c")
     b = check.expected_after(c, before, rec, impl="py")
     assert not any(check.compare(a, b).values())
+
+
+def test_device_fill_matches_numpy_pattern():
+    c = make(TINY, (0, 1), units=64, reqs=4, blocks=8)
+    c.admit([M.KvLayout((0, 1), 2, 8, ((0, 37),))], seed=21)
+    snap = c.snapshot()
+    pools = snap["pools"]
+    bts = [b.reshape(4, 8, 8) for b in snap["block_tables"]]
+    rs = c.req_slot[0]
+    for h in range(8):
+        g = 0 if h < 4 else 1
+        for b in range(TINY.blocks(37)):
+            unit = int(bts[g][rs, h, b])
+            ntok = min(16, 37 - 16 * b)
+            page = pools[g][unit * TINY.unit_bytes:(unit + 1) * TINY.unit_bytes]
+            page = page.reshape(2 * TINY.layers, TINY.plane_bytes)[:, : ntok * TINY.tok_bytes]
+            assert np.array_equal(page, pattern.page_bytes(21, rs, h, b, TINY, ntok))
+    # garbage fill of a free unit is keyed by (slot, unit)
+    free_unit = int(snap["rings"][1][snap["ring_head"][1] % c.n_units])
+    got = pools[1][free_unit * TINY.unit_bytes:(free_unit + 1) * TINY.unit_bytes]
+    assert np.array_equal(got, pattern.unit_garbage(100, 1, free_unit, TINY.unit_bytes))
 
 
 def test_wrong_source_rejected_on_host():

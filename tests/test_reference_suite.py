@@ -1,0 +1,51 @@
+"""Run the reference's OWN tests with our module standing in for tpsim.migration.
+
+The reference package (pkg/src/tpsim) is imported read-only from
+/root/reference with ``sys.modules["tpsim.migration"]`` pointing at
+paper_2605_05467_b200.migration, so the simulator engine, CLI and acceptance
+criteria all plan through the native planner. Only runs where the reference
+exists (the build container); the GPU box has no /root/reference.
+"""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+from conftest import ROOT
+
+REF = Path("/root/reference/pkg")
+
+pytestmark = pytest.mark.skipif(not REF.exists(), reason="reference tree not present")
+
+DRIVER = """
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {src!r})
+import paper_2605_05467_b200.migration as ours
+sys.modules["tpsim.migration"] = ours
+import tpsim, tpsim.engine, tpsim.cli
+assert tpsim.engine.head_transfers is ours.head_transfers
+assert tpsim.cli.migration_mod is ours
+import pytest
+sys.exit(pytest.main({args!r}))
+"""
+
+
+def test_reference_suites_pass_against_drop_in(tmp_path):
+    tests = REF / "tests"
+    args = [str(tests / f) for f in ("test_migration.py", "test_engine.py", "test_cli.py",
+                                     "test_acceptance.py")]
+    # AC-7 times the goodput policy planner (policy.py), which is not on this path
+    # and whose wall-clock budget depends on the host
+    args += ["-q", "-p", "no:cacheprovider", "--deselect",
+             str(tests / "test_acceptance.py") + "::test_ac7_planner_and_dispatch_latency"]
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1")
+    code = DRIVER.format(root=str(ROOT), src=str(REF / "src"), args=args)
+    res = subprocess.run([sys.executable, "-c", code], cwd=tmp_path, env=env, capture_output=True,
+                         text=True, timeout=900)
+    tail = res.stdout[-3000:] + res.stderr[-2000:]
+    assert res.returncode == 0, tail
+    assert "passed" in res.stdout and "failed" not in res.stdout, tail
+    assert "AC-1 repartition correctness: PASS" in res.stdout

@@ -101,6 +101,22 @@ def test_sequence_reuses_resident_slices():
     store.finish()
 
 
+def test_device_matrix_fill_matches_numpy_pattern():
+    from paper_2605_05467_b200 import pattern
+    store = ShardedWeightStore(MODEL, (0, 1))
+    store.load([(0, 1)])
+    for name, layer in (("q_proj", 0), ("o_proj", 1), ("lm_head", -1), ("input_layernorm", 0)):
+        m = next(x for x in MODEL.matrices if (x.name, x.layer) == (name, layer))
+        got = store.shard(1, name, layer).cpu().view(torch.int16).numpy().view(np.uint16)
+        if m.split == "col":
+            want = pattern.matrix(m.key, m.rows // 2, m.cols, m.rows // 2, 0, m.cols)
+        elif m.split == "row":
+            want = pattern.matrix(m.key, m.rows, m.cols // 2, 0, m.cols // 2, m.cols)
+        else:
+            want = pattern.matrix(m.key, m.rows, m.cols, 0, 0, m.cols)
+        assert np.array_equal(got, want), name
+
+
 def test_full_copy_mode_moves_nothing():
     gpus = (0, 1, 2, 3)
     store = ShardedWeightStore(MODEL, gpus, mode="full_copy_per_gpu")
