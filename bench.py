@@ -130,17 +130,25 @@ def build_workload(cfg: int, seqs: int | None):
     return workloads.config(cfg, **kw)
 
 
-def capacity_units(w, kv) -> int:
-    """Units per logical GPU: resident KV of the larger layout + incoming."""
+def capacity_units(w, kv) -> dict:
+    """Pool units per GPU at the peak of either switch direction: pages
+    resident before the switch + pages received (sources release only after
+    the copy)."""
     from paper_2605_05467_b200 import migration as M
-    need = {g: 0 for g in w.gpus}
-    for lays in (w.old, w.new):
-        for lay in lays:
-            for rid, ctx in lay.requests:
+    ctx = dict(w.requests)
+    peak = {g: 0 for g in w.gpus}
+    for a, b in ((w.old, w.new), (w.new, w.old)):
+        need = {g: 0 for g in w.gpus}
+        for lay in a:
+            for rid, c in lay.requests:
                 for g in lay.owners():
-                    need[g] += kv.blocks(ctx)
-    peak = max(need.values())
-    return int(peak * 1.05) + 64
+                    need[g] += kv.blocks(c)
+        arr = M.plan_repartition(a, b, kv.kv_bytes_per_token_per_head).as_array()
+        for src, dst, rid, lo, hi, _ in arr.tolist():
+            need[dst] += (hi - lo) * kv.blocks(ctx[rid])
+        for g in w.gpus:
+            peak[g] = max(peak[g], need[g])
+    return {g: n + 64 for g, n in peak.items()}
 
 
 def setup_ours(w, device):
@@ -206,17 +214,17 @@ class CpuReference:
                 for _, c in rr:
                     for gg in grp:
                         need[gg] += per * kv.blocks(c)
-        units = max(need.values()) + 16
+        units = [need[g] + 16 for g in w.gpus]
         self.geo = dict(layers=kv.layers, head_dim=kv.head_dim, dtype_bytes=kv.dtype_bytes,
                         block_tokens=kv.block_tokens, total_heads=H, max_blocks=max_blocks,
-                        n_req_slots=len(reqs), n_units=units)
+                        n_req_slots=len(reqs), n_units=max(units))
         n = len(w.gpus)
-        self.pools = [np.ones(units * kv.unit_bytes, np.uint8) for _ in range(n)]
+        self.pools = [np.ones(u * kv.unit_bytes, np.uint8) for u in units]
         self.tables = [np.full(len(reqs) * H * max_blocks, -1, np.int32) for _ in range(n)]
         rng = np.random.default_rng(0)
-        self.rings = [rng.permutation(units).astype(np.int32) for _ in range(n)]
+        self.rings = [rng.permutation(u).astype(np.int32) for u in units]
         self.head = [0] * n
-        self.tail = [units] * n
+        self.tail = list(units)
         adm = []
         for grp, _, rr in self.old:
             per = H // len(grp)

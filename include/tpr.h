@@ -65,22 +65,25 @@ typedef struct tpr_kv_geometry {
 } tpr_kv_geometry_t;
 
 /* The set of pools a plan touches, indexed by GPU slot (dense 0..n_gpus-1).
- * ring_head / ring_tail are monotonically increasing counters owned by the
- * host: the next allocation takes ring[ring_head % n_units], the next release
- * is stored at ring[ring_tail % n_units]. */
+ * units[g] is slot g's pool capacity (= its free-ring length; 0 means
+ * geometry.n_units). ring_head / ring_tail are monotonically increasing
+ * counters owned by the host: the next allocation takes
+ * ring[ring_head % units], the next release is stored at ring[ring_tail % units]. */
 typedef struct tpr_kv_cluster {
   int32_t n_gpus;
   int32_t _pad;
-  uint64_t pool[TPR_MAX_GPUS];        /* uint8 [n_units][unit_bytes]          */
+  uint64_t pool[TPR_MAX_GPUS];        /* uint8 [units][unit_bytes]            */
   uint64_t block_table[TPR_MAX_GPUS]; /* int32 [n_req_slots][H][max_blocks]   */
-  uint64_t free_ring[TPR_MAX_GPUS];   /* int32 [n_units]                      */
+  uint64_t free_ring[TPR_MAX_GPUS];   /* int32 [units]                        */
   int64_t ring_head[TPR_MAX_GPUS];
   int64_t ring_tail[TPR_MAX_GPUS];
+  int64_t units[TPR_MAX_GPUS];
 } tpr_kv_cluster_t;
 
 /* One transfer record on device, int32 x 6:
  *   {src_slot, dst_slot, req_slot, head_lo, head_hi (excl.), context_len}
- * src_slot == -1 means "allocate only" (admission of a new request).      */
+ * src_slot == -1 means "allocate only" (admission of a new request);
+ * dst_slot == -1 means "release only" (request finished or evicted).       */
 #define TPR_XFER_FIELDS 6
 
 /* Per-transfer scan output of K3 (int64 x 4): {mine_off, alloc_off, rel_off, units} */

@@ -38,9 +38,9 @@ typedef struct {
 /* Returns number of page moves, or -1 on allocation failure. status |= 1 for
  * a head not on src, |= 2 for an occupied destination entry. */
 int64_t oracle_kv_migrate(const oracle_geo* g, uint8_t** pools, int32_t** tables, int32_t** rings,
-                          int64_t* ring_head, int64_t* ring_tail, const int64_t* xf, int64_t n,
-                          int32_t n_threads, int32_t* status) {
-  const int64_t H = g->total_heads, MB = g->max_blocks, B = g->block_tokens, cap = g->n_units;
+                          const int64_t* ring_len, int64_t* ring_head, int64_t* ring_tail,
+                          const int64_t* xf, int64_t n, int32_t n_threads, int32_t* status) {
+  const int64_t H = g->total_heads, MB = g->max_blocks, B = g->block_tokens;
   const int64_t tok = (int64_t)g->head_dim * g->dtype_bytes;
   const int64_t plane = B * tok, unit = plane * 2 * g->layers;
   int64_t total = 0;
@@ -64,11 +64,14 @@ int64_t oracle_kv_migrate(const oracle_geo* g, uint8_t** pools, int32_t** tables
           su = tables[src][idx];
           if (su < 0) *status |= 1;
           tables[src][idx] = -1;
-          rings[src][ring_tail[src]++ % cap] = su;
+          rings[src][ring_tail[src]++ % ring_len[src]] = su;
         }
-        const int32_t du = rings[dst][ring_head[dst]++ % cap];
-        if (tables[dst][idx] >= 0) *status |= 2;
-        tables[dst][idx] = du;
+        int32_t du = -1;
+        if (dst >= 0) { /* dst < 0: release only */
+          du = rings[dst][ring_head[dst]++ % ring_len[dst]];
+          if (tables[dst][idx] >= 0) *status |= 2;
+          tables[dst][idx] = du;
+        }
         mv[k].su = su;
         mv[k].du = du;
         mv[k].src = src;
@@ -84,7 +87,7 @@ int64_t oracle_kv_migrate(const oracle_geo* g, uint8_t** pools, int32_t** tables
 #endif
   for (int64_t i = 0; i < total; ++i) {
     const page_move m = mv[i];
-    if (m.su < 0) continue;
+    if (m.su < 0 || m.du < 0) continue;
     const uint8_t* s = pools[m.src] + (int64_t)m.su * unit;
     uint8_t* d = pools[m.dst] + (int64_t)m.du * unit;
     const int64_t nb = m.ntok * tok;

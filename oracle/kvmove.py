@@ -47,8 +47,8 @@ def lib():
         _lib.oracle_kv_migrate.restype = ctypes.c_int64
         _lib.oracle_kv_migrate.argtypes = [
             ctypes.POINTER(OracleGeo), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
-            ctypes.POINTER(ctypes.c_int32)]
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+            ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
         _lib.oracle_copy_blocks.restype = None
         _lib.oracle_copy_blocks.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 6 + [ctypes.c_int32]
         _lib.oracle_max_threads.restype = ctypes.c_int32
@@ -74,9 +74,10 @@ def kv_migrate(geo: dict, pools, tables, rings, ring_head, ring_tail, records: n
     tails = np.asarray(ring_tail, dtype=np.int64).copy()
     rec = np.ascontiguousarray(records, dtype=np.int64)
     status = ctypes.c_int32(0)
+    lens = np.array([len(r) for r in rings], dtype=np.int64)  # a ring's length is its modulus
     n = lib().oracle_kv_migrate(ctypes.byref(g), _ptrs(pools), _ptrs(tables), _ptrs(rings),
-                                heads.ctypes.data, tails.ctypes.data, rec.ctypes.data, len(rec),
-                                n_threads, ctypes.byref(status))
+                                lens.ctypes.data, heads.ctypes.data, tails.ctypes.data,
+                                rec.ctypes.data, len(rec), n_threads, ctypes.byref(status))
     if n < 0:
         raise MemoryError("oracle allocation failed")
     return int(n), status.value, heads.tolist(), tails.tolist()
@@ -98,7 +99,7 @@ def copy_blocks(blocks, n_threads: int = 0) -> None:
 
 def kv_migrate_py(geo: dict, pools, tables, rings, ring_head, ring_tail, records):
     """Pure-Python page-by-page restatement (small cases only)."""
-    H, MB, B, cap = geo["total_heads"], geo["max_blocks"], geo["block_tokens"], geo["n_units"]
+    H, MB, B = geo["total_heads"], geo["max_blocks"], geo["block_tokens"]
     tok = geo["head_dim"] * geo["dtype_bytes"]
     plane = B * tok
     unit = plane * 2 * geo["layers"]
@@ -109,23 +110,24 @@ def kv_migrate_py(geo: dict, pools, tables, rings, ring_head, ring_tail, records
         pages = -(-ctx // B)
         for h in range(lo, hi):
             for b in range(pages):
-                tb_s = tables[src].reshape(-1, H, MB) if src >= 0 else None
-                tb_d = tables[dst].reshape(-1, H, MB)
-                su = -1
+                su = du = -1
                 if src >= 0:
+                    tb_s = tables[src].reshape(-1, H, MB)
                     su = int(tb_s[req, h, b])
                     status |= 1 if su < 0 else 0
                     tb_s[req, h, b] = -1
-                    rings[src][tails[src] % cap] = su
+                    rings[src][tails[src] % len(rings[src])] = su
                     tails[src] += 1
-                du = int(rings[dst][heads[dst] % cap])
-                heads[dst] += 1
-                status |= 2 if tb_d[req, h, b] >= 0 else 0
-                tb_d[req, h, b] = du
+                if dst >= 0:
+                    tb_d = tables[dst].reshape(-1, H, MB)
+                    du = int(rings[dst][heads[dst] % len(rings[dst])])
+                    heads[dst] += 1
+                    status |= 2 if tb_d[req, h, b] >= 0 else 0
+                    tb_d[req, h, b] = du
                 ntok = ctx - b * B if b == pages - 1 else B
                 moves.append((su, du, src, dst, ntok))
     for su, du, src, dst, ntok in moves:
-        if su < 0:
+        if su < 0 or du < 0:
             continue
         for p in range(2 * geo["layers"]):
             s0 = su * unit + p * plane

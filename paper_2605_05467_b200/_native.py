@@ -55,6 +55,7 @@ class KvClusterC(Structure):
         ("free_ring", c_uint64 * TPR_MAX_GPUS),
         ("ring_head", c_int64 * TPR_MAX_GPUS),
         ("ring_tail", c_int64 * TPR_MAX_GPUS),
+        ("units", c_int64 * TPR_MAX_GPUS),
     ]
 
 

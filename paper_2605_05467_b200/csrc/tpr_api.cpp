@@ -55,7 +55,8 @@ tpr::KvCopyParams copy_params(const tpr_kv_geometry_t* g) {
   return p;
 }
 
-int cluster_params(const tpr_kv_cluster_t* cl, tpr::KvClusterParams* out) {
+int cluster_params(const tpr_kv_cluster_t* cl, const tpr_kv_geometry_t* geo,
+                   tpr::KvClusterParams* out) {
   if (!cl) return fail(TPR_EINVAL, "null cluster");
   if (cl->n_gpus <= 0 || cl->n_gpus > TPR_MAX_GPUS)
     return fail(TPR_EINVAL, "n_gpus=%d outside [1, %d]", cl->n_gpus, TPR_MAX_GPUS);
@@ -66,6 +67,10 @@ int cluster_params(const tpr_kv_cluster_t* cl, tpr::KvClusterParams* out) {
     out->free_ring[g] = cl->free_ring[g];
     out->ring_head[g] = cl->ring_head[g];
     out->ring_tail[g] = cl->ring_tail[g];
+    out->units[g] = cl->units[g] > 0 ? cl->units[g] : geo->n_units;
+    if (out->units[g] > geo->n_units)
+      return fail(TPR_EINVAL, "slot %d: units %lld exceed geometry n_units %d", g,
+                  (long long)out->units[g], geo->n_units);
   }
   return TPR_OK;
 }
@@ -183,7 +188,7 @@ int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const
   int rc = check_geometry(geo);
   if (rc) return rc;
   tpr::KvClusterParams cp;
-  if ((rc = cluster_params(cl, &cp))) return rc;
+  if ((rc = cluster_params(cl, geo, &cp))) return rc;
   if (n_xfers < 0) return fail(TPR_EINVAL, "n_xfers < 0");
   if (n_xfers == 0) return TPR_OK;
   if (!d_xfers || !d_meta || !d_totals || !d_work || !d_status)
@@ -200,7 +205,7 @@ int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, con
   int rc = check_geometry(geo);
   if (rc) return rc;
   tpr::KvClusterParams cp;
-  if ((rc = cluster_params(cl, &cp))) return rc;
+  if ((rc = cluster_params(cl, geo, &cp))) return rc;
   if (n_units < 0) return fail(TPR_EINVAL, "n_units < 0");
   if (n_units > 0 && !d_work) return fail(TPR_EINVAL, "null work list");
   cudaError_t e = tpr::launch_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
@@ -261,7 +266,7 @@ int tpr_kv_fill(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const 
   int rc = check_geometry(geo);
   if (rc) return rc;
   tpr::KvClusterParams cp;
-  if ((rc = cluster_params(cl, &cp))) return rc;
+  if ((rc = cluster_params(cl, geo, &cp))) return rc;
   if (n_units > 0 && (!d_work || !d_work_ext)) return fail(TPR_EINVAL, "null buffer");
   cudaError_t e = tpr::launch_kv_fill(copy_params(geo), cp,
                                       reinterpret_cast<const int4*>(d_work),

@@ -19,6 +19,7 @@ struct KvClusterParams {
   uint64_t free_ring[TPR_MAX_GPUS];
   int64_t ring_head[TPR_MAX_GPUS];
   int64_t ring_tail[TPR_MAX_GPUS];
+  int64_t units[TPR_MAX_GPUS];  // ring capacity per slot (resolved, > 0)
 };
 
 // Derived page geometry for the copy/fill kernels.

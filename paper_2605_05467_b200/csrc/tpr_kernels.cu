@@ -164,11 +164,12 @@ __global__ void __launch_bounds__(kScanThreads)
       const int64_t nblk = ctx > 0 ? (ctx + block_tokens - 1) / block_tokens : 0;
       units = (int64_t)(r[4] - r[3]) * nblk;
       src = r[0] >= 0 ? r[0] : TPR_MAX_GPUS;
-      dst = r[1];
+      dst = r[1] >= 0 ? r[1] : TPR_MAX_GPUS;
       mine = (filter < 0 || r[0] == filter) ? units : 0;
     }
     const int64_t mine_off = block_keyed_exclusive(0, mine, s_tab, s_run[0]);
-    const int64_t alloc_off = block_keyed_exclusive(dst, units, s_tab, s_run[1]);
+    const int64_t alloc_off =
+        block_keyed_exclusive(dst, dst < TPR_MAX_GPUS ? units : 0, s_tab, s_run[1]);
     const int64_t rel_off =
         block_keyed_exclusive(src, src < TPR_MAX_GPUS ? units : 0, s_tab, s_run[2]);
     if (t < n) {
@@ -199,7 +200,6 @@ __global__ void __launch_bounds__(256)
                  int32_t* __restrict__ status) {
   const int64_t n_mine = totals[0];
   const int H = geo.total_heads, B = geo.block_tokens, MB = geo.max_blocks;
-  const int64_t cap = geo.n_units;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_mine;
        i += (int64_t)gridDim.x * blockDim.x) {
     // upper_bound(mine_off, i) - 1
@@ -226,15 +226,18 @@ __global__ void __launch_bounds__(256)
       if (src_unit < 0) atomicOr(status, TPR_STATUS_WRONG_SOURCE);
       bts[bt_idx] = -1;
       int32_t* ring_s = reinterpret_cast<int32_t*>(cl.free_ring[src]);
-      ring_s[(cl.ring_tail[src] + m[2] + local) % cap] = src_unit;
+      ring_s[(cl.ring_tail[src] + m[2] + local) % cl.units[src]] = src_unit;
     }
-    const int32_t* ring_d = reinterpret_cast<const int32_t*>(cl.free_ring[dst]);
-    const int32_t dst_unit = ring_d[(cl.ring_head[dst] + m[1] + local) % cap];
-    int32_t* btd = reinterpret_cast<int32_t*>(cl.block_table[dst]);
-    if (btd[bt_idx] >= 0) atomicOr(status, TPR_STATUS_DST_OCCUPIED);
-    btd[bt_idx] = dst_unit;
+    int32_t dst_unit = -1;
+    if (dst >= 0) {  // dst == -1: release only (request finished or evicted)
+      const int32_t* ring_d = reinterpret_cast<const int32_t*>(cl.free_ring[dst]);
+      dst_unit = ring_d[(cl.ring_head[dst] + m[1] + local) % cl.units[dst]];
+      int32_t* btd = reinterpret_cast<int32_t*>(cl.block_table[dst]);
+      if (btd[bt_idx] >= 0) atomicOr(status, TPR_STATUS_DST_OCCUPIED);
+      btd[bt_idx] = dst_unit;
+    }
 
-    work[i] = make_int4(src_unit, dst_unit, (src & 0xffff) | (dst << 16), ntok);
+    work[i] = make_int4(src_unit, dst_unit, (src & 0xffff) | ((dst & 0xffff) << 16), ntok);
     if (work_ext != nullptr) work_ext[i] = make_int4(req, h, b, t);
   }
 }

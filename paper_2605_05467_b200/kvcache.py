@@ -89,7 +89,12 @@ class PagedKvCluster:
         self.kv = kv
         self.gpu_ids = tuple(gpu_ids)
         self.slot_of = {g: i for i, g in enumerate(self.gpu_ids)}
-        self.n_units = int(units_per_gpu)
+        # pool capacity per GPU: one int for all, or {gpu id: units}
+        if isinstance(units_per_gpu, dict):
+            self.units = [int(units_per_gpu[g]) for g in self.gpu_ids]
+        else:
+            self.units = [int(units_per_gpu)] * len(self.gpu_ids)
+        self.n_units = max(self.units)
         self.max_requests = int(max_requests)
         self.max_blocks = int(max_blocks)
         default = torch.device(device)
@@ -99,14 +104,14 @@ class PagedKvCluster:
         H = kv.total_heads
         self.pools, self.block_tables, self.rings = [], [], []
         gen = np.random.default_rng(seed)
-        for dev in self.devices:
-            self.pools.append(torch.empty(self.n_units * kv.unit_bytes, dtype=torch.uint8, device=dev))
+        for dev, units in zip(self.devices, self.units):
+            self.pools.append(torch.empty(units * kv.unit_bytes, dtype=torch.uint8, device=dev))
             self.block_tables.append(torch.full((self.max_requests, H, self.max_blocks), -1,
                                                 dtype=torch.int32, device=dev))
-            order = gen.permutation(self.n_units) if fragmented else np.arange(self.n_units)
+            order = gen.permutation(units) if fragmented else np.arange(units)
             self.rings.append(torch.from_numpy(order.astype(np.int32)).to(dev))
         self.ring_head = [0] * len(self.gpu_ids)
-        self.ring_tail = [self.n_units] * len(self.gpu_ids)
+        self.ring_tail = list(self.units)
         # request bookkeeping (host is authoritative; device copies for checks)
         self.req_slot: dict[int, int] = {}
         self.ctx_of: dict[int, int] = {}
@@ -142,6 +147,7 @@ class PagedKvCluster:
             c.free_ring[s] = self.rings[s].data_ptr()
             c.ring_head[s] = self.ring_head[s]
             c.ring_tail[s] = self.ring_tail[s]
+            c.units[s] = self.units[s]
         return c
 
     @staticmethod
@@ -161,7 +167,9 @@ class PagedKvCluster:
         n = len(xf)
         units = self._units_per_record(xf)
         total = int(units.sum())
-        in_u = np.bincount(xf[:, 1], weights=units, minlength=self.n_gpus).astype(np.int64)
+        has_dst = xf[:, 1] >= 0
+        in_u = np.bincount(xf[has_dst, 1], weights=units[has_dst],
+                           minlength=self.n_gpus).astype(np.int64)
         has_src = xf[:, 0] >= 0
         out_u = np.bincount(xf[has_src, 0], weights=units[has_src],
                             minlength=self.n_gpus).astype(np.int64)
@@ -229,6 +237,35 @@ class PagedKvCluster:
                          self._work.data_ptr(), self._work_ext.data_ptr(), total, seed,
                          stream.cuda_stream)
         self.pattern_seed = seed
+        return total
+
+    def release(self, request_ids: Iterable[int], stream: torch.cuda.Stream | None = None) -> int:
+        """Free every page of finished / evicted requests (K3 with dst = -1:
+        block-table entries cleared, units pushed back on their owners' free
+        rings in (request, head, page) order). Returns #units released."""
+        stream = stream or torch.cuda.current_stream(self.home)
+        recs = []
+        for rid in request_ids:
+            rs = self.req_slot.get(rid)
+            if rs is None:
+                raise MigrationError(f"request {rid} is not resident")
+            own = self.owner[rs]
+            h = 0
+            while h < len(own):  # one record per run of heads on the same GPU
+                e = h
+                while e < len(own) and own[e] == own[h]:
+                    e += 1
+                recs.append((int(own[h]), -1, rs, h, e, int(self.slot_ctx[rs])))
+                h = e
+        if not recs:
+            return 0
+        total = self._remap(np.asarray(recs, np.int64), stream, want_ext=False)
+        for rid in request_ids:
+            rs = self.req_slot.pop(rid)
+            self.ctx_of.pop(rid, None)
+            self.owner[rs] = -1
+            self.slot_ctx[rs] = -1
+            self._free_req_slots.append(rs)
         return total
 
     def fill_garbage(self, seed: int = 99, stream: torch.cuda.Stream | None = None) -> None:

@@ -192,6 +192,13 @@ def main():
                       "per_tp_copies": M.weight_memory("per_tp_copies", P),
                       **{f"sharded_{t}": M.weight_memory("sharded", P, tp=t) for t in (1, 2, 4, 8)}}
 
+    # -- trace for the switch sweep (BASELINE config 5): the reference's bursty
+    # workload (scenarios.py:58-85, seed 11) -> (prompt_len, output_len) pairs ----
+    from tpsim.scenarios import bursty_spec
+    from tpsim.trace import generate_trace
+    trace = generate_trace(bursty_spec())
+    doc["bursty_trace"] = [[r.prompt_len, r.output_len] for r in trace[:1024]]
+
     # -- CLI migrate-plan ----------------------------------------------------------
     import tempfile
     with tempfile.TemporaryDirectory() as d:

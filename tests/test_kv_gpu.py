@@ -83,6 +83,31 @@ def test_engine_path_disjoint_groups():
     assert c.placement() == M.layout_placement(new)
 
 
+def test_release_then_readmit_bit_exact():
+    gpus = (0, 1, 2, 3)
+    reqs = [(i, 3 + 41 * i) for i in range(8)]
+    c = make(TINY, gpus, units=256, reqs=8, blocks=32)
+    tp2 = workloads.round_robin(workloads.tp_groups(gpus, 2), reqs, 8)
+    c.admit(tp2, seed=4)
+    free0 = [c.free_units(g) for g in gpus]
+    before = c.snapshot()
+    gone = [1, 4, 6]
+    rec = np.array([(int(c.owner[c.req_slot[r], h0]), -1, c.req_slot[r], h0, h0 + 4,
+                     c.ctx_of[r]) for r in gone for h0 in (0, 4)], np.int64)
+    n = c.release(gone)
+    want = check.expected_after(c, before, rec)
+    diff = check.compare(c.snapshot(), want)
+    assert not any(diff.values()), diff
+    assert n == sum(8 * TINY.blocks(ctx) for r, ctx in reqs if r in gone)
+    assert sum(c.free_units(g) for g in gpus) == sum(free0) + n
+    v = c.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+    # the freed pages are reused by a new request
+    c.admit([M.KvLayout((0, 1, 2, 3), 4, 8, ((100, 300),))], seed=4)
+    v = c.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
 def test_c_oracle_matches_python_oracle():
     gpus = (0, 1)
     c = make(TINY, gpus, units=128, reqs=4, blocks=8)

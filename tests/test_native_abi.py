@@ -31,7 +31,7 @@ def test_abi_version():
 
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_native.KvGeometryC) == 8 * 4
-    assert ctypes.sizeof(_native.KvClusterC) == 8 + 5 * 8 * _native.TPR_MAX_GPUS
+    assert ctypes.sizeof(_native.KvClusterC) == 8 + 6 * 8 * _native.TPR_MAX_GPUS
     assert ctypes.sizeof(_native.CopySegC) == 64
 
 

@@ -1,0 +1,147 @@
+"""BASELINE config 5: trace-driven switch sweep.
+
+All 12 ordered TP transitions among {1,2,4,8} on 8 GPU slots, 1..128 sequences,
+with contexts fixed at 4096 tokens or taken from the reference's bursty trace
+(scenarios.py:58-85, seed 11; committed as tests/golden: context = prompt +
+output/2, i.e. mid-decode). Llama-3.1-8B KV geometry.
+
+On one B200 the 8 slots are logical (all pools in one HBM). So each switch is
+bounded by HBM: t_roof = 2 * bytes / measured copy peak. Every point reports:
+
+* the measured switch latency (device events and host wall, synchronous);
+* GB/s and the fraction of that roofline;
+* the reference cost model's prediction for the same plan (default
+  CostModelParams, migration.py:77-98);
+* the CPU restatement's time for the small points.
+
+    python tools/sweep.py --out profiles/r01_sweep.jsonl
+"""
+
+from __future__ import annotations
+
+import argparse
+import gzip
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+
+    from paper_2605_05467_b200 import migration as M, workloads
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
+    from paper_2605_05467_b200.kvcache import PagedKvCluster
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "sweep.jsonl"))
+    ap.add_argument("--max-seqs", type=int, default=128)
+    ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--cpu-max-seqs", type=int, default=8)
+    args = ap.parse_args()
+
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    kv = LLAMA_3_1_8B.kv
+    gpus = tuple(range(8))
+    trace = json.load(gzip.open(ROOT / "tests" / "golden" / "reference_golden.json.gz", "rt"))["bursty_trace"]
+    trace_ctx = [p + o // 2 for p, o in trace]
+    seq_counts = [s for s in (1, 2, 4, 8, 16, 32, 64, 128) if s <= args.max_seqs]
+    max_ctx = max(4096, max(trace_ctx))
+    units = 2 * args.max_seqs * kv.blocks(4096) + 256
+    cluster = PagedKvCluster(kv, gpus, units_per_gpu=units, max_requests=args.max_seqs,
+                             max_blocks=kv.blocks(max_ctx), fragmented=True, seed=0)
+    params = M.CostModelParams()
+    out = open(args.out, "w")
+    stream = torch.cuda.current_stream()
+    for mode in ("fixed4096", "trace"):
+        for a in (1, 2, 4, 8):
+            for b in (1, 2, 4, 8):
+                if a == b:
+                    continue
+                for n in seq_counts:
+                    ctxs = [4096] * n if mode == "fixed4096" else trace_ctx[:n]
+                    reqs = [(i, c) for i, c in enumerate(ctxs)]
+                    la = workloads.round_robin(workloads.tp_groups(gpus, a), reqs, 8)
+                    lb = workloads.round_robin(workloads.tp_groups(gpus, b), reqs, 8)
+                    cluster.admit(la, seed=n)
+                    fwd = M.plan_repartition(la, lb, kv.kv_bytes_per_token_per_head)
+                    back = M.plan_repartition(lb, la, kv.kv_bytes_per_token_per_head)
+                    for p in (fwd, back):  # warm-up, leaves the cluster in layout A
+                        cluster.migrate(p, validate=False)
+                    torch.cuda.synchronize()
+                    dev_ms, host_ms = [], []
+                    for r in range(args.reps):
+                        p = fwd if r % 2 == 0 else back
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        t0 = time.perf_counter()
+                        e0.record(stream)
+                        plan = M.plan_repartition(*((la, lb) if r % 2 == 0 else (lb, la)),
+                                                  kv.kv_bytes_per_token_per_head)
+                        cluster.migrate(plan, validate=False)
+                        e1.record(stream)
+                        e1.synchronize()
+                        host_ms.append((time.perf_counter() - t0) * 1e3)
+                        dev_ms.append(e0.elapsed_time(e1))
+                    if args.reps % 2:
+                        cluster.migrate(back, validate=False)
+                    v = cluster.verify(seed=n)
+                    ok = v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
+                    cluster.release([r for r, _ in reqs])
+                    nbytes = fwd.total_bytes
+                    d = float(np.median(dev_ms))
+                    cpu_ms = cpu_point(la, lb, reqs, gpus, kv) if n <= args.cpu_max_seqs else None
+                    row = {
+                        "mode": mode, "tp_old": a, "tp_new": b, "seqs": n,
+                        "ctx_total": int(sum(ctxs)), "transfers": len(fwd), "bytes": nbytes,
+                        "device_ms": d, "host_ms": float(np.median(host_ms)),
+                        "gbs": nbytes / (d * 1e-3) / 1e9 if d > 0 else None,
+                        "hbm_frac": (2 * nbytes / (peak * 1e9)) / (d * 1e-3) if d > 0 else None,
+                        "predicted_ms_ref_model": M.switch_cost(M.WARM, fwd, params),
+                        "cpu_restatement_ms": cpu_ms, "bit_exact_property": ok,
+                    }
+                    out.write(json.dumps(row) + "\n")
+                    out.flush()
+                    print(json.dumps(row))
+    out.close()
+
+
+def cpu_point(la, lb, reqs, gpus, kv):
+    """Time the CPU restatement (planner + threaded page copies) on host pools."""
+    import os
+    from oracle import kvmove, plan_oracle as PO
+    H = kv.total_heads
+    old = [(l.group, H, list(l.requests)) for l in la]
+    new = [(l.group, H, list(l.requests)) for l in lb]
+    rslot = {r: i for i, (r, _) in enumerate(reqs)}
+    ctx = dict(reqs)
+    mb = max(kv.blocks(c) for _, c in reqs)
+    units = 2 * sum(kv.blocks(c) for _, c in reqs) + 16
+    geo = dict(layers=kv.layers, head_dim=kv.head_dim, dtype_bytes=kv.dtype_bytes,
+               block_tokens=kv.block_tokens, total_heads=H, max_blocks=mb, n_req_slots=len(reqs),
+               n_units=units)
+    pools = [np.ones(units * kv.unit_bytes, np.uint8) for _ in gpus]
+    tables = [np.full(len(reqs) * H * mb, -1, np.int32) for _ in gpus]
+    rings = [np.arange(units, dtype=np.int32) for _ in gpus]
+    heads, tails = [0] * len(gpus), [units] * len(gpus)
+    adm = [(-1, g, rslot[r], i * (H // len(grp)), (i + 1) * (H // len(grp)), c)
+           for grp, _, rr in old for r, c in rr for i, g in enumerate(grp)]
+    _, _, heads, tails = kvmove.kv_migrate(geo, pools, tables, rings, heads, tails,
+                                           np.array(adm, np.int64))
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    moves = PO.plan(old, new, kv.kv_bytes_per_token_per_head)
+    rec = np.array([(s, d, rslot[r], lo, hi, ctx[r]) for s, d, r, lo, hi, _ in moves],
+                   np.int64).reshape(-1, 6)
+    kvmove.kv_migrate(geo, pools, tables, rings, heads, tails, rec, threads)
+    return (time.perf_counter() - t0) * 1e3
+
+
+if __name__ == "__main__":
+    main()
