@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import torch
 
 from .kvcache import MigrationStats, PagedKvCluster
-from .migration import KvLayout, MigrationPlan, plan_repartition
+from .migration import KvLayout, MigrationPlan, head_transfers_array, plan_repartition
 from .weights import ReshardStats, ShardedWeightStore
 
 
@@ -85,6 +85,32 @@ class ReconfigurationExecutor:
         res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev)
         if sync:
             # the step's result: K3's status word, read back D2H
+            self._status_host.copy_(self.kv.status, non_blocking=True)
+            ev["end"].synchronize()
+            res.status = int(self._status_host.item())
+            res.host_ms = (time.perf_counter() - t0) * 1e3
+            res.device_ms = ev["start"].elapsed_time(ev["end"])
+        return res
+
+
+    def handoff(self, prefill: KvLayout, decode: KvLayout, sync: bool = True) -> SwitchResult:
+        """Prefill->decode KV handoff between disjoint groups.
+
+        The reference prices it as ``_pipelined_source_ms(_kv_bytes)`` when a
+        prefill completes (engine.py:340-354). The engine path plans with
+        ``head_transfers`` on arbitrary groups (engine.py:571-589); that is
+        exactly what runs here, through K3 + K1."""
+        t0 = time.perf_counter()
+        main = torch.cuda.current_stream(self.device)
+        ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
+        ev["start"].record(main)
+        plan = head_transfers_array(prefill, decode, self.kv.kv.kv_bytes_per_token_per_head)
+        self.kv_stream.wait_event(ev["start"])
+        stats = self.kv.migrate(plan, stream=self.kv_stream)
+        main.wait_stream(self.kv_stream)
+        ev["end"].record(main)
+        res = SwitchResult(plan=plan, kv=stats, weights=None, events=ev)
+        if sync:
             self._status_host.copy_(self.kv.status, non_blocking=True)
             ev["end"].synchronize()
             res.status = int(self._status_host.item())

@@ -1,0 +1,96 @@
+"""The execution hook end to end on B200: switch (KV + weights on two
+streams), prefill->decode handoff over disjoint groups, capacity admission
+with eviction through release."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import check
+from paper_2605_05467_b200 import geometry, migration as M, workloads
+from paper_2605_05467_b200.controller import ReconfigurationExecutor, measured_switch_cost
+from paper_2605_05467_b200.kvcache import PagedKvCluster
+from paper_2605_05467_b200.placement import BEST_EFFORT, FEASIBLE, Arrival, enforce_kv_capacity
+from paper_2605_05467_b200.weights import ShardedWeightStore
+
+pytestmark = pytest.mark.gpu
+
+MODEL = geometry.tiny_geometry()
+KV = MODEL.kv
+
+
+def test_switch_sequence_kv_and_weights():
+    gpus = tuple(range(8))
+    reqs = [(i, 7 + 13 * i) for i in range(16)]
+    lays = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2, 4, 8)}
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=1024, max_requests=16, max_blocks=16, fragmented=True)
+    kv.admit(lays[8], seed=3)
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load(workloads.tp_groups(gpus, 8))
+    ex = ReconfigurationExecutor(kv, store, time_kernels=True)
+    seq = [8, 4, 2, 1, 2, 8, 1, 4]
+    for a, b in zip(seq, seq[1:]):
+        before = kv.snapshot()
+        plan = M.plan_repartition(lays[a], lays[b], KV.kv_bytes_per_token_per_head)
+        rec = kv.records(plan, validate=False)
+        res = ex.switch(lays[a], lays[b], new_weight_groups=workloads.tp_groups(gpus, b))
+        assert res.status == 0 and res.device_ms > 0 and res.host_ms > 0
+        assert res.kv.bytes == plan.total_bytes
+        diff = check.compare(kv.snapshot(), check.expected_after(kv, before, rec))
+        assert not any(diff.values()), (a, b, diff)
+        assert store.verify() == 0
+    assert kv.placement() == M.layout_placement(lays[4])
+
+
+def test_prefill_decode_handoff():
+    gpus = (0, 1, 2, 3, 4, 5)
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=256, max_requests=8, max_blocks=16)
+    ex = ReconfigurationExecutor(kv)
+    prefill = M.KvLayout((0, 1), 2, 8, ((1, 100), (2, 33)))
+    kv.admit([prefill], seed=8)
+    decode = M.KvLayout((2, 3, 4, 5), 4, 8, ((1, 100), (2, 33)))
+    res = ex.handoff(prefill, decode)
+    assert res.status == 0
+    assert res.kv.bytes == 8 * (100 + 33) * KV.kv_bytes_per_token_per_head  # every head moves
+    assert kv.placement() == M.layout_placement(decode)
+    v = kv.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
+def test_capacity_admission_evicts_best_effort():
+    gpus = (0, 1, 2, 3)
+    kv = PagedKvCluster(KV, gpus, units_per_gpu={0: 128, 1: 128, 2: 64, 3: 64}, max_requests=8,
+                        max_blocks=8)
+    src = M.KvLayout((0, 1), 2, 8, ((1, 128), (2, 128), (3, 64)))
+    kv.admit([src], seed=2)  # 4 heads x (8 + 8 + 4) pages = 80 per GPU of (0, 1)
+    dst = M.KvLayout((2, 3), 2, 8, ())
+    arrivals = [Arrival(1, 128, BEST_EFFORT, 1.0), Arrival(2, 128, FEASIBLE, 2.0),
+                Arrival(3, 64, BEST_EFFORT, 0.5)]
+    kept, evicted = enforce_kv_capacity(kv, dst, arrivals)
+    # each GPU of (2,3) has 64 free pages; request 2 (feasible) takes 32, then 3 (oldest
+    # best-effort) takes 16, request 1 (32 more) no longer fits
+    assert [a.request_id for a in kept] == [2, 3]
+    assert [a.request_id for a in evicted] == [1]
+    kv.release([a.request_id for a in evicted])
+    ids = tuple((a.request_id, a.context_len) for a in kept)
+    old = M.KvLayout((0, 1), 2, 8, ids)
+    new = M.KvLayout((2, 3), 2, 8, ids)
+    plan = M.head_transfers_array(old, new, KV.kv_bytes_per_token_per_head)
+    kv.migrate(plan)
+    v = kv.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+    assert kv.free_units(0) == kv.free_units(1) == 128
+    assert kv.free_units(2) == kv.free_units(3) == 64 - 48
+
+
+def test_measured_switch_cost_adapter():
+    gpus = (0, 1)
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=128, max_requests=4, max_blocks=8)
+    ex = ReconfigurationExecutor(kv)
+    old = [M.KvLayout((0,), 1, 8, ((0, 50),)), M.KvLayout((1,), 1, 8, ((1, 50),))]
+    new = M.KvLayout((0, 1), 2, 8, ((0, 50), (1, 50)))
+    kv.admit(old, seed=1)
+    cost = measured_switch_cost(ex)
+    ms = cost(M.WARM, M.plan_repartition(old, new, KV.kv_bytes_per_token_per_head), M.CostModelParams())
+    assert ms > 0
+    assert kv.placement() == M.layout_placement(new)
