@@ -132,6 +132,19 @@ int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
 int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* d_work, int64_t n_units, void* stream);
 
+/* ---- K3 + K1 in one call ----------------------------------------------- */
+/* The switch fast path: async H2D copy of the records from pinned host memory
+ * (h_xfers, may be NULL when d_xfers is already filled), K3 (remap) and K1
+ * (page copy), all on `stream`. Same arguments as tpr_kv_remap; n_units must
+ * be the exact number of units this caller processes. */
+int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                  const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
+                  int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
+                  int32_t* d_status, void* stream);
+
+/* Stream-ordered host->device copy (pinned source for true asynchrony). */
+int tpr_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, void* stream);
+
 /* ---- K2: weight reshard = batched 2-D strided copy (device) ------------ */
 typedef struct tpr_copy_seg {
   uint64_t src;       /* device VA (local or peer)        */

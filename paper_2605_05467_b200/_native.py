@@ -24,7 +24,8 @@ TPR_STATUS_DST_OCCUPIED = 2
 # Every exported symbol of include/tpr.h; tests check the library exports all.
 EXPORTS = (
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads",
-    "tpr_kv_remap", "tpr_kv_migrate", "tpr_copy_prepare", "tpr_weight_reshard",
+    "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_switch", "tpr_memcpy_h2d",
+    "tpr_copy_prepare", "tpr_weight_reshard",
     "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
     "tpr_matrix_verify", "tpr_device_alloc", "tpr_device_free", "tpr_enable_peer",
     "tpr_ipc_get_handle", "tpr_ipc_open", "tpr_ipc_close",
@@ -80,6 +81,10 @@ _SIGNATURES = {
                                c_void_p, c_void_p]),
     "tpr_kv_migrate": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int64,
                                  c_void_p]),
+    "tpr_kv_switch": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
+                                c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                c_void_p]),
+    "tpr_memcpy_h2d": (c_int32, [c_uint64, c_void_p, c_uint64, c_void_p]),
     "tpr_copy_prepare": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, _P64]),
     "tpr_weight_reshard": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p]),
     "tpr_kv_fill": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,

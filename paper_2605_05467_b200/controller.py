@@ -53,35 +53,40 @@ class ReconfigurationExecutor:
         self.w_stream = torch.cuda.Stream(device=dev)
         self.time_kernels = time_kernels
         self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self.main_stream = torch.cuda.current_stream(dev)
 
     def switch(self, old_layouts: list[KvLayout], new_layouts: list[KvLayout],
                new_weight_groups=None, parked=(), sync: bool = True,
-               validate: bool = True) -> SwitchResult:
+               validate: bool = True, stream: torch.cuda.Stream | None = None) -> SwitchResult:
         """Stop-and-migrate TP switch. With ``sync`` the call returns after the
         switch completed on the device and reports measured latencies; without
-        it, work is only enqueued (the caller's current stream is joined)."""
+        it, work is only enqueued and ``stream`` (default: the device's default
+        stream) waits for it."""
         t0 = time.perf_counter()
-        main = torch.cuda.current_stream(self.device)
-        ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
+        main = stream or self.main_stream
+        ev = {}
+        if sync:
+            ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
+            ev["start"].record(main)
         if self.time_kernels:
             for k in ("k1_start", "k1_end", "k2_start", "k2_end"):
                 ev[k] = torch.cuda.Event(enable_timing=True)
-        ev["start"].record(main)
         plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
         if self.handshake is not None:
             self.handshake(plan)
-        self.kv_stream.wait_event(ev["start"])
+        self.kv_stream.wait_stream(main)
         kv_stats = self.kv.migrate(plan, stream=self.kv_stream, validate=validate,
                                    k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
         w_stats = None
         if self.weights is not None and new_weight_groups is not None:
-            self.w_stream.wait_event(ev["start"])
+            self.w_stream.wait_stream(main)
             w_stats = self.weights.reshard(
                 new_weight_groups, stream=self.w_stream, parked=parked,
                 events=(ev["k2_start"], ev["k2_end"]) if self.time_kernels else None)
             main.wait_stream(self.w_stream)
         main.wait_stream(self.kv_stream)
-        ev["end"].record(main)
+        if sync:
+            ev["end"].record(main)
         res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev)
         if sync:
             # the step's result: K3's status word, read back D2H

@@ -213,6 +213,41 @@ int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, con
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_migrate launch");
 }
 
+int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const int32_t* h_xfers,
+                  int32_t* d_xfers, int32_t n_xfers, int32_t filter_src, int64_t* d_meta,
+                  int64_t* d_totals, int64_t n_units, int32_t* d_work, int32_t* d_status,
+                  void* stream) {
+  int rc = check_geometry(geo);
+  if (rc) return rc;
+  tpr::KvClusterParams cp;
+  if ((rc = cluster_params(cl, geo, &cp))) return rc;
+  if (n_xfers < 0 || n_units < 0) return fail(TPR_EINVAL, "negative sizes");
+  if (n_xfers == 0) return TPR_OK;
+  if (!d_xfers || !d_meta || !d_totals || !d_status || (n_units > 0 && !d_work))
+    return fail(TPR_EINVAL, "null device buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (h_xfers) {
+    e = cudaMemcpyAsync(d_xfers, h_xfers, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n_xfers,
+                        cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch H2D");
+  }
+  if (n_units == 0) return TPR_OK;
+  e = tpr::launch_k3(*geo, cp, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
+                     reinterpret_cast<int4*>(d_work), nullptr, d_status, st);
+  if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
+  e = tpr::launch_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st);
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_switch K1");
+}
+
+int tpr_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, void* stream) {
+  if (bytes == 0) return TPR_OK;
+  if (!dst || !src) return fail(TPR_EINVAL, "null pointer");
+  cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice,
+                                  static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_memcpy_h2d");
+}
+
 int tpr_copy_prepare(tpr_copy_seg_t* segs, int32_t n, int64_t chunk, int64_t* prefix,
                      int64_t* n_items) {
   if (n < 0 || !prefix || !n_items) return fail(TPR_EINVAL, "bad copy_prepare arguments");

@@ -9,19 +9,20 @@ and it moves exactly ``plan.total_bytes`` bytes (migration.py:128-130).
 
 Memory model (per GPU slot):
 
-* pool         uint8  [n_units, unit_bytes]; a unit is one KV head x one page
+* pool         uint8  [units, unit_bytes]; a unit is one KV head x one page
                       of ``block_tokens`` tokens x all layers x {K, V}. The pool
                       shape does not depend on the TP degree.
 * block table  int32  [max_requests, H, max_blocks]; entry = unit id or -1.
                       Indexed by the GLOBAL head id, so a TP-N rank r reads rows
                       [r*H/N, (r+1)*H/N) -- shard selection at execution time.
-* free ring    int32  [n_units] + host-owned monotonic (head, tail) counters.
+* free ring    int32  [units] + host-owned monotonic (head, tail) counters.
                       Allocation pops at head, release pushes at tail.
 
-A migration is two device steps: K3 (``tpr_kv_remap``) allocates destination
-units and rewrites both block tables in the plan's sequential order, then K1
-(``tpr_kv_migrate``) copies the valid tokens. All GPU slots may live on one
-device ("logical ranks", one B200) or on their own devices.
+A migration is two device steps behind ONE native call (``tpr_kv_switch``):
+K3 allocates destination units and rewrites both block tables in the plan's
+sequential order, then K1 copies the valid tokens. The host side is kept to
+table lookups so that small switches are not host-bound. All GPU slots may
+live on one device ("logical ranks", one B200) or on their own devices.
 """
 
 from __future__ import annotations
@@ -37,6 +38,8 @@ from . import _native
 from .geometry import KvGeometry
 from .migration import BYTES, DST, HI, LO, REQ, SRC, KvLayout, MigrationError, MigrationPlan
 
+_LUT_MAX = 1 << 24  # ids below this use dense lookup tables, others a dict
+
 
 @dataclass
 class MigrationStats:
@@ -48,37 +51,62 @@ class MigrationStats:
 
 
 class _PinnedStaging:
-    """Double-buffered pinned host staging for H2D metadata uploads."""
+    """Double-buffered pinned host staging for H2D metadata.
+
+    ``stage`` copies an int32 array into the next pinned buffer (waiting for
+    the copy that used it two calls ago) and returns its address; the caller
+    launches the H2D copy and then calls ``fence(stream)``."""
 
     def __init__(self, nbytes: int = 1 << 16):
         self._bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-        self._events: list[torch.cuda.Event | None] = [None, None]
+        self._events: list = [None, None]
         self._i = 0
 
-    def upload(self, arr: np.ndarray, dst: torch.Tensor, stream: torch.cuda.Stream) -> int:
-        raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
-        n = raw.nbytes
+    def stage(self, arr: np.ndarray) -> int:
+        raw = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
         i = self._i
-        self._i ^= 1
         if self._events[i] is not None:
             self._events[i].synchronize()
-        if self._bufs[i].numel() < n:
-            self._bufs[i] = torch.empty(max(n, 2 * self._bufs[i].numel()), dtype=torch.uint8,
-                                        pin_memory=True)
-        host = self._bufs[i][:n]
-        host.numpy()[:] = raw
-        with torch.cuda.stream(stream):
-            dst.view(torch.uint8).reshape(-1)[:n].copy_(host, non_blocking=True)
+            self._events[i] = None
+        if self._bufs[i].numel() < raw.nbytes:
+            self._bufs[i] = torch.empty(max(raw.nbytes, 2 * self._bufs[i].numel()),
+                                        dtype=torch.uint8, pin_memory=True)
+        self._bufs[i].numpy()[: raw.nbytes] = raw
+        return self._bufs[i].data_ptr()
+
+    def fence(self, stream: torch.cuda.Stream) -> None:
         ev = torch.cuda.Event()
         ev.record(stream)
-        self._events[i] = ev
+        self._events[self._i] = ev
+        self._i ^= 1
+
+    def upload(self, arr: np.ndarray, dst: torch.Tensor, stream: torch.cuda.Stream) -> int:
+        """Stage ``arr`` and copy it into ``dst`` on ``stream``."""
+        ptr = self.stage(arr)
+        n = arr.nbytes
+        _native.call("tpr_memcpy_h2d", dst.data_ptr(), ptr, n, stream.cuda_stream)
+        self.fence(stream)
         return n
+
+
+class _Scratch:
+    """Grow-only device buffer used on one stream."""
+
+    def __init__(self, dtype, device):
+        self.t = torch.empty(0, dtype=dtype, device=device)
+
+    def get(self, n: int, stream: torch.cuda.Stream) -> torch.Tensor:
+        if self.t.numel() < n:
+            self.t = torch.empty(max(n, 2 * self.t.numel(), 1024), dtype=self.t.dtype,
+                                 device=self.t.device)
+            self.t.record_stream(stream)
+        return self.t
 
 
 class PagedKvCluster:
     """KV pools, block tables and free rings of a set of GPUs."""
 
-    def __init__(self, kv: KvGeometry, gpu_ids: Sequence[int], units_per_gpu: int,
+    def __init__(self, kv: KvGeometry, gpu_ids: Sequence[int], units_per_gpu,
                  max_requests: int, max_blocks: int, device: str | torch.device = "cuda",
                  devices: dict | None = None, fragmented: bool = False, seed: int = 0):
         if not 1 <= len(gpu_ids) <= _native.TPR_MAX_GPUS:
@@ -98,6 +126,8 @@ class PagedKvCluster:
         self.max_requests = int(max_requests)
         self.max_blocks = int(max_blocks)
         default = torch.device(device)
+        if default.type == "cuda" and default.index is None:
+            default = torch.device("cuda", torch.cuda.current_device())
         self.devices = [torch.device(devices[g]) if devices else default for g in self.gpu_ids]
         self.home = self.devices[0]
         self._single_device = len(set(self.devices)) == 1
@@ -118,16 +148,33 @@ class PagedKvCluster:
         self._free_req_slots = list(range(self.max_requests - 1, -1, -1))
         self.owner = np.full((self.max_requests, H), -1, dtype=np.int32)  # gpu slot per head
         self.slot_ctx = np.full(self.max_requests, -1, dtype=np.int32)
-        # scratch
+        # id -> slot lookup tables
+        ids = np.asarray(self.gpu_ids, dtype=np.int64)
+        self._gpu_lut = None
+        if ids.min() >= 0 and ids.max() < _LUT_MAX:
+            self._gpu_lut = np.full(int(ids.max()) + 1, -1, dtype=np.int64)
+            self._gpu_lut[ids] = np.arange(len(ids))
+        self._req_lut = np.full(1024, -1, dtype=np.int64)
+        # device scratch + the cached C view of the cluster
         self._staging = _PinnedStaging()
-        self._xf = torch.empty(0, dtype=torch.int32, device=self.home)
-        self._meta = torch.empty(0, dtype=torch.int64, device=self.home)
+        self._xf = _Scratch(torch.int32, self.home)
+        self._meta = _Scratch(torch.int64, self.home)
+        self._work = _Scratch(torch.int32, self.home)
+        self._work_ext = _Scratch(torch.int32, self.home)
         self._totals = torch.zeros(_native.TPR_TOTALS_LEN, dtype=torch.int64, device=self.home)
-        self._work = torch.empty(0, dtype=torch.int32, device=self.home)
-        self._work_ext = torch.empty(0, dtype=torch.int32, device=self.home)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.home)
         self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
                                         H, self.max_blocks, self.max_requests, self.n_units)
+        self._cl = _native.KvClusterC()
+        self._cl.n_gpus = self.n_gpus
+        for s in range(self.n_gpus):
+            self._cl.pool[s] = self.pools[s].data_ptr()
+            self._cl.block_table[s] = self.block_tables[s].data_ptr()
+            self._cl.free_ring[s] = self.rings[s].data_ptr()
+            self._cl.units[s] = self.units[s]
+        self._last_in = self._last_out = np.zeros(self.n_gpus, np.int64)
+        self.pattern_seed = 0
+        self._default_stream = torch.cuda.current_stream(self.home)
 
     # ------------------------------------------------------------------ utils
     @property
@@ -139,65 +186,100 @@ class PagedKvCluster:
         return self.ring_tail[s] - self.ring_head[s]
 
     def _cluster_c(self) -> _native.KvClusterC:
-        c = _native.KvClusterC()
-        c.n_gpus = self.n_gpus
+        c = self._cl
         for s in range(self.n_gpus):
-            c.pool[s] = self.pools[s].data_ptr()
-            c.block_table[s] = self.block_tables[s].data_ptr()
-            c.free_ring[s] = self.rings[s].data_ptr()
             c.ring_head[s] = self.ring_head[s]
             c.ring_tail[s] = self.ring_tail[s]
-            c.units[s] = self.units[s]
         return c
-
-    @staticmethod
-    def _grow(t: torch.Tensor, n: int) -> torch.Tensor:
-        if t.numel() >= n:
-            return t
-        return torch.empty(max(n, 2 * t.numel()), dtype=t.dtype, device=t.device)
 
     def _units_per_record(self, xf: np.ndarray) -> np.ndarray:
         B = self.kv.block_tokens
         nblk = (xf[:, 5].astype(np.int64) + B - 1) // B
         return (xf[:, 4] - xf[:, 3]).astype(np.int64) * nblk
 
-    # -------------------------------------------------------------- K3 driver
-    def _remap(self, xf: np.ndarray, stream: torch.cuda.Stream, want_ext: bool) -> int:
-        """Upload records, run K3, advance host ring counters; returns #units."""
-        n = len(xf)
+    def _gpu_slots(self, ids: np.ndarray) -> np.ndarray:
+        lut = self._gpu_lut
+        if lut is not None and len(ids) and ids.min() >= 0 and ids.max() < len(lut):
+            s = lut[ids]
+            if (s >= 0).all():
+                return s
+        try:
+            return np.fromiter((self.slot_of[g] for g in ids.tolist()), np.int64, len(ids))
+        except KeyError as exc:
+            raise MigrationError(f"gpu {exc.args[0]} is not part of this cluster") from None
+
+    def _req_slots(self, ids: np.ndarray) -> np.ndarray:
+        lut = self._req_lut
+        if len(ids) and ids.min() >= 0 and ids.max() < len(lut):
+            s = lut[ids]
+            if (s >= 0).all():
+                return s
+        try:
+            return np.fromiter((self.req_slot[r] for r in ids.tolist()), np.int64, len(ids))
+        except KeyError as exc:
+            raise MigrationError(f"request {exc.args[0]} is not resident") from None
+
+    def _set_req(self, rid: int, slot: int) -> None:
+        if 0 <= rid < _LUT_MAX:
+            if rid >= len(self._req_lut):
+                grown = np.full(max(rid + 1, 2 * len(self._req_lut)), -1, dtype=np.int64)
+                grown[: len(self._req_lut)] = self._req_lut
+                self._req_lut = grown
+            self._req_lut[rid] = slot
+
+    def _deltas(self, xf: np.ndarray, units: np.ndarray):
+        if len(xf) <= 64:  # small plans: plain loops beat numpy call overhead
+            in_u = [0] * self.n_gpus
+            out_u = [0] * self.n_gpus
+            for (s, d), u in zip(xf[:, :2].tolist(), units.tolist()):
+                if d >= 0:
+                    in_u[d] += u
+                if s >= 0:
+                    out_u[s] += u
+            return np.asarray(in_u, np.int64), np.asarray(out_u, np.int64)
+        has_dst = xf[:, 1] >= 0
+        has_src = xf[:, 0] >= 0
+        in_u = np.bincount(xf[has_dst, 1], weights=units[has_dst], minlength=self.n_gpus)
+        out_u = np.bincount(xf[has_src, 0], weights=units[has_src], minlength=self.n_gpus)
+        return in_u.astype(np.int64), out_u.astype(np.int64)
+
+    def _reserve(self, xf: np.ndarray):
+        """Capacity check + ring bookkeeping for records; returns (#units, in, out)."""
         units = self._units_per_record(xf)
         total = int(units.sum())
-        has_dst = xf[:, 1] >= 0
-        in_u = np.bincount(xf[has_dst, 1], weights=units[has_dst],
-                           minlength=self.n_gpus).astype(np.int64)
-        has_src = xf[:, 0] >= 0
-        out_u = np.bincount(xf[has_src, 0], weights=units[has_src],
-                            minlength=self.n_gpus).astype(np.int64)
+        in_u, out_u = self._deltas(xf, units)
         for s in range(self.n_gpus):
             free = self.ring_tail[s] - self.ring_head[s]
             if in_u[s] > free:
                 raise MigrationError(
                     f"gpu {self.gpu_ids[s]}: {in_u[s]} KV units needed, {free} free")
         self._last_in, self._last_out = in_u, out_u
-        if total == 0:  # e.g. zero-length contexts: nothing to allocate or move
-            return 0
-        with torch.cuda.stream(stream):  # scratch lives on the stream that uses it
-            self._xf = self._grow(self._xf, n * 6)
-            self._meta = self._grow(self._meta, n * 4)
-            self._work = self._grow(self._work, total * 4)
-            if want_ext:
-                self._work_ext = self._grow(self._work_ext, total * 4)
-            self._staging.upload(xf.astype(np.int32), self._xf, stream)
-        cl = self._cluster_c()
-        _native.call(
-            "tpr_kv_remap", ctypes.byref(self._geo), ctypes.byref(cl), self._xf.data_ptr(), n,
-            -1, self._meta.data_ptr(), self._totals.data_ptr(), total, self._work.data_ptr(),
-            self._work_ext.data_ptr() if want_ext else None, self.status.data_ptr(),
-            stream.cuda_stream,
-        )
+        return total, in_u, out_u
+
+    def _commit(self, in_u, out_u):
         for s in range(self.n_gpus):
             self.ring_head[s] += int(in_u[s])
             self.ring_tail[s] += int(out_u[s])
+
+    # -------------------------------------------------------------- K3 driver
+    def _remap(self, xf: np.ndarray, stream: torch.cuda.Stream, want_ext: bool) -> int:
+        """Upload records, run K3 only (admission / release); returns #units."""
+        total, in_u, out_u = self._reserve(xf)
+        if total == 0:  # e.g. zero-length contexts: nothing to allocate or move
+            return 0
+        n = len(xf)
+        d_xf = self._xf.get(n * 6, stream)
+        self._staging.upload(xf.astype(np.int32), d_xf, stream)
+        d_work = self._work.get(total * 4, stream)
+        d_ext = self._work_ext.get(total * 4, stream) if want_ext else None
+        cl = self._cluster_c()
+        _native.call(
+            "tpr_kv_remap", ctypes.byref(self._geo), ctypes.byref(cl), d_xf.data_ptr(), n, -1,
+            self._meta.get(n * 4, stream).data_ptr(), self._totals.data_ptr(), total,
+            d_work.data_ptr(), d_ext.data_ptr() if want_ext else None, self.status.data_ptr(),
+            stream.cuda_stream,
+        )
+        self._commit(in_u, out_u)
         return total
 
     # -------------------------------------------------------------- admission
@@ -205,7 +287,7 @@ class PagedKvCluster:
               stream: torch.cuda.Stream | None = None) -> int:
         """Allocate pages for new requests in their canonical layout and fill
         them with the placement-invariant synthetic pattern. Returns #units."""
-        stream = stream or torch.cuda.current_stream(self.home)
+        stream = stream or self._default_stream
         H = self.kv.total_heads
         recs = []
         for lay in layouts:
@@ -222,6 +304,7 @@ class PagedKvCluster:
                     raise MigrationError("no free request slots")
                 rs = self._free_req_slots.pop()
                 self.req_slot[rid] = rs
+                self._set_req(rid, rs)
                 self.ctx_of[rid] = int(ctx)
                 self.slot_ctx[rs] = int(ctx)
                 for r, s in enumerate(slots):
@@ -231,11 +314,12 @@ class PagedKvCluster:
             return 0
         xf = np.asarray(recs, dtype=np.int64)
         total = self._remap(xf, stream, want_ext=True)
-        cl = self._cluster_c()
-        with torch.cuda.device(self.home):
-            _native.call("tpr_kv_fill", ctypes.byref(self._geo), ctypes.byref(cl),
-                         self._work.data_ptr(), self._work_ext.data_ptr(), total, seed,
-                         stream.cuda_stream)
+        if total:
+            cl = self._cluster_c()
+            with torch.cuda.device(self.home):
+                _native.call("tpr_kv_fill", ctypes.byref(self._geo), ctypes.byref(cl),
+                             self._work.t.data_ptr(), self._work_ext.t.data_ptr(), total, seed,
+                             stream.cuda_stream)
         self.pattern_seed = seed
         return total
 
@@ -243,7 +327,8 @@ class PagedKvCluster:
         """Free every page of finished / evicted requests (K3 with dst = -1:
         block-table entries cleared, units pushed back on their owners' free
         rings in (request, head, page) order). Returns #units released."""
-        stream = stream or torch.cuda.current_stream(self.home)
+        stream = stream or self._default_stream
+        request_ids = list(request_ids)
         recs = []
         for rid in request_ids:
             rs = self.req_slot.get(rid)
@@ -262,6 +347,8 @@ class PagedKvCluster:
         total = self._remap(np.asarray(recs, np.int64), stream, want_ext=False)
         for rid in request_ids:
             rs = self.req_slot.pop(rid)
+            if 0 <= rid < len(self._req_lut):
+                self._req_lut[rid] = -1
             self.ctx_of.pop(rid, None)
             self.owner[rs] = -1
             self.slot_ctx[rs] = -1
@@ -270,9 +357,11 @@ class PagedKvCluster:
 
     def fill_garbage(self, seed: int = 99, stream: torch.cuda.Stream | None = None) -> None:
         """Fill whole pools with per-unit garbage (so stale bytes are visible)."""
-        stream = stream or torch.cuda.current_stream(self.home)
+        stream = stream or self._default_stream
         for s in range(self.n_gpus):
-            _native.call("tpr_pool_fill", ctypes.byref(self._geo), self.pools[s].data_ptr(), s,
+            geo = _native.KvGeometryC(*[getattr(self._geo, f) for f, _ in self._geo._fields_])
+            geo.n_units = self.units[s]
+            _native.call("tpr_pool_fill", ctypes.byref(geo), self.pools[s].data_ptr(), s,
                          seed, stream.cuda_stream)
 
     # -------------------------------------------------------------- migration
@@ -282,15 +371,9 @@ class PagedKvCluster:
         n = len(arr)
         if n == 0:
             return np.zeros((0, 6), dtype=np.int64)
-        try:
-            src = np.fromiter((self.slot_of[g] for g in arr[:, SRC].tolist()), np.int64, n)
-            dst = np.fromiter((self.slot_of[g] for g in arr[:, DST].tolist()), np.int64, n)
-        except KeyError as exc:
-            raise MigrationError(f"gpu {exc.args[0]} is not part of this cluster") from None
-        try:
-            req = np.fromiter((self.req_slot[r] for r in arr[:, REQ].tolist()), np.int64, n)
-        except KeyError as exc:
-            raise MigrationError(f"request {exc.args[0]} is not resident") from None
+        src = self._gpu_slots(arr[:, SRC])
+        dst = self._gpu_slots(arr[:, DST])
+        req = self._req_slots(arr[:, REQ])
         ctx = self.slot_ctx[req].astype(np.int64)
         lo, hi = arr[:, LO], arr[:, HI]
         if ((lo < 0) | (hi > self.kv.total_heads) | (lo >= hi)).any():
@@ -321,32 +404,55 @@ class PagedKvCluster:
                 validate: bool = True, k1_events: tuple | None = None) -> MigrationStats:
         """Execute ``plan``: K3 remap + K1 page copy, stream-ordered, no host sync.
 
-        ``k1_events`` = (start, end) CUDA events recorded around K1.
+        ``k1_events`` = (start, end) CUDA events recorded around K1 (this
+        splits the fused call in two so the events can sit between them).
         """
-        stream = stream or torch.cuda.current_stream(self.home)
+        stream = stream or self._default_stream
         xf = self.records(plan, validate)
-        if len(xf) == 0:
+        n = len(xf)
+        if n == 0:
             return MigrationStats(0, 0, 0, {}, {})
         if not self._single_device:
-            raise MigrationError("multi-device clusters migrate through kvcache_dist")
-        units = self._remap(xf, stream, want_ext=False)
-        if k1_events:
-            k1_events[0].record(stream)
+            raise MigrationError("multi-device clusters migrate through distributed.py")
+        total, in_u, out_u = self._reserve(xf)
         cl = self._cluster_c()
-        _native.call("tpr_kv_migrate", ctypes.byref(self._geo), ctypes.byref(cl),
-                     self._work.data_ptr(), units, stream.cuda_stream)
+        d_xf = self._xf.get(n * 6, stream)
+        d_meta = self._meta.get(n * 4, stream)
+        d_work = self._work.get(max(total, 1) * 4, stream)
+        h_ptr = self._staging.stage(xf.astype(np.int32))
         if k1_events:
+            _native.call("tpr_kv_switch", ctypes.byref(self._geo), ctypes.byref(cl), h_ptr,
+                         d_xf.data_ptr(), n, -1, d_meta.data_ptr(), self._totals.data_ptr(), 0,
+                         d_work.data_ptr(), self.status.data_ptr(), stream.cuda_stream)
+            if total:
+                _native.call("tpr_kv_remap", ctypes.byref(self._geo), ctypes.byref(cl),
+                             d_xf.data_ptr(), n, -1, d_meta.data_ptr(), self._totals.data_ptr(),
+                             total, d_work.data_ptr(), None, self.status.data_ptr(),
+                             stream.cuda_stream)
+            k1_events[0].record(stream)
+            _native.call("tpr_kv_migrate", ctypes.byref(self._geo), ctypes.byref(cl),
+                         d_work.data_ptr(), total, stream.cuda_stream)
             k1_events[1].record(stream)
+        else:
+            _native.call("tpr_kv_switch", ctypes.byref(self._geo), ctypes.byref(cl), h_ptr,
+                         d_xf.data_ptr(), n, -1, d_meta.data_ptr(), self._totals.data_ptr(), total,
+                         d_work.data_ptr(), self.status.data_ptr(), stream.cuda_stream)
+        self._staging.fence(stream)
+        self._commit(in_u, out_u)
         # host placement bookkeeping (apply_plan semantics)
-        heads = np.arange(self.kv.total_heads)
-        mask = (heads >= xf[:, 3:4]) & (heads < xf[:, 4:5])
-        rows = np.repeat(xf[:, 2], self.kv.total_heads).reshape(-1, self.kv.total_heads)
-        self.owner[rows[mask], np.broadcast_to(heads, mask.shape)[mask]] = \
-            np.broadcast_to(xf[:, 1:2], mask.shape)[mask]
+        if n <= 64:
+            for s, d, r, lo, hi, _ in xf.tolist():
+                self.owner[r, lo:hi] = d
+        else:
+            heads = np.arange(self.kv.total_heads)
+            mask = (heads >= xf[:, 3:4]) & (heads < xf[:, 4:5])
+            rows = np.broadcast_to(xf[:, 2:3], mask.shape)
+            self.owner[rows[mask], np.broadcast_to(heads, mask.shape)[mask]] = \
+                np.broadcast_to(xf[:, 1:2], mask.shape)[mask]
         return MigrationStats(
-            transfers=len(xf), units=units, bytes=int(plan.as_array()[:, BYTES].sum()),
-            in_units={self.gpu_ids[s]: int(v) for s, v in enumerate(self._last_in) if v},
-            out_units={self.gpu_ids[s]: int(v) for s, v in enumerate(self._last_out) if v},
+            transfers=n, units=total, bytes=plan.total_bytes,
+            in_units={self.gpu_ids[s]: int(v) for s, v in enumerate(in_u) if v},
+            out_units={self.gpu_ids[s]: int(v) for s, v in enumerate(out_u) if v},
         )
 
     # ------------------------------------------------------------ inspection
@@ -361,18 +467,20 @@ class PagedKvCluster:
     def verify(self, seed: int | None = None, stream: torch.cuda.Stream | None = None) -> dict:
         """Full-size device check: block tables realise the host placement and
         every owned page carries its pattern. Returns counts (host sync)."""
-        stream = stream or torch.cuda.current_stream(self.home)
         seed = self.pattern_seed if seed is None else seed
         out = {"placement_errors": 0, "word_mismatches": 0, "pages_checked": 0}
         for s in range(self.n_gpus):
             dev = self.devices[s]
+            st = stream or torch.cuda.current_stream(dev)
             ctx = torch.from_numpy(self.slot_ctx).to(dev)
             owner = torch.from_numpy(self.owner).to(dev)
             counts = torch.zeros(3, dtype=torch.int64, device=dev)
+            geo = _native.KvGeometryC(*[getattr(self._geo, f) for f, _ in self._geo._fields_])
+            geo.n_units = self.units[s]
             with torch.cuda.device(dev):
-                _native.call("tpr_kv_verify", ctypes.byref(self._geo), self.pools[s].data_ptr(),
+                _native.call("tpr_kv_verify", ctypes.byref(geo), self.pools[s].data_ptr(),
                              self.block_tables[s].data_ptr(), ctx.data_ptr(), owner.data_ptr(), s,
-                             seed, counts.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+                             seed, counts.data_ptr(), st.cuda_stream)
             c = counts.cpu().tolist()
             out["placement_errors"] += c[0]
             out["word_mismatches"] += c[1]

@@ -17,6 +17,7 @@ reference's exact-equality event-oracle test holds bit for bit.
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 from typing import Iterable
 
@@ -196,6 +197,16 @@ class _GroupTable:
         return off
 
 
+_scratch = threading.local()
+
+
+def _out_buffer(rows: int) -> np.ndarray:
+    buf = getattr(_scratch, "out", None)
+    if buf is None or len(buf) < rows:
+        buf = _scratch.out = np.empty((max(rows, 4096), 6), dtype=np.int64)
+    return buf
+
+
 def _plan_native(rows: list[tuple[int, int, tuple, int, tuple, int]], total_heads: int,
                  kvb: int) -> np.ndarray:
     """rows: (request id, ctx, old group, old tp, new group, new tp) in plan order."""
@@ -203,27 +214,20 @@ def _plan_native(rows: list[tuple[int, int, tuple, int, tuple, int]], total_head
     if n == 0:
         return np.zeros((0, 6), dtype=np.int64)
     table = _GroupTable()
-    req = np.empty(n, np.int64)
-    ctx = np.empty(n, np.int64)
-    oo = np.empty(n, np.int32)
-    ot = np.empty(n, np.int32)
-    no = np.empty(n, np.int32)
-    nt = np.empty(n, np.int32)
-    for i, (r, c, og, otp, ng, ntp) in enumerate(rows):
-        req[i] = r
-        ctx[i] = c
-        oo[i] = table.offset(og)
-        ot[i] = otp
-        no[i] = table.offset(ng)
-        nt[i] = ntp
+    cols = np.array([(r, c, table.offset(og), otp, table.offset(ng), ntp)
+                     for r, c, og, otp, ng, ntp in rows], dtype=np.int64)
+    req = np.ascontiguousarray(cols[:, 0])
+    ctx = np.ascontiguousarray(cols[:, 1])
+    meta = np.ascontiguousarray(cols[:, 2:6].T, dtype=np.int32)  # old_off, old_tp, new_off, new_tp
     ids = np.asarray(table.ids, dtype=np.int64)
     cap = n * total_heads
-    out = np.empty((cap, 6), dtype=np.int64)
+    out = _out_buffer(cap)
     n_out = _native.c_int64(0)
+    base = meta.ctypes.data
     _native.call(
-        "tpr_plan_heads", n, req.ctypes.data, ctx.ctypes.data, oo.ctypes.data, ot.ctypes.data,
-        no.ctypes.data, nt.ctypes.data, ids.ctypes.data, total_heads, int(kvb), cap,
-        out.ctypes.data, _native.ctypes.byref(n_out),
+        "tpr_plan_heads", n, req.ctypes.data, ctx.ctypes.data, base, base + 4 * n, base + 8 * n,
+        base + 12 * n, ids.ctypes.data, total_heads, int(kvb), cap, out.ctypes.data,
+        _native.ctypes.byref(n_out),
     )
     return out[: n_out.value].copy()
 

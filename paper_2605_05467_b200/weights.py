@@ -92,6 +92,9 @@ class ShardedWeightStore:
         self.slice_off = np.concatenate([[0], np.cumsum(self.slice_bytes)[:-1]]).astype(np.int64)
         self.bytes_per_slice = int(self.slice_bytes.sum())
         self.is_col = np.array([m.split == "col" for m in self.split])
+        self._step = np.where(self.is_col, self.slice_bytes,
+                              np.array([m.cols // MAX_TP for m in self.split], np.int64) * es)
+        self._seg_rows = np.where(self.is_col, 1, np.array([m.rows for m in self.split], np.int64))
         self.rows = np.array([m.rows for m in self.split], dtype=np.int64)
         self.cols = np.array([m.cols for m in self.split], dtype=np.int64)
         self.index = {(m.name, m.layer): i for i, m in enumerate(self.split)}
@@ -222,31 +225,24 @@ class ShardedWeightStore:
         x, y = new_res[g]
         s_new = y - x
         dbase = new_arena.data_ptr()
-        es = self.model.dtype_bytes
-        out = []
-        rps = self.rows // MAX_TP
-        cps = self.cols // MAX_TP
-        for src, lo, hi in moves[g]:
+        # Within a matrix region of an arena holding s slices, slice k starts at
+        # k * step: whole rows for column-parallel matrices (step = one slice,
+        # contiguous), a column block for row-parallel ones (step = cols/8
+        # elements, rows strided by s * step).
+        step = self._step
+        runs = moves[g]
+        seg = np.zeros((len(runs), len(self.split), 8), dtype=np.int64)
+        for i, (src, lo, hi) in enumerate(runs):
             ha, hb = self.resident[src]
             s_src = hb - ha
-            sbase = self.arena[src].data_ptr()
-            k = hi - lo
-            n = len(self.split)
-            seg = np.zeros((n, 8), dtype=np.int64)
-            col = self.is_col
-            # column-parallel: contiguous rows of whole matrix rows
-            seg[:, 0] = np.where(col, sbase + s_src * self.slice_off + (lo - ha) * rps * self.cols * es,
-                                 sbase + s_src * self.slice_off + (lo - ha) * cps * es)
-            seg[:, 1] = np.where(col, dbase + s_new * self.slice_off + (lo - x) * rps * self.cols * es,
-                                 dbase + s_new * self.slice_off + (lo - x) * cps * es)
-            seg[:, 2] = np.where(col, 1, self.rows)
-            seg[:, 3] = np.where(col, k * rps * self.cols * es, k * cps * es)
-            seg[:, 4] = np.where(col, seg[:, 3], s_src * cps * es)
-            seg[:, 5] = np.where(col, seg[:, 3], s_new * cps * es)
-            out.append(seg)
-        if not out:
-            return np.zeros((0, 8), dtype=np.int64)
-        return np.concatenate(out)
+            row_bytes = (hi - lo) * step
+            seg[i, :, 0] = self.arena[src].data_ptr() + s_src * self.slice_off + (lo - ha) * step
+            seg[i, :, 1] = dbase + s_new * self.slice_off + (lo - x) * step
+            seg[i, :, 2] = self._seg_rows
+            seg[i, :, 3] = row_bytes
+            seg[i, :, 4] = np.where(self.is_col, row_bytes, s_src * step)
+            seg[i, :, 5] = np.where(self.is_col, row_bytes, s_new * step)
+        return seg.reshape(-1, 8)
 
     def reshard(self, new_groups: Sequence[Sequence[int]], stream: torch.cuda.Stream | None = None,
                 events: tuple | None = None, parked: Sequence[int] = ()) -> ReshardStats:
@@ -300,21 +296,24 @@ class ShardedWeightStore:
         return stats
 
     def _launch(self, seg: np.ndarray, dev: torch.device, stream: torch.cuda.Stream) -> None:
+        """Normalise segments (host), upload segments + item prefix through
+        pinned staging, launch K2."""
+        from .kvcache import _PinnedStaging, _Scratch
+
         n = len(seg)
-        prefix = np.zeros(n + 1, dtype=np.int64)
+        buf = np.empty(seg.size + n + 1, dtype=np.int64)
+        buf[: seg.size] = seg.reshape(-1)
         n_items = ctypes.c_int64(0)
-        _native.call("tpr_copy_prepare", seg.ctypes.data, n, CHUNK_BYTES, prefix.ctypes.data,
-                     ctypes.byref(n_items))
-        host = torch.from_numpy(np.concatenate([seg.reshape(-1), prefix])).pin_memory()
-        with torch.cuda.stream(stream):
-            d = torch.empty(host.numel(), dtype=torch.int64, device=dev)
-            d.copy_(host, non_blocking=True)
-        # keep host staging alive until the copy is done
-        self._pending_host = host
+        _native.call("tpr_copy_prepare", buf.ctypes.data, n, CHUNK_BYTES,
+                     buf.ctypes.data + seg.nbytes, ctypes.byref(n_items))
+        if dev not in self._segs_dev:
+            self._segs_dev[dev] = (_PinnedStaging(), _Scratch(torch.int64, dev))
+        staging, scratch = self._segs_dev[dev]
+        d = scratch.get(buf.size, stream)
         with torch.cuda.device(dev):
+            staging.upload(buf, d, stream)
             _native.call("tpr_weight_reshard", d.data_ptr(), d.data_ptr() + seg.nbytes, n,
                          n_items.value, CHUNK_BYTES, stream.cuda_stream)
-        self._segs_dev[dev] = d
 
     def finish(self) -> None:
         """Wait for the last reshard's copies."""
