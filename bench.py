@@ -331,6 +331,114 @@ def run_cpu_reference(w, steps: int, warmup: int, sample_seqs: int):
 
 
 # ---------------------------------------------------------------------------
+# N > 1: one process per GPU, real cross-GPU switch (push KV, pull weights)
+# ---------------------------------------------------------------------------
+
+def distributed_workload(world: int, seqs: int | None):
+    """Weak scaling: TP(N/2) <-> TP(N) over N GPUs, 16 seqs x 4096 per GPU,
+    Llama-3.1-8B KV + sharded weights (N=4 is BASELINE configs[1])."""
+    from paper_2605_05467_b200 import workloads
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
+    return workloads.transition(LLAMA_3_1_8B, world, max(world // 2, 1), world,
+                                seqs or 16 * world, 4096, weights=True,
+                                name=f"Llama-3.1-8B TP{max(world // 2, 1)}<->TP{world} "
+                                     f"{seqs or 16 * world}x4096 KV+weights, {world} GPUs")
+
+
+def run_distributed(args, w, rank: int, world: int, local: int):
+    import datetime
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_05467_b200.distributed import (DistributedExecutor, DistributedKvCluster,
+                                                   DistributedWeightStore)
+
+    n_dev = torch.cuda.device_count()
+    device = torch.device("cuda", local % n_dev)
+    torch.cuda.set_device(device)
+    dist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
+    kv = w.model.kv
+    units = capacity_units(w, kv)
+    max_ctx = max(c for _, c in w.requests)
+    cl = DistributedKvCluster(kv, w.gpus, units_per_gpu=max(units.values()),
+                              max_requests=len(w.requests), max_blocks=kv.blocks(max_ctx),
+                              device=device, fragmented=True, seed=rank)
+    cl.admit(w.old, seed=1234)
+    slices = max(8 // len(g) for g in (w.old_weight_groups or [()]) + (w.new_weight_groups or [()]) if g)
+    ws = DistributedWeightStore(w.model, w.gpus, device=device, max_slices=slices)
+    ws.load(w.old_weight_groups)
+    ex = DistributedExecutor(cl, ws)
+
+    def step(fwd):
+        if fwd:
+            return ex.switch(w.old, w.new, new_weight_groups=w.new_weight_groups)
+        return ex.switch(w.new, w.old, new_weight_groups=w.old_weight_groups)
+
+    fwd = True
+    for _ in range(max(args.warmup, 1)):
+        step(fwd)
+        fwd = not fwd
+    dev_ms, wall_ms, kv_bytes, w_bytes, k1 = 0.0, [], 0, 0, []
+    with ClockSampler(device.index) as clk:
+        dist.barrier()
+        clk.start()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(cl.stream)
+            plan, ks, wst, ms = ex.switch(*((w.old, w.new) if fwd else (w.new, w.old)),
+                                          new_weight_groups=w.new_weight_groups if fwd else w.old_weight_groups,
+                                          k1_events=(e[2], e[3]))
+            e[1].record(cl.stream)
+            fwd = not fwd
+            torch.cuda.synchronize(device)
+            # the switch's device span on this rank: KV stream start -> end (K2 ran alongside)
+            dev_ms += e[0].elapsed_time(e[1])
+            k1.append(e[2].elapsed_time(e[3]))
+            wall_ms.append(ms)
+            kv_bytes += ks.bytes
+            w_bytes += wst.bytes if wst else 0
+        wall = time.perf_counter() - t0
+        clk.stop()
+        dist.barrier()
+    t = torch.tensor([dev_ms, wall], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, wall = float(t[0]), float(t[1])
+    v1 = cl.verify()
+    v2 = ws.verify()
+    ok = torch.tensor([int(v1["placement_errors"] == 0 and v1["word_mismatches"] == 0 and v2 == 0)])
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    ws.close()
+    cl.close()
+    dist.destroy_process_group()
+    if rank != 0:
+        return
+    total = kv_bytes + w_bytes
+    hbm, src = peaks()
+    line = {
+        "metric": METRIC, "value": total / (dev_ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": w.name, "model": w.model.name, "seqs": len(w.requests),
+                   "ctx": w.requests[0][1], "parallelism": f"{world} processes, one GPU slot each, "
+                   "KV pushed / weights pulled through CUDA-IPC peer mappings",
+                   "devices_used": n_dev, "kv_bytes_per_step": kv_bytes / args.steps,
+                   "weight_bytes_per_step": w_bytes / args.steps,
+                   "l2": "inputs larger than L2"},
+        "roofline": {"bound": "nvlink" if n_dev >= world else "hbm", "kernel": "tpr_k1_kv_migrate",
+                     "k1_ms_rank0": float(np.mean(k1)), "peak_hbm": hbm, "peak_source": src},
+        "clocks": clk.summary(),
+        "e2e": {"value": total / wall / 1e9, "unit": "GB/s", "ms_per_step": wall / args.steps * 1e3,
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": 0},
+        "gpu_launches": args.steps * 4,
+        "bit_exact_property": bool(ok.item()),
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
 # main
 # ---------------------------------------------------------------------------
 
@@ -350,7 +458,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    w = build_workload(args.config, args.seqs)
+    w = build_workload(args.config, args.seqs) if world == 1 else distributed_workload(world, args.seqs)
 
     if args.impl == "reference":
         if rank != 0:
@@ -374,9 +482,9 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = torch.device("cuda", local if world > 1 else 0)
+        run_distributed(args, w, rank, world, local)
+        return
+    device = torch.device("cuda", 0)
     torch.cuda.set_device(device)
 
     def barrier():

@@ -32,9 +32,10 @@ import torch
 import torch.distributed as dist
 
 from . import _native
-from .geometry import KvGeometry
+from .geometry import MAX_TP, KvGeometry, ModelGeometry
 from .kvcache import MigrationStats, _PinnedStaging
-from .migration import BYTES, KvLayout, MigrationError, MigrationPlan
+from .migration import BYTES, KvLayout, MigrationError, MigrationPlan, plan_repartition
+from .weights import ReshardStats, ShardedWeightStore, groups_ranges
 
 
 class _CudaArray:
@@ -274,6 +275,13 @@ class DistributedKvCluster:
 
     def migrate(self, plan: MigrationPlan, k1_events=None) -> MigrationStats:
         """Collective over the group: every rank passes the same plan."""
+        pending = self.launch(plan, k1_events)
+        self.stream.synchronize()
+        dist.barrier(group=self.group)  # every page has landed everywhere
+        return self.finish(plan, pending)
+
+    def launch(self, plan: MigrationPlan, k1_events=None):
+        """Handshake, then enqueue this rank's K3 + K1 on ``self.stream``."""
         rec = self.records(plan)
         in_u, out_u = self._advance(rec)
         handshake(rec, self.ring_head, self.ring_tail, self.group)  # also the start barrier
@@ -287,8 +295,11 @@ class DistributedKvCluster:
                              self._work.data_ptr(), n, self.stream.cuda_stream)
             if k1_events:
                 k1_events[1].record(self.stream)
-        self.stream.synchronize()
-        dist.barrier(group=self.group)  # every page has landed everywhere
+        return rec, in_u, out_u, n
+
+    def finish(self, plan: MigrationPlan, pending) -> MigrationStats:
+        """Host bookkeeping once every rank's pages have landed (after the barrier)."""
+        rec, in_u, out_u, n = pending
         self._commit(in_u, out_u)
         heads = np.arange(self.kv.total_heads)
         mask = (heads >= rec[:, 3:4]) & (heads < rec[:, 4:5])
@@ -330,5 +341,177 @@ class DistributedKvCluster:
             b.free()
 
 
-__all__ = ["DistributedKvCluster", "DeviceBuffer", "handshake", "ring_deltas", "my_units",
-           "plan_digest", "units_per_record", "KvLayout"]
+# ---------------------------------------------------------------------------
+# weights: K2 pulls missing slices from peers' arenas over IPC
+# ---------------------------------------------------------------------------
+
+class _PeerPtr:
+    """A peer's arena as seen through its IPC mapping (only .data_ptr())."""
+
+    def __init__(self, ptr: int):
+        self.ptr = ptr
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class DistributedWeightStore(ShardedWeightStore):
+    """The sharded weights of ONE GPU (this rank) + IPC views of its peers.
+
+    Each rank owns two arenas (double buffer) sized for ``max_slices`` slices.
+    Both are registered with every peer once. A reshard rebuilds a GPU's shard
+    into its idle arena by pulling slices from the peers' current arenas
+    (remote loads over NVLink, local ones from HBM). The pull uses the same
+    planner as the single-process store, so every rank computes the same
+    source choice and egress balance. After the barrier the GPUs that rebuilt
+    flip to the other arena; the old one stays readable until the next
+    reshard, which starts after a barrier."""
+
+    def __init__(self, model: ModelGeometry, gpu_ids, device: torch.device, group=None,
+                 max_slices: int = MAX_TP, mode: str = "sharded"):
+        super().__init__(model, gpu_ids, device=device, mode=mode)
+        self.group = group
+        self.rank = dist.get_rank(group)
+        if len(self.gpu_ids) != dist.get_world_size(group):
+            raise MigrationError("one GPU per rank")
+        self.me = self.gpu_ids[self.rank]
+        self.device = torch.device(device)
+        self.max_slices = MAX_TP if mode == "full_copy_per_gpu" else int(max_slices)
+        cap = max(self.max_slices * self.bytes_per_slice, 16)
+        self.bufs = [DeviceBuffer(cap, self.device), DeviceBuffer(cap, self.device)]
+        handles = [b.handle() for b in self.bufs]
+        allh = [None] * len(self.gpu_ids)
+        dist.all_gather_object(allh, handles, group=group)
+        self.peer_bufs = {}
+        for r, g in enumerate(self.gpu_ids):
+            self.peer_bufs[g] = ([b.ptr for b in self.bufs] if g == self.me
+                                 else [open_peer(h) for h in allh[r]])
+        self.cur = {g: 0 for g in self.gpu_ids}
+        self.stream = torch.cuda.Stream(device=self.device)
+
+    def _views(self):
+        arena = {}
+        for g in self.gpu_ids:
+            a, b = self.resident[g]
+            if g == self.me:
+                arena[g] = self.bufs[self.cur[g]].tensor[: (b - a) * self.bytes_per_slice]
+            else:
+                arena[g] = _PeerPtr(self.peer_bufs[g][self.cur[g]])
+        self.arena = arena
+
+    def load(self, groups, stream=None) -> None:
+        act = groups_ranges(groups)
+        if set(act) != set(self.gpu_ids):
+            raise MigrationError("groups must cover exactly the store's GPUs")
+        for g in self.gpu_ids:
+            self.resident[g] = (0, MAX_TP) if self.mode == "full_copy_per_gpu" else act[g]
+            self.active[g] = act[g]
+            if self.resident[g][1] - self.resident[g][0] > self.max_slices:
+                raise MigrationError(f"gpu {g}: shard exceeds max_slices={self.max_slices}")
+        self._views()
+        rep_bytes = sum(m.rows * m.cols for m in self.replicated) * self.model.dtype_bytes
+        self.rep_arena = {self.me: torch.empty(max(rep_bytes, 16), dtype=torch.uint8, device=self.device)}
+        st = stream or self.stream
+        with torch.cuda.device(self.device):
+            self._fill(self.me, st)
+        st.synchronize()
+        dist.barrier(group=self.group)
+
+    def launch(self, new_groups, parked=(), events=None):
+        """Plan (same on every rank) and enqueue this rank's K2 pull."""
+        act, new_res, moves = self.plan(new_groups, parked)
+        for g in parked:
+            act[g] = new_res[g]
+        stats = ReshardStats(egress={g: 0 for g in self.gpu_ids}, ingress={g: 0 for g in self.gpu_ids})
+        for g in self.gpu_ids:
+            if not moves[g]:
+                stats.views += 1
+                continue
+            x, y = new_res[g]
+            if y - x > self.max_slices:
+                raise MigrationError(f"gpu {g}: shard exceeds max_slices={self.max_slices}")
+            for src, lo, hi in moves[g]:
+                nb = (hi - lo) * self.bytes_per_slice
+                if src == g:
+                    stats.local_bytes += nb
+                else:
+                    stats.remote_bytes += nb
+                    stats.egress[src] += nb
+                    stats.ingress[g] += nb
+        if events:
+            events[0].record(self.stream)
+        if moves[self.me]:
+            target = self.bufs[1 - self.cur[self.me]].tensor
+            seg = np.ascontiguousarray(self._segments(self.me, new_res, moves, target))
+            stats.segments = len(seg)
+            self._launch(seg, self.device, self.stream)
+        if events:
+            events[1].record(self.stream)
+        return act, new_res, moves, stats
+
+    def finish(self, pending) -> ReshardStats:
+        """After the barrier: flip rebuilt GPUs to their new arena."""
+        act, new_res, moves, stats = pending
+        for g in self.gpu_ids:
+            if moves[g]:
+                self.cur[g] ^= 1
+        self.resident = new_res
+        self.active = act
+        self._views()
+        return stats
+
+    def reshard(self, new_groups, stream=None, events=None, parked=()) -> ReshardStats:
+        pending = self.launch(new_groups, parked, events)
+        self.stream.synchronize()
+        dist.barrier(group=self.group)
+        return self.finish(pending)
+
+    def verify(self, stream=None) -> int:
+        saved = self.gpu_ids
+        try:
+            self.gpu_ids = (self.me,)
+            return super().verify(stream)
+        finally:
+            self.gpu_ids = saved
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        for g, ptrs in self.peer_bufs.items():
+            if g != self.me:
+                for p in ptrs:
+                    _native.call("tpr_ipc_close", p)
+        dist.barrier(group=self.group)
+        self.arena = {}
+        for b in self.bufs:
+            b.free()
+
+
+class DistributedExecutor:
+    """One-process-per-GPU TP switch: handshake, this rank's K3 + K1 push on
+    one stream and its K2 pull on another, one barrier, commit."""
+
+    def __init__(self, kv: DistributedKvCluster, weights: DistributedWeightStore | None = None):
+        self.kv = kv
+        self.weights = weights
+
+    def switch(self, old_layouts, new_layouts, new_weight_groups=None, parked=(),
+               k1_events=None, k2_events=None):
+        import time
+        t0 = time.perf_counter()
+        plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
+        kv_pending = self.kv.launch(plan, k1_events)
+        w_pending = None
+        if self.weights is not None and new_weight_groups is not None:
+            w_pending = self.weights.launch(new_weight_groups, parked, k2_events)
+        self.kv.stream.synchronize()
+        if self.weights is not None:
+            self.weights.stream.synchronize()
+        dist.barrier(group=self.kv.group)
+        kv_stats = self.kv.finish(plan, kv_pending)
+        w_stats = self.weights.finish(w_pending) if w_pending is not None else None
+        return plan, kv_stats, w_stats, (time.perf_counter() - t0) * 1e3
+
+
+__all__ = ["DistributedKvCluster", "DistributedWeightStore", "DistributedExecutor", "DeviceBuffer",
+           "handshake", "ring_deltas", "my_units", "plan_digest", "units_per_record", "KvLayout"]

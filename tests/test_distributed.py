@@ -99,6 +99,65 @@ def _gpu_worker(rank, world, path, outdir, q):
         q.put((rank, traceback.format_exc(), -1))
 
 
+def _exec_worker(rank, world, path, q):
+    import sys
+    sys.path.insert(0, str(ROOT))
+    try:
+        from paper_2605_05467_b200 import geometry, migration as M, workloads
+        from paper_2605_05467_b200.distributed import (DistributedExecutor, DistributedKvCluster,
+                                                       DistributedWeightStore)
+        _init(rank, world, path)
+        torch.cuda.set_device(0)
+        model = geometry.tiny_geometry()
+        gpus = tuple(range(world))
+        reqs = [(i, 9 + 17 * i) for i in range(6)]
+        tps = [t for t in (1, 2, 4) if t <= world]
+        lays = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in tps}
+        dev = torch.device("cuda", 0)
+        kv = DistributedKvCluster(model.kv, gpus, units_per_gpu=512, max_requests=8, max_blocks=16,
+                                  device=dev, fragmented=True, seed=rank)
+        kv.admit(lays[1], seed=5)
+        ws = DistributedWeightStore(model, gpus, device=dev)
+        ws.load(workloads.tp_groups(gpus, 1))
+        ex = DistributedExecutor(kv, ws)
+        seq = [1, 2, 1] if world == 2 else [1, 2, 4, 2, 4, 1]
+        results = []
+        for a, b in zip(seq, seq[1:]):
+            plan, ks, wst, ms = ex.switch(lays[a], lays[b], new_weight_groups=workloads.tp_groups(gpus, b))
+            results.append((a, b, ks.bytes, wst.local_bytes, wst.remote_bytes, wst.views))
+            assert ws.verify() == 0, (a, b)
+        v = kv.verify()
+        bad_w = ws.verify()
+        ws.close()
+        kv.close()
+        dist.destroy_process_group()
+        q.put((rank, v, bad_w, results))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc(), -1, None))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_executor_kv_and_weights(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "store")
+        procs = [ctx.Process(target=_exec_worker, args=(r, world, path, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        res = sorted((q.get(timeout=300) for _ in procs), key=lambda x: x[0])
+        for p in procs:
+            p.join(timeout=60)
+    for rank, v, bad_w, results in res:
+        assert results is not None, v
+        assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0, v
+        assert bad_w == 0
+    # every rank computed the same global stats for every switch
+    assert all(r[3] == res[0][3] for r in res)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 4])
 def test_multiprocess_push_migration_bit_exact(world):

@@ -28,9 +28,12 @@ def main():
     ap.add_argument("--n", type=int, default=300)
     ap.add_argument("--config", type=int, default=0)
     args = ap.parse_args()
+    import bench
+
     w = workloads.config(args.config, weights=False) if args.config else workloads.config(0)
     kv = w.model.kv
-    c = PagedKvCluster(kv, w.gpus, units_per_gpu=4096, max_requests=len(w.requests),
+    c = PagedKvCluster(kv, w.gpus, units_per_gpu=bench.capacity_units(w, kv),
+                       max_requests=len(w.requests),
                        max_blocks=kv.blocks(max(x for _, x in w.requests)))
     c.admit(w.old)
     ex = ReconfigurationExecutor(c)
