@@ -13,9 +13,12 @@ live in one B200's HBM (the 1-GPU mode: every byte is an HBM read + write).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N>1) every rank runs the same workload on its own GPU
-(replicas: the cross-GPU P2P path is not exercised by this harness yet) and
-rank 0 prints value = bytes moved by all ranks / max-over-ranks time.
+Under torchrun (N>1) there is one process per GPU slot and the switch is real
+and cross-GPU: TP(N/2) <-> TP(N) over the N GPUs (16 seqs x 4096 per GPU, so
+per-GPU work is fixed: weak scaling). KV pages are pushed and weight slices
+pulled through CUDA-IPC peer mappings, with device-side barriers over IPC
+flags. Rank 0 prints value = bytes moved by all ranks / max-over-ranks device
+time. (On a box with fewer GPUs than ranks, ranks share devices.)
 """
 
 from __future__ import annotations
@@ -409,6 +412,7 @@ def run_distributed(args, w, rank: int, world: int, local: int):
     v2 = ws.verify()
     ok = torch.tensor([int(v1["placement_errors"] == 0 and v1["word_mismatches"] == 0 and v2 == 0)])
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    ex.close()
     ws.close()
     cl.close()
     dist.destroy_process_group()

@@ -192,6 +192,15 @@ int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch_el
                       int64_t row0, int64_t col0, int64_t full_cols, uint64_t key,
                       int32_t elem_bytes, int64_t* d_mismatch, void* stream);
 
+/* ---- device-side barrier (one process per GPU) ------------------------ */
+/* Stream-ordered barrier across `world` ranks without a host collective:
+ * rank `rank` stores `epoch` into slot [rank] of every rank's flag array
+ * (peer_flags[r] = device VA of rank r's uint64 [world] array, IPC-mapped;
+ * release semantics at system scope), then spins until every slot of its own
+ * array (peer_flags[rank]) reaches `epoch` (acquire). Epochs must increase. */
+int tpr_device_barrier(const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch,
+                       void* stream);
+
 /* ---- peer memory (one process per GPU) -------------------------------- */
 /* Whole-allocation device memory (cudaMalloc): the pointer is the allocation
  * base, so its IPC handle maps exactly this buffer in a peer process. */

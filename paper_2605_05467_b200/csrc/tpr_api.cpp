@@ -358,6 +358,14 @@ int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch, i
 // ---------------------------------------------------------------------------
 // Peer memory
 // ---------------------------------------------------------------------------
+int tpr_device_barrier(const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch,
+                       void* stream) {
+  if (!peer_flags || world <= 0 || world > TPR_MAX_GPUS || rank < 0 || rank >= world)
+    return fail(TPR_EINVAL, "bad barrier arguments (rank %d, world %d)", rank, world);
+  cudaError_t e = tpr::launch_barrier(peer_flags, rank, world, epoch, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_device_barrier launch");
+}
+
 int tpr_device_alloc(uint64_t bytes, uint64_t* dptr) {
   if (!dptr) return fail(TPR_EINVAL, "null output pointer");
   void* p = nullptr;

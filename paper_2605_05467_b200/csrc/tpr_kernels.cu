@@ -431,6 +431,34 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device barrier over IPC-mapped flag arrays: lane r signals rank r, then
+// lane r waits for rank r's signal in the local array.
+// ---------------------------------------------------------------------------
+struct BarrierParams {
+  uint64_t flags[TPR_MAX_GPUS];
+};
+
+__global__ void tpr_barrier_kernel(BarrierParams p, int32_t rank, int32_t world, uint64_t epoch) {
+  const int lane = threadIdx.x;
+  // order every store this stream issued before (K1 pushes into peer pools,
+  // K3 block-table writes) ahead of the signal, at system scope
+  __threadfence_system();
+  if (lane < world) {
+    unsigned long long* peer = reinterpret_cast<unsigned long long*>(p.flags[lane]) + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer), "l"(epoch) : "memory");
+    const unsigned long long* mine =
+        reinterpret_cast<const unsigned long long*>(p.flags[rank]) + lane;
+    unsigned long long v = 0;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+}
+
 }  // namespace tpr
 
 // ===========================================================================
@@ -506,6 +534,14 @@ cudaError_t launch_kv_verify(const tpr_kv_geometry_t& geo, const KvCopyParams& p
                              unsigned long long* counts, cudaStream_t st) {
   tpr_kv_verify_kernel<<<sm_count() * 8, 256, 0, st>>>(geo, p, pool, bt, ctx, owner, slot, seed,
                                                        counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_barrier(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch,
+                           cudaStream_t st) {
+  BarrierParams p{};
+  for (int i = 0; i < world; ++i) p.flags[i] = flags[i];
+  tpr_barrier_kernel<<<1, 32, 0, st>>>(p, rank, world, epoch);
   return cudaGetLastError();
 }
 

@@ -280,11 +280,15 @@ class DistributedKvCluster:
         dist.barrier(group=self.group)  # every page has landed everywhere
         return self.finish(plan, pending)
 
-    def launch(self, plan: MigrationPlan, k1_events=None):
-        """Handshake, then enqueue this rank's K3 + K1 on ``self.stream``."""
+    def launch(self, plan: MigrationPlan, k1_events=None, host_handshake: bool = True):
+        """Handshake, then enqueue this rank's K3 + K1 on ``self.stream``.
+
+        With ``host_handshake=False`` the caller provides the start barrier on
+        the stream (DeviceBarrier) and no host collective runs."""
         rec = self.records(plan)
         in_u, out_u = self._advance(rec)
-        handshake(rec, self.ring_head, self.ring_tail, self.group)  # also the start barrier
+        if host_handshake:
+            handshake(rec, self.ring_head, self.ring_tail, self.group)  # also the start barrier
         n = my_units(rec, self.slot, self.kv.block_tokens)
         if n:
             cl = self._run_k3(rec, self.slot, n, want_ext=False)
@@ -487,30 +491,92 @@ class DistributedWeightStore(ShardedWeightStore):
             b.free()
 
 
-class DistributedExecutor:
-    """One-process-per-GPU TP switch: handshake, this rank's K3 + K1 push on
-    one stream and its K2 pull on another, one barrier, commit."""
+class DeviceBarrier:
+    """Stream-ordered barrier across the group through IPC-mapped flags
+    (``tpr_device_barrier``): no host collective on the switch path."""
 
-    def __init__(self, kv: DistributedKvCluster, weights: DistributedWeightStore | None = None):
+    def __init__(self, device: torch.device, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.flags = DeviceBuffer(8 * self.world, torch.device(device))
+        self.flags.tensor.zero_()
+        torch.cuda.synchronize(device)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, self.flags.handle(), group=group)
+        ptrs = [self.flags.ptr if r == self.rank else open_peer(h) for r, h in enumerate(allh)]
+        self._peers = ptrs
+        self.ptrs = (ctypes.c_uint64 * self.world)(*ptrs)
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def __call__(self, stream: torch.cuda.Stream) -> None:
+        self.epoch += 1
+        _native.call("tpr_device_barrier", self.ptrs, self.rank, self.world, self.epoch,
+                     stream.cuda_stream)
+
+    def close(self):
+        dist.barrier(group=self.group)
+        for r, p in enumerate(self._peers):
+            if r != self.rank:
+                _native.call("tpr_ipc_close", p)
+        dist.barrier(group=self.group)
+        self.flags.free()
+
+
+class DistributedExecutor:
+    """One-process-per-GPU TP switch: start barrier, this rank's K3 + K1 push
+    on one stream and its K2 pull on another, end barrier, commit.
+
+    ``device_barrier=True`` (default) runs both barriers as tiny kernels over
+    IPC-mapped flags, so a switch costs no host collective; the metadata
+    handshake (plan digest + ring counters, an all-gather) is then optional
+    (``check_every`` switches, 0 = never)."""
+
+    def __init__(self, kv: DistributedKvCluster, weights: DistributedWeightStore | None = None,
+                 device_barrier: bool = True, check_every: int = 0):
         self.kv = kv
         self.weights = weights
+        self.barrier = DeviceBarrier(kv.device, kv.group) if device_barrier else None
+        self.check_every = check_every
+        self.n = 0
 
     def switch(self, old_layouts, new_layouts, new_weight_groups=None, parked=(),
                k1_events=None, k2_events=None):
         import time
         t0 = time.perf_counter()
+        self.n += 1
         plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
-        kv_pending = self.kv.launch(plan, k1_events)
+        kst = self.kv.stream
+        wst = self.weights.stream if self.weights is not None else None
+        if self.barrier is None:
+            kv_pending = self.kv.launch(plan, k1_events)
+        else:
+            if self.check_every and self.n % self.check_every == 0:
+                handshake(self.kv.records(plan), self.kv.ring_head, self.kv.ring_tail, self.kv.group)
+            self.barrier(kst)  # every rank is here: peers' pools / tables / rings are quiescent
+            kv_pending = self.kv.launch(plan, k1_events, host_handshake=False)
         w_pending = None
         if self.weights is not None and new_weight_groups is not None:
+            wst.wait_stream(kst)
             w_pending = self.weights.launch(new_weight_groups, parked, k2_events)
-        self.kv.stream.synchronize()
-        if self.weights is not None:
-            self.weights.stream.synchronize()
-        dist.barrier(group=self.kv.group)
+        if self.barrier is None:
+            kst.synchronize()
+            if wst is not None:
+                wst.synchronize()
+            dist.barrier(group=self.kv.group)
+        else:
+            if wst is not None:
+                kst.wait_stream(wst)
+            self.barrier(kst)  # every rank's pushes and pulls have completed
+            kst.synchronize()
         kv_stats = self.kv.finish(plan, kv_pending)
         w_stats = self.weights.finish(w_pending) if w_pending is not None else None
         return plan, kv_stats, w_stats, (time.perf_counter() - t0) * 1e3
+
+    def close(self):
+        if self.barrier is not None:
+            self.barrier.close()
 
 
 __all__ = ["DistributedKvCluster", "DistributedWeightStore", "DistributedExecutor", "DeviceBuffer",

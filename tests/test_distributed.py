@@ -99,7 +99,7 @@ def _gpu_worker(rank, world, path, outdir, q):
         q.put((rank, traceback.format_exc(), -1))
 
 
-def _exec_worker(rank, world, path, q):
+def _exec_worker(rank, world, path, q, device_barrier=True):
     import sys
     sys.path.insert(0, str(ROOT))
     try:
@@ -119,7 +119,7 @@ def _exec_worker(rank, world, path, q):
         kv.admit(lays[1], seed=5)
         ws = DistributedWeightStore(model, gpus, device=dev)
         ws.load(workloads.tp_groups(gpus, 1))
-        ex = DistributedExecutor(kv, ws)
+        ex = DistributedExecutor(kv, ws, device_barrier=device_barrier, check_every=2)
         seq = [1, 2, 1] if world == 2 else [1, 2, 4, 2, 4, 1]
         results = []
         for a, b in zip(seq, seq[1:]):
@@ -128,6 +128,7 @@ def _exec_worker(rank, world, path, q):
             assert ws.verify() == 0, (a, b)
         v = kv.verify()
         bad_w = ws.verify()
+        ex.close()
         ws.close()
         kv.close()
         dist.destroy_process_group()
@@ -138,13 +139,14 @@ def _exec_worker(rank, world, path, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 4])
-def test_distributed_executor_kv_and_weights(world):
+@pytest.mark.parametrize("world,device_barrier", [(2, True), (4, True), (2, False)])
+def test_distributed_executor_kv_and_weights(world, device_barrier):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with tempfile.TemporaryDirectory() as d:
         path = os.path.join(d, "store")
-        procs = [ctx.Process(target=_exec_worker, args=(r, world, path, q)) for r in range(world)]
+        procs = [ctx.Process(target=_exec_worker, args=(r, world, path, q, device_barrier),
+                             daemon=True) for r in range(world)]
         for p in procs:
             p.start()
         res = sorted((q.get(timeout=300) for _ in procs), key=lambda x: x[0])
@@ -166,7 +168,8 @@ def test_multiprocess_push_migration_bit_exact(world):
     q = ctx.Queue()
     with tempfile.TemporaryDirectory() as d:
         path = os.path.join(d, "store")
-        procs = [ctx.Process(target=_gpu_worker, args=(r, world, path, d, q)) for r in range(world)]
+        procs = [ctx.Process(target=_gpu_worker, args=(r, world, path, d, q), daemon=True)
+                 for r in range(world)]
         for p in procs:
             p.start()
         res = sorted((q.get(timeout=300) for _ in procs), key=lambda x: x[0])
