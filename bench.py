@@ -371,7 +371,9 @@ def run_distributed(args, w, rank: int, world: int, local: int):
     slices = max(8 // len(g) for g in (w.old_weight_groups or [()]) + (w.new_weight_groups or [()]) if g)
     ws = DistributedWeightStore(w.model, w.gpus, device=device, max_slices=slices)
     ws.load(w.old_weight_groups)
-    ex = DistributedExecutor(cl, ws)
+    # ranks sharing one device are time-sliced, so a spinning device barrier
+    # would wait for a context switch; use the host barrier there
+    ex = DistributedExecutor(cl, ws, device_barrier=n_dev >= world)
 
     def step(fwd):
         if fwd:
@@ -457,7 +459,12 @@ def main():
     ap.add_argument("--cpu-sample-seqs", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--engine", choices=("vector", "bulk"), default=None,
+                    help="K1/K2 copy engine (default: the library default)")
     args = ap.parse_args()
+    if args.engine and args.impl == "ours":
+        from paper_2605_05467_b200 import _native
+        _native.set_copy_engine(args.engine)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -94,6 +94,13 @@ typedef struct tpr_kv_cluster {
 #define TPR_TOTALS_LEN (1 + 2 * TPR_MAX_GPUS)
 
 /* ---- host utilities -------------------------------------------------- */
+/* Copy engine of K1 and K2 (process-wide): TPR_ENGINE_VECTOR = warp-wide
+ * 16-B ld/st (default), TPR_ENGINE_BULK = TMA cp.async.bulk through shared
+ * memory, one issuing thread per CTA. */
+#define TPR_ENGINE_VECTOR 0
+#define TPR_ENGINE_BULK 1
+int tpr_set_copy_engine(int32_t engine);
+int tpr_get_copy_engine(void);
 int tpr_version(void);
 const char* tpr_last_error(void);
 int tpr_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);

@@ -23,6 +23,7 @@ TPR_STATUS_DST_OCCUPIED = 2
 
 # Every exported symbol of include/tpr.h; tests check the library exports all.
 EXPORTS = (
+    "tpr_set_copy_engine", "tpr_get_copy_engine",
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads",
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_switch", "tpr_memcpy_h2d",
     "tpr_copy_prepare", "tpr_weight_reshard",
@@ -72,6 +73,8 @@ _P64 = POINTER(c_int64)
 _P32 = POINTER(c_int32)
 
 _SIGNATURES = {
+    "tpr_set_copy_engine": (c_int32, [c_int32]),
+    "tpr_get_copy_engine": (c_int32, []),
     "tpr_version": (c_int32, []),
     "tpr_last_error": (c_char_p, []),
     "tpr_device_info": (c_int32, [_P32, _P32, _P32]),
@@ -133,6 +136,21 @@ def load() -> ctypes.CDLL:
         )
     _lib = lib
     return lib
+
+
+ENGINES = {"vector": 0, "bulk": 1}
+
+
+def set_copy_engine(name: str) -> None:
+    """K1/K2 copy engine: "vector" (16-B ld/st, default) or "bulk" (TMA)."""
+    if name not in ENGINES:
+        raise ValueError(f"unknown copy engine {name!r}; choose from {sorted(ENGINES)}")
+    call("tpr_set_copy_engine", ENGINES[name])
+
+
+def copy_engine() -> str:
+    v = load().tpr_get_copy_engine()
+    return next(k for k, e in ENGINES.items() if e == v)
 
 
 def check(rc: int, what: str) -> None:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -75,6 +76,21 @@ int cluster_params(const tpr_kv_cluster_t* cl, const tpr_kv_geometry_t* geo,
   return TPR_OK;
 }
 
+std::atomic<int> g_engine{TPR_ENGINE_VECTOR};
+
+cudaError_t run_k1(const tpr::KvCopyParams& p, const tpr::KvClusterParams& cl, const int4* work,
+                   int64_t n, cudaStream_t st) {
+  return g_engine.load() == TPR_ENGINE_BULK ? tpr::launch_k1_bulk(p, cl, work, n, st)
+                                            : tpr::launch_k1(p, cl, work, n, st);
+}
+
+cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
+                   int64_t n_items, int64_t chunk, cudaStream_t st) {
+  return g_engine.load() == TPR_ENGINE_BULK
+             ? tpr::launch_k2_bulk(segs, prefix, n_segs, n_items, chunk, st)
+             : tpr::launch_k2(segs, prefix, n_segs, n_items, chunk, st);
+}
+
 }  // namespace
 
 namespace tpr {
@@ -96,6 +112,15 @@ int sm_count() {
 extern "C" {
 
 int tpr_version(void) { return TPR_ABI_VERSION; }
+
+int tpr_set_copy_engine(int32_t engine) {
+  if (engine != TPR_ENGINE_VECTOR && engine != TPR_ENGINE_BULK)
+    return fail(TPR_EINVAL, "unknown copy engine %d", engine);
+  g_engine.store(engine);
+  return TPR_OK;
+}
+
+int tpr_get_copy_engine(void) { return g_engine.load(); }
 
 const char* tpr_last_error(void) { return g_err.c_str(); }
 
@@ -208,7 +233,7 @@ int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, con
   if ((rc = cluster_params(cl, geo, &cp))) return rc;
   if (n_units < 0) return fail(TPR_EINVAL, "n_units < 0");
   if (n_units > 0 && !d_work) return fail(TPR_EINVAL, "null work list");
-  cudaError_t e = tpr::launch_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
+  cudaError_t e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
                                  n_units, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_migrate launch");
 }
@@ -236,7 +261,7 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, cons
   e = tpr::launch_k3(*geo, cp, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
                      reinterpret_cast<int4*>(d_work), nullptr, d_status, st);
   if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
-  e = tpr::launch_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st);
+  e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st);
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_switch K1");
 }
 
@@ -288,7 +313,7 @@ int tpr_weight_reshard(const tpr_copy_seg_t* d_segs, const int64_t* d_prefix, in
   if (n_segs < 0 || n_items < 0 || chunk <= 0) return fail(TPR_EINVAL, "bad reshard arguments");
   if (n_items == 0) return TPR_OK;
   if (!d_segs || !d_prefix) return fail(TPR_EINVAL, "null segment buffers");
-  cudaError_t e = tpr::launch_k2(d_segs, d_prefix, n_segs, n_items, chunk,
+  cudaError_t e = run_k2(d_segs, d_prefix, n_segs, n_items, chunk,
                                  static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_weight_reshard launch");
 }

@@ -1,0 +1,317 @@
+// TMA bulk-copy engine for K1 / K2 (sm_100a): global -> shared -> global with
+// cp.async.bulk, an mbarrier per shared-memory stage and bulk-group
+// completion tracking. One elected thread per CTA issues every copy, so the
+// SMs spend almost no instructions on data movement; the copy engine moves the
+// bytes. Pieces are <= kPiece bytes, 16-B aligned, multiples of 16 B.
+//
+// Pipeline per CTA (S stages, lookahead L = S - 2 loads in flight):
+//   load piece j+L into stage (j+L)%S once the store that last read that
+//   stage (piece j-2) has finished reading shared memory
+//   (cp.async.bulk.wait_group.read 1); wait for piece j's load (mbarrier
+//   parity); store piece j; commit its bulk group.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tpr.h"
+#include "tpr_common.cuh"
+#include "tpr_internal.h"
+
+namespace tpr {
+
+constexpr int kStages = 6;
+constexpr int kLookahead = kStages - 2;
+constexpr uint32_t kPiece = 16384;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst_smem, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_smem),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(src_smem), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---- piece sources ---------------------------------------------------------
+
+// K1: the CTA's work items (grid-stride) -> pieces. A full page item is one
+// contiguous span cut into kPiece pieces; a partial page item is one piece
+// per plane row (ntok valid tokens).
+struct KvPieces {
+  const int4* work;
+  int64_t n_items;
+  KvCopyParams p;
+  const KvClusterParams* cl;  // the kernel's __grid_constant__ parameter
+  int64_t item;
+  // current item
+  const char* s;
+  char* d;
+  int64_t rows_left, row_bytes, pitch, off;
+
+  __device__ void start(int64_t first) {
+    item = first;
+    rows_left = 0;
+  }
+  __device__ bool load_item() {
+    while (item < n_items) {
+      const int64_t u = item / p.items_per_unit;
+      const int g = (int)(item - u * p.items_per_unit);
+      item += gridDim.x;
+      const int4 w = work[u];
+      const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
+      const int row0 = g * p.rows_per_item;
+      const int nr = min(p.rows_per_item, p.rows - row0);
+      s = reinterpret_cast<const char*>(cl->pool[src_slot]) + (int64_t)w.x * p.unit_bytes +
+          (int64_t)row0 * p.pitch;
+      d = reinterpret_cast<char*>(cl->pool[dst_slot]) + (int64_t)w.y * p.unit_bytes +
+          (int64_t)row0 * p.pitch;
+      const int64_t nb = (int64_t)ntok * p.tok_bytes;
+      if (nb == p.pitch) {  // contiguous planes
+        rows_left = 1;
+        row_bytes = nb * nr;
+      } else {
+        rows_left = nr;
+        row_bytes = nb;
+      }
+      pitch = p.pitch;
+      off = 0;
+      if (row_bytes > 0) return true;
+    }
+    return false;
+  }
+  __device__ bool next(const char*& src, char*& dst, uint32_t& nb) {
+    if (rows_left == 0 && !load_item()) return false;
+    const int64_t take = min((int64_t)kPiece, row_bytes - off);
+    src = s + off;
+    dst = d + off;
+    nb = (uint32_t)take;
+    off += take;
+    if (off == row_bytes) {
+      off = 0;
+      s += pitch;
+      d += pitch;
+      --rows_left;
+    }
+    return true;
+  }
+};
+
+// K2: the CTA's segment items (grid-stride over the same item space as the
+// vector engine) -> pieces.
+struct SegPieces {
+  const tpr_copy_seg_t* segs;
+  const int64_t* prefix;
+  int32_t n_segs;
+  int64_t n_items, chunk, item;
+  const char* s;
+  char* d;
+  int64_t rows_left, row_bytes, sp, dp, off;
+  bool aligned;
+
+  __device__ void start(int64_t first) {
+    item = first;
+    rows_left = 0;
+  }
+  __device__ bool load_item() {
+    while (item < n_items) {
+      if (!load_one()) continue;
+      if (aligned) return true;
+      // unaligned segment (never for the Llama geometries): plain byte copy by
+      // the issuing thread, then move on
+      for (int64_t r = 0; r < rows_left; ++r)
+        for (int64_t b = 0; b < row_bytes; ++b) d[r * dp + b] = s[r * sp + b];
+      rows_left = 0;
+    }
+    return false;
+  }
+  __device__ bool load_one() {
+    {
+      int lo = 0, hi = n_segs;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (prefix[mid] <= item) lo = mid; else hi = mid;
+      }
+      const tpr_copy_seg_t sg = segs[lo];
+      const int64_t k = item - prefix[lo];
+      item += gridDim.x;
+      int64_t r0, nr, b0, nb;
+      if (sg.row_bytes <= chunk) {
+        const int64_t rpi = chunk / sg.row_bytes;
+        r0 = k * rpi;
+        nr = min(rpi, sg.rows - r0);
+        b0 = 0;
+        nb = sg.row_bytes;
+      } else {
+        const int64_t ipr = (sg.row_bytes + chunk - 1) / chunk;
+        r0 = k / ipr;
+        nr = 1;
+        b0 = (k - r0 * ipr) * chunk;
+        nb = min(chunk, sg.row_bytes - b0);
+      }
+      s = reinterpret_cast<const char*>(sg.src) + r0 * sg.src_pitch + b0;
+      d = reinterpret_cast<char*>(sg.dst) + r0 * sg.dst_pitch + b0;
+      rows_left = nr;
+      row_bytes = nb;
+      sp = sg.src_pitch;
+      dp = sg.dst_pitch;
+      off = 0;
+      aligned = (sg.flags & TPR_SEG_ALIGNED16) != 0;
+      if (nr > 0 && nb > 0) return true;
+      rows_left = 0;
+    }
+    return false;
+  }
+  __device__ bool next(const char*& src, char*& dst, uint32_t& nb) {
+    if (rows_left == 0 && !load_item()) return false;
+    const int64_t take = min((int64_t)kPiece, row_bytes - off);
+    src = s + off;
+    dst = d + off;
+    nb = (uint32_t)take;
+    off += take;
+    if (off == row_bytes) {
+      off = 0;
+      s += sp;
+      d += dp;
+      --rows_left;
+    }
+    return true;
+  }
+};
+
+template <class Source>
+__device__ __forceinline__ void bulk_pipeline(Source& src_it) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar[kStages];
+  __shared__ char* pdst[kStages];
+  __shared__ uint32_t pnb[kStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kStages; ++s) bar_init(&bar[s]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint32_t base = smem_u32(smem);
+  int64_t issued = 0, stored = 0;
+  bool more = true;
+  auto issue = [&]() {
+    const char* s;
+    char* d;
+    uint32_t nb;
+    if (!src_it.next(s, d, nb)) {
+      more = false;
+      return;
+    }
+    const int t = (int)(issued % kStages);
+    if (issued >= kStages) bulk_wait_read_1();  // store of piece issued-S done reading
+    pdst[t] = d;
+    pnb[t] = nb;
+    bulk_load(base + (uint32_t)t * kPiece, s, nb, &bar[t]);
+    ++issued;
+  };
+  while (more && issued < kLookahead) issue();
+  while (stored < issued) {
+    if (more) issue();
+    const int t = (int)(stored % kStages);
+    bar_wait(&bar[t], (uint32_t)((stored / kStages) & 1));
+    bulk_store(pdst[t], base + (uint32_t)t * kPiece, pnb[t]);
+    ++stored;
+  }
+  bulk_wait_all();
+}
+
+__global__ void __launch_bounds__(32)
+    tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
+                           const __grid_constant__ KvClusterParams cl) {
+  KvPieces it;
+  it.work = work;
+  it.n_items = n_units * p.items_per_unit;
+  it.p = p;
+  it.cl = &cl;
+  it.start(blockIdx.x);
+  bulk_pipeline(it);
+}
+
+__global__ void __launch_bounds__(32)
+    tpr_k2_copy_segments_bulk(const tpr_copy_seg_t* __restrict__ segs,
+                              const int64_t* __restrict__ prefix, int32_t n_segs, int64_t n_items,
+                              int64_t chunk) {
+  SegPieces it;
+  it.segs = segs;
+  it.prefix = prefix;
+  it.n_segs = n_segs;
+  it.n_items = n_items;
+  it.chunk = chunk;
+  it.start(blockIdx.x);
+  bulk_pipeline(it);
+}
+
+static int bulk_grid(const void* fn, int64_t items) {
+  static const int smem = kStages * kPiece;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  if (items < grid) grid = items;
+  return grid < 1 ? 1 : (int)grid;
+}
+
+cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
+                           int64_t n_units, cudaStream_t st) {
+  if (n_units <= 0) return cudaSuccess;
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk),
+                             n_units * p.items_per_unit);
+  tpr_k1_kv_migrate_bulk<<<grid, 32, kStages * kPiece, st>>>(work, n_units, p, cl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
+                           int64_t n_items, int64_t chunk, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk), n_items);
+  tpr_k2_copy_segments_bulk<<<grid, 32, kStages * kPiece, st>>>(segs, prefix, n_segs, n_items,
+                                                                 chunk);
+  return cudaGetLastError();
+}
+
+}  // namespace tpr
