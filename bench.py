@@ -39,6 +39,11 @@ sys.path.insert(0, str(ROOT))
 METRIC = "TP-switch latency (ms) and KV+weight reshard GB/s vs NVLink/HBM roofline"
 
 
+def _engine_name() -> str:
+    from paper_2605_05467_b200 import _native
+    return _native.copy_engine()
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -154,7 +159,7 @@ def capacity_units(w, kv) -> dict:
     return {g: n + 64 for g, n in peak.items()}
 
 
-def setup_ours(w, device):
+def setup_ours(w, device, overlap=None):
     import torch
     from paper_2605_05467_b200.controller import ReconfigurationExecutor
     from paper_2605_05467_b200.kvcache import PagedKvCluster
@@ -171,7 +176,7 @@ def setup_ours(w, device):
         store = ShardedWeightStore(w.model, w.gpus, device=device)
         store.load(w.old_weight_groups)
     torch.cuda.synchronize()
-    return ReconfigurationExecutor(cluster, store, time_kernels=True)
+    return ReconfigurationExecutor(cluster, store, time_kernels=True, overlap=overlap)
 
 
 def one_switch(ex, w, forward: bool, sync: bool):
@@ -461,6 +466,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", choices=("vector", "bulk"), default=None,
                     help="K1/K2 copy engine (default: the library default)")
+    ap.add_argument("--overlap", choices=("auto", "on", "off"), default="auto",
+                    help="K1 || K2 on two streams (auto: only across devices)")
     args = ap.parse_args()
     if args.engine and args.impl == "ours":
         from paper_2605_05467_b200 import _native
@@ -502,7 +509,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    ex = setup_ours(w, device)
+    ex = setup_ours(w, device, overlap={"auto": None, "on": True, "off": False}[args.overlap])
     fwd = True
     for _ in range(max(args.warmup, 1)):
         one_switch(ex, w, fwd, sync=True)
@@ -592,7 +599,8 @@ def main():
         "config": {
             "workload": w.name, "model": w.model.name, "logical_gpus_per_device": len(w.gpus),
             "seqs": len(w.requests), "ctx": w.requests[0][1],
-            "switch": "alternating forward/reverse, full stop-and-migrate (plan+K3+K1||K2)",
+            "switch": "alternating forward/reverse, full stop-and-migrate (plan+K3+K1+K2)",
+            "k1_k2_overlap": ex.overlap, "copy_engine": _engine_name(),
             "kv_bytes_per_step": kv_per_step, "weight_bytes_per_step": w_bytes / args.steps,
             "l2": "inputs larger than L2 (>= 24 GiB moved per step)",
             "parallelism": "replicas" if world > 1 else "1 GPU, logical ranks",
@@ -600,7 +608,10 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "kernel": "tpr_k1_kv_migrate",
                      "k1_ms": k1_avg, "k2_ms": float(np.mean(k2_ms)) if k2_ms else None,
-                     "peak_source": hbm_src},
+                     "peak_source": hbm_src,
+                     # the whole switch (K3 + K1 + K2 + gaps): all bytes read + written
+                     "step_achieved": 2 * total_bytes / args.steps / (ms / args.steps * 1e-3) / 1e9,
+                     "step_frac": 2 * total_bytes / (ms * 1e-3) / 1e9 / hbm},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -43,14 +43,21 @@ class ReconfigurationExecutor:
     """Executes TP switches on a PagedKvCluster (+ optional ShardedWeightStore)."""
 
     def __init__(self, kv: PagedKvCluster, weights: ShardedWeightStore | None = None,
-                 handshake=None, time_kernels: bool = False):
+                 handshake=None, time_kernels: bool = False, overlap: bool | None = None):
         self.kv = kv
         self.weights = weights
         self.handshake = handshake  # callable(plan) for multi-process metadata exchange
         dev = kv.home
         self.device = dev
         self.kv_stream = torch.cuda.Stream(device=dev)
-        self.w_stream = torch.cuda.Stream(device=dev)
+        # K1 || K2 on two streams pays off when they use different links (KV
+        # pushes egress, weight pulls ingress). With every slot in one HBM both
+        # are bound by the same bandwidth, so by default they run back to back
+        # on one stream and each kernel streams at full rate.
+        if overlap is None:
+            overlap = not kv._single_device
+        self.overlap = overlap
+        self.w_stream = torch.cuda.Stream(device=dev) if overlap else self.kv_stream
         self.time_kernels = time_kernels
         self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.main_stream = torch.cuda.current_stream(dev)
