@@ -323,7 +323,18 @@ def cpu_model() -> str:
     return "unknown"
 
 
+CPU_SAMPLE_KV_BYTES = 4 << 30  # resident KV of the CPU sample (host RAM bound)
+
+
+def cpu_sample_seqs(w, requested: int) -> int:
+    """At most `requested` sequences and at most ~4 GiB of resident KV."""
+    kvb = w.model.kv.kv_bytes_per_token_per_head * w.model.n_kv_heads
+    per_seq = max(kvb * c for _, c in w.requests)
+    return max(1, min(requested, len(w.requests), CPU_SAMPLE_KV_BYTES // per_seq))
+
+
 def run_cpu_reference(w, steps: int, warmup: int, sample_seqs: int):
+    sample_seqs = cpu_sample_seqs(w, sample_seqs)
     threads = cpu_threads()
     ref = CpuReference(w, sample_seqs, threads)
     for _ in range(warmup):

@@ -21,6 +21,7 @@ import torch
 
 from .kvcache import MigrationStats, PagedKvCluster
 from .migration import KvLayout, MigrationPlan, head_transfers_array, plan_repartition
+from .tracing import nvtx
 from .weights import ReshardStats, ShardedWeightStore
 
 
@@ -78,18 +79,23 @@ class ReconfigurationExecutor:
         if self.time_kernels:
             for k in ("k1_start", "k1_end", "k2_start", "k2_end"):
                 ev[k] = torch.cuda.Event(enable_timing=True)
-        plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
+        with nvtx("plan"):
+            plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
         if self.handshake is not None:
-            self.handshake(plan)
+            with nvtx("handshake"):
+                self.handshake(plan)
         self.kv_stream.wait_stream(main)
-        kv_stats = self.kv.migrate(plan, stream=self.kv_stream, validate=validate,
-                                   k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
+        with nvtx("kv K3+K1"):
+            kv_stats = self.kv.migrate(
+                plan, stream=self.kv_stream, validate=validate,
+                k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
         w_stats = None
         if self.weights is not None and new_weight_groups is not None:
             self.w_stream.wait_stream(main)
-            w_stats = self.weights.reshard(
-                new_weight_groups, stream=self.w_stream, parked=parked,
-                events=(ev["k2_start"], ev["k2_end"]) if self.time_kernels else None)
+            with nvtx("weights K2"):
+                w_stats = self.weights.reshard(
+                    new_weight_groups, stream=self.w_stream, parked=parked,
+                    events=(ev["k2_start"], ev["k2_end"]) if self.time_kernels else None)
             main.wait_stream(self.w_stream)
         main.wait_stream(self.kv_stream)
         if sync:

@@ -77,4 +77,8 @@ def config(idx: int, **kw) -> Workload:
         return transition(LLAMA_3_1_70B, 8, 4, 8, kw.get("seqs", 8), kw.get("ctx", 32768),
                           weights=kw.get("weights", False),
                           name="cfg4 Llama-3.1-70B TP4->TP8 8x32768")
+    if idx == 4:  # the north star's headline: Llama-3.1-8B at 32k context, TP2 <-> TP4 + weights
+        return transition(LLAMA_3_1_8B, 4, 2, 4, kw.get("seqs", 8), kw.get("ctx", 32768),
+                          weights=kw.get("weights", True),
+                          name="headline Llama-3.1-8B TP2->TP4 8x32768 KV+weights")
     raise ValueError(idx)

@@ -32,6 +32,21 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
+@pytest.fixture(autouse=True)
+def _release_cuda_cache(request):
+    """Give cached device memory back after every GPU test, so the full-size
+    tests (up to ~150 GiB) find HBM free."""
+    yield
+    if "gpu" in request.keywords:
+        import gc
+
+        import torch
+        gc.collect()
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+
+
 @lru_cache(maxsize=1)
 def golden() -> dict:
     with gzip.open(GOLDEN, "rt") as f:

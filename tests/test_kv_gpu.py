@@ -56,6 +56,26 @@ def test_all_transitions_bit_exact(tp_old, tp_new, fragmented):
     assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
 
 
+@pytest.mark.parametrize("H,tp_old,tp_new", [(2, 1, 2), (2, 2, 1), (4, 4, 1), (4, 1, 4), (4, 2, 4),
+                                             (16, 8, 2), (16, 1, 8), (16, 4, 8), (16, 8, 1)])
+def test_head_counts_bit_exact(H, tp_old, tp_new):
+    # the AC-1 head counts (test_migration.py:115-121) beyond Llama's 8
+    kv = geometry.KvGeometry(layers=1, head_dim=16, total_heads=H)
+    n = max(tp_old, tp_new)
+    gpus = tuple(range(10, 10 + n))  # non-zero gpu ids exercise the id -> slot tables
+    rng = np.random.default_rng(H * 100 + tp_old * 10 + tp_new)
+    reqs = [(int(r), int(c)) for r, c in zip(rng.permutation(1000)[:9], rng.integers(1, 90, size=9))]
+    old = workloads.round_robin(workloads.tp_groups(gpus, tp_old), reqs, H)
+    new = workloads.round_robin(workloads.tp_groups(gpus, tp_new), reqs, H)
+    c = make(kv, gpus, units=1024, reqs=12, blocks=8)
+    c.admit(old, seed=6)
+    plan = M.plan_repartition(old, new, kv.kv_bytes_per_token_per_head)
+    migrate_and_compare(c, plan)
+    assert c.placement() == M.layout_placement(new)
+    v = c.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
 def test_chain_of_switches_and_back():
     gpus = (0, 1, 2, 3)
     reqs = [(i, 1 + 37 * i) for i in range(10)]  # ragged, incl. 1-token request
@@ -196,6 +216,26 @@ def test_cfg1_full_size_bit_exact():
     migrate_and_compare(c, plan)
     v = c.verify()
     assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
+@pytest.mark.slow
+def test_cfg4_70b_32k_full_size_property():
+    # BASELINE configs[3]: Llama-3.1-70B TP4 <-> TP8, 8 x 32768 tokens, 640 KiB pages;
+    # the largest single-B200 case (70 GiB moved per direction)
+    import bench
+    w = workloads.config(3)
+    kv = w.model.kv
+    c = PagedKvCluster(kv, w.gpus, units_per_gpu=bench.capacity_units(w, kv), max_requests=8,
+                       max_blocks=kv.blocks(32768), fragmented=True, seed=2)
+    c.admit(w.old, seed=8)
+    for a, b in ((w.old, w.new), (w.new, w.old)):
+        plan = M.plan_repartition(a, b, kv.kv_bytes_per_token_per_head)
+        assert plan.total_bytes == 70 * 2**30
+        c.migrate(plan)
+        v = c.verify()
+        assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
+        assert v["pages_checked"] == 8 * 8 * 2048
+        assert c.placement() == M.layout_placement(b)
 
 
 @pytest.mark.slow

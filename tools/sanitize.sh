@@ -1,0 +1,6 @@
+set -x
+export PYTHONDONTWRITEBYTECODE=1
+timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --error-exitcode 9 python __graft_entry__.py > gpurun_out/sanitize_memcheck_smoke.log 2>&1; echo rc=$? >> gpurun_out/sanitize_memcheck_smoke.log
+timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool racecheck --error-exitcode 9 python __graft_entry__.py > gpurun_out/sanitize_racecheck_smoke.log 2>&1; echo rc=$? >> gpurun_out/sanitize_racecheck_smoke.log
+timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_kv_gpu.py tests/test_bulk_engine_gpu.py tests/test_weights_gpu.py -q -x -k "not full_size and not cfg" > gpurun_out/sanitize_memcheck_tests.log 2>&1; echo rc=$? >> gpurun_out/sanitize_memcheck_tests.log
+timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool synccheck --error-exitcode 9 python __graft_entry__.py > gpurun_out/sanitize_synccheck_smoke.log 2>&1; echo rc=$? >> gpurun_out/sanitize_synccheck_smoke.log
