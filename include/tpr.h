@@ -199,6 +199,16 @@ int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch_el
                       int64_t row0, int64_t col0, int64_t full_cols, uint64_t key,
                       int32_t elem_bytes, int64_t* d_mismatch, void* stream);
 
+/* ---- library baselines (measurement only) ------------------------------ */
+/* The paper's straw-man ("cudaMemcpyAsync ... issue a
+ * separate request for each memory page"): copy n (src, dst, bytes) pages with
+ * one cudaMemcpyAsync each (method 0) or one cudaMemcpyBatchAsync (method 1).
+ * Arrays are host memory. */
+#define TPR_BASELINE_MEMCPY 0
+#define TPR_BASELINE_MEMCPY_BATCH 1
+int tpr_baseline_copy_pages(const uint64_t* src, const uint64_t* dst, const uint64_t* bytes,
+                            int64_t n, int32_t method, void* stream);
+
 /* ---- device-side barrier (one process per GPU) ------------------------ */
 /* Stream-ordered barrier across `world` ranks without a host collective:
  * rank `rank` stores `epoch` into slot [rank] of every rank's flag array

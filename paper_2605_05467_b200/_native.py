@@ -28,7 +28,8 @@ EXPORTS = (
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_switch", "tpr_memcpy_h2d",
     "tpr_copy_prepare", "tpr_weight_reshard",
     "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
-    "tpr_matrix_verify", "tpr_device_barrier", "tpr_device_alloc", "tpr_device_free",
+    "tpr_matrix_verify", "tpr_baseline_copy_pages", "tpr_device_barrier", "tpr_device_alloc",
+    "tpr_device_free",
     "tpr_enable_peer",
     "tpr_ipc_get_handle", "tpr_ipc_open", "tpr_ipc_close",
 )
@@ -100,6 +101,8 @@ _SIGNATURES = {
                                   c_int64, c_uint64, c_int32, c_void_p]),
     "tpr_matrix_verify": (c_int32, [c_uint64, c_int64, c_int64, c_int64, c_int64, c_int64,
                                     c_int64, c_uint64, c_int32, c_void_p, c_void_p]),
+    "tpr_baseline_copy_pages": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                          c_void_p]),
     "tpr_device_barrier": (c_int32, [c_void_p, c_int32, c_int32, c_uint64, c_void_p]),
     "tpr_device_alloc": (c_int32, [c_uint64, POINTER(c_uint64)]),
     "tpr_device_free": (c_int32, [c_uint64]),

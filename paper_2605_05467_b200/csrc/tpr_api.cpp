@@ -383,6 +383,44 @@ int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch, i
 // ---------------------------------------------------------------------------
 // Peer memory
 // ---------------------------------------------------------------------------
+int tpr_baseline_copy_pages(const uint64_t* src, const uint64_t* dst, const uint64_t* bytes,
+                            int64_t n, int32_t method, void* stream) {
+  if (n < 0 || (n > 0 && (!src || !dst || !bytes))) return fail(TPR_EINVAL, "bad page list");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (method == TPR_BASELINE_MEMCPY) {
+    for (int64_t i = 0; i < n; ++i) {
+      cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(dst[i]),
+                                      reinterpret_cast<const void*>(src[i]), bytes[i],
+                                      cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
+    }
+    return TPR_OK;
+  }
+  if (method == TPR_BASELINE_MEMCPY_BATCH) {
+#if CUDART_VERSION >= 12080
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0;
+    size_t fail_idx = 0;
+    const int64_t kMax = 1 << 20;  // the API takes size_t counts; chunk very long lists
+    for (int64_t off = 0; off < n; off += kMax) {
+      const size_t cnt = (size_t)std::min<int64_t>(kMax, n - off);
+      cudaError_t e = cudaMemcpyBatchAsync(
+          reinterpret_cast<void**>(const_cast<uint64_t*>(dst + off)),
+          reinterpret_cast<void**>(const_cast<uint64_t*>(src + off)),
+          reinterpret_cast<size_t*>(const_cast<uint64_t*>(bytes + off)), cnt, &attr, &attr_idx, 1,
+          &fail_idx, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyBatchAsync");
+    }
+    return TPR_OK;
+#else
+    return fail(TPR_EINVAL, "cudaMemcpyBatchAsync needs CUDA >= 12.8");
+#endif
+  }
+  return fail(TPR_EINVAL, "unknown baseline method %d", method);
+}
+
 int tpr_device_barrier(const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch,
                        void* stream) {
   if (!peer_flags || world <= 0 || world > TPR_MAX_GPUS || rank < 0 || rank >= world)
