@@ -398,6 +398,8 @@ int tpr_baseline_copy_pages(const uint64_t* src, const uint64_t* dst, const uint
   }
   if (method == TPR_BASELINE_MEMCPY_BATCH) {
 #if CUDART_VERSION >= 12080
+    if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread)
+      return fail(TPR_EINVAL, "cudaMemcpyBatchAsync needs an explicitly created stream");
     cudaMemcpyAttributes attr{};
     attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
     attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;

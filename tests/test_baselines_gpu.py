@@ -18,8 +18,10 @@ def test_baseline_copy_pages(method):
     s = np.ascontiguousarray(src.data_ptr() + offs, dtype=np.uint64)
     d = np.ascontiguousarray(dst.data_ptr() + offs[::-1].copy(), dtype=np.uint64)
     b = np.full(len(offs), 4096, np.uint64)
+    side = torch.cuda.Stream()  # the batch API refuses the legacy default stream
+    side.wait_stream(torch.cuda.current_stream())
     _native.call("tpr_baseline_copy_pages", s.ctypes.data, d.ctypes.data, b.ctypes.data, len(s),
-                 method, torch.cuda.current_stream().cuda_stream)
+                 method, side.cuda_stream)
     torch.cuda.synchronize()
     hs, hd = src.cpu().numpy(), dst.cpu().numpy()
     for so, do in zip(offs, offs[::-1]):

@@ -47,7 +47,8 @@ def main():
     args = ap.parse_args()
     kv = LLAMA_3_1_8B.kv
     H = kv.total_heads
-    st = torch.cuda.current_stream()
+    st = torch.cuda.Stream()  # explicit stream: cudaMemcpyBatchAsync refuses the legacy one
+    torch.cuda.set_stream(st)
     out = open(args.out, "w")
     for fragmented in (True, False):
         for tokens in map(int, args.tokens.split(",")):
