@@ -376,7 +376,11 @@ def run_distributed(args, w, rank: int, world: int, local: int):
     n_dev = torch.cuda.device_count()
     device = torch.device("cuda", local % n_dev)
     torch.cuda.set_device(device)
-    dist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
+    # NCCL carries the control plane (IPC-handle exchange, optional handshake)
+    # when every rank has its own GPU; ranks that share a device use gloo
+    backend = "nccl" if n_dev >= world else "gloo"
+    dist.init_process_group(backend, timeout=datetime.timedelta(minutes=10),
+                            **({"device_id": device} if backend == "nccl" else {}))
     kv = w.model.kv
     units = capacity_units(w, kv)
     max_ctx = max(c for _, c in w.requests)
@@ -400,7 +404,7 @@ def run_distributed(args, w, rank: int, world: int, local: int):
     for _ in range(max(args.warmup, 1)):
         step(fwd)
         fwd = not fwd
-    dev_ms, wall_ms, kv_bytes, w_bytes, k1 = 0.0, [], 0, 0, []
+    dev_ms, wall_ms, kv_bytes, w_bytes, k1, h2d = 0.0, [], 0, 0, [], 0
     with ClockSampler(device.index) as clk:
         dist.barrier()
         clk.start()
@@ -420,15 +424,18 @@ def run_distributed(args, w, rank: int, world: int, local: int):
             wall_ms.append(ms)
             kv_bytes += ks.bytes
             w_bytes += wst.bytes if wst else 0
+            h2d += len(plan) * 24 + (wst.segments * 72 + 8 if wst and wst.segments else 0)
         wall = time.perf_counter() - t0
         clk.stop()
         dist.barrier()
-    t = torch.tensor([dev_ms, wall], dtype=torch.float64)
+    cdev = device if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([dev_ms, wall], dtype=torch.float64, device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms, wall = float(t[0]), float(t[1])
     v1 = cl.verify()
     v2 = ws.verify()
-    ok = torch.tensor([int(v1["placement_errors"] == 0 and v1["word_mismatches"] == 0 and v2 == 0)])
+    ok = torch.tensor([int(v1["placement_errors"] == 0 and v1["word_mismatches"] == 0 and v2 == 0)],
+                      device=cdev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     ex.close()
     ws.close()
@@ -453,7 +460,7 @@ def run_distributed(args, w, rank: int, world: int, local: int):
                      "k1_ms_rank0": float(np.mean(k1)), "peak_hbm": hbm, "peak_source": src},
         "clocks": clk.summary(),
         "e2e": {"value": total / wall / 1e9, "unit": "GB/s", "ms_per_step": wall / args.steps * 1e3,
-                "h2d_bytes_per_step": None, "d2h_bytes_per_step": 0},
+                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": 0},
         "gpu_launches": args.steps * 4,
         "bit_exact_property": bool(ok.item()),
     }
