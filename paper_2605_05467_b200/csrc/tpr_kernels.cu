@@ -285,19 +285,14 @@ __global__ void __launch_bounds__(kCopyThreads)
   const unsigned lane = threadIdx.x & 31u;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // each warp owns a contiguous run of items: one binary search, then the
-  // segment cursor only moves forward
-  const int64_t per = (n_items + nwarps - 1) / nwarps;
-  const int64_t first = gwarp * per;
-  const int64_t last = min(n_items, first + per);
-  if (first >= last) return;
-  int lo = 0, hi = n_segs;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (prefix[mid] <= first) lo = mid; else hi = mid;
-  }
-  for (int64_t item = first; item < last; ++item) {
-    while (prefix[lo + 1] <= item) ++lo;
+  // items are dealt round-robin over warps: neighbouring warps stream
+  // neighbouring chunks (measured faster than contiguous runs per warp)
+  for (int64_t item = gwarp; item < n_items; item += nwarps) {
+    int lo = 0, hi = n_segs;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (prefix[mid] <= item) lo = mid; else hi = mid;
+    }
     const tpr_copy_seg_t sg = segs[lo];
     const int64_t k = item - prefix[lo];
     int64_t r0, nr, b0, nb;
