@@ -28,6 +28,7 @@ switch is then views only (the paper's zero-overhead weight switching).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -38,7 +39,7 @@ from . import _native
 from .geometry import MAX_TP, MatrixSpec, ModelGeometry
 from .migration import MigrationError
 
-CHUNK_BYTES = 32 * 1024  # K2 work-item size
+CHUNK_BYTES = int(os.environ.get("TPR_K2_CHUNK", 32 * 1024))  # K2 work-item size (bytes)
 
 
 @dataclass

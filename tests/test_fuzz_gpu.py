@@ -1,0 +1,106 @@
+"""Random walks over the block manager on B200, every step checked against
+the oracle replay: admissions, releases, and TP switches between random
+partitions of 8 GPU slots (mixed TP levels in one config), with pools small
+enough that capacity errors happen. A rejected operation must leave device
+state untouched."""
+
+import numpy as np
+import pytest
+
+from oracle import check
+from paper_2605_05467_b200 import geometry, migration as M
+from paper_2605_05467_b200.kvcache import PagedKvCluster
+
+pytestmark = pytest.mark.gpu
+
+KV = geometry.KvGeometry(layers=1, head_dim=16, total_heads=8, block_tokens=4)
+GPUS = tuple(range(8))
+
+
+def random_groups(rng):
+    gpus = list(rng.permutation(GPUS))
+    out, i = [], 0
+    while i < len(gpus):
+        s = int(rng.choice([x for x in (1, 2, 4, 8) if i + x <= len(gpus)]))
+        out.append(tuple(int(g) for g in gpus[i:i + s]))
+        i += s
+    return out
+
+
+def layouts(groups, reqs, rng):
+    per = [[] for _ in groups]
+    for r in reqs:
+        per[int(rng.integers(len(groups)))].append(r)
+    return [M.KvLayout(g, len(g), 8, tuple(p)) for g, p in zip(groups, per)]
+
+
+def same_state(a, b):
+    return (all(np.array_equal(x, y) for x, y in zip(a["block_tables"], b["block_tables"]))
+            and all(np.array_equal(x, y) for x, y in zip(a["rings"], b["rings"]))
+            and a["ring_head"] == b["ring_head"] and a["ring_tail"] == b["ring_tail"])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_walk(seed):
+    rng = np.random.default_rng(seed)
+    c = PagedKvCluster(KV, GPUS, units_per_gpu=96, max_requests=24, max_blocks=32,
+                       fragmented=True, seed=seed)
+    c.fill_garbage(seed=seed)
+    groups = random_groups(rng)
+    cur = [M.KvLayout(g, len(g), 8, ()) for g in groups]
+    next_id = 0
+    stats = {"admit": 0, "release": 0, "switch": 0, "rejected": 0}
+    for step in range(60):
+        op = rng.choice(["admit", "release", "switch"], p=[0.35, 0.2, 0.45])
+        before = c.snapshot()
+        try:
+            if op == "admit":
+                n = int(rng.integers(1, 4))
+                new_reqs = [(next_id + i, int(rng.integers(1, 60))) for i in range(n)]
+                g = cur[int(rng.integers(len(cur)))]
+                lay = M.KvLayout(g.group, g.tp, 8, tuple(new_reqs))
+                c.admit([lay], seed=7)
+                next_id += n
+                cur = [M.KvLayout(x.group, x.tp, 8, x.requests + (tuple(new_reqs) if x is g else ()))
+                       for x in cur]
+            elif op == "release":
+                resident = [r for lay in cur for r in lay.requests]
+                if not resident:
+                    continue
+                k = int(rng.integers(1, len(resident) + 1))
+                gone = [resident[i][0] for i in rng.choice(len(resident), size=k, replace=False)]
+                rec = []
+                for rid in gone:
+                    rs = c.req_slot[rid]
+                    own = c.owner[rs]
+                    h = 0
+                    while h < 8:
+                        e = h
+                        while e < 8 and own[e] == own[h]:
+                            e += 1
+                        rec.append((int(own[h]), -1, rs, h, e, c.ctx_of[rid]))
+                        h = e
+                c.release(gone)
+                want = check.expected_after(c, before, np.array(rec, np.int64))
+                assert not any(check.compare(c.snapshot(), want).values())
+                cur = [M.KvLayout(x.group, x.tp, 8, tuple(r for r in x.requests if r[0] not in gone))
+                       for x in cur]
+            else:
+                resident = [r for lay in cur for r in lay.requests]
+                new = layouts(random_groups(rng), resident, rng)
+                plan = M.plan_repartition(cur, new, KV.kv_bytes_per_token_per_head)
+                rec = c.records(plan)
+                c.migrate(plan)
+                want = check.expected_after(c, before, rec)
+                diff = check.compare(c.snapshot(), want)
+                assert not any(diff.values()), (step, diff)
+                cur = new
+            stats[op] += 1
+        except M.MigrationError as exc:
+            assert "units needed" in str(exc) or "request slots" in str(exc), exc
+            assert same_state(c.snapshot(), before), f"step {step}: rejected {op} changed state"
+            stats["rejected"] += 1
+        v = c.verify(seed=7)
+        assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0, (step, v)
+        assert c.placement() == M.layout_placement(cur)
+    assert stats["switch"] >= 10 and stats["admit"] >= 5
