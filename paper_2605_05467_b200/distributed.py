@@ -231,22 +231,27 @@ class DistributedKvCluster:
 
     def admit(self, layouts, seed: int = 1) -> int:
         """Every rank calls with the same layouts; each allocates + fills its pages."""
-        H = self.kv.total_heads
-        recs = []
+        recs, new = [], []
+        free = list(self._free_req_slots)
         for lay in layouts:
             hpr = lay.heads_per_rank
             for rid, ctx in lay.requests:
-                if rid in self.req_slot:
+                if rid in self.req_slot or any(rid == x[0] for x in new):
                     raise MigrationError(f"request {rid} already resident")
-                rs = self._free_req_slots.pop()
-                self.req_slot[rid] = rs
-                self.slot_ctx[rs] = int(ctx)
-                for r, g in enumerate(lay.group):
-                    s = self.slot_of[g]
-                    self.owner[rs, r * hpr:(r + 1) * hpr] = s
-                    recs.append((-1, s, rs, r * hpr, (r + 1) * hpr, int(ctx)))
+                if not free:
+                    raise MigrationError("no free request slots")
+                rs = free.pop()
+                runs = [(self.slot_of[g], r * hpr, (r + 1) * hpr) for r, g in enumerate(lay.group)]
+                new.append((rid, rs, int(ctx), runs))
+                recs.extend((-1, s, rs, lo, hi, int(ctx)) for s, lo, hi in runs)
         rec = np.asarray(recs, np.int64).reshape(-1, 6)
-        in_u, out_u = self._advance(rec)
+        in_u, out_u = self._advance(rec)  # capacity check before any state change
+        self._free_req_slots = free
+        for rid, rs, ctx, runs in new:
+            self.req_slot[rid] = rs
+            self.slot_ctx[rs] = ctx
+            for s, lo, hi in runs:
+                self.owner[rs, lo:hi] = s
         mine = rec[rec[:, 1] == self.slot]
         n = int(units_per_record(mine, self.kv.block_tokens).sum())
         if n:

@@ -289,31 +289,39 @@ class PagedKvCluster:
         them with the placement-invariant synthetic pattern. Returns #units."""
         stream = stream or self._default_stream
         H = self.kv.total_heads
-        recs = []
+        recs, new = [], []  # new: (rid, slot, ctx, [(gpu slot, lo, hi)])
+        free = list(self._free_req_slots)
+        seen = set()
         for lay in layouts:
             if lay.total_heads != H:
                 raise MigrationError("all layouts must share total_heads")
             hpr = lay.heads_per_rank
             slots = [self.slot_of[g] for g in lay.group]
             for rid, ctx in lay.requests:
-                if rid in self.req_slot:
+                if rid in self.req_slot or rid in seen:
                     raise MigrationError(f"request {rid} already resident")
                 if self.kv.blocks(ctx) > self.max_blocks:
                     raise MigrationError(f"request {rid}: {ctx} tokens exceed max_blocks")
-                if not self._free_req_slots:
+                if not free:
                     raise MigrationError("no free request slots")
-                rs = self._free_req_slots.pop()
-                self.req_slot[rid] = rs
-                self._set_req(rid, rs)
-                self.ctx_of[rid] = int(ctx)
-                self.slot_ctx[rs] = int(ctx)
-                for r, s in enumerate(slots):
-                    self.owner[rs, r * hpr:(r + 1) * hpr] = s
-                    recs.append((-1, s, rs, r * hpr, (r + 1) * hpr, int(ctx)))
+                seen.add(rid)
+                rs = free.pop()
+                runs = [(s, r * hpr, (r + 1) * hpr) for r, s in enumerate(slots)]
+                new.append((rid, rs, int(ctx), runs))
+                recs.extend((-1, s, rs, lo, hi, int(ctx)) for s, lo, hi in runs)
         if not recs:
             return 0
         xf = np.asarray(recs, dtype=np.int64)
-        total = self._remap(xf, stream, want_ext=True)
+        total = self._remap(xf, stream, want_ext=True)  # raises before any state change
+        # commit host bookkeeping only once the device work is enqueued
+        self._free_req_slots = free
+        for rid, rs, ctx, runs in new:
+            self.req_slot[rid] = rs
+            self._set_req(rid, rs)
+            self.ctx_of[rid] = ctx
+            self.slot_ctx[rs] = ctx
+            for s, lo, hi in runs:
+                self.owner[rs, lo:hi] = s
         if total:
             cl = self._cluster_c()
             with torch.cuda.device(self.home):
