@@ -587,6 +587,14 @@ def main():
                "ms_per_step": e2e_s / args.steps * 1e3,
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": 4}
 
+    # ---- after the timed regions: full-size correctness of the final state ----
+    # every owned page carries its placement-invariant pattern, every block-table
+    # entry realises the host placement, every weight shard equals its slice
+    vkv = ex.kv.verify()
+    vw = ex.weights.verify() if ex.weights is not None else 0
+    bit_exact = (vkv["placement_errors"] == 0 and vkv["word_mismatches"] == 0
+                 and vkv["status"] == 0 and vw == 0 and status == 0)
+
     if world > 1:
         dist.destroy_process_group()
     if rank != 0:
@@ -635,6 +643,8 @@ def main():
         "e2e": e2e,
         "gpu_launches": launches,
         "status": status,
+        "bit_exact_property": bit_exact,
+        "pages_verified": vkv["pages_checked"],
     }
     print(json.dumps(line))
 
