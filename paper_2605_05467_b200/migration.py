@@ -18,8 +18,7 @@ from __future__ import annotations
 
 import math
 import threading
-from dataclasses import dataclass
-from typing import Iterable
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -83,39 +82,39 @@ class Transfer:
     bytes: int
 
 
+@dataclass
 class MigrationPlan:
     """Transfer list + handshake + predicted latencies (migration.py:60-74).
 
-    Accepts a list of ``Transfer`` like the reference dataclass. Plans built by
-    the native planner hold an int64 [n, 6] array
-    (src, dst, request, head_lo, head_hi, bytes) and build ``Transfer`` objects
-    lazily, so the execution path never pays for Python objects.
+    A dataclass with the reference's fields, so ``dataclasses.fields`` /
+    ``asdict`` / ``replace`` and equality behave the same. Plans built by the
+    native planner hold an int64 [n, 6] array (src, dst, request, head_lo,
+    head_hi, bytes) and build ``Transfer`` objects lazily (``transfers`` is a
+    property over that storage), so the execution path never pays for Python
+    objects.
     """
 
-    def __init__(self, transfers: Iterable[Transfer] | None = None, handshake_ms: float = 0.0,
-                 predicted_latency_ms: dict | None = None):
-        self._list: list[Transfer] | None = list(transfers) if transfers is not None else []
-        self._arr: np.ndarray | None = None
-        self.handshake_ms = handshake_ms
-        self.predicted_latency_ms = {} if predicted_latency_ms is None else predicted_latency_ms
+    transfers: list[Transfer] = field(default_factory=list)
+    handshake_ms: float = 0.0
+    predicted_latency_ms: dict = field(default_factory=dict)
 
     @classmethod
     def from_array(cls, arr: np.ndarray, handshake_ms: float = 0.0) -> "MigrationPlan":
-        plan = cls(handshake_ms=handshake_ms)
+        plan = cls.__new__(cls)
         plan._list = None
         plan._arr = np.ascontiguousarray(arr, dtype=np.int64).reshape(-1, 6)
+        plan.handshake_ms = handshake_ms
+        plan.predicted_latency_ms = {}
         return plan
 
-    @property
-    def transfers(self) -> list[Transfer]:
+    def _get_transfers(self) -> list[Transfer]:
         if self._list is None:
             self._list = [Transfer(*map(int, row)) for row in self._arr]
         # the caller may mutate the list; the array view is rebuilt on demand
         self._arr = None
         return self._list
 
-    @transfers.setter
-    def transfers(self, value):
+    def _set_transfers(self, value) -> None:
         self._list = list(value)
         self._arr = None
 
@@ -147,15 +146,13 @@ class MigrationPlan:
             out[int(src)] = int(arr[arr[:, SRC] == src, BYTES].sum())
         return out
 
-    def __eq__(self, other):
-        if not isinstance(other, MigrationPlan):
-            return NotImplemented
-        return (self.transfers == other.transfers and self.handshake_ms == other.handshake_ms
-                and self.predicted_latency_ms == other.predicted_latency_ms)
-
     def __repr__(self):
-        return (f"MigrationPlan(transfers=<{len(self)}>, handshake_ms={self.handshake_ms}, "
+        return (f"MigrationPlan(transfers=<{len(self)} transfers>, handshake_ms={self.handshake_ms}, "
                 f"predicted_latency_ms={self.predicted_latency_ms})")
+
+
+# the dataclass __init__ assigns `transfers` through this property
+MigrationPlan.transfers = property(MigrationPlan._get_transfers, MigrationPlan._set_transfers)
 
 
 @dataclass(frozen=True)

@@ -211,6 +211,21 @@ def test_reversibility_same_bytes():
         assert M.plan_repartition(a, b, 4096).total_bytes == M.plan_repartition([b], a, 4096).total_bytes
 
 
+def test_plan_is_a_dataclass_like_the_reference():
+    import dataclasses
+    plan = M.plan_repartition([lay([1], 8, [(0, 10)]), lay([2], 8, [(1, 10)])],
+                              lay([1, 2], 8, [(0, 10), (1, 10)]), 4096, handshake_ms=0.5)
+    assert [f.name for f in dataclasses.fields(plan)] == ["transfers", "handshake_ms",
+                                                          "predicted_latency_ms"]
+    d = dataclasses.asdict(plan)
+    assert d["handshake_ms"] == 0.5 and len(d["transfers"]) == 2
+    q = dataclasses.replace(plan, handshake_ms=1.0)
+    assert q.transfers == plan.transfers and q.handshake_ms == 1.0
+    assert plan == M.MigrationPlan(list(plan.transfers), 0.5, {})
+    for cls in (M.KvLayout, M.Transfer, M.CostModelParams):
+        assert dataclasses.is_dataclass(cls)
+
+
 def test_plan_mutation_keeps_array_in_sync():
     plan = M.plan_repartition([lay([1], 8, [(0, 10)]), lay([2], 8, [(1, 10)])],
                               lay([1, 2], 8, [(0, 10), (1, 10)]), 4096)
