@@ -470,9 +470,27 @@ namespace tpr {
 
 static int copy_grid(const void* fn, int threads, int64_t want_warps) {
   int sms = sm_count();
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
-  if (per_sm < 1) per_sm = 1;
+  // occupancy per (kernel, device) is fixed: query once (the query costs
+  // microseconds, which matters for small switches)
+  static thread_local const void* cached_fn[8] = {nullptr};
+  static thread_local int cached_dev[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  static thread_local int cached_occ[8] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int per_sm = 0;
+  for (int i = 0; i < 8; ++i)
+    if (cached_fn[i] == fn && cached_dev[i] == dev) per_sm = cached_occ[i];
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+    if (per_sm < 1) per_sm = 1;
+    for (int i = 0; i < 8; ++i)
+      if (cached_fn[i] == nullptr) {
+        cached_fn[i] = fn;
+        cached_dev[i] = dev;
+        cached_occ[i] = per_sm;
+        break;
+      }
+  }
   const int64_t want_blocks = (want_warps * 32 + threads - 1) / threads;
   int64_t grid = (int64_t)sms * per_sm;
   if (want_blocks < grid) grid = want_blocks;

@@ -59,25 +59,27 @@ class _PinnedStaging:
 
     def __init__(self, nbytes: int = 1 << 16):
         self._bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-        self._events: list = [None, None]
+        self._views = [b.numpy() for b in self._bufs]
+        self._events = [torch.cuda.Event(), torch.cuda.Event()]
+        self._armed = [False, False]
         self._i = 0
 
     def stage(self, arr: np.ndarray) -> int:
         raw = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
         i = self._i
-        if self._events[i] is not None:
+        if self._armed[i]:
             self._events[i].synchronize()
-            self._events[i] = None
+            self._armed[i] = False
         if self._bufs[i].numel() < raw.nbytes:
             self._bufs[i] = torch.empty(max(raw.nbytes, 2 * self._bufs[i].numel()),
                                         dtype=torch.uint8, pin_memory=True)
-        self._bufs[i].numpy()[: raw.nbytes] = raw
+            self._views[i] = self._bufs[i].numpy()
+        self._views[i][: raw.nbytes] = raw
         return self._bufs[i].data_ptr()
 
     def fence(self, stream: torch.cuda.Stream) -> None:
-        ev = torch.cuda.Event()
-        ev.record(stream)
-        self._events[self._i] = ev
+        self._events[self._i].record(stream)
+        self._armed[self._i] = True
         self._i ^= 1
 
     def upload(self, arr: np.ndarray, dst: torch.Tensor, stream: torch.cuda.Stream) -> int:
@@ -245,9 +247,22 @@ class PagedKvCluster:
 
     def _reserve(self, xf: np.ndarray):
         """Capacity check + ring bookkeeping for records; returns (#units, in, out)."""
-        units = self._units_per_record(xf)
-        total = int(units.sum())
-        in_u, out_u = self._deltas(xf, units)
+        if len(xf) <= 64:
+            B = self.kv.block_tokens
+            in_u = [0] * self.n_gpus
+            out_u = [0] * self.n_gpus
+            total = 0
+            for s, d, _, lo, hi, ctx in xf.tolist():
+                u = (hi - lo) * (-(-ctx // B))
+                total += u
+                if d >= 0:
+                    in_u[d] += u
+                if s >= 0:
+                    out_u[s] += u
+        else:
+            units = self._units_per_record(xf)
+            total = int(units.sum())
+            in_u, out_u = self._deltas(xf, units)
         for s in range(self.n_gpus):
             free = self.ring_tail[s] - self.ring_head[s]
             if in_u[s] > free:
@@ -379,6 +394,19 @@ class PagedKvCluster:
         n = len(arr)
         if n == 0:
             return np.zeros((0, 6), dtype=np.int64)
+        if n <= 32 and not validate:  # small plans: dict lookups beat numpy call overhead
+            H = self.kv.total_heads
+            out = []
+            for s, d, r, lo, hi, _ in arr.tolist():
+                ss, ds, rs = self.slot_of.get(s), self.slot_of.get(d), self.req_slot.get(r)
+                if ss is None or ds is None:
+                    raise MigrationError(f"gpu {s if ss is None else d} is not part of this cluster")
+                if rs is None:
+                    raise MigrationError(f"request {r} is not resident")
+                if not 0 <= lo < hi <= H:
+                    raise MigrationError("head range outside [0, total_heads)")
+                out.append((ss, ds, rs, lo, hi, self.ctx_of[r]))
+            return np.array(out, dtype=np.int64)
         src = self._gpu_slots(arr[:, SRC])
         dst = self._gpu_slots(arr[:, DST])
         req = self._req_slots(arr[:, REQ])
