@@ -119,7 +119,8 @@ __device__ __forceinline__ int64_t block_keyed_exclusive(int key, int64_t val,
                                                          int64_t* s_run)  // [kKeys]
 {
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kScanWarps * kKeys; i += blockDim.x) s_tab[i] = 0;
+  const int nwarps = blockDim.x >> 5;  // sized to the plan: small plans scan with one warp
+  for (int i = threadIdx.x; i < nwarps * kKeys; i += blockDim.x) s_tab[i] = 0;
   __syncthreads();
   const unsigned peers = __match_any_sync(kFull, key);
   const unsigned lower = peers & ((1u << lane) - 1u);
@@ -134,7 +135,7 @@ __device__ __forceinline__ int64_t block_keyed_exclusive(int key, int64_t val,
   if (threadIdx.x < kKeys) {
     const int k = threadIdx.x;
     int64_t run = s_run[k];
-    for (int w = 0; w < kScanWarps; ++w) {
+    for (int w = 0; w < nwarps; ++w) {
       const int64_t t = s_tab[w * kKeys + k];
       s_tab[w * kKeys + k] = run;
       run += t;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(kScanThreads)
   __shared__ int64_t s_run[3][kKeys];
   for (int i = threadIdx.x; i < 3 * kKeys; i += blockDim.x) (&s_run[0][0])[i] = 0;
   __syncthreads();
-  for (int base = 0; base < n; base += kScanThreads) {
+  for (int base = 0; base < n; base += blockDim.x) {
     const int t = base + threadIdx.x;
     int src = TPR_MAX_GPUS, dst = TPR_MAX_GPUS;
     int64_t units = 0, mine = 0;
@@ -501,7 +502,10 @@ cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
                       const int32_t* xf, int32_t n, int32_t filter, int64_t* meta,
                       int64_t* totals, int64_t n_hint, int4* work, int4* work_ext,
                       int32_t* status, cudaStream_t st) {
-  tpr_k3_scan<<<1, kScanThreads, 0, st>>>(xf, n, geo.block_tokens, filter, meta, totals);
+  int threads = ((n + 31) / 32) * 32;
+  if (threads > kScanThreads) threads = kScanThreads;
+  if (threads < 32) threads = 32;
+  tpr_k3_scan<<<1, threads, 0, st>>>(xf, n, geo.block_tokens, filter, meta, totals);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (n_hint <= 0) n_hint = 1;
