@@ -333,20 +333,24 @@ def cpu_sample_seqs(w, requested: int) -> int:
     return max(1, min(requested, len(w.requests), CPU_SAMPLE_KV_BYTES // per_seq))
 
 
-def run_cpu_reference(w, steps: int, warmup: int, sample_seqs: int):
+def run_cpu_reference(w, steps: int, warmup: int, sample_seqs: int, min_seconds: float = 0.0):
+    """Time the CPU restatement: `steps` switches of the sample, continuing
+    until at least `min_seconds` of CPU work have been timed."""
     sample_seqs = cpu_sample_seqs(w, sample_seqs)
     threads = cpu_threads()
     ref = CpuReference(w, sample_seqs, threads)
     for _ in range(warmup):
         ref.step()
     t0 = time.perf_counter()
-    moved = 0
-    for _ in range(steps):
+    moved = done = 0
+    while done < steps or time.perf_counter() - t0 < min_seconds:
         moved += ref.step()
+        done += 1
     dt = time.perf_counter() - t0
-    return {"value": moved / dt / 1e9, "ms_per_step": dt / steps * 1e3, "bytes": moved,
-            "threads": threads, "sample": f"{sample_seqs} of {len(w.requests)} seqs "
-            f"(+ the same share of every weight slice copy), alternating switches"}
+    return {"value": moved / dt / 1e9, "ms_per_step": dt / done * 1e3, "bytes": moved,
+            "threads": threads, "seconds": dt,
+            "sample": f"{sample_seqs} of {len(w.requests)} seqs (+ the same share of every "
+                      f"weight slice copy), {done} alternating switches, {dt:.1f} s timed"}
 
 
 # ---------------------------------------------------------------------------
@@ -480,6 +484,8 @@ def main():
     ap.add_argument("--config", type=int, default=1, help="BASELINE configs[] index (0-based)")
     ap.add_argument("--seqs", type=int, default=None)
     ap.add_argument("--cpu-sample-seqs", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="minimum timed CPU work of the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--engine", choices=("vector", "bulk"), default=None,
@@ -613,7 +619,8 @@ def main():
             traffic = None
     cpu = None
     if not args.no_cpu:
-        r = run_cpu_reference(w, 2, 1, min(args.cpu_sample_seqs, len(w.requests)))
+        r = run_cpu_reference(w, 2, 1, min(args.cpu_sample_seqs, len(w.requests)),
+                              min_seconds=args.cpu_seconds)
         cpu = {"value": r["value"], "unit": "GB/s", "cores": r["threads"], "kind": "port",
                "sample": r["sample"], "cpu": cpu_model()}
     value = total_bytes * world / (ms * 1e-3) / 1e9
