@@ -36,7 +36,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .geometry import MAX_TP, MatrixSpec, ModelGeometry
+from .geometry import MAX_TP, ModelGeometry
 from .migration import MigrationError
 
 CHUNK_BYTES = int(os.environ.get("TPR_K2_CHUNK", 32 * 1024))  # K2 work-item size (bytes)
@@ -104,8 +104,7 @@ class ShardedWeightStore:
         self.active: dict[int, tuple[int, int]] = {}
         self.arena: dict[int, torch.Tensor] = {}
         self.rep_arena: dict[int, torch.Tensor] = {}
-        self._segs_dev = {}
-        self._prefix_dev = {}
+        self._segs_dev = {}  # device -> (pinned staging, device scratch) for K2 segments
 
     # ----------------------------------------------------------------- load
     def load(self, groups: Sequence[Sequence[int]], stream: torch.cuda.Stream | None = None) -> None:

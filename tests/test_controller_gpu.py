@@ -2,9 +2,7 @@
 streams), prefill->decode handoff over disjoint groups, capacity admission
 with eviction through release."""
 
-import numpy as np
 import pytest
-import torch
 
 from oracle import check
 from paper_2605_05467_b200 import geometry, migration as M, workloads

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import torch
 
-from oracle import check, kvmove
+from oracle import check
 from paper_2605_05467_b200 import geometry, migration as M, pattern, workloads
 from paper_2605_05467_b200.kvcache import PagedKvCluster
 

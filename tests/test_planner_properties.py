@@ -2,7 +2,6 @@
 restatement: random GPU ids, mixed TP levels across groups, random request
 order, disjoint groups through head_transfers (engine path)."""
 
-import pytest
 from hypothesis import given, settings
 from hypothesis import strategies as st
 

@@ -21,7 +21,6 @@ overhead + HBM, not NVLink.
 from __future__ import annotations
 
 import argparse
-import ctypes
 import json
 import sys
 import time
