@@ -159,7 +159,7 @@ def capacity_units(w, kv) -> dict:
     return {g: n + 64 for g, n in peak.items()}
 
 
-def setup_ours(w, device, overlap=None):
+def setup_ours(w, device, overlap=None, weights_mode="sharded"):
     import torch
     from paper_2605_05467_b200.controller import ReconfigurationExecutor
     from paper_2605_05467_b200.kvcache import PagedKvCluster
@@ -173,7 +173,7 @@ def setup_ours(w, device, overlap=None):
     cluster.admit(w.old, seed=1234)
     store = None
     if w.old_weight_groups is not None:
-        store = ShardedWeightStore(w.model, w.gpus, device=device)
+        store = ShardedWeightStore(w.model, w.gpus, device=device, mode=weights_mode)
         store.load(w.old_weight_groups)
     torch.cuda.synchronize()
     return ReconfigurationExecutor(cluster, store, time_kernels=True, overlap=overlap)
@@ -492,6 +492,9 @@ def main():
                     help="K1/K2 copy engine (default: the library default)")
     ap.add_argument("--overlap", choices=("auto", "on", "off"), default="auto",
                     help="K1 || K2 on two streams (auto: only across devices)")
+    ap.add_argument("--weights-mode", choices=("sharded", "full_copy_per_gpu"), default="sharded",
+                    help="weight storage (weight_memory modes): sharded moves missing slices, "
+                         "full_copy_per_gpu (the paper's design) switches by views only")
     args = ap.parse_args()
     if args.engine and args.impl == "ours":
         from paper_2605_05467_b200 import _native
@@ -533,7 +536,8 @@ def main():
         if world > 1:
             dist.barrier()
 
-    ex = setup_ours(w, device, overlap={"auto": None, "on": True, "off": False}[args.overlap])
+    ex = setup_ours(w, device, overlap={"auto": None, "on": True, "off": False}[args.overlap],
+                    weights_mode=args.weights_mode)
     fwd = True
     for _ in range(max(args.warmup, 1)):
         one_switch(ex, w, fwd, sync=True)
@@ -634,6 +638,7 @@ def main():
             "seqs": len(w.requests), "ctx": w.requests[0][1],
             "switch": "alternating forward/reverse, full stop-and-migrate (plan+K3+K1+K2)",
             "k1_k2_overlap": ex.overlap, "copy_engine": _engine_name(),
+            "weights_mode": args.weights_mode,
             "kv_bytes_per_step": kv_per_step, "weight_bytes_per_step": w_bytes / args.steps,
             "l2": "inputs larger than L2 (>= 24 GiB moved per step)",
             "parallelism": "replicas" if world > 1 else "1 GPU, logical ranks",
