@@ -214,9 +214,12 @@ int tpr_baseline_copy_pages(const uint64_t* src, const uint64_t* dst, const uint
  * rank `rank` stores `epoch` into slot [rank] of every rank's flag array
  * (peer_flags[r] = device VA of rank r's uint64 [world] array, IPC-mapped;
  * release semantics at system scope), then spins until every slot of its own
- * array (peer_flags[rank]) reaches `epoch` (acquire). Epochs must increase. */
+ * array (peer_flags[rank]) reaches `epoch` (acquire). Epochs must increase.
+ * A peer missing for timeout_ns ends the spin and ORs
+ * TPR_STATUS_BARRIER_TIMEOUT into *d_status (device int32, nullable). */
+#define TPR_STATUS_BARRIER_TIMEOUT 4
 int tpr_device_barrier(const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch,
-                       void* stream);
+                       uint64_t timeout_ns, int32_t* d_status, void* stream);
 
 /* ---- peer memory (one process per GPU) -------------------------------- */
 /* Whole-allocation device memory (cudaMalloc): the pointer is the allocation

@@ -20,6 +20,7 @@ TPR_META_FIELDS = 4
 TPR_TOTALS_LEN = 1 + 2 * TPR_MAX_GPUS
 TPR_STATUS_WRONG_SOURCE = 1
 TPR_STATUS_DST_OCCUPIED = 2
+TPR_STATUS_BARRIER_TIMEOUT = 4
 
 # Every exported symbol of include/tpr.h; tests check the library exports all.
 EXPORTS = (
@@ -103,7 +104,8 @@ _SIGNATURES = {
                                     c_int64, c_uint64, c_int32, c_void_p, c_void_p]),
     "tpr_baseline_copy_pages": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                           c_void_p]),
-    "tpr_device_barrier": (c_int32, [c_void_p, c_int32, c_int32, c_uint64, c_void_p]),
+    "tpr_device_barrier": (c_int32, [c_void_p, c_int32, c_int32, c_uint64, c_uint64, c_void_p,
+                                     c_void_p]),
     "tpr_device_alloc": (c_int32, [c_uint64, POINTER(c_uint64)]),
     "tpr_device_free": (c_int32, [c_uint64]),
     "tpr_enable_peer": (c_int32, [c_int32]),

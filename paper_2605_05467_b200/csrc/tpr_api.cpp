@@ -424,10 +424,11 @@ int tpr_baseline_copy_pages(const uint64_t* src, const uint64_t* dst, const uint
 }
 
 int tpr_device_barrier(const uint64_t* peer_flags, int32_t rank, int32_t world, uint64_t epoch,
-                       void* stream) {
+                       uint64_t timeout_ns, int32_t* d_status, void* stream) {
   if (!peer_flags || world <= 0 || world > TPR_MAX_GPUS || rank < 0 || rank >= world)
     return fail(TPR_EINVAL, "bad barrier arguments (rank %d, world %d)", rank, world);
-  cudaError_t e = tpr::launch_barrier(peer_flags, rank, world, epoch, static_cast<cudaStream_t>(stream));
+  cudaError_t e = tpr::launch_barrier(peer_flags, rank, world, epoch, timeout_ns, d_status,
+                                      static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_device_barrier launch");
 }
 

@@ -57,7 +57,7 @@ cudaError_t launch_kv_verify(const tpr_kv_geometry_t& geo, const KvCopyParams& p
                              const int32_t* owner, int32_t slot, uint64_t seed,
                              unsigned long long* counts, cudaStream_t st);
 cudaError_t launch_barrier(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch,
-                           cudaStream_t st);
+                           uint64_t timeout_ns, int32_t* status, cudaStream_t st);
 cudaError_t launch_matrix(char* buf, int64_t rows, int64_t cols, int64_t pitch, int64_t row0,
                           int64_t col0, int64_t full_cols, uint64_t key, int32_t elem_bytes,
                           bool verify, unsigned long long* mismatch, cudaStream_t st);

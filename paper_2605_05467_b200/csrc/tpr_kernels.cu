@@ -442,7 +442,14 @@ struct BarrierParams {
   uint64_t flags[TPR_MAX_GPUS];
 };
 
-__global__ void tpr_barrier_kernel(BarrierParams p, int32_t rank, int32_t world, uint64_t epoch) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void tpr_barrier_kernel(BarrierParams p, int32_t rank, int32_t world, uint64_t epoch,
+                                   uint64_t timeout_ns, int32_t* status) {
   const int lane = threadIdx.x;
   // order every store this stream issued before (K1 pushes into peer pools,
   // K3 block-table writes) ahead of the signal, at system scope
@@ -452,11 +459,17 @@ __global__ void tpr_barrier_kernel(BarrierParams p, int32_t rank, int32_t world,
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer), "l"(epoch) : "memory");
     const unsigned long long* mine =
         reinterpret_cast<const unsigned long long*>(p.flags[rank]) + lane;
+    const uint64_t t0 = globaltimer_ns();
     unsigned long long v = 0;
     while (true) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
       if (v >= epoch) break;
-      __nanosleep(64);
+      // a peer that never arrives (crashed rank) must not wedge the GPU
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        if (status) atomicOr(status, TPR_STATUS_BARRIER_TIMEOUT);
+        break;
+      }
+      __nanosleep(256);
     }
   }
   __syncwarp();
@@ -562,10 +575,10 @@ cudaError_t launch_kv_verify(const tpr_kv_geometry_t& geo, const KvCopyParams& p
 }
 
 cudaError_t launch_barrier(const uint64_t* flags, int32_t rank, int32_t world, uint64_t epoch,
-                           cudaStream_t st) {
+                           uint64_t timeout_ns, int32_t* status, cudaStream_t st) {
   BarrierParams p{};
   for (int i = 0; i < world; ++i) p.flags[i] = flags[i];
-  tpr_barrier_kernel<<<1, 32, 0, st>>>(p, rank, world, epoch);
+  tpr_barrier_kernel<<<1, 32, 0, st>>>(p, rank, world, epoch, timeout_ns, status);
   return cudaGetLastError();
 }
 

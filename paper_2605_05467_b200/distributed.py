@@ -500,10 +500,12 @@ class DeviceBarrier:
     """Stream-ordered barrier across the group through IPC-mapped flags
     (``tpr_device_barrier``): no host collective on the switch path."""
 
-    def __init__(self, device: torch.device, group=None):
+    def __init__(self, device: torch.device, group=None, timeout_s: float = 30.0):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.timeout_ns = int(timeout_s * 1e9)
+        self.status = torch.zeros(1, dtype=torch.int32, device=torch.device(device))
         self.flags = DeviceBuffer(8 * self.world, torch.device(device))
         self.flags.tensor.zero_()
         torch.cuda.synchronize(device)
@@ -518,7 +520,12 @@ class DeviceBarrier:
     def __call__(self, stream: torch.cuda.Stream) -> None:
         self.epoch += 1
         _native.call("tpr_device_barrier", self.ptrs, self.rank, self.world, self.epoch,
-                     stream.cuda_stream)
+                     self.timeout_ns, self.status.data_ptr(), stream.cuda_stream)
+
+    def check(self) -> None:
+        """Raise if a barrier gave up waiting (host sync on the status word)."""
+        if int(self.status.item()) & _native.TPR_STATUS_BARRIER_TIMEOUT:
+            raise MigrationError("device barrier timed out: a peer rank never arrived")
 
     def close(self):
         dist.barrier(group=self.group)
@@ -575,6 +582,7 @@ class DistributedExecutor:
                 kst.wait_stream(wst)
             self.barrier(kst)  # every rank's pushes and pulls have completed
             kst.synchronize()
+            self.barrier.check()
         kv_stats = self.kv.finish(plan, kv_pending)
         w_stats = self.weights.finish(w_pending) if w_pending is not None else None
         return plan, kv_stats, w_stats, (time.perf_counter() - t0) * 1e3
