@@ -138,6 +138,52 @@ def _exec_worker(rank, world, path, q, device_barrier=True):
         q.put((rank, traceback.format_exc(), -1, None))
 
 
+def _barrier_timeout_worker(rank, world, path, q):
+    import sys
+    sys.path.insert(0, str(ROOT))
+    try:
+        from paper_2605_05467_b200.distributed import DeviceBarrier
+        from paper_2605_05467_b200.migration import MigrationError
+        _init(rank, world, path)
+        torch.cuda.set_device(0)
+        bar = DeviceBarrier(torch.device("cuda", 0), timeout_s=0.5)
+        st = torch.cuda.Stream()
+        bar(st)                      # both ranks arrive: passes
+        st.synchronize()
+        bar.check()
+        raised = None
+        if rank == 0:                # rank 1 "crashes": rank 0 must time out, not hang
+            bar(st)
+            st.synchronize()
+            try:
+                bar.check()
+                raised = False
+            except MigrationError:
+                raised = True
+        dist.barrier()
+        q.put((rank, raised))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+def test_device_barrier_times_out_instead_of_hanging():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "store")
+        procs = [ctx.Process(target=_barrier_timeout_worker, args=(r, 2, path, q), daemon=True)
+                 for r in range(2)]
+        for p in procs:
+            p.start()
+        res = sorted(q.get(timeout=120) for _ in procs)
+        for p in procs:
+            p.join(timeout=60)
+    assert res == [(0, True), (1, None)], res
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,device_barrier", [(2, True), (4, True), (2, False)])
 def test_distributed_executor_kv_and_weights(world, device_barrier):
