@@ -2,7 +2,7 @@
 // cp.async.bulk, an mbarrier per shared-memory stage and bulk-group
 // completion tracking. One elected thread per CTA issues every copy, so the
 // SMs spend almost no instructions on data movement; the copy engine moves the
-// bytes. Pieces are <= kPiece bytes, 16-B aligned, multiples of 16 B.
+// bytes. Pieces are <= `piece` bytes, 16-B aligned, multiples of 16 B.
 //
 // Pipeline per CTA (S stages, lookahead L = S - 2 loads in flight):
 //   load piece j+L into stage (j+L)%S once the store that last read that
@@ -11,6 +11,7 @@
 //   parity); store piece j; commit its bulk group.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "tpr.h"
 #include "tpr_common.cuh"
@@ -18,9 +19,7 @@
 
 namespace tpr {
 
-constexpr int kStages = 6;
-constexpr int kLookahead = kStages - 2;
-constexpr uint32_t kPiece = 16384;
+constexpr int kMaxStages = 16;  // shared-memory ring: stages x piece bytes (runtime)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -71,13 +70,14 @@ __device__ __forceinline__ void bulk_wait_all() {
 // ---- piece sources ---------------------------------------------------------
 
 // K1: the CTA's work items (grid-stride) -> pieces. A full page item is one
-// contiguous span cut into kPiece pieces; a partial page item is one piece
+// contiguous span cut into `piece`-byte pieces; a partial page item is one piece
 // per plane row (ntok valid tokens).
 struct KvPieces {
   const int4* work;
   int64_t n_items;
   KvCopyParams p;
   const KvClusterParams* cl;  // the kernel's __grid_constant__ parameter
+  uint32_t piece;
   int64_t item;
   // current item
   const char* s;
@@ -117,7 +117,7 @@ struct KvPieces {
   }
   __device__ bool next(const char*& src, char*& dst, uint32_t& nb) {
     if (rows_left == 0 && !load_item()) return false;
-    const int64_t take = min((int64_t)kPiece, row_bytes - off);
+    const int64_t take = min((int64_t)piece, row_bytes - off);
     src = s + off;
     dst = d + off;
     nb = (uint32_t)take;
@@ -137,6 +137,7 @@ struct KvPieces {
 struct SegPieces {
   const tpr_copy_seg_t* segs;
   const int64_t* prefix;
+  uint32_t piece;
   int32_t n_segs;
   int64_t n_items, chunk, item;
   const char* s;
@@ -199,7 +200,7 @@ struct SegPieces {
   }
   __device__ bool next(const char*& src, char*& dst, uint32_t& nb) {
     if (rows_left == 0 && !load_item()) return false;
-    const int64_t take = min((int64_t)kPiece, row_bytes - off);
+    const int64_t take = min((int64_t)piece, row_bytes - off);
     src = s + off;
     dst = d + off;
     nb = (uint32_t)take;
@@ -215,13 +216,15 @@ struct SegPieces {
 };
 
 template <class Source>
-__device__ __forceinline__ void bulk_pipeline(Source& src_it) {
+__device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar[kStages];
-  __shared__ char* pdst[kStages];
-  __shared__ uint32_t pnb[kStages];
+  __shared__ __align__(8) uint64_t bar[kMaxStages];
+  __shared__ char* pdst[kMaxStages];
+  __shared__ uint32_t pnb[kMaxStages];
   if (threadIdx.x != 0) return;
-  for (int s = 0; s < kStages; ++s) bar_init(&bar[s]);
+  const uint32_t piece = src_it.piece;
+  const int lookahead = stages - 2;  // => the refilled stage's last store may still be pending
+  for (int s = 0; s < stages; ++s) bar_init(&bar[s]);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const uint32_t base = smem_u32(smem);
   int64_t issued = 0, stored = 0;
@@ -234,19 +237,19 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it) {
       more = false;
       return;
     }
-    const int t = (int)(issued % kStages);
-    if (issued >= kStages) bulk_wait_read_1();  // store of piece issued-S done reading
+    const int t = (int)(issued % stages);
+    if (issued >= stages) bulk_wait_read_1();  // store of piece issued-S done reading
     pdst[t] = d;
     pnb[t] = nb;
-    bulk_load(base + (uint32_t)t * kPiece, s, nb, &bar[t]);
+    bulk_load(base + (uint32_t)t * piece, s, nb, &bar[t]);
     ++issued;
   };
-  while (more && issued < kLookahead) issue();
+  while (more && issued < lookahead) issue();
   while (stored < issued) {
     if (more) issue();
-    const int t = (int)(stored % kStages);
-    bar_wait(&bar[t], (uint32_t)((stored / kStages) & 1));
-    bulk_store(pdst[t], base + (uint32_t)t * kPiece, pnb[t]);
+    const int t = (int)(stored % stages);
+    bar_wait(&bar[t], (uint32_t)((stored / stages) & 1));
+    bulk_store(pdst[t], base + (uint32_t)t * piece, pnb[t]);
     ++stored;
   }
   bulk_wait_all();
@@ -254,42 +257,68 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it) {
 
 __global__ void __launch_bounds__(32)
     tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
-                           const __grid_constant__ KvClusterParams cl) {
+                           const __grid_constant__ KvClusterParams cl, int32_t stages,
+                           uint32_t piece) {
   KvPieces it;
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
   it.cl = &cl;
+  it.piece = piece;
   it.start(blockIdx.x);
-  bulk_pipeline(it);
+  bulk_pipeline(it, stages);
 }
 
 __global__ void __launch_bounds__(32)
     tpr_k2_copy_segments_bulk(const tpr_copy_seg_t* __restrict__ segs,
                               const int64_t* __restrict__ prefix, int32_t n_segs, int64_t n_items,
-                              int64_t chunk) {
+                              int64_t chunk, int32_t stages, uint32_t piece) {
   SegPieces it;
   it.segs = segs;
   it.prefix = prefix;
   it.n_segs = n_segs;
   it.n_items = n_items;
   it.chunk = chunk;
+  it.piece = piece;
   it.start(blockIdx.x);
-  bulk_pipeline(it);
+  bulk_pipeline(it, stages);
+}
+
+// Ring shape: TPR_BULK_STAGES x TPR_BULK_PIECE bytes of shared memory per CTA
+// (defaults 6 x 16 KiB), read once per process.
+struct BulkConfig {
+  int stages = 6;
+  uint32_t piece = 16384;
+  int smem() const { return stages * (int)piece; }
+};
+
+static const BulkConfig& bulk_config() {
+  static BulkConfig cfg = [] {
+    BulkConfig c;
+    if (const char* v = getenv("TPR_BULK_STAGES")) c.stages = atoi(v);
+    if (const char* v = getenv("TPR_BULK_PIECE")) c.piece = (uint32_t)atoi(v);
+    if (c.stages < 3) c.stages = 3;
+    if (c.stages > kMaxStages) c.stages = kMaxStages;
+    c.piece = (c.piece / 16) * 16;
+    if (c.piece < 1024) c.piece = 1024;
+    while (c.smem() > 227 * 1024 && c.stages > 3) --c.stages;
+    return c;
+  }();
+  return cfg;
 }
 
 static int bulk_grid(const void* fn, int64_t items) {
-  static const int smem = kStages * kPiece;
+  const BulkConfig& c = bulk_config();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
     cudaFuncSetAttribute(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
     configured = true;
   }
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, c.smem());
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sm_count() * per_sm;
   if (items < grid) grid = items;
@@ -299,18 +328,20 @@ static int bulk_grid(const void* fn, int64_t items) {
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            int64_t n_units, cudaStream_t st) {
   if (n_units <= 0) return cudaSuccess;
+  const BulkConfig& c = bulk_config();
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk),
                              n_units * p.items_per_unit);
-  tpr_k1_kv_migrate_bulk<<<grid, 32, kStages * kPiece, st>>>(work, n_units, p, cl);
+  tpr_k1_kv_migrate_bulk<<<grid, 32, c.smem(), st>>>(work, n_units, p, cl, c.stages, c.piece);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
+  const BulkConfig& c = bulk_config();
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk), n_items);
-  tpr_k2_copy_segments_bulk<<<grid, 32, kStages * kPiece, st>>>(segs, prefix, n_segs, n_items,
-                                                                 chunk);
+  tpr_k2_copy_segments_bulk<<<grid, 32, c.smem(), st>>>(segs, prefix, n_segs, n_items, chunk,
+                                                         c.stages, c.piece);
   return cudaGetLastError();
 }
 
