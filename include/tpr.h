@@ -94,9 +94,9 @@ typedef struct tpr_kv_cluster {
 #define TPR_TOTALS_LEN (1 + 2 * TPR_MAX_GPUS)
 
 /* ---- host utilities -------------------------------------------------- */
-/* Copy engine of K1 and K2 (process-wide): TPR_ENGINE_VECTOR = warp-wide
- * 16-B ld/st (default), TPR_ENGINE_BULK = TMA cp.async.bulk through shared
- * memory, one issuing thread per CTA. */
+/* Copy engine of K1 and K2 (process-wide): TPR_ENGINE_BULK (default) = TMA
+ * cp.async.bulk global->shared->global through an mbarrier ring, one issuing
+ * thread per CTA; TPR_ENGINE_VECTOR = warp-wide 16-B ld/st. */
 #define TPR_ENGINE_VECTOR 0
 #define TPR_ENGINE_BULK 1
 int tpr_set_copy_engine(int32_t engine);

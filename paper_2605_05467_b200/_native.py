@@ -147,7 +147,7 @@ ENGINES = {"vector": 0, "bulk": 1}
 
 
 def set_copy_engine(name: str) -> None:
-    """K1/K2 copy engine: "vector" (16-B ld/st, default) or "bulk" (TMA)."""
+    """K1/K2 copy engine: "bulk" (TMA, default) or "vector" (16-B ld/st)."""
     if name not in ENGINES:
         raise ValueError(f"unknown copy engine {name!r}; choose from {sorted(ENGINES)}")
     call("tpr_set_copy_engine", ENGINES[name])

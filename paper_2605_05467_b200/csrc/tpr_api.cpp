@@ -76,7 +76,10 @@ int cluster_params(const tpr_kv_cluster_t* cl, const tpr_kv_geometry_t* geo,
   return TPR_OK;
 }
 
-std::atomic<int> g_engine{TPR_ENGINE_VECTOR};
+// TMA bulk engine by default: K1 at the measured HBM copy peak with one
+// issuing thread per CTA (profiles/README.md); the vector engine stays
+// selectable (tpr_set_copy_engine) for comparison.
+std::atomic<int> g_engine{TPR_ENGINE_BULK};
 
 cudaError_t run_k1(const tpr::KvCopyParams& p, const tpr::KvClusterParams& cl, const int4* work,
                    int64_t n, cudaStream_t st) {

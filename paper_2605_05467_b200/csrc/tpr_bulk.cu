@@ -11,6 +11,7 @@
 //   parity); store piece j; commit its bulk group.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "tpr.h"
@@ -284,38 +285,55 @@ __global__ void __launch_bounds__(32)
   bulk_pipeline(it, stages);
 }
 
-// Ring shape: TPR_BULK_STAGES x TPR_BULK_PIECE bytes of shared memory per CTA
-// (defaults 6 x 16 KiB), read once per process.
+// Ring shape per kernel (shared memory = stages x piece per CTA). Measured on
+// B200 (profiles/README.md): K1 streams whole 32 KiB page chunks and is
+// fastest with one CTA per SM and 32 KiB pieces (6 x 32 KiB = 192 KiB, at the
+// measured copy peak); K2's row-parallel slices are 1-7 KiB rows, so it wants
+// more issuing CTAs per SM (4 x 16 KiB = 64 KiB, 3 CTAs/SM). Override with
+// TPR_BULK_K1 / TPR_BULK_K2 = "<stages>x<piece bytes>".
 struct BulkConfig {
-  int stages = 6;
-  uint32_t piece = 16384;
+  int stages;
+  uint32_t piece;
   int smem() const { return stages * (int)piece; }
 };
 
-static const BulkConfig& bulk_config() {
-  static BulkConfig cfg = [] {
-    BulkConfig c;
-    if (const char* v = getenv("TPR_BULK_STAGES")) c.stages = atoi(v);
-    if (const char* v = getenv("TPR_BULK_PIECE")) c.piece = (uint32_t)atoi(v);
-    if (c.stages < 3) c.stages = 3;
-    if (c.stages > kMaxStages) c.stages = kMaxStages;
-    c.piece = (c.piece / 16) * 16;
-    if (c.piece < 1024) c.piece = 1024;
-    while (c.smem() > 227 * 1024 && c.stages > 3) --c.stages;
-    return c;
-  }();
-  return cfg;
+static BulkConfig parse_bulk(const char* env, BulkConfig c) {
+  if (const char* v = getenv(env)) {
+    int st = 0;
+    unsigned pc = 0;
+    if (sscanf(v, "%dx%u", &st, &pc) == 2) {
+      c.stages = st;
+      c.piece = pc;
+    }
+  }
+  if (c.stages < 3) c.stages = 3;
+  if (c.stages > kMaxStages) c.stages = kMaxStages;
+  c.piece = (c.piece / 16) * 16;
+  if (c.piece < 1024) c.piece = 1024;
+  while (c.smem() > 227 * 1024 && c.stages > 3) --c.stages;
+  return c;
 }
 
-static int bulk_grid(const void* fn, int64_t items) {
-  const BulkConfig& c = bulk_config();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
-    configured = true;
+static const BulkConfig& k1_config() {
+  static BulkConfig c = parse_bulk("TPR_BULK_K1", BulkConfig{6, 32768});
+  return c;
+}
+static const BulkConfig& k2_config() {
+  static BulkConfig c = parse_bulk("TPR_BULK_K2", BulkConfig{4, 16384});
+  return c;
+}
+
+static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items) {
+  static thread_local const void* done[4] = {nullptr};
+  bool seen = false;
+  for (auto f : done) seen |= (f == fn);
+  if (!seen) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
+    for (auto& f : done)
+      if (!f) {
+        f = fn;
+        break;
+      }
   }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, c.smem());
@@ -328,8 +346,8 @@ static int bulk_grid(const void* fn, int64_t items) {
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            int64_t n_units, cudaStream_t st) {
   if (n_units <= 0) return cudaSuccess;
-  const BulkConfig& c = bulk_config();
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk),
+  const BulkConfig& c = k1_config();
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
                              n_units * p.items_per_unit);
   tpr_k1_kv_migrate_bulk<<<grid, 32, c.smem(), st>>>(work, n_units, p, cl, c.stages, c.piece);
   return cudaGetLastError();
@@ -338,8 +356,8 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
-  const BulkConfig& c = bulk_config();
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk), n_items);
+  const BulkConfig& c = k2_config();
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk), c, n_items);
   tpr_k2_copy_segments_bulk<<<grid, 32, c.smem(), st>>>(segs, prefix, n_segs, n_items, chunk,
                                                          c.stages, c.piece);
   return cudaGetLastError();

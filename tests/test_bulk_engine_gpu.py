@@ -1,6 +1,7 @@
-"""The TMA bulk-copy engine (cp.async.bulk through shared memory) must give
-the same bytes as the oracle, for K1 (pages, incl. partial last pages) and
-K2 (contiguous and strided weight segments)."""
+"""Both copy engines -- the TMA bulk engine (cp.async.bulk through shared
+memory, the default) and the 16-B vector engine -- must give the same bytes as
+the oracle, for K1 (pages, incl. partial last pages) and K2 (contiguous and
+strided weight segments)."""
 
 import numpy as np
 import pytest
@@ -13,25 +14,27 @@ from paper_2605_05467_b200.weights import ShardedWeightStore
 
 pytestmark = pytest.mark.gpu
 
+DEFAULT = "bulk"
 
-@pytest.fixture
-def bulk():
-    _native.set_copy_engine("bulk")
-    yield
-    _native.set_copy_engine("vector")
+
+@pytest.fixture(params=["bulk", "vector"])
+def engine(request):
+    _native.set_copy_engine(request.param)
+    yield request.param
+    _native.set_copy_engine(DEFAULT)
 
 
 def test_engine_switch_roundtrip():
-    assert _native.copy_engine() == "vector"
-    _native.set_copy_engine("bulk")
-    assert _native.copy_engine() == "bulk"
+    assert _native.copy_engine() == DEFAULT
     _native.set_copy_engine("vector")
+    assert _native.copy_engine() == "vector"
+    _native.set_copy_engine(DEFAULT)
     with pytest.raises(ValueError):
         _native.set_copy_engine("dma")
 
 
 @pytest.mark.parametrize("tp_old,tp_new", [(1, 8), (8, 2), (2, 4), (4, 1)])
-def test_bulk_kv_bit_exact(bulk, tp_old, tp_new):
+def test_kv_bit_exact(engine, tp_old, tp_new):
     kv = geometry.KvGeometry(layers=3, head_dim=64, total_heads=8)  # 24 KiB pages: >1 piece each
     gpus = tuple(range(8))
     rng = np.random.default_rng(tp_old + 10 * tp_new)
@@ -51,8 +54,26 @@ def test_bulk_kv_bit_exact(bulk, tp_old, tp_new):
     assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
 
 
+def test_large_pages_cross_piece_boundaries(engine):
+    # 70B-shaped pages (640 KiB = 20 x 32 KiB pieces) with ragged last pages
+    kv = geometry.LLAMA_3_1_70B.kv
+    gpus = (0, 1)
+    reqs = [(0, 33), (1, 16), (2, 1), (3, 47)]
+    c = PagedKvCluster(kv, gpus, units_per_gpu=64, max_requests=4, max_blocks=4, fragmented=True)
+    c.fill_garbage(seed=5)
+    old = workloads.round_robin([(0,), (1,)], reqs, 8)
+    new = workloads.round_robin([(0, 1)], reqs, 8)
+    c.admit(old, seed=6)
+    before = c.snapshot()
+    plan = M.plan_repartition(old, new, kv.kv_bytes_per_token_per_head)
+    rec = c.records(plan)
+    c.migrate(plan)
+    diff = check.compare(c.snapshot(), check.expected_after(c, before, rec))
+    assert not any(diff.values()), diff
+
+
 @pytest.mark.parametrize("tp_old,tp_new", [(8, 1), (2, 4), (4, 2)])
-def test_bulk_weights_bit_exact(bulk, tp_old, tp_new):
+def test_weights_bit_exact(engine, tp_old, tp_new):
     model = geometry.tiny_geometry(hidden=512, intermediate=1024, vocab=2048)
     gpus = tuple(range(8))
     store = ShardedWeightStore(model, gpus)
@@ -63,7 +84,7 @@ def test_bulk_weights_bit_exact(bulk, tp_old, tp_new):
 
 
 @pytest.mark.slow
-def test_bulk_cfg2_full_size_property(bulk):
+def test_cfg2_full_size_property(engine):
     w = workloads.config(1, weights=False)
     kv = w.model.kv
     c = PagedKvCluster(kv, w.gpus, units_per_gpu=65536 + 64, max_requests=64, max_blocks=256,
