@@ -383,6 +383,12 @@ def run_distributed(args, w, rank: int, world: int, local: int):
     # NCCL carries the control plane (IPC-handle exchange, optional handshake)
     # when every rank has its own GPU; ranks that share a device use gloo
     backend = "nccl" if n_dev >= world else "gloo"
+    if n_dev >= world and not args.engine:
+        # TMA bulk copies into/out of peer mappings over NVLink have not been
+        # validated on multi-GPU hardware yet (every box here has one GPU);
+        # across devices use the 16-B vector engine, which is plain ld/st
+        from paper_2605_05467_b200 import _native
+        _native.set_copy_engine("vector")
     dist.init_process_group(backend, timeout=datetime.timedelta(minutes=10),
                             **({"device_id": device} if backend == "nccl" else {}))
     kv = w.model.kv
