@@ -116,9 +116,9 @@ struct KvPieces {
     }
     return false;
   }
-  __device__ bool next(const char*& src, char*& dst, uint32_t& nb) {
+  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes) {
     if (rows_left == 0 && !load_item()) return false;
-    const int64_t take = min((int64_t)piece, row_bytes - off);
+    const int64_t take = min((int64_t)max_bytes, row_bytes - off);
     src = s + off;
     dst = d + off;
     nb = (uint32_t)take;
@@ -199,9 +199,9 @@ struct SegPieces {
     }
     return false;
   }
-  __device__ bool next(const char*& src, char*& dst, uint32_t& nb) {
+  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes) {
     if (rows_left == 0 && !load_item()) return false;
-    const int64_t take = min((int64_t)piece, row_bytes - off);
+    const int64_t take = min((int64_t)max_bytes, row_bytes - off);
     src = s + off;
     dst = d + off;
     nb = (uint32_t)take;
@@ -216,12 +216,22 @@ struct SegPieces {
   }
 };
 
+constexpr int kMaxSub = 16;  // copies packed into one shared-memory stage
+
+// One elected thread runs the pipeline. A stage is `piece` bytes of shared
+// memory filled with up to kMaxSub consecutive copies (one 32 KiB page chunk,
+// or many short rows of partial pages / row-parallel weight slices). The
+// stage's loads all complete on one mbarrier; its stores form one bulk group,
+// so small copies still keep a full stage of bytes in flight.
 template <class Source>
 __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[kMaxStages];
-  __shared__ char* pdst[kMaxStages];
-  __shared__ uint32_t pnb[kMaxStages];
+  __shared__ char* pdst[kMaxStages][kMaxSub];
+  __shared__ uint32_t pnb[kMaxStages][kMaxSub];
+  __shared__ uint32_t poff[kMaxStages][kMaxSub];
+  __shared__ int pcnt[kMaxStages];
+  __shared__ const char* psrc[kMaxSub];  // sources of the stage being filled
   if (threadIdx.x != 0) return;
   const uint32_t piece = src_it.piece;
   const int lookahead = stages - 2;  // => the refilled stage's last store may still be pending
@@ -231,18 +241,37 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
   int64_t issued = 0, stored = 0;
   bool more = true;
   auto issue = [&]() {
-    const char* s;
-    char* d;
-    uint32_t nb;
-    if (!src_it.next(s, d, nb)) {
-      more = false;
-      return;
-    }
     const int t = (int)(issued % stages);
-    if (issued >= stages) bulk_wait_read_1();  // store of piece issued-S done reading
-    pdst[t] = d;
-    pnb[t] = nb;
-    bulk_load(base + (uint32_t)t * piece, s, nb, &bar[t]);
+    uint32_t used = 0;
+    int n = 0;
+    while (n < kMaxSub && piece - used >= 1024) {
+      const char* s;
+      char* d;
+      uint32_t nb;
+      if (!src_it.next(s, d, nb, piece - used)) {
+        more = false;
+        break;
+      }
+      psrc[n] = s;
+      pdst[t][n] = d;
+      pnb[t][n] = nb;
+      poff[t][n] = used;
+      used += nb;
+      ++n;
+    }
+    if (n == 0) return;
+    if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
+    pcnt[t] = n;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[t])),
+                 "r"(used)
+                 : "memory");
+    for (int i = 0; i < n; ++i) {
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              base + (uint32_t)t * piece + poff[t][i]),
+          "l"(psrc[i]), "r"(pnb[t][i]), "r"(smem_u32(&bar[t]))
+          : "memory");
+    }
     ++issued;
   };
   while (more && issued < lookahead) issue();
@@ -250,7 +279,11 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
     if (more) issue();
     const int t = (int)(stored % stages);
     bar_wait(&bar[t], (uint32_t)((stored / stages) & 1));
-    bulk_store(pdst[t], base + (uint32_t)t * piece, pnb[t]);
+    for (int i = 0; i < pcnt[t]; ++i)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pdst[t][i]),
+                   "r"(base + (uint32_t)t * piece + poff[t][i]), "r"(pnb[t][i])
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     ++stored;
   }
   bulk_wait_all();
