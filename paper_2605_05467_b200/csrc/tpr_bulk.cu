@@ -242,12 +242,30 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
   bool more = true;
   auto issue = [&]() {
     const int t = (int)(issued % stages);
-    uint32_t used = 0;
-    int n = 0;
-    while (n < kMaxSub && piece - used >= 1024) {
-      const char* s;
-      char* d;
-      uint32_t nb;
+    const char* s;
+    char* d;
+    uint32_t nb;
+    if (!src_it.next(s, d, nb, piece)) {
+      more = false;
+      return;
+    }
+    if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
+    if (nb == piece) {  // fast path: one copy fills the stage (full-page chunks)
+      pcnt[t] = 1;
+      pdst[t][0] = d;
+      pnb[t][0] = nb;
+      poff[t][0] = 0;
+      bulk_load(base + (uint32_t)t * piece, s, nb, &bar[t]);
+      ++issued;
+      return;
+    }
+    psrc[0] = s;
+    pdst[t][0] = d;
+    pnb[t][0] = nb;
+    poff[t][0] = 0;
+    uint32_t used = nb;
+    int n = 1;
+    while (n < kMaxSub && piece - used >= 1024) {  // pack further short copies
       if (!src_it.next(s, d, nb, piece - used)) {
         more = false;
         break;
@@ -259,8 +277,6 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
       used += nb;
       ++n;
     }
-    if (n == 0) return;
-    if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
     pcnt[t] = n;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[t])),
                  "r"(used)
