@@ -70,30 +70,6 @@ __device__ __forceinline__ void bulk_wait_all() {
 
 // ---- piece sources ---------------------------------------------------------
 
-// Strided items (the ntok valid tokens of every plane of a partial last page,
-// or a row-parallel weight slice: many short rows at a pitch) are copied by
-// the whole warp with 16-B loads/stores instead of one TMA copy per row.
-__device__ __forceinline__ void warp_rows_copy(const char* s, char* d, int64_t nr, int64_t nb,
-                                               int64_t sp, int64_t dp, unsigned lane) {
-  const uint32_t vpr = (uint32_t)(nb >> 4), nvec = vpr * (uint32_t)nr;
-  for (uint32_t base = 0; base < nvec; base += 32u * 4u) {
-    int4 v[4];
-    uint32_t row[4], col[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t k = base + (uint32_t)u * 32u + lane;
-      row[u] = k / vpr;
-      col[u] = k - row[u] * vpr;
-      if (k < nvec) v[u] = *(reinterpret_cast<const int4*>(s + row[u] * sp) + col[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t k = base + (uint32_t)u * 32u + lane;
-      if (k < nvec) *(reinterpret_cast<int4*>(d + row[u] * dp) + col[u]) = v[u];
-    }
-  }
-}
-
 // K1: the CTA's work items (grid-stride) -> pieces. A full page item is one
 // contiguous span cut into `piece`-byte pieces; a partial page item is one piece
 // per plane row (ntok valid tokens).
@@ -140,17 +116,8 @@ struct KvPieces {
     }
     return false;
   }
-  // Every lane calls next() in lockstep (the item sequence is deterministic);
-  // strided items are copied here by the warp, contiguous spans become pieces.
-  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes,
-                       unsigned lane) {
-    while (rows_left == 0 || (rows_left > 1 && off == 0)) {
-      if (rows_left == 0 && !load_item()) return false;
-      if (rows_left > 1) {  // partial page: ntok valid tokens in each of nr planes
-        warp_rows_copy(s, d, rows_left, row_bytes, pitch, pitch, lane);
-        rows_left = 0;
-      }
-    }
+  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes) {
+    if (rows_left == 0 && !load_item()) return false;
     const int64_t take = min((int64_t)max_bytes, row_bytes - off);
     src = s + off;
     dst = d + off;
@@ -178,7 +145,6 @@ struct SegPieces {
   char* d;
   int64_t rows_left, row_bytes, sp, dp, off;
   bool aligned;
-  unsigned lane;
 
   __device__ void start(int64_t first) {
     item = first;
@@ -188,12 +154,10 @@ struct SegPieces {
     while (item < n_items) {
       if (!load_one()) continue;
       if (aligned) return true;
-      // unaligned segment (never for the Llama geometries): byte copy by the
-      // warp, then move on
-      for (int64_t k = lane; k < rows_left * row_bytes; k += 32) {
-        const int64_t r = k / row_bytes, b = k - r * row_bytes;
-        d[r * dp + b] = s[r * sp + b];
-      }
+      // unaligned segment (never for the Llama geometries): plain byte copy by
+      // the issuing thread, then move on
+      for (int64_t r = 0; r < rows_left; ++r)
+        for (int64_t b = 0; b < row_bytes; ++b) d[r * dp + b] = s[r * sp + b];
       rows_left = 0;
     }
     return false;
@@ -235,16 +199,8 @@ struct SegPieces {
     }
     return false;
   }
-  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes,
-                       unsigned lane_) {
-    lane = lane_;
-    while (rows_left == 0 || (rows_left > 1 && off == 0)) {
-      if (rows_left == 0 && !load_item()) return false;
-      if (rows_left > 1) {  // row-parallel slice: short rows at a pitch
-        warp_rows_copy(s, d, rows_left, row_bytes, sp, dp, lane);
-        rows_left = 0;
-      }
-    }
+  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes) {
+    if (rows_left == 0 && !load_item()) return false;
     const int64_t take = min((int64_t)max_bytes, row_bytes - off);
     src = s + off;
     dst = d + off;
@@ -267,9 +223,6 @@ constexpr int kMaxSub = 16;  // copies packed into one shared-memory stage
 // or many short rows of partial pages / row-parallel weight slices). The
 // stage's loads all complete on one mbarrier; its stores form one bulk group,
 // so small copies still keep a full stage of bytes in flight.
-// All 32 lanes walk the (deterministic) item sequence in lockstep: strided
-// items are copied by the whole warp inside Source::next, and lane 0 alone
-// keeps the shared-memory bookkeeping and issues every TMA copy.
 template <class Source>
 __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -279,15 +232,11 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
   __shared__ uint32_t poff[kMaxStages][kMaxSub];
   __shared__ int pcnt[kMaxStages];
   __shared__ const char* psrc[kMaxSub];  // sources of the stage being filled
-  const unsigned lane = threadIdx.x & 31u;
-  const bool leader = lane == 0;
+  if (threadIdx.x != 0) return;
   const uint32_t piece = src_it.piece;
   const int lookahead = stages - 2;  // => the refilled stage's last store may still be pending
-  if (leader) {
-    for (int s = 0; s < stages; ++s) bar_init(&bar[s]);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncwarp();
+  for (int s = 0; s < stages; ++s) bar_init(&bar[s]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const uint32_t base = smem_u32(smem);
   int64_t issued = 0, stored = 0;
   bool more = true;
@@ -296,76 +245,64 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
     const char* s;
     char* d;
     uint32_t nb;
-    if (!src_it.next(s, d, nb, piece, lane)) {
+    if (!src_it.next(s, d, nb, piece)) {
       more = false;
       return;
     }
-    if (leader && issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
+    if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
     if (nb == piece) {  // fast path: one copy fills the stage (full-page chunks)
-      if (leader) {
-        pcnt[t] = 1;
-        pdst[t][0] = d;
-        pnb[t][0] = nb;
-        poff[t][0] = 0;
-        bulk_load(base + (uint32_t)t * piece, s, nb, &bar[t]);
-      }
-      ++issued;
-      return;
-    }
-    if (leader) {
-      psrc[0] = s;
+      pcnt[t] = 1;
       pdst[t][0] = d;
       pnb[t][0] = nb;
       poff[t][0] = 0;
+      bulk_load(base + (uint32_t)t * piece, s, nb, &bar[t]);
+      ++issued;
+      return;
     }
+    psrc[0] = s;
+    pdst[t][0] = d;
+    pnb[t][0] = nb;
+    poff[t][0] = 0;
     uint32_t used = nb;
     int n = 1;
     while (n < kMaxSub && piece - used >= 1024) {  // pack further short copies
-      if (!src_it.next(s, d, nb, piece - used, lane)) {
+      if (!src_it.next(s, d, nb, piece - used)) {
         more = false;
         break;
       }
-      if (leader) {
-        psrc[n] = s;
-        pdst[t][n] = d;
-        pnb[t][n] = nb;
-        poff[t][n] = used;
-      }
+      psrc[n] = s;
+      pdst[t][n] = d;
+      pnb[t][n] = nb;
+      poff[t][n] = used;
       used += nb;
       ++n;
     }
-    if (leader) {
-      pcnt[t] = n;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       smem_u32(&bar[t])),
-                   "r"(used)
-                   : "memory");
-      for (int i = 0; i < n; ++i) {
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                base + (uint32_t)t * piece + poff[t][i]),
-            "l"(psrc[i]), "r"(pnb[t][i]), "r"(smem_u32(&bar[t]))
-            : "memory");
-      }
+    pcnt[t] = n;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[t])),
+                 "r"(used)
+                 : "memory");
+    for (int i = 0; i < n; ++i) {
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              base + (uint32_t)t * piece + poff[t][i]),
+          "l"(psrc[i]), "r"(pnb[t][i]), "r"(smem_u32(&bar[t]))
+          : "memory");
     }
     ++issued;
   };
   while (more && issued < lookahead) issue();
   while (stored < issued) {
     if (more) issue();
-    if (leader) {
-      const int t = (int)(stored % stages);
-      bar_wait(&bar[t], (uint32_t)((stored / stages) & 1));
-      for (int i = 0; i < pcnt[t]; ++i)
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                         pdst[t][i]),
-                     "r"(base + (uint32_t)t * piece + poff[t][i]), "r"(pnb[t][i])
-                     : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
+    const int t = (int)(stored % stages);
+    bar_wait(&bar[t], (uint32_t)((stored / stages) & 1));
+    for (int i = 0; i < pcnt[t]; ++i)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pdst[t][i]),
+                   "r"(base + (uint32_t)t * piece + poff[t][i]), "r"(pnb[t][i])
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     ++stored;
   }
-  if (leader) bulk_wait_all();
+  bulk_wait_all();
 }
 
 __global__ void __launch_bounds__(32)
