@@ -69,6 +69,24 @@ class KvLayout:
         per = self.heads_per_rank
         return tuple(g for g in self.group for _ in range(per))
 
+    def request_arrays(self) -> tuple[np.ndarray, np.ndarray]:
+        """(request ids, context lengths) as int64 arrays, cached when immutable.
+
+        The planner's vectorised path reads these instead of walking the
+        tuples; a layout built with a list of requests is re-read every call.
+        """
+        cached = self.__dict__.get("_req_arrays")
+        if cached is not None:
+            return cached
+        if self.requests:
+            arr = np.asarray(self.requests, dtype=np.int64).reshape(-1, 2)
+            out = (np.ascontiguousarray(arr[:, 0]), np.ascontiguousarray(arr[:, 1]))
+        else:
+            out = (np.zeros(0, np.int64), np.zeros(0, np.int64))
+        if isinstance(self.requests, tuple):
+            self.__dict__["_req_arrays"] = out  # frozen: bypass __setattr__
+        return out
+
 
 @dataclass(frozen=True)
 class Transfer:
@@ -213,10 +231,68 @@ def _plan_native(rows: list[tuple[int, int, tuple, int, tuple, int]], total_head
     table = _GroupTable()
     cols = np.array([(r, c, table.offset(og), otp, table.offset(ng), ntp)
                      for r, c, og, otp, ng, ntp in rows], dtype=np.int64)
-    req = np.ascontiguousarray(cols[:, 0])
-    ctx = np.ascontiguousarray(cols[:, 1])
     meta = np.ascontiguousarray(cols[:, 2:6].T, dtype=np.int32)  # old_off, old_tp, new_off, new_tp
-    ids = np.asarray(table.ids, dtype=np.int64)
+    return _call_planner(np.ascontiguousarray(cols[:, 0]), np.ascontiguousarray(cols[:, 1]), meta,
+                         np.asarray(table.ids, dtype=np.int64), total_heads, kvb)
+
+
+def _layout_table(layouts) -> tuple[np.ndarray, np.ndarray, _GroupTable]:
+    """Per-layout (group offset, tp) into one shared group table."""
+    table = _GroupTable()
+    off = np.array([table.offset(lay.group) for lay in layouts], dtype=np.int32)
+    tp = np.array([lay.tp for lay in layouts], dtype=np.int32)
+    return off, tp, table
+
+
+# below this many requests the row walk beats numpy's per-call overhead
+_VECTORISE_MIN_REQUESTS = 48
+
+
+def _plan_vectorised(old_layouts, new_layouts, total_heads: int, kvb: int):
+    """plan_repartition's matching + validation on cached per-layout arrays.
+
+    Same checks, order and messages as the row-by-row path below; returns None
+    (use that path) when an old request id repeats, where the reference's
+    last-one-wins dict semantics apply (migration.py:160-163).
+    """
+    if not old_layouts and not new_layouts:
+        return None
+    o = [lay.request_arrays() for lay in old_layouts]
+    nw = [lay.request_arrays() for lay in new_layouts]
+    if not o or not nw:
+        return None
+    old_ids = np.concatenate([a for a, _ in o])
+    new_ids = np.concatenate([a for a, _ in nw])
+    order = np.argsort(old_ids, kind="stable")
+    sorted_old = old_ids[order]
+    if len(sorted_old) > 1 and bool((sorted_old[1:] == sorted_old[:-1]).any()):
+        return None
+    if len(new_ids) != len(old_ids) or not np.array_equal(np.sort(new_ids), sorted_old):
+        raise MigrationError("new layouts must carry exactly the old requests")
+    n = len(new_ids)
+    if n == 0:
+        return np.zeros((0, 6), dtype=np.int64)
+    pos = order[np.searchsorted(sorted_old, new_ids)]
+    old_ctx = np.concatenate([c for _, c in o])[pos]
+    new_ctx = np.concatenate([c for _, c in nw])
+    bad = np.flatnonzero(old_ctx != new_ctx)
+    if len(bad):
+        raise MigrationError(f"request {int(new_ids[bad[0]])}: context length changed")
+    off, tp, table = _layout_table([*old_layouts, *new_layouts])
+    n_old = len(old_layouts)
+    old_lay = np.repeat(np.arange(n_old), [len(a) for a, _ in o])[pos]
+    new_lay = np.repeat(np.arange(len(new_layouts)), [len(a) for a, _ in nw]) + n_old
+    meta = np.empty((4, n), dtype=np.int32)
+    meta[0], meta[1] = off[old_lay], tp[old_lay]
+    meta[2], meta[3] = off[new_lay], tp[new_lay]
+    return _call_planner(new_ids, new_ctx, meta, np.asarray(table.ids, dtype=np.int64),
+                         total_heads, kvb)
+
+
+def _call_planner(req: np.ndarray, ctx: np.ndarray, meta: np.ndarray, ids: np.ndarray,
+                  total_heads: int, kvb: int) -> np.ndarray:
+    """tpr_plan_heads over int64 req/ctx and int32 meta [4][n]."""
+    n = len(req)
     cap = n * total_heads
     out = _out_buffer(cap)
     n_out = _native.c_int64(0)
@@ -241,8 +317,14 @@ def head_transfers(old: KvLayout, new: KvLayout, kv_bytes_per_token_per_head: in
 def head_transfers_array(old: KvLayout, new: KvLayout, kvb: int) -> MigrationPlan:
     if old.total_heads != new.total_heads:
         raise MigrationError("head counts differ between layouts")
-    rows = [(r, c, old.group, old.tp, new.group, new.tp) for r, c in old.requests]
-    return MigrationPlan.from_array(_plan_native(rows, old.total_heads, kvb))
+    req, ctx = old.request_arrays()
+    if len(req) == 0:
+        return MigrationPlan.from_array(np.zeros((0, 6), dtype=np.int64))
+    off, tp, table = _layout_table([old, new])
+    meta = np.empty((4, len(req)), dtype=np.int32)
+    meta[0], meta[1], meta[2], meta[3] = off[0], tp[0], off[1], tp[1]
+    return MigrationPlan.from_array(_call_planner(
+        req, ctx, meta, np.asarray(table.ids, dtype=np.int64), old.total_heads, kvb))
 
 
 def plan_repartition(old_layouts: list[KvLayout], new_layouts, kv_bytes_per_token_per_head: int,
@@ -260,6 +342,13 @@ def plan_repartition(old_layouts: list[KvLayout], new_layouts, kv_bytes_per_toke
         raise MigrationError(f"GPU sets differ: old={sorted(old_gpus)} new={sorted(new_gpus)}")
     if len({lay.total_heads for lay in [*old_layouts, *new_layouts]}) != 1:
         raise MigrationError("all layouts must share total_heads")
+    total_heads = new_layouts[0].total_heads if new_layouts else (
+        old_layouts[0].total_heads if old_layouts else 1)
+    fast = None
+    if sum(len(lay.requests) for lay in new_layouts) >= _VECTORISE_MIN_REQUESTS:
+        fast = _plan_vectorised(old_layouts, new_layouts, total_heads, kv_bytes_per_token_per_head)
+    if fast is not None:
+        return MigrationPlan.from_array(fast, handshake_ms=handshake_ms)
     source: dict[int, tuple[KvLayout, int]] = {}
     for lay in old_layouts:
         for rid, ctx in lay.requests:
@@ -274,8 +363,6 @@ def plan_repartition(old_layouts: list[KvLayout], new_layouts, kv_bytes_per_toke
             if old_ctx != ctx:
                 raise MigrationError(f"request {rid}: context length changed")
             rows.append((rid, ctx, old.group, old.tp, lay.group, lay.tp))
-    total_heads = new_layouts[0].total_heads if new_layouts else (
-        old_layouts[0].total_heads if old_layouts else 1)
     arr = _plan_native(rows, total_heads, kv_bytes_per_token_per_head)
     return MigrationPlan.from_array(arr, handshake_ms=handshake_ms)
 

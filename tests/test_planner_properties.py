@@ -78,3 +78,44 @@ def test_head_transfers_disjoint_groups(data):
     assert got == want
     # disjoint groups: every head of every request moves
     assert sum(t[4] - t[3] for t in got) == H * len(reqs)
+
+
+def _both_paths(lo, ln, kvb):
+    """plan_repartition through the row walk and through the vectorised path."""
+    out = []
+    saved = M._VECTORISE_MIN_REQUESTS
+    for threshold in (10**9, 0):
+        M._VECTORISE_MIN_REQUESTS = threshold
+        try:
+            out.append(("ok", M.plan_repartition(lo, ln, kvb).as_array().tolist()))
+        except M.MigrationError as exc:
+            out.append(("err", str(exc)))
+        finally:
+            M._VECTORISE_MIN_REQUESTS = saved
+    return out
+
+
+@settings(max_examples=300, deadline=None)
+@given(transitions(), st.sampled_from(["none", "drop", "ctx", "dup_old", "dup_new"]), st.data())
+def test_vectorised_planner_matches_row_walk(t, corrupt, data):
+    """Plans and error messages agree between the two planning paths,
+    including invalid inputs (missing / duplicated requests, changed context)."""
+    H, og, old, ng, new, kvb = t
+    old = [list(r) for r in old]
+    new = [list(r) for r in new]
+    flat_new = [(i, j) for i, rs in enumerate(new) for j in range(len(rs))]
+    if corrupt != "none" and flat_new:
+        i, j = data.draw(st.sampled_from(flat_new))
+        rid, ctx = new[i][j]
+        if corrupt == "drop":
+            del new[i][j]
+        elif corrupt == "ctx":
+            new[i][j] = (rid, ctx + 1)
+        elif corrupt == "dup_old":
+            old[0].append((rid, ctx))
+        else:
+            new[i].append((rid, ctx))
+    lo = [M.KvLayout(g, len(g), H, tuple(r)) for g, r in zip(og, old)]
+    ln = [M.KvLayout(g, len(g), H, tuple(r)) for g, r in zip(ng, new)]
+    rows, vec = _both_paths(lo, ln, kvb)
+    assert rows == vec

@@ -76,19 +76,22 @@ def main():
                     for p in (fwd, back):  # warm-up, leaves the cluster in layout A
                         cluster.migrate(p, validate=False)
                     torch.cuda.synchronize()
-                    dev_ms, host_ms = [], []
+                    dev_ms, host_ms, exec_ms, plan_ms = [], [], [], []
                     for r in range(args.reps):
                         p = fwd if r % 2 == 0 else back
-                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0, ep, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                         t0 = time.perf_counter()
                         e0.record(stream)
                         plan = M.plan_repartition(*((la, lb) if r % 2 == 0 else (lb, la)),
                                                   kv.kv_bytes_per_token_per_head)
+                        plan_ms.append((time.perf_counter() - t0) * 1e3)
+                        ep.record(stream)
                         cluster.migrate(plan, validate=False)
                         e1.record(stream)
                         e1.synchronize()
                         host_ms.append((time.perf_counter() - t0) * 1e3)
                         dev_ms.append(e0.elapsed_time(e1))
+                        exec_ms.append(ep.elapsed_time(e1))
                     if args.reps % 2:
                         cluster.migrate(back, validate=False)
                     v = cluster.verify(seed=n)
@@ -96,6 +99,7 @@ def main():
                     cluster.release([r for r, _ in reqs])
                     nbytes = fwd.total_bytes
                     d = float(np.median(dev_ms))
+                    x = float(np.median(exec_ms))
                     cpu_ms = cpu_point(la, lb, reqs, gpus, kv) if n <= args.cpu_max_seqs else None
                     row = {
                         "mode": mode, "tp_old": a, "tp_new": b, "seqs": n,
@@ -103,6 +107,9 @@ def main():
                         "device_ms": d, "host_ms": float(np.median(host_ms)),
                         "gbs": nbytes / (d * 1e-3) / 1e9 if d > 0 else None,
                         "hbm_frac": (2 * nbytes / (peak * 1e9)) / (d * 1e-3) if d > 0 else None,
+                        # without the host planning the GPU idles through
+                        "plan_host_ms": float(np.median(plan_ms)), "exec_device_ms": x,
+                        "exec_hbm_frac": (2 * nbytes / (peak * 1e9)) / (x * 1e-3) if x > 0 else None,
                         "predicted_ms_ref_model": M.switch_cost(M.WARM, fwd, params),
                         "cpu_restatement_ms": cpu_ms, "bit_exact_property": ok,
                     }

@@ -27,7 +27,13 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=str(ROOT / "profiles" / "weight_sweep.jsonl"))
+    ap.add_argument("--reps", type=int, default=5, help="timed a->b reshards (median)")
+    ap.add_argument("--engine", choices=["bulk", "vector"], default="bulk")
+    ap.add_argument("--only", default="", help="comma list of slots:a:b, e.g. 8:2:4")
     args = ap.parse_args()
+    from paper_2605_05467_b200 import _native
+    _native.set_copy_engine(args.engine)
+    only = {tuple(int(v) for v in x.split(":")) for x in args.only.split(",") if x}
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     out = open(args.out, "w")
@@ -35,27 +41,29 @@ def main():
         gpus = tuple(range(n))
         for a in levels:
             for b in levels:
-                if a == b:
+                if a == b or (only and (n, a, b) not in only):
                     continue
-                # untimed pass first: the first touch of freshly cudaMalloc'd
-                # arenas costs ~0.1 ms/GB once per process; serving reuses them
-                warm = ShardedWeightStore(LLAMA_3_1_8B, gpus)
-                warm.load(workloads.tp_groups(gpus, a))
-                warm.reshard(workloads.tp_groups(gpus, b))
-                torch.cuda.synchronize()
-                del warm
+                # a->b timed, b->a untimed, repeated; the first pair is warm-up
+                # (the first touch of freshly cudaMalloc'd arenas costs ~0.1
+                # ms/GB once per process; the caching allocator reuses them)
                 store = ShardedWeightStore(LLAMA_3_1_8B, gpus)
                 store.load(workloads.tp_groups(gpus, a))
                 torch.cuda.synchronize()
                 st = torch.cuda.current_stream()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s = store.reshard(workloads.tp_groups(gpus, b), stream=st, events=(e0, e1))
-                torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1)
+                times = []
+                for r in range(args.reps + 1):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s = store.reshard(workloads.tp_groups(gpus, b), stream=st, events=(e0, e1))
+                    torch.cuda.synchronize()
+                    if r:
+                        times.append(e0.elapsed_time(e1))
+                    if r < args.reps:
+                        store.reshard(workloads.tp_groups(gpus, a), stream=st)
+                ms = sorted(times)[len(times) // 2]
                 bad = store.verify()
                 row = {"gpus": n, "tp_old": a, "tp_new": b, "views": s.views,
                        "local_bytes": s.local_bytes, "remote_bytes": s.remote_bytes,
-                       "segments": s.segments, "k2_ms": ms,
+                       "segments": s.segments, "k2_ms": ms, "k2_ms_min": min(times),
                        "gbs": s.bytes / (ms * 1e-3) / 1e9 if s.bytes else None,
                        "hbm_frac": (2 * s.bytes / (peak * 1e9)) / (ms * 1e-3) if s.bytes else None,
                        "max_ingress": max(s.ingress.values()), "max_egress": max(s.egress.values()),
