@@ -169,9 +169,13 @@ typedef struct tpr_copy_seg {
  * the given chunk size. Returns the number of items in *n_items. */
 int tpr_copy_prepare(tpr_copy_seg_t* segs, int32_t n, int64_t chunk_bytes,
                      int64_t* prefix, int64_t* n_items);
+/* d_claim: optional device int64 that is 0 when the kernel starts (stream
+ * order; e.g. uploaded with the segments). With it, CTAs claim batches of
+ * items dynamically (no tail when CTAs run at different speeds); NULL keeps
+ * the static grid-stride schedule. The kernel leaves it non-zero. */
 int tpr_weight_reshard(const tpr_copy_seg_t* d_segs, const int64_t* d_prefix,
                        int32_t n_segs, int64_t n_items, int64_t chunk_bytes,
-                       void* stream);
+                       int64_t* d_claim, void* stream);
 
 /* ---- synthetic data + full-size property checks (device) --------------- */
 /* Pattern fill of every work unit's valid tokens in its destination pool

@@ -92,7 +92,8 @@ _SIGNATURES = {
                                 c_void_p]),
     "tpr_memcpy_h2d": (c_int32, [c_uint64, c_void_p, c_uint64, c_void_p]),
     "tpr_copy_prepare": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, _P64]),
-    "tpr_weight_reshard": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p]),
+    "tpr_weight_reshard": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p,
+                                     c_void_p]),
     "tpr_kv_fill": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
                               c_int64, c_uint64, c_void_p]),
     "tpr_pool_fill": (c_int32, [POINTER(KvGeometryC), c_uint64, c_int32, c_uint64, c_void_p]),

@@ -88,9 +88,9 @@ cudaError_t run_k1(const tpr::KvCopyParams& p, const tpr::KvClusterParams& cl, c
 }
 
 cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
-                   int64_t n_items, int64_t chunk, cudaStream_t st) {
+                   int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st) {
   return g_engine.load() == TPR_ENGINE_BULK
-             ? tpr::launch_k2_bulk(segs, prefix, n_segs, n_items, chunk, st)
+             ? tpr::launch_k2_bulk(segs, prefix, n_segs, n_items, chunk, claim, st)
              : tpr::launch_k2(segs, prefix, n_segs, n_items, chunk, st);
 }
 
@@ -312,12 +312,12 @@ int tpr_copy_prepare(tpr_copy_seg_t* segs, int32_t n, int64_t chunk, int64_t* pr
 }
 
 int tpr_weight_reshard(const tpr_copy_seg_t* d_segs, const int64_t* d_prefix, int32_t n_segs,
-                       int64_t n_items, int64_t chunk, void* stream) {
+                       int64_t n_items, int64_t chunk, int64_t* d_claim, void* stream) {
   if (n_segs < 0 || n_items < 0 || chunk <= 0) return fail(TPR_EINVAL, "bad reshard arguments");
   if (n_items == 0) return TPR_OK;
   if (!d_segs || !d_prefix) return fail(TPR_EINVAL, "null segment buffers");
-  cudaError_t e = run_k2(d_segs, d_prefix, n_segs, n_items, chunk,
-                                 static_cast<cudaStream_t>(stream));
+  cudaError_t e = run_k2(d_segs, d_prefix, n_segs, n_items, chunk, d_claim,
+                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_weight_reshard launch");
 }
 

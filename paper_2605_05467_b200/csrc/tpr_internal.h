@@ -46,7 +46,7 @@ cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            int64_t n_units, cudaStream_t st);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
-                           int64_t n_items, int64_t chunk, cudaStream_t st);
+                           int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            const int4* work_ext, int64_t n_units, uint64_t seed,
                            cudaStream_t st);

@@ -301,8 +301,10 @@ class ShardedWeightStore:
         from .kvcache import _PinnedStaging, _Scratch
 
         n = len(seg)
-        buf = np.empty(seg.size + n + 1, dtype=np.int64)
+        # segments | prefix[n + 1] | dynamic-claim counter (uploaded as 0)
+        buf = np.empty(seg.size + n + 2, dtype=np.int64)
         buf[: seg.size] = seg.reshape(-1)
+        buf[-1] = 0
         n_items = ctypes.c_int64(0)
         _native.call("tpr_copy_prepare", buf.ctypes.data, n, CHUNK_BYTES,
                      buf.ctypes.data + seg.nbytes, ctypes.byref(n_items))
@@ -313,7 +315,8 @@ class ShardedWeightStore:
         with torch.cuda.device(dev):
             staging.upload(buf, d, stream)
             _native.call("tpr_weight_reshard", d.data_ptr(), d.data_ptr() + seg.nbytes, n,
-                         n_items.value, CHUNK_BYTES, stream.cuda_stream)
+                         n_items.value, CHUNK_BYTES, d.data_ptr() + 8 * (buf.size - 1),
+                         stream.cuda_stream)
 
     def finish(self) -> None:
         """Wait for the last reshard's copies."""

@@ -66,8 +66,9 @@ def aggregate_pipelined(c, su, du, st, chunk_pages: int = 512):
 
     def launch(desc, stream):
         d, off, n, items = desc
+        # descriptors are reused across launches: static schedule (no claim counter)
         _native.call("tpr_weight_reshard", d.data_ptr(), d.data_ptr() + off, n, items, CHUNK_BYTES,
-                     stream.cuda_stream)
+                     None, stream.cuda_stream)
 
     chunks = [(su[i:i + chunk_pages], du[i:i + chunk_pages]) for i in range(0, len(su), chunk_pages)]
     packs, unpacks = [], []

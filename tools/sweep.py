@@ -44,6 +44,9 @@ def main():
     ap.add_argument("--max-seqs", type=int, default=128)
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--cpu-max-seqs", type=int, default=8)
+    ap.add_argument("--modes", default="fixed4096,trace")
+    ap.add_argument("--k1-reps", type=int, default=2,
+                    help="extra switches timed with events around K1 alone (k1_ms)")
     args = ap.parse_args()
 
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
@@ -60,7 +63,7 @@ def main():
     params = M.CostModelParams()
     out = open(args.out, "w")
     stream = torch.cuda.current_stream()
-    for mode in ("fixed4096", "trace"):
+    for mode in args.modes.split(","):
         for a in (1, 2, 4, 8):
             for b in (1, 2, 4, 8):
                 if a == b:
@@ -94,6 +97,14 @@ def main():
                         exec_ms.append(ep.elapsed_time(e1))
                     if args.reps % 2:
                         cluster.migrate(back, validate=False)
+                    k1_ms = []
+                    for r in range(2 * args.k1_reps):  # fwd/back pairs: ends in layout A
+                        k0, k1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                        cluster.migrate(fwd if r % 2 == 0 else back, validate=False,
+                                        k1_events=(k0, k1))
+                        k1.synchronize()
+                        if r % 2 == 0:
+                            k1_ms.append(k0.elapsed_time(k1))
                     v = cluster.verify(seed=n)
                     ok = v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
                     cluster.release([r for r, _ in reqs])
@@ -110,6 +121,9 @@ def main():
                         # without the host planning the GPU idles through
                         "plan_host_ms": float(np.median(plan_ms)), "exec_device_ms": x,
                         "exec_hbm_frac": (2 * nbytes / (peak * 1e9)) / (x * 1e-3) if x > 0 else None,
+                        "k1_ms": float(np.median(k1_ms)) if k1_ms else None,
+                        "k1_hbm_frac": (2 * nbytes / (peak * 1e9)) / (float(np.median(k1_ms)) * 1e-3)
+                        if k1_ms else None,
                         "predicted_ms_ref_model": M.switch_cost(M.WARM, fwd, params),
                         "cpu_restatement_ms": cpu_ms, "bit_exact_property": ok,
                     }
