@@ -43,6 +43,8 @@ enum tpr_status {
   TPR_EINVAL = -1,     /* bad argument                                   */
   TPR_ECUDA = -2,      /* CUDA runtime error                             */
   TPR_ECAPACITY = -3,  /* output buffer too small                        */
+  TPR_ENOTFOUND = -4,  /* id outside the caller's lookup tables: resolve  */
+                       /* it with the caller's own maps and retry there   */
 };
 
 /* Device-side status bits written by the K3 remap kernel (status word). */
@@ -138,6 +140,35 @@ int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
 /* Copies the valid tokens of every work unit from pool[src] to pool[dst]. */
 int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* d_work, int64_t n_units, void* stream);
+
+/* ---- switch bookkeeping (host) ----------------------------------------- */
+/* Plan rows -> K3 records, per-GPU-slot unit deltas and the plan checks of
+ * migration.py:192-207, in one pass over the plan (replaces the per-transfer
+ * Python walk between plan_repartition and the device).
+ *   plan      int64 [n][6] {src_gpu, dst_gpu, request_id, head_lo, head_hi,
+ *             bytes} (the MigrationPlan SoA, tpr_plan_heads' output)
+ *   gpu_lut   [gpu id] -> slot, -1 absent;  gpu_ids [slot] -> gpu id
+ *   req_lut   [request id] -> request slot, -1 absent
+ *   slot_ctx  [request slot] -> context tokens
+ *   owner     [request slot][total_heads] -> GPU slot holding the head
+ *   validate  0: ids and head ranges only; 1: also bytes == (hi-lo)*ctx*kvb,
+ *             no (request, head) moved twice, every head on its src_gpu
+ *   records   int32 [n][6] {src slot, dst slot, request slot, lo, hi, ctx}
+ *   in_units / out_units [n_slots]: units entering / leaving each slot;
+ *   *total_units = units moved.
+ * Errors: TPR_ENOTFOUND when an id is outside a table (the caller falls back
+ * to its maps, which either resolve it or raise the reference error);
+ * TPR_EINVAL with the reference's MigrationError text otherwise. */
+int tpr_kv_records(const int64_t* plan, int64_t n, const int64_t* gpu_lut, int64_t gpu_lut_len,
+                   const int64_t* gpu_ids, int32_t n_slots, const int64_t* req_lut,
+                   int64_t req_lut_len, const int32_t* slot_ctx, const int32_t* owner,
+                   int32_t n_req_slots, int32_t total_heads, int32_t block_tokens, int64_t kvb,
+                   int32_t validate, int32_t* records, int64_t* in_units, int64_t* out_units,
+                   int64_t* total_units);
+
+/* After a switch is enqueued: owner[req slot][h] = dst slot for every head of
+ * every record (apply_plan, migration.py:192-207, on the host placement). */
+int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads);
 
 /* ---- K3 + K1 in one call ----------------------------------------------- */
 /* The switch fast path: async H2D copy of the records from pinned host memory

@@ -21,12 +21,14 @@ TPR_TOTALS_LEN = 1 + 2 * TPR_MAX_GPUS
 TPR_STATUS_WRONG_SOURCE = 1
 TPR_STATUS_DST_OCCUPIED = 2
 TPR_STATUS_BARRIER_TIMEOUT = 4
+TPR_ENOTFOUND = -4  # an id outside the caller's lookup tables (use the Python maps)
 
 # Every exported symbol of include/tpr.h; tests check the library exports all.
 EXPORTS = (
     "tpr_set_copy_engine", "tpr_get_copy_engine",
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads",
-    "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_switch", "tpr_memcpy_h2d",
+    "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
+    "tpr_memcpy_h2d",
     "tpr_copy_prepare", "tpr_weight_reshard",
     "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
     "tpr_matrix_verify", "tpr_baseline_copy_pages", "tpr_device_barrier", "tpr_device_alloc",
@@ -87,6 +89,10 @@ _SIGNATURES = {
                                c_void_p, c_void_p]),
     "tpr_kv_migrate": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int64,
                                  c_void_p]),
+    "tpr_kv_records": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int32, c_void_p,
+                                 c_int64, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64,
+                                 c_int32, c_void_p, c_void_p, c_void_p, _P64]),
+    "tpr_kv_apply_owner": (c_int32, [c_void_p, c_int64, c_void_p, c_int32]),
     "tpr_kv_switch": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                 c_void_p]),

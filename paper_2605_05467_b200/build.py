@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libtpr.so"
 
-SOURCES = [CSRC / "tpr_kernels.cu", CSRC / "tpr_bulk.cu", CSRC / "tpr_api.cpp"]
+SOURCES = [CSRC / "tpr_kernels.cu", CSRC / "tpr_bulk.cu", CSRC / "tpr_api.cpp", CSRC / "tpr_host.cpp"]
 HEADERS = [INCLUDE / "tpr.h", CSRC / "tpr_common.cuh", CSRC / "tpr_internal.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -27,6 +27,13 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+int vfail(int code, const char* fmt, va_list ap) {
+  char buf[512];
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  g_err = buf;
+  return code;
+}
+
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(TPR_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
@@ -97,6 +104,14 @@ cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_
 }  // namespace
 
 namespace tpr {
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vfail(code, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
 int sm_count() {
   static int cache[64] = {0};
   int dev = 0;

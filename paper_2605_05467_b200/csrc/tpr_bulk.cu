@@ -392,8 +392,10 @@ __global__ void __launch_bounds__(32)
 // B200 (profiles/README.md): K1 streams whole 32 KiB page chunks and is
 // fastest with one CTA per SM and 32 KiB pieces (6 x 32 KiB = 192 KiB, at the
 // measured copy peak); K2's row-parallel slices are 1-7 KiB rows, so it wants
-// more issuing CTAs per SM (4 x 16 KiB = 64 KiB, 3 CTAs/SM). Override with
-// TPR_BULK_K1 / TPR_BULK_K2 = "<stages>x<piece bytes>".
+// more issuing CTAs per SM: 3 x 32 KiB = 96 KiB, 2 CTAs/SM (with dynamic
+// claims; 4 x 16 KiB / 3 CTAs/SM is within 1%, >= 128 KiB rings lose 25-45%,
+// profiles/README.md). Override with TPR_BULK_K1 / TPR_BULK_K2 =
+// "<stages>x<piece bytes>".
 struct BulkConfig {
   int stages;
   uint32_t piece;
@@ -422,7 +424,7 @@ static const BulkConfig& k1_config() {
   return c;
 }
 static const BulkConfig& k2_config() {
-  static BulkConfig c = parse_bulk("TPR_BULK_K2", BulkConfig{4, 16384});
+  static BulkConfig c = parse_bulk("TPR_BULK_K2", BulkConfig{3, 32768});
   return c;
 }
 

@@ -1,0 +1,135 @@
+// Host bookkeeping of one switch (include/tpr.h "switch bookkeeping"): plan
+// rows -> K3 records + per-slot unit deltas + the plan checks of
+// migration.py:192-207, and the host placement update after the enqueue.
+// Replaces the per-transfer Python walk of kvcache.PagedKvCluster.records /
+// _reserve (which stays as the fallback for ids outside the lookup tables).
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "tpr.h"
+#include "tpr_internal.h"
+
+namespace {
+
+// Generation-stamped (request slot, head) marks for the "moved twice" check,
+// reused across calls so nothing is cleared per switch.
+struct Stamps {
+  std::vector<uint32_t> mark;
+  uint32_t gen = 0;
+  uint32_t* begin(size_t n) {
+    if (mark.size() < n) mark.assign(n, 0), gen = 0;
+    if (++gen == 0) {  // wrapped: clear once every 2^32 calls
+      std::fill(mark.begin(), mark.end(), 0u);
+      gen = 1;
+    }
+    return mark.data();
+  }
+};
+thread_local Stamps g_stamps;
+
+}  // namespace
+
+extern "C" {
+
+int tpr_kv_records(const int64_t* plan, int64_t n, const int64_t* gpu_lut, int64_t gpu_lut_len,
+                   const int64_t* gpu_ids, int32_t n_slots, const int64_t* req_lut,
+                   int64_t req_lut_len, const int32_t* slot_ctx, const int32_t* owner,
+                   int32_t n_req_slots, int32_t total_heads, int32_t block_tokens, int64_t kvb,
+                   int32_t validate, int32_t* records, int64_t* in_units, int64_t* out_units,
+                   int64_t* total_units) {
+  using tpr::set_error;
+  if (n < 0 || (n > 0 && (!plan || !records)) || !in_units || !out_units || !total_units)
+    return set_error(TPR_EINVAL, "bad tpr_kv_records arguments");
+  if (n_slots < 1 || n_slots > TPR_MAX_GPUS || total_heads < 1 || block_tokens < 1)
+    return set_error(TPR_EINVAL, "bad tpr_kv_records geometry");
+  for (int s = 0; s < n_slots; ++s) in_units[s] = out_units[s] = 0;
+  *total_units = 0;
+  if (!gpu_lut || !req_lut || !slot_ctx || !owner) return set_error(TPR_ENOTFOUND, "no lookup tables");
+  // pass 1 -- ids (all sources, all destinations, all requests: the order in
+  // which the Python path would raise), the context of each request
+  auto slot_of = [&](int64_t id) -> int64_t {
+    return (id >= 0 && id < gpu_lut_len) ? gpu_lut[id] : -1;
+  };
+  for (int c = 0; c < 2; ++c)
+    for (int64_t t = 0; t < n; ++t)
+      if (slot_of(plan[t * 6 + c]) < 0) return set_error(TPR_ENOTFOUND, "gpu id not in table");
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t r = plan[t * 6 + 2];
+    const int64_t rs = (r >= 0 && r < req_lut_len) ? req_lut[r] : -1;
+    if (rs < 0 || rs >= n_req_slots) return set_error(TPR_ENOTFOUND, "request id not in table");
+  }
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t lo = plan[t * 6 + 3], hi = plan[t * 6 + 4];
+    if (lo < 0 || hi > total_heads || lo >= hi)
+      return set_error(TPR_EINVAL, "head range outside [0, total_heads)");
+  }
+  if (validate) {
+    for (int64_t t = 0; t < n; ++t) {
+      const int64_t* p = plan + t * 6;
+      const int64_t ctx = slot_ctx[req_lut[p[2]]];
+      if (p[5] != (p[4] - p[3]) * ctx * kvb)
+        return set_error(TPR_EINVAL,
+                         "transfer bytes disagree with "
+                         "(head_hi-head_lo)*context_len*kv_bytes_per_token_per_head");
+    }
+    uint32_t* mark = g_stamps.begin((size_t)n_req_slots * total_heads);
+    const uint32_t gen = g_stamps.gen;
+    for (int64_t t = 0; t < n; ++t) {
+      const int64_t* p = plan + t * 6;
+      uint32_t* row = mark + (size_t)req_lut[p[2]] * total_heads;
+      for (int64_t h = p[3]; h < p[4]; ++h) {
+        if (row[h] == gen) return set_error(TPR_EINVAL, "a (request, head) is moved twice in one plan");
+        row[h] = gen;
+      }
+    }
+    for (int64_t t = 0; t < n; ++t) {
+      const int64_t* p = plan + t * 6;
+      const int64_t rs = req_lut[p[2]], src = slot_of(p[0]);
+      const int32_t* own = owner + (size_t)rs * total_heads;
+      for (int64_t h = p[3]; h < p[4]; ++h) {
+        if (own[h] == src) continue;
+        if (own[h] >= 0 && own[h] < n_slots)
+          return set_error(TPR_EINVAL, "transfer of request %lld head %lld from gpu %lld, but it is on %lld",
+                           (long long)p[2], (long long)h, (long long)p[0],
+                           (long long)gpu_ids[own[h]]);
+        return set_error(TPR_EINVAL, "transfer of request %lld head %lld from gpu %lld, but it is on None",
+                         (long long)p[2], (long long)h, (long long)p[0]);
+      }
+    }
+  }
+  // pass 2 -- records and unit deltas
+  int64_t total = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t* p = plan + t * 6;
+    const int32_t s = (int32_t)slot_of(p[0]), d = (int32_t)slot_of(p[1]);
+    const int32_t rs = (int32_t)req_lut[p[2]];
+    const int32_t ctx = slot_ctx[rs];
+    const int64_t units = (p[4] - p[3]) * ((ctx + block_tokens - 1) / block_tokens);
+    int32_t* rec = records + t * 6;
+    rec[0] = s;
+    rec[1] = d;
+    rec[2] = rs;
+    rec[3] = (int32_t)p[3];
+    rec[4] = (int32_t)p[4];
+    rec[5] = ctx;
+    in_units[d] += units;
+    out_units[s] += units;
+    total += units;
+  }
+  *total_units = total;
+  return TPR_OK;
+}
+
+int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads) {
+  if (n < 0 || (n > 0 && (!records || !owner)) || total_heads < 1)
+    return tpr::set_error(TPR_EINVAL, "bad tpr_kv_apply_owner arguments");
+  for (int64_t t = 0; t < n; ++t) {
+    const int32_t* r = records + t * 6;
+    int32_t* row = owner + (size_t)r[2] * total_heads;
+    for (int32_t h = r[3]; h < r[4]; ++h) row[h] = r[1];
+  }
+  return TPR_OK;
+}
+
+}  // extern "C"

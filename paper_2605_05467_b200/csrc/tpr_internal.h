@@ -8,6 +8,9 @@
 
 namespace tpr {
 
+// Sets tpr_last_error() (printf-style) and returns `code`.
+int set_error(int code, const char* fmt, ...);
+
 constexpr int kCopyThreads = 256;  // 8 warps per CTA, warp-independent items
 constexpr int kCopyUnroll = 8;     // 8 x 16 B x 32 lanes = 4 KiB in flight per warp
 constexpr int kRowsPerItemTarget = 32 * 1024;  // bytes of one K1 work item

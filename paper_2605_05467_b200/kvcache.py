@@ -77,6 +77,19 @@ class _PinnedStaging:
         self._views[i][: raw.nbytes] = raw
         return self._bufs[i].data_ptr()
 
+    def acquire(self, nbytes: int) -> tuple[int, np.ndarray]:
+        """The next pinned buffer (address, uint8 view of ``nbytes``) to be
+        written in place; ``fence`` after the H2D copy that reads it."""
+        i = self._i
+        if self._armed[i]:
+            self._events[i].synchronize()
+            self._armed[i] = False
+        if self._bufs[i].numel() < nbytes:
+            self._bufs[i] = torch.empty(max(nbytes, 2 * self._bufs[i].numel()),
+                                        dtype=torch.uint8, pin_memory=True)
+            self._views[i] = self._bufs[i].numpy()
+        return self._bufs[i].data_ptr(), self._views[i][:nbytes]
+
     def fence(self, stream: torch.cuda.Stream) -> None:
         self._events[self._i].record(stream)
         self._armed[self._i] = True
@@ -175,6 +188,8 @@ class PagedKvCluster:
             self._cl.free_ring[s] = self.rings[s].data_ptr()
             self._cl.units[s] = self.units[s]
         self._last_in = self._last_out = np.zeros(self.n_gpus, np.int64)
+        self._gpu_ids_arr = np.asarray(self.gpu_ids, dtype=np.int64)
+        self._n_units_c = ctypes.c_int64(0)
         self.pattern_seed = 0
         self._default_stream = torch.cuda.current_stream(self.home)
 
@@ -227,6 +242,7 @@ class PagedKvCluster:
                 grown = np.full(max(rid + 1, 2 * len(self._req_lut)), -1, dtype=np.int64)
                 grown[: len(self._req_lut)] = self._req_lut
                 self._req_lut = grown
+                self._rec_tables = None
             self._req_lut[rid] = slot
 
     def _deltas(self, xf: np.ndarray, units: np.ndarray):
@@ -263,13 +279,16 @@ class PagedKvCluster:
             units = self._units_per_record(xf)
             total = int(units.sum())
             in_u, out_u = self._deltas(xf, units)
+        self._check_capacity(in_u)
+        self._last_in, self._last_out = in_u, out_u
+        return total, in_u, out_u
+
+    def _check_capacity(self, in_u) -> None:
         for s in range(self.n_gpus):
             free = self.ring_tail[s] - self.ring_head[s]
             if in_u[s] > free:
                 raise MigrationError(
                     f"gpu {self.gpu_ids[s]}: {in_u[s]} KV units needed, {free} free")
-        self._last_in, self._last_out = in_u, out_u
-        return total, in_u, out_u
 
     def _commit(self, in_u, out_u):
         for s in range(self.n_gpus):
@@ -388,12 +407,45 @@ class PagedKvCluster:
                          seed, stream.cuda_stream)
 
     # -------------------------------------------------------------- migration
+    def _native_records(self, arr: np.ndarray, validate: bool, out: np.ndarray):
+        """``tpr_kv_records``: plan rows -> int32 records in ``out`` + unit
+        deltas, with the reference checks. None when an id is outside the
+        lookup tables (the Python path resolves it or raises its error)."""
+        if self._gpu_lut is None:
+            return None
+        tables = self.__dict__.get("_rec_tables")
+        if tables is None:  # the cluster's table pointers (rebuilt when _req_lut grows)
+            tables = self._rec_tables = (
+                self._gpu_lut.ctypes.data, len(self._gpu_lut), self._gpu_ids_arr.ctypes.data,
+                self.n_gpus, self._req_lut.ctypes.data, len(self._req_lut),
+                self.slot_ctx.ctypes.data, self.owner.ctypes.data, self.max_requests,
+                self.kv.total_heads, self.kv.block_tokens, self.kv.kv_bytes_per_token_per_head)
+        deltas = np.empty((2, self.n_gpus), np.int64)
+        dp = deltas.ctypes.data
+        lib = _native.load()
+        rc = lib.tpr_kv_records(arr.ctypes.data, len(arr), *tables, int(validate),
+                                out.ctypes.data, dp, dp + 8 * self.n_gpus,
+                                ctypes.byref(self._n_units_c))
+        if rc == _native.TPR_ENOTFOUND:
+            return None
+        if rc != 0:
+            raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
+        return self._n_units_c.value, deltas[0], deltas[1]
+
     def records(self, plan: MigrationPlan, validate: bool = True) -> np.ndarray:
         """Plan -> int64 [n, 6] device records (slots), with reference checks."""
         arr = plan.as_array()
         n = len(arr)
         if n == 0:
             return np.zeros((0, 6), dtype=np.int64)
+        rec = np.empty((n, 6), dtype=np.int32)
+        if self._native_records(arr, validate, rec) is not None:
+            return rec.astype(np.int64)
+        return self._records_py(arr, validate)
+
+    def _records_py(self, arr: np.ndarray, validate: bool) -> np.ndarray:
+        """records() for ids outside the lookup tables (dict maps)."""
+        n = len(arr)
         if n <= 32 and not validate:  # small plans: dict lookups beat numpy call overhead
             H = self.kv.total_heads
             out = []
@@ -444,18 +496,27 @@ class PagedKvCluster:
         splits the fused call in two so the events can sit between them).
         """
         stream = stream or self._default_stream
-        xf = self.records(plan, validate)
-        n = len(xf)
+        arr = plan.as_array()
+        n = len(arr)
         if n == 0:
             return MigrationStats(0, 0, 0, {}, {})
         if not self._single_device:
             raise MigrationError("multi-device clusters migrate through distributed.py")
-        total, in_u, out_u = self._reserve(xf)
+        # records go straight into the pinned staging buffer the H2D reads
+        h_ptr, raw = self._staging.acquire(n * 6 * 4)
+        xf32 = raw.view(np.int32).reshape(n, 6)
+        fast = self._native_records(arr, validate, xf32)
+        if fast is None:
+            xf = self._records_py(arr, validate)
+            total, in_u, out_u = self._reserve(xf)
+            xf32[:] = xf
+        else:
+            total, in_u, out_u = fast
+            self._check_capacity(in_u)
         cl = self._cluster_c()
         d_xf = self._xf.get(n * 6, stream)
         d_meta = self._meta.get(n * 4, stream)
         d_work = self._work.get(max(total, 1) * 4, stream)
-        h_ptr = self._staging.stage(xf.astype(np.int32))
         if k1_events:
             _native.call("tpr_kv_switch", ctypes.byref(self._geo), ctypes.byref(cl), h_ptr,
                          d_xf.data_ptr(), n, -1, d_meta.data_ptr(), self._totals.data_ptr(), 0,
@@ -476,15 +537,8 @@ class PagedKvCluster:
         self._staging.fence(stream)
         self._commit(in_u, out_u)
         # host placement bookkeeping (apply_plan semantics)
-        if n <= 64:
-            for s, d, r, lo, hi, _ in xf.tolist():
-                self.owner[r, lo:hi] = d
-        else:
-            heads = np.arange(self.kv.total_heads)
-            mask = (heads >= xf[:, 3:4]) & (heads < xf[:, 4:5])
-            rows = np.broadcast_to(xf[:, 2:3], mask.shape)
-            self.owner[rows[mask], np.broadcast_to(heads, mask.shape)[mask]] = \
-                np.broadcast_to(xf[:, 1:2], mask.shape)[mask]
+        _native.call("tpr_kv_apply_owner", xf32.ctypes.data, n, self.owner.ctypes.data,
+                     self.kv.total_heads)
         return MigrationStats(
             transfers=n, units=total, bytes=plan.total_bytes,
             in_units={self.gpu_ids[s]: int(v) for s, v in enumerate(in_u) if v},
