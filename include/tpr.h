@@ -43,8 +43,9 @@ enum tpr_status {
   TPR_EINVAL = -1,     /* bad argument                                   */
   TPR_ECUDA = -2,      /* CUDA runtime error                             */
   TPR_ECAPACITY = -3,  /* output buffer too small                        */
-  TPR_ENOTFOUND = -4,  /* id outside the caller's lookup tables: resolve  */
-                       /* it with the caller's own maps and retry there   */
+  TPR_ENOTFOUND = -4,  /* input outside this fast path (an id outside the */
+                       /* caller's tables, a repeated id): use the        */
+                       /* caller's general path, which resolves or raises */
 };
 
 /* Device-side status bits written by the K3 remap kernel (status word). */
@@ -119,6 +120,21 @@ int tpr_plan_heads(int32_t n_req, const int64_t* req_ids, const int64_t* ctx,
                    const int32_t* new_off, const int32_t* new_tp,
                    const int64_t* gpu_ids, int32_t total_heads, int64_t kvb,
                    int64_t capacity, int64_t* out, int64_t* n_out);
+
+/* plan_repartition (migration.py:137-189) after its GPU-set / head-count
+ * checks: layouts are flattened, layout j holding *_count[j] consecutive
+ * requests (ids, context lengths) of group gpu_ids[*_goff[j] .. +*_tp[j]).
+ * Checks that the new layouts carry exactly the old requests and that no
+ * context length changed (the reference's messages, in its order), then plans
+ * every new request in new-layout order as tpr_plan_heads. An old request id
+ * that repeats returns TPR_ENOTFOUND (the reference's last-one-wins dict
+ * semantics stay with the caller's general path). */
+int tpr_plan_repartition(int32_t n_old, const int64_t* old_count, const int32_t* old_goff,
+                         const int32_t* old_tp, const int64_t* old_req, const int64_t* old_ctx,
+                         int32_t n_new, const int64_t* new_count, const int32_t* new_goff,
+                         const int32_t* new_tp, const int64_t* new_req, const int64_t* new_ctx,
+                         const int64_t* gpu_ids, int32_t total_heads, int64_t kvb,
+                         int64_t capacity, int64_t* out, int64_t* n_out);
 
 /* ---- K3: block-table remap + free-ring allocation (device) ------------- */
 /* d_xfers: int32 [n][6] transfer records (device). d_meta: int64 [n][4]

@@ -26,7 +26,7 @@ TPR_ENOTFOUND = -4  # an id outside the caller's lookup tables (use the Python m
 # Every exported symbol of include/tpr.h; tests check the library exports all.
 EXPORTS = (
     "tpr_set_copy_engine", "tpr_get_copy_engine",
-    "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads",
+    "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads", "tpr_plan_repartition",
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
     "tpr_memcpy_h2d",
     "tpr_copy_prepare", "tpr_weight_reshard",
@@ -84,6 +84,9 @@ _SIGNATURES = {
     "tpr_device_info": (c_int32, [_P32, _P32, _P32]),
     "tpr_plan_heads": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p, _P64]),
+    "tpr_plan_repartition": (c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_int32, c_int64, c_int64, c_void_p, _P64]),
     "tpr_kv_remap": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int32,
                                c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                c_void_p, c_void_p]),

@@ -4,7 +4,9 @@
 // Replaces the per-transfer Python walk of kvcache.PagedKvCluster.records /
 // _reserve (which stays as the fallback for ids outside the lookup tables).
 #include <algorithm>
+#include <climits>
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "tpr.h"
@@ -119,6 +121,69 @@ int tpr_kv_records(const int64_t* plan, int64_t n, const int64_t* gpu_lut, int64
   }
   *total_units = total;
   return TPR_OK;
+}
+
+int tpr_plan_repartition(int32_t n_old, const int64_t* old_count, const int32_t* old_goff,
+                         const int32_t* old_tp, const int64_t* old_req, const int64_t* old_ctx,
+                         int32_t n_new, const int64_t* new_count, const int32_t* new_goff,
+                         const int32_t* new_tp, const int64_t* new_req, const int64_t* new_ctx,
+                         const int64_t* gpu_ids, int32_t total_heads, int64_t kvb,
+                         int64_t capacity, int64_t* out, int64_t* n_out) {
+  using tpr::set_error;
+  if (n_old < 0 || n_new < 0 || !n_out || total_heads < 1)
+    return set_error(TPR_EINVAL, "bad tpr_plan_repartition arguments");
+  thread_local std::vector<std::pair<int64_t, int32_t>> by_id;  // (old request id, old index)
+  thread_local std::vector<int32_t> layout_of, match;
+  thread_local std::vector<uint8_t> seen;
+  thread_local std::vector<int32_t> meta;
+  int64_t n_o = 0, n_n = 0;
+  for (int32_t j = 0; j < n_old; ++j) n_o += old_count[j];
+  for (int32_t j = 0; j < n_new; ++j) n_n += new_count[j];
+  by_id.resize(n_o);
+  layout_of.resize(n_o);
+  for (int32_t j = 0, i = 0; j < n_old; ++j)
+    for (int64_t k = 0; k < old_count[j]; ++k, ++i) {
+      by_id[i] = {old_req[i], i};
+      layout_of[i] = j;
+    }
+  std::sort(by_id.begin(), by_id.end());
+  for (int64_t i = 1; i < n_o; ++i)
+    if (by_id[i].first == by_id[i - 1].first)  // last-one-wins dict semantics: general path
+      return set_error(TPR_ENOTFOUND, "old request id %lld repeats", (long long)by_id[i].first);
+  // carried requests == old requests (migration.py:160-166)
+  match.resize(n_n);
+  seen.assign(n_o, 0);
+  bool carried = n_n == n_o;
+  for (int64_t i = 0; carried && i < n_n; ++i) {
+    auto it = std::lower_bound(by_id.begin(), by_id.end(), std::make_pair(new_req[i], INT32_MIN));
+    if (it == by_id.end() || it->first != new_req[i] || seen[it->second]) {
+      carried = false;
+      break;
+    }
+    seen[it->second] = 1;
+    match[i] = it->second;
+  }
+  if (!carried) return set_error(TPR_EINVAL, "new layouts must carry exactly the old requests");
+  for (int64_t i = 0; i < n_n; ++i)  // migration.py:172-173, in plan order
+    if (old_ctx[match[i]] != new_ctx[i])
+      return set_error(TPR_EINVAL, "request %lld: context length changed", (long long)new_req[i]);
+  // per-request groups in plan order, then the head planner
+  meta.resize(4 * n_n);
+  for (int32_t j = 0, i = 0; j < n_new; ++j)
+    for (int64_t k = 0; k < new_count[j]; ++k, ++i) {
+      const int32_t oj = layout_of[match[i]];
+      meta[i] = old_goff[oj];
+      meta[n_n + i] = old_tp[oj];
+      meta[2 * n_n + i] = new_goff[j];
+      meta[3 * n_n + i] = new_tp[j];
+    }
+  if (n_n == 0) {
+    *n_out = 0;
+    return TPR_OK;
+  }
+  return tpr_plan_heads((int32_t)n_n, new_req, new_ctx, meta.data(), meta.data() + n_n,
+                        meta.data() + 2 * n_n, meta.data() + 3 * n_n, gpu_ids, total_heads, kvb,
+                        capacity, out, n_out);
 }
 
 int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads) {

@@ -244,49 +244,45 @@ def _layout_table(layouts) -> tuple[np.ndarray, np.ndarray, _GroupTable]:
     return off, tp, table
 
 
-# below this many requests the row walk beats numpy's per-call overhead
-_VECTORISE_MIN_REQUESTS = 48
+# below this many requests the row walk's lower fixed cost wins (measured on
+# this host: 36 vs 60 us at 1 request, 98 vs 66 us at 32, 277 vs 85 us at 128)
+_NATIVE_MIN_REQUESTS = 24
 
 
-def _plan_vectorised(old_layouts, new_layouts, total_heads: int, kvb: int):
-    """plan_repartition's matching + validation on cached per-layout arrays.
+def _plan_layouts(old_layouts, new_layouts, total_heads: int, kvb: int):
+    """plan_repartition's matching, checks and planning in libtpr
+    (``tpr_plan_repartition``) over the layouts' cached request arrays.
 
     Same checks, order and messages as the row-by-row path below; returns None
     (use that path) when an old request id repeats, where the reference's
     last-one-wins dict semantics apply (migration.py:160-163).
     """
-    if not old_layouts and not new_layouts:
-        return None
     o = [lay.request_arrays() for lay in old_layouts]
     nw = [lay.request_arrays() for lay in new_layouts]
-    if not o or not nw:
-        return None
-    old_ids = np.concatenate([a for a, _ in o])
-    new_ids = np.concatenate([a for a, _ in nw])
-    order = np.argsort(old_ids, kind="stable")
-    sorted_old = old_ids[order]
-    if len(sorted_old) > 1 and bool((sorted_old[1:] == sorted_old[:-1]).any()):
-        return None
-    if len(new_ids) != len(old_ids) or not np.array_equal(np.sort(new_ids), sorted_old):
-        raise MigrationError("new layouts must carry exactly the old requests")
-    n = len(new_ids)
-    if n == 0:
-        return np.zeros((0, 6), dtype=np.int64)
-    pos = order[np.searchsorted(sorted_old, new_ids)]
-    old_ctx = np.concatenate([c for _, c in o])[pos]
-    new_ctx = np.concatenate([c for _, c in nw])
-    bad = np.flatnonzero(old_ctx != new_ctx)
-    if len(bad):
-        raise MigrationError(f"request {int(new_ids[bad[0]])}: context length changed")
     off, tp, table = _layout_table([*old_layouts, *new_layouts])
     n_old = len(old_layouts)
-    old_lay = np.repeat(np.arange(n_old), [len(a) for a, _ in o])[pos]
-    new_lay = np.repeat(np.arange(len(new_layouts)), [len(a) for a, _ in nw]) + n_old
-    meta = np.empty((4, n), dtype=np.int32)
-    meta[0], meta[1] = off[old_lay], tp[old_lay]
-    meta[2], meta[3] = off[new_lay], tp[new_lay]
-    return _call_planner(new_ids, new_ctx, meta, np.asarray(table.ids, dtype=np.int64),
-                         total_heads, kvb)
+    cnt = np.array([len(a) for a, _ in o] + [len(a) for a, _ in nw], dtype=np.int64)
+    cat = (lambda parts: np.concatenate(parts) if len(parts) > 1 else parts[0]) if o and nw else None
+    if cat is None:
+        return None
+    old_req, old_ctx = cat([a for a, _ in o]), cat([c for _, c in o])
+    new_req, new_ctx = cat([a for a, _ in nw]), cat([c for _, c in nw])
+    ids = np.asarray(table.ids, dtype=np.int64)
+    cap = max(len(new_req), 1) * total_heads
+    out = _out_buffer(cap)
+    n_out = _native.c_int64(0)
+    lib = _native.load()
+    cp, op, tpp = cnt.ctypes.data, off.ctypes.data, tp.ctypes.data
+    rc = lib.tpr_plan_repartition(
+        n_old, cp, op, tpp, old_req.ctypes.data, old_ctx.ctypes.data,
+        len(new_layouts), cp + 8 * n_old, op + 4 * n_old, tpp + 4 * n_old,
+        new_req.ctypes.data, new_ctx.ctypes.data, ids.ctypes.data, total_heads, int(kvb), cap,
+        out.ctypes.data, _native.ctypes.byref(n_out))
+    if rc == _native.TPR_ENOTFOUND:
+        return None
+    if rc != 0:
+        raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
+    return out[: n_out.value].copy()
 
 
 def _call_planner(req: np.ndarray, ctx: np.ndarray, meta: np.ndarray, ids: np.ndarray,
@@ -345,8 +341,8 @@ def plan_repartition(old_layouts: list[KvLayout], new_layouts, kv_bytes_per_toke
     total_heads = new_layouts[0].total_heads if new_layouts else (
         old_layouts[0].total_heads if old_layouts else 1)
     fast = None
-    if sum(len(lay.requests) for lay in new_layouts) >= _VECTORISE_MIN_REQUESTS:
-        fast = _plan_vectorised(old_layouts, new_layouts, total_heads, kv_bytes_per_token_per_head)
+    if sum(len(lay.requests) for lay in new_layouts) >= _NATIVE_MIN_REQUESTS:
+        fast = _plan_layouts(old_layouts, new_layouts, total_heads, kv_bytes_per_token_per_head)
     if fast is not None:
         return MigrationPlan.from_array(fast, handshake_ms=handshake_ms)
     source: dict[int, tuple[KvLayout, int]] = {}

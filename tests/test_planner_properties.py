@@ -81,23 +81,24 @@ def test_head_transfers_disjoint_groups(data):
 
 
 def _both_paths(lo, ln, kvb):
-    """plan_repartition through the row walk and through the vectorised path."""
+    """plan_repartition through the row walk and through libtpr's
+    tpr_plan_repartition (the default path)."""
     out = []
-    saved = M._VECTORISE_MIN_REQUESTS
+    saved = M._NATIVE_MIN_REQUESTS
     for threshold in (10**9, 0):
-        M._VECTORISE_MIN_REQUESTS = threshold
+        M._NATIVE_MIN_REQUESTS = threshold
         try:
             out.append(("ok", M.plan_repartition(lo, ln, kvb).as_array().tolist()))
         except M.MigrationError as exc:
             out.append(("err", str(exc)))
         finally:
-            M._VECTORISE_MIN_REQUESTS = saved
+            M._NATIVE_MIN_REQUESTS = saved
     return out
 
 
 @settings(max_examples=300, deadline=None)
 @given(transitions(), st.sampled_from(["none", "drop", "ctx", "dup_old", "dup_new"]), st.data())
-def test_vectorised_planner_matches_row_walk(t, corrupt, data):
+def test_native_repartition_matches_row_walk(t, corrupt, data):
     """Plans and error messages agree between the two planning paths,
     including invalid inputs (missing / duplicated requests, changed context)."""
     H, og, old, ng, new, kvb = t
