@@ -187,10 +187,14 @@ int tpr_kv_records(const int64_t* plan, int64_t n, const int64_t* gpu_lut, int64
 int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads);
 
 /* ---- K3 + K1 in one call ----------------------------------------------- */
-/* The switch fast path: async H2D copy of the records from pinned host memory
- * (h_xfers, may be NULL when d_xfers is already filled), K3 (remap) and K1
- * (page copy), all on `stream`. Same arguments as tpr_kv_remap; n_units must
- * be the exact number of units this caller processes. */
+/* The switch fast path: K3 (remap) and K1 (page copy), all on `stream`.
+ * h_xfers (may be NULL when d_xfers is already filled): when it is pinned host
+ * memory, K3 reads the records in place over PCIe (zero-copy) and copies them
+ * into d_xfers; pageable records are first copied H2D. Small plans run K3 as
+ * one fused CTA; K3b and K1 use programmatic dependent launch. h_xfers must
+ * stay untouched until the stream passes this call. Same arguments as
+ * tpr_kv_remap; n_units must be the exact number of units this caller
+ * processes. */
 int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                   const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                   int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
@@ -198,6 +202,8 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
 
 /* Stream-ordered host->device copy (pinned source for true asynchrony). */
 int tpr_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, void* stream);
+/* Stream-ordered device->host copy (pinned destination), e.g. the status word. */
+int tpr_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, void* stream);
 
 /* ---- K2: weight reshard = batched 2-D strided copy (device) ------------ */
 typedef struct tpr_copy_seg {

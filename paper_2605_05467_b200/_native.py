@@ -28,7 +28,7 @@ EXPORTS = (
     "tpr_set_copy_engine", "tpr_get_copy_engine",
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads", "tpr_plan_repartition",
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
-    "tpr_memcpy_h2d",
+    "tpr_memcpy_h2d", "tpr_memcpy_d2h",
     "tpr_copy_prepare", "tpr_weight_reshard",
     "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
     "tpr_matrix_verify", "tpr_baseline_copy_pages", "tpr_device_barrier", "tpr_device_alloc",
@@ -100,6 +100,7 @@ _SIGNATURES = {
                                 c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                 c_void_p]),
     "tpr_memcpy_h2d": (c_int32, [c_uint64, c_void_p, c_uint64, c_void_p]),
+    "tpr_memcpy_d2h": (c_int32, [c_void_p, c_uint64, c_uint64, c_void_p]),
     "tpr_copy_prepare": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, _P64]),
     "tpr_weight_reshard": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p,
                                      c_void_p]),
@@ -154,6 +155,21 @@ def load() -> ctypes.CDLL:
 
 
 ENGINES = {"vector": 0, "bulk": 1}
+
+
+def k3_fuse_units() -> int:
+    """Plan size (units) up to which K3 runs as one fused CTA (mirrors
+    tpr_api.cpp: TPR_K3_FUSE_UNITS, default 4096)."""
+    import os
+    v = os.environ.get("TPR_K3_FUSE_UNITS", "")
+    return int(v) if v else 4096
+
+
+def kv_switch_launches(units: int) -> int:
+    """Kernels one tpr_kv_switch launches: K3 (fused, or scan + remap) + K1."""
+    if units <= 0:
+        return 0
+    return 2 if units <= k3_fuse_units() else 3
 
 
 def set_copy_engine(name: str) -> None:

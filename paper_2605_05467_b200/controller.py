@@ -19,6 +19,7 @@ from dataclasses import dataclass, field
 
 import torch
 
+from . import _native
 from .kvcache import MigrationStats, PagedKvCluster
 from .migration import KvLayout, MigrationPlan, head_transfers_array, plan_repartition
 from .tracing import nvtx
@@ -62,6 +63,20 @@ class ReconfigurationExecutor:
         self.time_kernels = time_kernels
         self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.main_stream = torch.cuda.current_stream(dev)
+        # reused per synchronous switch (each one waits for its end event)
+        self._ev_sync = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+
+    def _finish(self, res: SwitchResult, main: torch.cuda.Stream, t0: float) -> SwitchResult:
+        """Synchronous tail: the step's result (K3's status word) read back D2H,
+        then the host waits for the end event."""
+        _native.call("tpr_memcpy_d2h", self._status_host.data_ptr(), self.kv.status.data_ptr(), 4,
+                     main.cuda_stream)
+        res.events["end"].record(main)
+        res.events["end"].synchronize()
+        res.status = int(self._status_host[0])
+        res.host_ms = (time.perf_counter() - t0) * 1e3
+        res.device_ms = res.events["start"].elapsed_time(res.events["end"])
+        return res
 
     def switch(self, old_layouts: list[KvLayout], new_layouts: list[KvLayout],
                new_weight_groups=None, parked=(), sync: bool = True,
@@ -74,7 +89,7 @@ class ReconfigurationExecutor:
         main = stream or self.main_stream
         ev = {}
         if sync:
-            ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
+            ev = {"start": self._ev_sync[0], "end": self._ev_sync[1]}
             ev["start"].record(main)
         if self.time_kernels:
             for k in ("k1_start", "k1_end", "k2_start", "k2_end"):
@@ -84,32 +99,30 @@ class ReconfigurationExecutor:
         if self.handshake is not None:
             with nvtx("handshake"):
                 self.handshake(plan)
-        self.kv_stream.wait_stream(main)
+        # one stream unless K1 and K2 overlap: no cross-stream event waits on
+        # the (latency-bound) small-switch path
+        ks = self.kv_stream if self.overlap else main
+        if ks is not main:
+            ks.wait_stream(main)
         with nvtx("kv K3+K1"):
             kv_stats = self.kv.migrate(
-                plan, stream=self.kv_stream, validate=validate,
+                plan, stream=ks, validate=validate,
                 k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
         w_stats = None
         if self.weights is not None and new_weight_groups is not None:
-            self.w_stream.wait_stream(main)
+            ws = self.w_stream if self.overlap else main
+            if ws is not main:
+                ws.wait_stream(main)
             with nvtx("weights K2"):
                 w_stats = self.weights.reshard(
-                    new_weight_groups, stream=self.w_stream, parked=parked,
+                    new_weight_groups, stream=ws, parked=parked,
                     events=(ev["k2_start"], ev["k2_end"]) if self.time_kernels else None)
-            main.wait_stream(self.w_stream)
-        main.wait_stream(self.kv_stream)
-        if sync:
-            ev["end"].record(main)
+            if ws is not main:
+                main.wait_stream(ws)
+        if ks is not main:
+            main.wait_stream(ks)
         res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev)
-        if sync:
-            # the step's result: K3's status word, read back D2H
-            self._status_host.copy_(self.kv.status, non_blocking=True)
-            ev["end"].synchronize()
-            res.status = int(self._status_host.item())
-            res.host_ms = (time.perf_counter() - t0) * 1e3
-            res.device_ms = ev["start"].elapsed_time(ev["end"])
-        return res
-
+        return self._finish(res, main, t0) if sync else res
 
     def handoff(self, prefill: KvLayout, decode: KvLayout, sync: bool = True) -> SwitchResult:
         """Prefill->decode KV handoff between disjoint groups.
@@ -123,17 +136,16 @@ class ReconfigurationExecutor:
         ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
         ev["start"].record(main)
         plan = head_transfers_array(prefill, decode, self.kv.kv.kv_bytes_per_token_per_head)
-        self.kv_stream.wait_event(ev["start"])
-        stats = self.kv.migrate(plan, stream=self.kv_stream)
-        main.wait_stream(self.kv_stream)
-        ev["end"].record(main)
+        ks = self.kv_stream if self.overlap else main
+        if ks is not main:
+            ks.wait_event(ev["start"])
+        stats = self.kv.migrate(plan, stream=ks)
+        if ks is not main:
+            main.wait_stream(ks)
         res = SwitchResult(plan=plan, kv=stats, weights=None, events=ev)
         if sync:
-            self._status_host.copy_(self.kv.status, non_blocking=True)
-            ev["end"].synchronize()
-            res.status = int(self._status_host.item())
-            res.host_ms = (time.perf_counter() - t0) * 1e3
-            res.device_ms = ev["start"].elapsed_time(ev["end"])
+            return self._finish(res, main, t0)
+        ev["end"].record(main)
         return res
 
 

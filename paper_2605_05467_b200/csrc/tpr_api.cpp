@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -89,9 +90,29 @@ int cluster_params(const tpr_kv_cluster_t* cl, const tpr_kv_geometry_t* geo,
 std::atomic<int> g_engine{TPR_ENGINE_BULK};
 
 cudaError_t run_k1(const tpr::KvCopyParams& p, const tpr::KvClusterParams& cl, const int4* work,
-                   int64_t n, cudaStream_t st) {
-  return g_engine.load() == TPR_ENGINE_BULK ? tpr::launch_k1_bulk(p, cl, work, n, st)
-                                            : tpr::launch_k1(p, cl, work, n, st);
+                   int64_t n, cudaStream_t st, bool pdl) {
+  return g_engine.load() == TPR_ENGINE_BULK ? tpr::launch_k1_bulk(p, cl, work, n, st, pdl)
+                                            : tpr::launch_k1(p, cl, work, n, st, pdl);
+}
+
+// Records in caller memory the device can read directly: pinned (page-locked)
+// host memory under unified addressing, or device memory. Then K3 reads them
+// in place and the separate H2D copy disappears from the switch.
+const int32_t* device_view(const int32_t* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice ||
+      a.type == cudaMemoryTypeManaged)
+    return static_cast<const int32_t*>(a.devicePointer);
+  return nullptr;  // pageable
+}
+
+int64_t env_i64(const char* name, int64_t dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? strtoll(v, nullptr, 10) : dflt;
 }
 
 cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
@@ -104,6 +125,18 @@ cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_
 }  // namespace
 
 namespace tpr {
+bool pdl_enabled() {
+  static const bool on = env_i64("TPR_PDL", 1) != 0;
+  return on;
+}
+
+int64_t k3_fuse_units() {
+  // one 1024-thread CTA expands up to 4 units per thread faster than a second
+  // launch + dependency gap (measured, profiles/README.md)
+  static const int64_t n = env_i64("TPR_K3_FUSE_UNITS", 4096);
+  return n;
+}
+
 int set_error(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -236,8 +269,8 @@ int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const
   if (n_xfers == 0) return TPR_OK;
   if (!d_xfers || !d_meta || !d_totals || !d_work || !d_status)
     return fail(TPR_EINVAL, "null device buffer");
-  cudaError_t e = tpr::launch_k3(*geo, cp, d_xfers, n_xfers, filter_src, d_meta, d_totals,
-                                 n_units_hint, reinterpret_cast<int4*>(d_work),
+  cudaError_t e = tpr::launch_k3(*geo, cp, d_xfers, const_cast<int32_t*>(d_xfers), n_xfers, filter_src, d_meta,
+                                 d_totals, n_units_hint, reinterpret_cast<int4*>(d_work),
                                  reinterpret_cast<int4*>(d_work_ext), d_status,
                                  static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_remap launch");
@@ -251,8 +284,8 @@ int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, con
   if ((rc = cluster_params(cl, geo, &cp))) return rc;
   if (n_units < 0) return fail(TPR_EINVAL, "n_units < 0");
   if (n_units > 0 && !d_work) return fail(TPR_EINVAL, "null work list");
-  cudaError_t e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
-                                 n_units, static_cast<cudaStream_t>(stream));
+  cudaError_t e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units,
+                         static_cast<cudaStream_t>(stream), tpr::pdl_enabled());
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_migrate launch");
 }
 
@@ -270,16 +303,25 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, cons
     return fail(TPR_EINVAL, "null device buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
+  // records K3 reads: pinned host records in place (zero-copy), else an H2D
+  // copy into d_xfers first
+  const int32_t* xin = d_xfers;
   if (h_xfers) {
-    e = cudaMemcpyAsync(d_xfers, h_xfers, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n_xfers,
-                        cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch H2D");
+    const int32_t* mapped = n_units > 0 ? device_view(h_xfers) : nullptr;
+    if (mapped) {
+      xin = mapped;
+    } else {
+      e = cudaMemcpyAsync(d_xfers, h_xfers, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n_xfers,
+                          cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch H2D");
+    }
   }
   if (n_units == 0) return TPR_OK;
-  e = tpr::launch_k3(*geo, cp, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
+  e = tpr::launch_k3(*geo, cp, xin, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
                      reinterpret_cast<int4*>(d_work), nullptr, d_status, st);
   if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
-  e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st);
+  e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st,
+             tpr::pdl_enabled());
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_switch K1");
 }
 
@@ -289,6 +331,14 @@ int tpr_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, void* stream) 
   cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice,
                                   static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_memcpy_h2d");
+}
+
+int tpr_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, void* stream) {
+  if (bytes == 0) return TPR_OK;
+  if (!dst || !src) return fail(TPR_EINVAL, "null pointer");
+  cudaError_t e = cudaMemcpyAsync(dst, reinterpret_cast<const void*>(src), bytes,
+                                  cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_memcpy_d2h");
 }
 
 int tpr_copy_prepare(tpr_copy_seg_t* segs, int32_t n, int64_t chunk, int64_t* prefix,

@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(32)
                            const __grid_constant__ KvClusterParams cl, int32_t stages,
                            uint32_t piece) {
   if (threadIdx.x != 0) return;
+  pdl_wait();  // K3's work list (launched with programmatic serialization)
   KvPieces it;
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
@@ -429,33 +430,41 @@ static const BulkConfig& k2_config() {
 }
 
 static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items) {
-  static thread_local const void* done[4] = {nullptr};
-  bool seen = false;
-  for (auto f : done) seen |= (f == fn);
-  if (!seen) {
+  // attribute + occupancy per (kernel, device) are fixed: set/query once (the
+  // occupancy query costs microseconds of host time per small switch)
+  static thread_local const void* done_fn[8] = {nullptr};
+  static thread_local int done_dev[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  static thread_local int done_occ[8] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int per_sm = 0;
+  for (int i = 0; i < 8; ++i)
+    if (done_fn[i] == fn && done_dev[i] == dev) per_sm = done_occ[i];
+  if (per_sm == 0) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
-    for (auto& f : done)
-      if (!f) {
-        f = fn;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, c.smem());
+    if (per_sm < 1) per_sm = 1;
+    for (int i = 0; i < 8; ++i)
+      if (done_fn[i] == nullptr) {
+        done_fn[i] = fn;
+        done_dev[i] = dev;
+        done_occ[i] = per_sm;
         break;
       }
   }
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, c.smem());
-  if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sm_count() * per_sm;
   if (items < grid) grid = items;
   return grid < 1 ? 1 : (int)grid;
 }
 
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
-                           int64_t n_units, cudaStream_t st) {
+                           int64_t n_units, cudaStream_t st, bool pdl) {
   if (n_units <= 0) return cudaSuccess;
   const BulkConfig& c = k1_config();
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
                              n_units * p.items_per_unit);
-  tpr_k1_kv_migrate_bulk<<<grid, 32, c.smem(), st>>>(work, n_units, p, cl, c.stages, c.piece);
-  return cudaGetLastError();
+  return launch_ex(tpr_k1_kv_migrate_bulk, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl,
+                   work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece);
 }
 
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,

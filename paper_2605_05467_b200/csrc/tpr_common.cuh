@@ -49,3 +49,15 @@ TPR_HD uint64_t tpr_matrix_elem(uint64_t key, uint64_t row, uint64_t col,
 
 // Flags of tpr_copy_seg_t.flags (set by tpr_copy_prepare).
 #define TPR_SEG_ALIGNED16 1ll
+
+#if defined(__CUDACC__)
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may become resident while its
+// predecessor on the stream is still running; griddepcontrol.wait blocks until
+// that predecessor has completed and its memory is visible (a no-op after a
+// normal launch). launch_dependents lets the dependent grid start early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif

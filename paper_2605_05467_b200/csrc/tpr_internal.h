@@ -37,17 +37,43 @@ struct KvCopyParams {
 
 int sm_count();
 
+// Programmatic dependent launch of K3b/K1 behind their producer (TPR_PDL=0
+// turns it off) and the plan size (units) up to which K3 runs as one fused
+// CTA (TPR_K3_FUSE_UNITS, 0 = never).
+bool pdl_enabled();
+int64_t k3_fuse_units();
+
+// cudaLaunchKernelEx with the programmatic-serialization attribute when `pdl`.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t st, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? attr : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
+// xf_in: records as the caller holds them (device memory, or mapped pinned
+// host memory read zero-copy); xf: the device copy K3b reads (may equal xf_in).
 cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
-                      const int32_t* xf, int32_t n, int32_t filter, int64_t* meta,
-                      int64_t* totals, int64_t n_hint, int4* work, int4* work_ext,
-                      int32_t* status, cudaStream_t st);
+                      const int32_t* xf_in, int32_t* xf, int32_t n, int32_t filter,
+                      int64_t* meta, int64_t* totals, int64_t n_hint, int4* work,
+                      int4* work_ext, int32_t* status, cudaStream_t st);
+// pdl: launched right behind K3 on the same stream (waits for it on device)
 cudaError_t launch_k1(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
-                      int64_t n_units, cudaStream_t st);
+                      int64_t n_units, cudaStream_t st, bool pdl);
 cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                       int64_t n_items, int64_t chunk, cudaStream_t st);
 // TMA bulk-copy engine variants (tpr_bulk.cu)
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
-                           int64_t n_units, cudaStream_t st);
+                           int64_t n_units, cudaStream_t st, bool pdl);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

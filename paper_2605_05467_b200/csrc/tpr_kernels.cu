@@ -148,9 +148,14 @@ __device__ __forceinline__ int64_t block_keyed_exclusive(int key, int64_t val,
   return out;
 }
 
-__global__ void __launch_bounds__(kScanThreads)
-    tpr_k3_scan(const int32_t* __restrict__ xf, int32_t n, int32_t block_tokens,
-                int32_t filter, int64_t* __restrict__ meta, int64_t* __restrict__ totals) {
+// Scan body (one CTA). Records are read from `xf_in`, which may be the
+// caller's pinned host buffer (mapped: zero-copy over PCIe, no separate H2D
+// copy) and are written to `xf` (device) when the two differ.
+__device__ __forceinline__ void k3_scan_body(const int32_t* xf_in,  // may alias xf
+                                             int32_t* xf, int32_t n,
+                                             int32_t block_tokens, int32_t filter,
+                                             int64_t* __restrict__ meta,
+                                             int64_t* __restrict__ totals) {
   __shared__ int64_t s_tab[kScanWarps * kKeys];
   __shared__ int64_t s_run[3][kKeys];
   for (int i = threadIdx.x; i < 3 * kKeys; i += blockDim.x) (&s_run[0][0])[i] = 0;
@@ -160,7 +165,15 @@ __global__ void __launch_bounds__(kScanThreads)
     int src = TPR_MAX_GPUS, dst = TPR_MAX_GPUS;
     int64_t units = 0, mine = 0;
     if (t < n) {
-      const int32_t* r = xf + (int64_t)t * TPR_XFER_FIELDS;
+      int32_t r[TPR_XFER_FIELDS];
+      const int32_t* in = xf_in + (int64_t)t * TPR_XFER_FIELDS;
+#pragma unroll
+      for (int f = 0; f < TPR_XFER_FIELDS; ++f) r[f] = in[f];
+      if (xf_in != xf) {
+        int32_t* o = xf + (int64_t)t * TPR_XFER_FIELDS;
+#pragma unroll
+        for (int f = 0; f < TPR_XFER_FIELDS; ++f) o[f] = r[f];
+      }
       const int32_t ctx = r[5];
       const int64_t nblk = ctx > 0 ? (ctx + block_tokens - 1) / block_tokens : 0;
       units = (int64_t)(r[4] - r[3]) * nblk;
@@ -189,20 +202,28 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+__global__ void __launch_bounds__(kScanThreads)
+    tpr_k3_scan(const int32_t* xf_in, int32_t* xf, int32_t n,
+                int32_t block_tokens, int32_t filter, int64_t* __restrict__ meta,
+                int64_t* __restrict__ totals) {
+  pdl_trigger();  // the remap grid may get resident; it waits for this scan
+  k3_scan_body(xf_in, xf, n, block_tokens, filter, meta, totals);
+}
+
 // ---------------------------------------------------------------------------
 // K3b: expand every processed head-block into a work unit. Thread per unit;
 // the owning transfer is found by binary search over mine_off. Order inside a
 // transfer is head-major, block-minor (the order a sequential replay walks).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-    tpr_k3_remap(const int32_t* __restrict__ xf, int32_t n, const int64_t* __restrict__ meta,
-                 const int64_t* __restrict__ totals, tpr_kv_geometry_t geo,
-                 KvClusterParams cl, int4* __restrict__ work, int4* __restrict__ work_ext,
-                 int32_t* __restrict__ status) {
-  const int64_t n_mine = totals[0];
+__device__ __forceinline__ void k3_remap_body(const int32_t* __restrict__ xf, int32_t n,
+                                              const int64_t* __restrict__ meta, int64_t n_mine,
+                                              const tpr_kv_geometry_t& geo,
+                                              const KvClusterParams& cl, int4* __restrict__ work,
+                                              int4* __restrict__ work_ext,
+                                              int32_t* __restrict__ status, int64_t first,
+                                              int64_t stride) {
   const int H = geo.total_heads, B = geo.block_tokens, MB = geo.max_blocks;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_mine;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = first; i < n_mine; i += stride) {
     // upper_bound(mine_off, i) - 1
     int lo = 0, hi = n;
     while (hi - lo > 1) {
@@ -243,6 +264,31 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+__global__ void __launch_bounds__(256)
+    tpr_k3_remap(const int32_t* __restrict__ xf, int32_t n, const int64_t* __restrict__ meta,
+                 const int64_t* __restrict__ totals, tpr_kv_geometry_t geo,
+                 KvClusterParams cl, int4* __restrict__ work, int4* __restrict__ work_ext,
+                 int32_t* __restrict__ status) {
+  pdl_trigger();  // K1 may get resident; it waits for the whole remap grid
+  pdl_wait();     // the scan's offsets
+  k3_remap_body(xf, n, meta, totals[0], geo, cl, work, work_ext, status,
+                (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+// K3 fused (small plans): one CTA scans, then the same CTA expands every unit.
+// Saves the second launch and its dependency gap; the scan's meta/totals are
+// re-read from L2 by the block that wrote them (visible after __syncthreads).
+__global__ void __launch_bounds__(kScanThreads)
+    tpr_k3_fused(const int32_t* xf_in, int32_t* xf, int32_t n,
+                 int32_t filter, int64_t* __restrict__ meta, int64_t* __restrict__ totals,
+                 tpr_kv_geometry_t geo, KvClusterParams cl, int4* __restrict__ work,
+                 int4* __restrict__ work_ext, int32_t* __restrict__ status) {
+  pdl_trigger();
+  k3_scan_body(xf_in, xf, n, geo.block_tokens, filter, meta, totals);
+  __syncthreads();
+  k3_remap_body(xf, n, meta, totals[0], geo, cl, work, work_ext, status, threadIdx.x, blockDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // K1: paged-KV head-shard migration. A work item is `rows_per_item` rows
 // ((layer, K|V) planes) of one page; a full page (ntok == B) is one contiguous
@@ -253,6 +299,7 @@ template <int kUnroll>
 __global__ void __launch_bounds__(kCopyThreads)
     tpr_k1_kv_migrate(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
                       KvClusterParams cl) {
+  pdl_wait();  // K3's work list (launched with programmatic serialization)
   const unsigned lane = threadIdx.x & 31u;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -512,31 +559,41 @@ static int copy_grid(const void* fn, int threads, int64_t want_warps) {
 }
 
 cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
-                      const int32_t* xf, int32_t n, int32_t filter, int64_t* meta,
-                      int64_t* totals, int64_t n_hint, int4* work, int4* work_ext,
-                      int32_t* status, cudaStream_t st) {
+                      const int32_t* xf_in, int32_t* xf, int32_t n, int32_t filter,
+                      int64_t* meta, int64_t* totals, int64_t n_hint, int4* work,
+                      int4* work_ext, int32_t* status, cudaStream_t st) {
   int threads = ((n + 31) / 32) * 32;
   if (threads > kScanThreads) threads = kScanThreads;
   if (threads < 32) threads = 32;
-  tpr_k3_scan<<<1, threads, 0, st>>>(xf, n, geo.block_tokens, filter, meta, totals);
+  if (n_hint <= 0) n_hint = 1;
+  const bool pdl = pdl_enabled();
+  if (n_hint <= k3_fuse_units()) {
+    // small plan: one CTA scans and expands (one launch instead of two)
+    int ft = threads;
+    const int64_t want = ((n_hint + 31) / 32) * 32;
+    if (want > ft) ft = (int)(want < kScanThreads ? want : kScanThreads);
+    tpr_k3_fused<<<1, ft, 0, st>>>(xf_in, xf, n, filter, meta, totals, geo, cl, work, work_ext,
+                                   status);
+    return cudaGetLastError();
+  }
+  tpr_k3_scan<<<1, threads, 0, st>>>(xf_in, xf, n, geo.block_tokens, filter, meta, totals);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (n_hint <= 0) n_hint = 1;
   int64_t blocks = (n_hint + 255) / 256;
   const int64_t max_blocks = (int64_t)sm_count() * 8;
   if (blocks > max_blocks) blocks = max_blocks;
-  tpr_k3_remap<<<(unsigned)blocks, 256, 0, st>>>(xf, n, meta, totals, geo, cl, work, work_ext,
-                                                 status);
-  return cudaGetLastError();
+  return launch_ex(tpr_k3_remap, dim3((unsigned)blocks), dim3(256), 0, st, pdl,
+                   (const int32_t*)xf, n, (const int64_t*)meta, (const int64_t*)totals, geo, cl,
+                   work, work_ext, status);
 }
 
 cudaError_t launch_k1(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
-                      int64_t n_units, cudaStream_t st) {
+                      int64_t n_units, cudaStream_t st, bool pdl) {
   if (n_units <= 0) return cudaSuccess;
   const void* fn = reinterpret_cast<const void*>(&tpr_k1_kv_migrate<kCopyUnroll>);
   const int grid = copy_grid(fn, kCopyThreads, n_units * p.items_per_unit);
-  tpr_k1_kv_migrate<kCopyUnroll><<<grid, kCopyThreads, 0, st>>>(work, n_units, p, cl);
-  return cudaGetLastError();
+  return launch_ex(tpr_k1_kv_migrate<kCopyUnroll>, dim3(grid), dim3(kCopyThreads), 0, st, pdl,
+                   work, n_units, p, cl);
 }
 
 cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
