@@ -98,7 +98,11 @@ cudaError_t run_k1(const tpr::KvCopyParams& p, const tpr::KvClusterParams& cl, c
 // Records in caller memory the device can read directly: pinned (page-locked)
 // host memory under unified addressing, or device memory. Then K3 reads them
 // in place and the separate H2D copy disappears from the switch.
+int64_t env_i64(const char* name, int64_t dflt);
+
 const int32_t* device_view(const int32_t* h) {
+  static const bool on = env_i64("TPR_ZERO_COPY", 1) != 0;  // 0: always copy H2D first
+  if (!on) return nullptr;
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
     cudaGetLastError();

@@ -54,7 +54,7 @@ def main():
     args = ap.parse_args()
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
-    env = {k: os.environ.get(k, "") for k in ("TPR_PDL", "TPR_K3_FUSE_UNITS")}
+    env = {k: os.environ.get(k, "") for k in ("TPR_PDL", "TPR_K3_FUSE_UNITS", "TPR_ZERO_COPY")}
     kv = LLAMA_3_1_8B.kv
     out = open(args.out, "a") if args.out else None
     torch.cuda.set_device(0)
