@@ -201,6 +201,18 @@ def setup_ours(w, device, overlap=None, weights_mode="sharded"):
     return ReconfigurationExecutor(cluster, store, time_kernels=True, overlap=overlap)
 
 
+def weights_note(w, w_bytes) -> str:
+    if w.old_weight_groups is None:
+        if w.model.name.endswith("70B"):
+            return ("KV only at N=1: 8 logical slots of 70B shards (2 full copies at TP4) exceed one "
+                    "180 GB HBM; K2 on the 70B matrix shapes: tools/weight_sweep.py --model 70b")
+        return "KV only (the BASELINE config names no weight reshard)"
+    if w_bytes == 0:
+        return ("weight reshard runs, but after the first switch every new shard lies inside a "
+                "resident slice range (reuse): steady-state switches are views, 0 bytes")
+    return "sharded weights: missing slices rebuilt by K2 every switch"
+
+
 def one_switch(ex, w, forward: bool, sync: bool):
     if forward:
         return ex.switch(w.old, w.new, new_weight_groups=w.new_weight_groups,
@@ -649,7 +661,10 @@ def main():
     prof = ROOT / "profiles" / "k1_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(prof.read_text())
+            # DRAM bytes of the captured launch: only valid for that workload
+            if tj.get("workload") == w.name:
+                traffic = tj.get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
     cpu = None
@@ -671,6 +686,7 @@ def main():
             "k1_k2_overlap": ex.overlap, "copy_engine": _engine_name(),
             "weights_mode": args.weights_mode,
             "kv_bytes_per_step": kv_per_step, "weight_bytes_per_step": w_bytes / args.steps,
+            "weights_note": weights_note(w, w_bytes),
             "l2": "inputs larger than L2 (>= 24 GiB moved per step)",
             "parallelism": "replicas" if world > 1 else "1 GPU, logical ranks",
         },

@@ -5,6 +5,14 @@ rebuilt (local + fetched), K2 time (CUDA events on its stream), GB/s and the
 HBM-roofline fraction, and a pattern check of every resulting shard.
 
     python tools/weight_sweep.py --out profiles/r01_weight_sweep.jsonl
+
+Llama-3.1-70B: its full sharded copy is 141 GB, so 8 logical slots of it
+cannot sit in one 180 GB HBM. ``--model 70b --layers 20`` keeps every 70B
+matrix shape (and the embedding / lm_head) with 20 of the 80 decoder layers:
+K2's per-byte behaviour (row lengths, segment mix) is that of the full model
+and bytes scale linearly with the layer count.
+
+    python tools/weight_sweep.py --model 70b --layers 20 --sets 8:4,8 --sets 4:2,4
 """
 
 from __future__ import annotations
@@ -22,7 +30,9 @@ def main():
     import torch
 
     from paper_2605_05467_b200 import workloads
-    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
+    import dataclasses
+
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B, LLAMA_3_1_70B
     from paper_2605_05467_b200.weights import ShardedWeightStore
 
     ap = argparse.ArgumentParser()
@@ -30,14 +40,24 @@ def main():
     ap.add_argument("--reps", type=int, default=5, help="timed a->b reshards (median)")
     ap.add_argument("--engine", choices=["bulk", "vector"], default="bulk")
     ap.add_argument("--only", default="", help="comma list of slots:a:b, e.g. 8:2:4")
+    ap.add_argument("--model", choices=["8b", "70b"], default="8b")
+    ap.add_argument("--layers", type=int, default=None, help="decoder layers kept (default: all)")
+    ap.add_argument("--sets", action="append", default=None,
+                    help="slots:levels, e.g. 8:2,4,8 (repeatable)")
     args = ap.parse_args()
+    model = LLAMA_3_1_8B if args.model == "8b" else LLAMA_3_1_70B
+    if args.layers is not None and args.layers != model.layers:
+        model = dataclasses.replace(model, name=f"{model.name} ({args.layers} of {model.layers} layers)",
+                                    layers=args.layers, matrices=())
+    sets = [(4, (1, 2, 4)), (8, (2, 4, 8))] if not args.sets else [
+        (int(x.split(":")[0]), tuple(int(v) for v in x.split(":")[1].split(","))) for x in args.sets]
     from paper_2605_05467_b200 import _native
     _native.set_copy_engine(args.engine)
     only = {tuple(int(v) for v in x.split(":")) for x in args.only.split(",") if x}
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     out = open(args.out, "w")
-    for n, levels in ((4, (1, 2, 4)), (8, (2, 4, 8))):
+    for n, levels in sets:
         gpus = tuple(range(n))
         for a in levels:
             for b in levels:
@@ -46,7 +66,7 @@ def main():
                 # a->b timed, b->a untimed, repeated; the first pair is warm-up
                 # (the first touch of freshly cudaMalloc'd arenas costs ~0.1
                 # ms/GB once per process; the caching allocator reuses them)
-                store = ShardedWeightStore(LLAMA_3_1_8B, gpus)
+                store = ShardedWeightStore(model, gpus)
                 store.load(workloads.tp_groups(gpus, a))
                 torch.cuda.synchronize()
                 st = torch.cuda.current_stream()
@@ -61,7 +81,7 @@ def main():
                         store.reshard(workloads.tp_groups(gpus, a), stream=st)
                 ms = sorted(times)[len(times) // 2]
                 bad = store.verify()
-                row = {"gpus": n, "tp_old": a, "tp_new": b, "views": s.views,
+                row = {"model": model.name, "gpus": n, "tp_old": a, "tp_new": b, "views": s.views,
                        "local_bytes": s.local_bytes, "remote_bytes": s.remote_bytes,
                        "segments": s.segments, "k2_ms": ms, "k2_ms_min": min(times),
                        "gbs": s.bytes / (ms * 1e-3) / 1e9 if s.bytes else None,
