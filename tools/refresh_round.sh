@@ -1,9 +1,15 @@
 # Re-measure everything the docs cite (one B200). Outputs under gpurun_out/.
+#   bash tools/refresh_round.sh [tag]     (default tag: final)
+T=${1:-final}
+O=gpurun_out
 set -x
-timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/final_pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/final_pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/final_bench_n1.json 2> gpurun_out/final_bench_n1.err
-timeout 600 python bench.py --config 4 > gpurun_out/final_bench_headline.json 2> gpurun_out/final_bench_headline.err
-for c in 0 2 3; do timeout 600 python bench.py --config $c --no-cpu > gpurun_out/final_bench_cfg$c.json 2> gpurun_out/final_bench_cfg$c.err; done
-timeout 600 python bench.py --weights-mode full_copy_per_gpu --no-cpu > gpurun_out/final_bench_fullcopy.json 2> gpurun_out/final_bench_fullcopy.err
-timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/final_bench_ref.json 2> gpurun_out/final_bench_ref.err
-timeout 900 python tools/sweep.py --out gpurun_out/final_sweep.jsonl > gpurun_out/final_sweep.log 2>&1
+timeout 1200 python -m pytest tests -q -m gpu > $O/${T}_pytest_gpu.log 2>&1; echo rc=$? >> $O/${T}_pytest_gpu.log
+timeout 600 python bench.py > $O/${T}_bench_n1.json 2> $O/${T}_bench_n1.err
+timeout 600 python bench.py --config 4 > $O/${T}_bench_headline.json 2> $O/${T}_bench_headline.err
+for c in 0 2 3; do timeout 600 python bench.py --config $c --no-cpu > $O/${T}_bench_cfg$c.json 2> $O/${T}_bench_cfg$c.err; done
+timeout 600 python bench.py --weights-mode full_copy_per_gpu --no-cpu > $O/${T}_bench_fullcopy.json 2> $O/${T}_bench_fullcopy.err
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/${T}_bench_ref.json 2> $O/${T}_bench_ref.err
+timeout 300 python tools/small_switch.py --out $O/${T}_small_switch.jsonl > $O/${T}_small_switch.log 2>&1
+timeout 900 python tools/weight_sweep.py --out $O/${T}_weight_sweep.jsonl > $O/${T}_weight_sweep.log 2>&1
+timeout 900 python tools/weight_sweep.py --model 70b --layers 20 --sets 8:4,8 --sets 4:2,4 --out $O/${T}_weight_sweep_70b.jsonl > $O/${T}_weight_sweep_70b.log 2>&1
+timeout 1500 python tools/sweep.py --out $O/${T}_sweep.jsonl > $O/${T}_sweep.log 2>&1

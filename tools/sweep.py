@@ -41,7 +41,10 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=str(ROOT / "profiles" / "sweep.jsonl"))
-    ap.add_argument("--max-seqs", type=int, default=128)
+    ap.add_argument("--max-seqs", type=int, default=128,
+                    help="largest sequence count with fixed 4096-token contexts")
+    ap.add_argument("--trace-max-seqs", type=int, default=256,
+                    help="largest sequence count with bursty-trace contexts")
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--cpu-max-seqs", type=int, default=8)
     ap.add_argument("--modes", default="fixed4096,trace")
@@ -55,81 +58,103 @@ def main():
     gpus = tuple(range(8))
     trace = json.load(gzip.open(ROOT / "tests" / "golden" / "reference_golden.json.gz", "rt"))["bursty_trace"]
     trace_ctx = [p + o // 2 for p, o in trace]
-    seq_counts = [s for s in (1, 2, 4, 8, 16, 32, 64, 128) if s <= args.max_seqs]
-    max_ctx = max(4096, max(trace_ctx))
-    units = 2 * args.max_seqs * kv.blocks(4096) + 256
-    cluster = PagedKvCluster(kv, gpus, units_per_gpu=units, max_requests=args.max_seqs,
-                             max_blocks=kv.blocks(max_ctx), fragmented=True, seed=0)
     params = M.CostModelParams()
     out = open(args.out, "w")
     stream = torch.cuda.current_stream()
-    for mode in args.modes.split(","):
+
+    def slot_units(layouts):
+        """Pool units each slot holds for ``layouts`` (one page per head-block)."""
+        need = [0] * len(gpus)
+        for lay in layouts:
+            for _, c in lay.requests:
+                for g in lay.owners():
+                    need[g] += kv.blocks(c)
+        return need
+
+    def points(mode):
+        top = args.max_seqs if mode == "fixed4096" else args.trace_max_seqs
         for a in (1, 2, 4, 8):
             for b in (1, 2, 4, 8):
                 if a == b:
                     continue
-                for n in seq_counts:
+                for n in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+                    if n > top:
+                        continue
                     ctxs = [4096] * n if mode == "fixed4096" else trace_ctx[:n]
                     reqs = [(i, c) for i, c in enumerate(ctxs)]
                     la = workloads.round_robin(workloads.tp_groups(gpus, a), reqs, 8)
                     lb = workloads.round_robin(workloads.tp_groups(gpus, b), reqs, 8)
-                    cluster.admit(la, seed=n)
-                    fwd = M.plan_repartition(la, lb, kv.kv_bytes_per_token_per_head)
-                    back = M.plan_repartition(lb, la, kv.kv_bytes_per_token_per_head)
-                    for p in (fwd, back):  # warm-up, leaves the cluster in layout A
-                        cluster.migrate(p, validate=False)
-                    torch.cuda.synchronize()
-                    dev_ms, host_ms, exec_ms, plan_ms = [], [], [], []
-                    for r in range(args.reps):
-                        p = fwd if r % 2 == 0 else back
-                        e0, ep, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-                        t0 = time.perf_counter()
-                        e0.record(stream)
-                        plan = M.plan_repartition(*((la, lb) if r % 2 == 0 else (lb, la)),
-                                                  kv.kv_bytes_per_token_per_head)
-                        plan_ms.append((time.perf_counter() - t0) * 1e3)
-                        ep.record(stream)
-                        cluster.migrate(plan, validate=False)
-                        e1.record(stream)
-                        e1.synchronize()
-                        host_ms.append((time.perf_counter() - t0) * 1e3)
-                        dev_ms.append(e0.elapsed_time(e1))
-                        exec_ms.append(ep.elapsed_time(e1))
-                    if args.reps % 2:
-                        cluster.migrate(back, validate=False)
-                    k1_ms = []
-                    for r in range(2 * args.k1_reps):  # fwd/back pairs: ends in layout A
-                        k0, k1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
-                        cluster.migrate(fwd if r % 2 == 0 else back, validate=False,
-                                        k1_events=(k0, k1))
-                        k1.synchronize()
-                        if r % 2 == 0:
-                            k1_ms.append(k0.elapsed_time(k1))
-                    v = cluster.verify(seed=n)
-                    ok = v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
-                    cluster.release([r for r, _ in reqs])
-                    nbytes = fwd.total_bytes
-                    d = float(np.median(dev_ms))
-                    x = float(np.median(exec_ms))
-                    cpu_ms = cpu_point(la, lb, reqs, gpus, kv) if n <= args.cpu_max_seqs else None
-                    row = {
-                        "mode": mode, "tp_old": a, "tp_new": b, "seqs": n,
-                        "ctx_total": int(sum(ctxs)), "transfers": len(fwd), "bytes": nbytes,
-                        "device_ms": d, "host_ms": float(np.median(host_ms)),
-                        "gbs": nbytes / (d * 1e-3) / 1e9 if d > 0 else None,
-                        "hbm_frac": (2 * nbytes / (peak * 1e9)) / (d * 1e-3) if d > 0 else None,
-                        # without the host planning the GPU idles through
-                        "plan_host_ms": float(np.median(plan_ms)), "exec_device_ms": x,
-                        "exec_hbm_frac": (2 * nbytes / (peak * 1e9)) / (x * 1e-3) if x > 0 else None,
-                        "k1_ms": float(np.median(k1_ms)) if k1_ms else None,
-                        "k1_hbm_frac": (2 * nbytes / (peak * 1e9)) / (float(np.median(k1_ms)) * 1e-3)
-                        if k1_ms else None,
-                        "predicted_ms_ref_model": M.switch_cost(M.WARM, fwd, params),
-                        "cpu_restatement_ms": cpu_ms, "bit_exact_property": ok,
-                    }
-                    out.write(json.dumps(row) + "\n")
-                    out.flush()
-                    print(json.dumps(row))
+                    yield a, b, n, ctxs, reqs, la, lb
+
+    for mode in args.modes.split(","):
+        # one cluster per mode, sized for its largest point: old and new pages
+        # coexist while a switch runs (sources are released after the copy)
+        units, max_ctx, max_n = 0, 0, 0
+        for a, b, n, ctxs, reqs, la, lb in points(mode):
+            units = max(units, max(x + y for x, y in zip(slot_units(la), slot_units(lb))))
+            max_ctx, max_n = max(max_ctx, max(ctxs)), max(max_n, n)
+        cluster = PagedKvCluster(kv, gpus, units_per_gpu=units + 256, max_requests=max_n,
+                                 max_blocks=kv.blocks(max_ctx), fragmented=True, seed=0)
+        for a, b, n, ctxs, reqs, la, lb in points(mode):
+            cluster.admit(la, seed=n)
+            fwd = M.plan_repartition(la, lb, kv.kv_bytes_per_token_per_head)
+            back = M.plan_repartition(lb, la, kv.kv_bytes_per_token_per_head)
+            for p in (fwd, back):  # warm-up, leaves the cluster in layout A
+                cluster.migrate(p, validate=False)
+            torch.cuda.synchronize()
+            dev_ms, host_ms, exec_ms, plan_ms = [], [], [], []
+            for r in range(args.reps):
+                p = fwd if r % 2 == 0 else back
+                e0, ep, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                t0 = time.perf_counter()
+                e0.record(stream)
+                plan = M.plan_repartition(*((la, lb) if r % 2 == 0 else (lb, la)),
+                                          kv.kv_bytes_per_token_per_head)
+                plan_ms.append((time.perf_counter() - t0) * 1e3)
+                ep.record(stream)
+                cluster.migrate(plan, validate=False)
+                e1.record(stream)
+                e1.synchronize()
+                host_ms.append((time.perf_counter() - t0) * 1e3)
+                dev_ms.append(e0.elapsed_time(e1))
+                exec_ms.append(ep.elapsed_time(e1))
+            if args.reps % 2:
+                cluster.migrate(back, validate=False)
+            k1_ms = []
+            for r in range(2 * args.k1_reps):  # fwd/back pairs: ends in layout A
+                k0, k1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                cluster.migrate(fwd if r % 2 == 0 else back, validate=False,
+                                k1_events=(k0, k1))
+                k1.synchronize()
+                if r % 2 == 0:
+                    k1_ms.append(k0.elapsed_time(k1))
+            v = cluster.verify(seed=n)
+            ok = v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
+            cluster.release([r for r, _ in reqs])
+            nbytes = fwd.total_bytes
+            d = float(np.median(dev_ms))
+            x = float(np.median(exec_ms))
+            cpu_ms = cpu_point(la, lb, reqs, gpus, kv) if n <= args.cpu_max_seqs else None
+            row = {
+                "mode": mode, "tp_old": a, "tp_new": b, "seqs": n,
+                "ctx_total": int(sum(ctxs)), "transfers": len(fwd), "bytes": nbytes,
+                "device_ms": d, "host_ms": float(np.median(host_ms)),
+                "gbs": nbytes / (d * 1e-3) / 1e9 if d > 0 else None,
+                "hbm_frac": (2 * nbytes / (peak * 1e9)) / (d * 1e-3) if d > 0 else None,
+                # without the host planning the GPU idles through
+                "plan_host_ms": float(np.median(plan_ms)), "exec_device_ms": x,
+                "exec_hbm_frac": (2 * nbytes / (peak * 1e9)) / (x * 1e-3) if x > 0 else None,
+                "k1_ms": float(np.median(k1_ms)) if k1_ms else None,
+                "k1_hbm_frac": (2 * nbytes / (peak * 1e9)) / (float(np.median(k1_ms)) * 1e-3)
+                if k1_ms else None,
+                "predicted_ms_ref_model": M.switch_cost(M.WARM, fwd, params),
+                "cpu_restatement_ms": cpu_ms, "bit_exact_property": ok,
+            }
+            out.write(json.dumps(row) + "\n")
+            out.flush()
+            print(json.dumps(row))
+        del cluster
+        torch.cuda.empty_cache()
     out.close()
 
 
