@@ -104,6 +104,15 @@ typedef struct tpr_kv_cluster {
 #define TPR_ENGINE_BULK 1
 int tpr_set_copy_engine(int32_t engine);
 int tpr_get_copy_engine(void);
+/* Launch-path knobs of tpr_kv_switch (process-wide; initial values from the
+ * environment variables in brackets):
+ *   "k3_fuse_units" [TPR_K3_FUSE_UNITS, 4096]: plans up to this many units
+ *                   run K3 as one fused CTA (scan + remap), 0 = never;
+ *   "pdl"           [TPR_PDL, 1]: programmatic dependent launch of K3b / K1;
+ *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place.
+ * tpr_get_tuning returns the current value, -1 for an unknown key. */
+int tpr_set_tuning(const char* key, int64_t value);
+int64_t tpr_get_tuning(const char* key);
 int tpr_version(void);
 const char* tpr_last_error(void);
 int tpr_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);

@@ -25,7 +25,7 @@ TPR_ENOTFOUND = -4  # an id outside the caller's lookup tables (use the Python m
 
 # Every exported symbol of include/tpr.h; tests check the library exports all.
 EXPORTS = (
-    "tpr_set_copy_engine", "tpr_get_copy_engine",
+    "tpr_set_copy_engine", "tpr_get_copy_engine", "tpr_set_tuning", "tpr_get_tuning",
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads", "tpr_plan_repartition",
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
     "tpr_memcpy_h2d", "tpr_memcpy_d2h",
@@ -79,6 +79,8 @@ _P32 = POINTER(c_int32)
 _SIGNATURES = {
     "tpr_set_copy_engine": (c_int32, [c_int32]),
     "tpr_get_copy_engine": (c_int32, []),
+    "tpr_set_tuning": (c_int32, [c_char_p, c_int64]),
+    "tpr_get_tuning": (c_int64, [c_char_p]),
     "tpr_version": (c_int32, []),
     "tpr_last_error": (c_char_p, []),
     "tpr_device_info": (c_int32, [_P32, _P32, _P32]),
@@ -158,11 +160,20 @@ ENGINES = {"vector": 0, "bulk": 1}
 
 
 def k3_fuse_units() -> int:
-    """Plan size (units) up to which K3 runs as one fused CTA (mirrors
-    tpr_api.cpp: TPR_K3_FUSE_UNITS, default 4096)."""
-    import os
-    v = os.environ.get("TPR_K3_FUSE_UNITS", "")
-    return int(v) if v else 4096
+    """Plan size (units) up to which K3 runs as one fused CTA."""
+    return int(load().tpr_get_tuning(b"k3_fuse_units"))
+
+
+TUNING_KEYS = ("k3_fuse_units", "pdl", "zero_copy")
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Launch-path knob of tpr_kv_switch (see include/tpr.h)."""
+    call("tpr_set_tuning", key.encode(), int(value))
+
+
+def get_tuning(key: str) -> int:
+    return int(load().tpr_get_tuning(key.encode()))
 
 
 def kv_switch_launches(units: int) -> int:

@@ -100,9 +100,22 @@ cudaError_t run_k1(const tpr::KvCopyParams& p, const tpr::KvClusterParams& cl, c
 // in place and the separate H2D copy disappears from the switch.
 int64_t env_i64(const char* name, int64_t dflt);
 
+// Launch-path knobs (process-wide): initialised from the environment, changed
+// at run time with tpr_set_tuning (tests cover every combination).
+std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1};
+
+int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
+  int64_t v = k.load(std::memory_order_relaxed);
+  if (v < 0) {
+    v = env_i64(env, dflt);
+    if (v < 0) v = 0;
+    k.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 const int32_t* device_view(const int32_t* h) {
-  static const bool on = env_i64("TPR_ZERO_COPY", 1) != 0;  // 0: always copy H2D first
-  if (!on) return nullptr;
+  if (!knob(g_zero_copy, "TPR_ZERO_COPY", 1)) return nullptr;  // 0: always copy H2D first
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
     cudaGetLastError();
@@ -129,16 +142,12 @@ cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_
 }  // namespace
 
 namespace tpr {
-bool pdl_enabled() {
-  static const bool on = env_i64("TPR_PDL", 1) != 0;
-  return on;
-}
+bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
 
 int64_t k3_fuse_units() {
   // one 1024-thread CTA expands up to 4 units per thread faster than a second
   // launch + dependency gap (measured, profiles/README.md)
-  static const int64_t n = env_i64("TPR_K3_FUSE_UNITS", 4096);
-  return n;
+  return knob(g_fuse, "TPR_K3_FUSE_UNITS", 4096);
 }
 
 int set_error(int code, const char* fmt, ...) {
@@ -176,6 +185,24 @@ int tpr_set_copy_engine(int32_t engine) {
 }
 
 int tpr_get_copy_engine(void) { return g_engine.load(); }
+
+int tpr_set_tuning(const char* key, int64_t value) {
+  if (!key) return fail(TPR_EINVAL, "null tuning key");
+  if (value < 0) return fail(TPR_EINVAL, "tuning value must be >= 0");
+  if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
+  else if (!strcmp(key, "pdl")) g_pdl.store(value != 0);
+  else if (!strcmp(key, "zero_copy")) g_zero_copy.store(value != 0);
+  else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
+  return TPR_OK;
+}
+
+int64_t tpr_get_tuning(const char* key) {
+  if (!key) return -1;
+  if (!strcmp(key, "k3_fuse_units")) return tpr::k3_fuse_units();
+  if (!strcmp(key, "pdl")) return tpr::pdl_enabled() ? 1 : 0;
+  if (!strcmp(key, "zero_copy")) return knob(g_zero_copy, "TPR_ZERO_COPY", 1);
+  return -1;
+}
 
 const char* tpr_last_error(void) { return g_err.c_str(); }
 

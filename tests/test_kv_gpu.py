@@ -91,6 +91,56 @@ def test_chain_of_switches_and_back():
     assert v["pages_checked"] == sum(8 * TINY.blocks(ctx) for _, ctx in reqs)
 
 
+LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
+    "split_plain_h2d": dict(k3_fuse_units=0, pdl=0, zero_copy=0),
+    "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=1, zero_copy=1),
+    "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=1, zero_copy=1),
+    "fused_plain_h2d": dict(k3_fuse_units=1 << 30, pdl=0, zero_copy=0),
+}
+
+
+@pytest.fixture
+def launch_path(request):
+    from paper_2605_05467_b200 import _native
+    saved = {k: _native.get_tuning(k) for k in _native.TUNING_KEYS}
+    for k, v in LAUNCH_PATHS[request.param].items():
+        _native.set_tuning(k, v)
+    yield request.param
+    for k, v in saved.items():
+        _native.set_tuning(k, v)
+
+
+@pytest.mark.parametrize("launch_path", sorted(LAUNCH_PATHS), indirect=True)
+def test_launch_paths_bit_exact(launch_path):
+    # fused single-CTA K3 vs scan + remap, with and without programmatic
+    # dependent launch and zero-copy records: identical pools, tables, rings
+    gpus = tuple(range(8))
+    rng = np.random.default_rng(77)
+    reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 300, size=40))]
+    lay = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2, 4, 8)}
+    c = make(TINY, gpus, units=4096, reqs=48, blocks=24, fragmented=True, seed=3)
+    c.admit(lay[2], seed=8)
+    for a, b in ((2, 8), (8, 1), (1, 4), (4, 2)):
+        plan = M.plan_repartition(lay[a], lay[b], TINY.kv_bytes_per_token_per_head)
+        migrate_and_compare(c, plan)
+    v = c.verify(seed=8)
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
+def test_large_plan_takes_split_k3_and_matches_oracle():
+    # > k3_fuse_units units with the default knobs: scan + remap launches
+    from paper_2605_05467_b200 import _native
+    gpus = (0, 1, 2, 3)
+    reqs = [(i, 16 * 40) for i in range(40)]  # 40 blocks x 8 heads x 40 reqs = 12800 units
+    lay = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 4)}
+    c = make(TINY, gpus, units=8192, reqs=40, blocks=40, fragmented=True, seed=5)
+    c.admit(lay[1], seed=3)
+    plan = M.plan_repartition(lay[1], lay[4], TINY.kv_bytes_per_token_per_head)
+    stats = migrate_and_compare(c, plan)
+    assert stats.units > _native.k3_fuse_units()
+    assert _native.kv_switch_launches(stats.units) == 3
+
+
 def test_engine_path_disjoint_groups():
     # prefill->decode handoff style: head_transfers between disjoint groups
     gpus = (0, 1, 2, 3, 4, 5)

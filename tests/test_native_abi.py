@@ -13,7 +13,7 @@ from paper_2605_05467_b200 import _native
 
 def declared_symbols():
     text = (ROOT / "include" / "tpr.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(tpr_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tpr_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -23,6 +23,23 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(_native.EXPORTS)
     for name in names:
         assert hasattr(lib, name), name
+
+
+def test_tuning_knobs_roundtrip():
+    lib = _native.load()
+    saved = {k: _native.get_tuning(k) for k in _native.TUNING_KEYS}
+    try:
+        assert saved["k3_fuse_units"] >= 0 and saved["pdl"] in (0, 1) and saved["zero_copy"] in (0, 1)
+        _native.set_tuning("k3_fuse_units", 0)
+        assert _native.get_tuning("k3_fuse_units") == 0
+        _native.set_tuning("pdl", 5)
+        assert _native.get_tuning("pdl") == 1
+        assert lib.tpr_set_tuning(b"nope", 1) == -1 and b"unknown tuning key" in lib.tpr_last_error()
+        assert lib.tpr_set_tuning(b"pdl", -1) == -1
+        assert lib.tpr_get_tuning(b"nope") == -1
+    finally:
+        for k, v in saved.items():
+            _native.set_tuning(k, v)
 
 
 def test_abi_version():
