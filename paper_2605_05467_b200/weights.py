@@ -176,11 +176,16 @@ class ShardedWeightStore:
         return (b - a) * self.bytes_per_slice + self.rep_arena[gpu].numel()
 
     # -------------------------------------------------------------- reshard
-    def plan(self, new_groups: Sequence[Sequence[int]], parked: Sequence[int] = ()):
+    def plan(self, new_groups: Sequence[Sequence[int]], parked: Sequence[int] = (),
+             trim: bool = False):
         """Host reshard planner: new resident ranges, sources of missing slices.
 
         ``parked`` GPUs leave service (scale-in): they keep their resident
-        slices, which stay available as sources. Returns (new_active,
+        slices, which stay available as sources. ``trim`` shrinks a GPU whose
+        resident range is larger than its new shard to exactly that shard (a
+        local compaction copy that frees the extra slices, e.g. for KV pages);
+        without it the shard is a view and the extra slices stay resident for
+        reuse by a later switch. Returns (new_active,
         new_resident, moves) where moves[g] is a list of (src_gpu, slice_lo,
         slice_hi) runs building g's new arena (empty when the new shard is a
         view of resident slices).
@@ -197,7 +202,7 @@ class ShardedWeightStore:
                 continue
             x, y = act[g]
             a, b = self.resident[g]
-            if a <= x and y <= b:
+            if a <= x and y <= b and not (trim and (a, b) != (x, y)):
                 new_res[g] = (a, b)
                 moves[g] = []
                 continue
@@ -245,13 +250,14 @@ class ShardedWeightStore:
         return seg.reshape(-1, 8)
 
     def reshard(self, new_groups: Sequence[Sequence[int]], stream: torch.cuda.Stream | None = None,
-                events: tuple | None = None, parked: Sequence[int] = ()) -> ReshardStats:
+                events: tuple | None = None, parked: Sequence[int] = (),
+                trim: bool = False) -> ReshardStats:
         """Move to ``new_groups``: K2 copies for every GPU whose new shard is not
         resident; views for the rest. Stream-ordered, no host sync: new arenas
         are allocated and old ones released on ``stream`` (the caching
         allocator reuses a block on the same stream only after the K2 that
         last touched it), so the host may run ahead without holding memory."""
-        act, new_res, moves = self.plan(new_groups, parked)
+        act, new_res, moves = self.plan(new_groups, parked, trim)
         for g in parked:
             act[g] = new_res[g]
         stats = ReshardStats(egress={g: 0 for g in self.gpu_ids}, ingress={g: 0 for g in self.gpu_ids})

@@ -101,6 +101,23 @@ def test_sequence_reuses_resident_slices():
     store.finish()
 
 
+def test_trim_compacts_and_stays_bit_exact():
+    gpus = (0, 1, 2, 3)
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load(workloads.tp_groups(gpus, 4))
+    store.reshard(workloads.tp_groups(gpus, 1))          # every GPU gathers all 8 slices
+    pieces = host_pieces(store)
+    kept = store.reshard(workloads.tp_groups(gpus, 2))   # views: the full copy stays resident
+    assert kept.views == 4 and kept.bytes == 0
+    trimmed = store.reshard(workloads.tp_groups(gpus, 2), trim=True)  # compact to TP2 halves
+    assert trimmed.remote_bytes == 0 and trimmed.local_bytes == 4 * 4 * store.bytes_per_slice
+    assert store.resident == groups_ranges(workloads.tp_groups(gpus, 2))
+    torch.cuda.synchronize()
+    check_against_oracle(store, pieces, workloads.tp_groups(gpus, 2))
+    assert store.verify() == 0
+    store.finish()
+
+
 def test_device_matrix_fill_matches_numpy_pattern():
     from paper_2605_05467_b200 import pattern
     store = ShardedWeightStore(MODEL, (0, 1))

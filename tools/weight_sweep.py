@@ -78,7 +78,10 @@ def main():
                     if r:
                         times.append(e0.elapsed_time(e1))
                     if r < args.reps:
-                        store.reshard(workloads.tp_groups(gpus, a), stream=st)
+                        # back to exactly TP-a residency (trim drops slices a
+                        # TP-b shard kept for reuse), so every timed a->b
+                        # reshard rebuilds what a fresh TP-a deployment would
+                        store.reshard(workloads.tp_groups(gpus, a), stream=st, trim=True)
                 ms = sorted(times)[len(times) // 2]
                 bad = store.verify()
                 row = {"model": model.name, "gpus": n, "tp_old": a, "tp_new": b, "views": s.views,
