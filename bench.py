@@ -210,6 +210,9 @@ def weights_note(w, w_bytes) -> str:
     if w_bytes == 0:
         return ("weight reshard runs, but after the first switch every new shard lies inside a "
                 "resident slice range (reuse): steady-state switches are views, 0 bytes")
+    if w.trim_on_reverse:
+        return ("sharded weights: the consolidation gathers 7/8 of the model onto GPU0 (K2), the "
+                "reverse switch compacts GPU0 back to its TP8 slice (trim)")
     return "sharded weights: missing slices rebuilt by K2 every switch"
 
 
@@ -218,7 +221,7 @@ def one_switch(ex, w, forward: bool, sync: bool):
         return ex.switch(w.old, w.new, new_weight_groups=w.new_weight_groups,
                          parked=w.parked, sync=sync, validate=False)
     return ex.switch(w.new, w.old, new_weight_groups=w.old_weight_groups, parked=(),
-                     sync=sync, validate=False)
+                     sync=sync, validate=False, trim=w.trim_on_reverse)
 
 
 # ---------------------------------------------------------------------------

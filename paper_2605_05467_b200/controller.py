@@ -80,11 +80,13 @@ class ReconfigurationExecutor:
 
     def switch(self, old_layouts: list[KvLayout], new_layouts: list[KvLayout],
                new_weight_groups=None, parked=(), sync: bool = True,
-               validate: bool = True, stream: torch.cuda.Stream | None = None) -> SwitchResult:
+               validate: bool = True, stream: torch.cuda.Stream | None = None,
+               trim: bool = False) -> SwitchResult:
         """Stop-and-migrate TP switch. With ``sync`` the call returns after the
         switch completed on the device and reports measured latencies; without
         it, work is only enqueued and ``stream`` (default: the device's default
-        stream) waits for it."""
+        stream) waits for it. ``trim`` compacts GPUs whose resident weight
+        slices exceed their new shard (ShardedWeightStore.reshard)."""
         t0 = time.perf_counter()
         main = stream or self.main_stream
         ev = {}
@@ -115,7 +117,7 @@ class ReconfigurationExecutor:
                 ws.wait_stream(main)
             with nvtx("weights K2"):
                 w_stats = self.weights.reshard(
-                    new_weight_groups, stream=ws, parked=parked,
+                    new_weight_groups, stream=ws, parked=parked, trim=trim,
                     events=(ev["k2_start"], ev["k2_end"]) if self.time_kernels else None)
             if ws is not main:
                 main.wait_stream(ws)

@@ -34,6 +34,9 @@ class Workload:
     old_weight_groups: list[tuple[int, ...]] | None  # None: KV only
     new_weight_groups: list[tuple[int, ...]] | None
     parked: tuple[int, ...] = ()  # GPUs left idle by the new config (weights untouched)
+    # the reverse switch compacts weights to the old shards (frees the slices a
+    # consolidation gathered), so every forward switch gathers them again
+    trim_on_reverse: bool = False
 
     @property
     def requests(self):
@@ -41,7 +44,8 @@ class Workload:
 
     def reversed(self) -> "Workload":
         return Workload(self.name + " (reverse)", self.model, self.gpus, self.new, self.old,
-                        self.new_weight_groups, self.old_weight_groups, self.parked)
+                        self.new_weight_groups, self.old_weight_groups, self.parked,
+                        self.trim_on_reverse)
 
 
 def transition(model, n_gpus, tp_old, tp_new, n_seqs, ctx, weights=True, name=None) -> Workload:
@@ -72,7 +76,8 @@ def config(idx: int, **kw) -> Workload:
             KvLayout((g,), 1, m.n_kv_heads, ()) for g in gpus[1:]]
         w = kw.get("weights", True)
         return Workload("cfg3 Llama-3.1-8B TP8->TP1 consolidation 64x4096", m, gpus, old, new,
-                        [gpus] if w else None, [(0,)] if w else None, parked=gpus[1:])
+                        [gpus] if w else None, [(0,)] if w else None, parked=gpus[1:],
+                        trim_on_reverse=True)
     if idx == 3:  # 70B TP4 <-> TP8, 8 x 32k
         return transition(LLAMA_3_1_70B, 8, 4, 8, kw.get("seqs", 8), kw.get("ctx", 32768),
                           weights=kw.get("weights", False),
