@@ -195,6 +195,60 @@ int tpr_kv_records(const int64_t* plan, int64_t n, const int64_t* gpu_lut, int64
  * every record (apply_plan, migration.py:192-207, on the host placement). */
 int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads);
 
+/* ---- one call per switch: layouts -> plan -> records -> K3 + K1 -------- */
+/* Caller-owned state of one single-device cluster for tpr_kv_switch_layouts.
+ * Lookup tables as in tpr_kv_records; plan/records are host outputs (records
+ * pinned, so K3 reads them in place); the d_* buffers are device scratch. */
+typedef struct tpr_switch_tables {
+  const int64_t* gpu_lut;  /* [gpu id] -> slot, -1 absent                     */
+  int64_t gpu_lut_len;
+  const int64_t* gpu_ids;  /* [slot] -> gpu id                                */
+  const int64_t* req_lut;  /* [request id] -> request slot, -1 absent         */
+  int64_t req_lut_len;
+  const int32_t* slot_ctx; /* [request slot] -> context tokens                */
+  int32_t* owner;          /* [request slot][H] -> gpu slot; updated          */
+  int64_t kvb;             /* kv_bytes_per_token_per_head                      */
+  int32_t validate;        /* as tpr_kv_records                                */
+  int32_t _pad0;
+  int64_t* plan;           /* out: int64 [plan_cap][6], the MigrationPlan SoA  */
+  int64_t plan_cap;
+  int32_t* records;        /* out: int32 [plan_cap][6] K3 records (pinned)     */
+  int64_t in_units[TPR_MAX_GPUS];  /* out: units allocated per slot            */
+  int64_t out_units[TPR_MAX_GPUS]; /* out: units released per slot             */
+  int64_t n_plan;          /* out: transfers (or the plan_cap needed)          */
+  int64_t total_units;     /* out: units moved (or the work_cap needed)        */
+  int32_t* d_xfers;        /* device int32 [xfers_cap][6]                      */
+  int64_t* d_meta;         /* device int64 [xfers_cap][4]                      */
+  int64_t xfers_cap;
+  int64_t* d_totals;       /* device int64 [TPR_TOTALS_LEN]                    */
+  int32_t* d_work;         /* device int32x4 [work_cap]                        */
+  int64_t work_cap;
+  int32_t* d_status;       /* device int32                                     */
+} tpr_switch_tables_t;
+
+/* The host half of a switch, no device work (plan_repartition,
+ * migration.py:137-189, then tpr_kv_records and the capacity check).
+ * `layouts` packs the old then the new KvLayouts as int64:
+ *   n_old, n_new, then per layout: total_heads, tp, group[tp], count,
+ *   (request id, context length) x count.
+ * Returns TPR_ENOTFOUND when the switch needs the caller's general path: any
+ * check the reference reports (GPU sets, head counts, carried requests,
+ * context lengths, placement, capacity), a repeated old request id or an id
+ * outside the tables; nothing is modified then. TPR_ECAPACITY: plan_cap too
+ * small (n_plan = the capacity needed). */
+int tpr_switch_prepare(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                       const int64_t* layouts, int64_t layouts_len, tpr_switch_tables_t* t);
+
+/* tpr_switch_prepare, then K3 + K1 on `stream` (tpr_kv_switch over the
+ * pinned records) and the host placement update (tpr_kv_apply_owner). The
+ * caller commits in_units/out_units to its ring counters and keeps `records`
+ * untouched until the stream passes. TPR_ECAPACITY also when the device
+ * scratch is too small (n_plan / total_units = what is needed); nothing is
+ * launched then. */
+int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                          const int64_t* layouts, int64_t layouts_len, tpr_switch_tables_t* t,
+                          void* stream);
+
 /* ---- K3 + K1 in one call ----------------------------------------------- */
 /* The switch fast path: K3 (remap) and K1 (page copy), all on `stream`.
  * h_xfers (may be NULL when d_xfers is already filled): when it is pinned host

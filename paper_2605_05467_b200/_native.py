@@ -28,6 +28,7 @@ EXPORTS = (
     "tpr_set_copy_engine", "tpr_get_copy_engine", "tpr_set_tuning", "tpr_get_tuning",
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads", "tpr_plan_repartition",
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
+    "tpr_switch_prepare", "tpr_kv_switch_layouts",
     "tpr_memcpy_h2d", "tpr_memcpy_d2h",
     "tpr_copy_prepare", "tpr_weight_reshard",
     "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
@@ -73,6 +74,22 @@ class CopySegC(Structure):
     ]
 
 
+class SwitchTablesC(Structure):
+    _fields_ = [
+        ("gpu_lut", c_void_p), ("gpu_lut_len", c_int64), ("gpu_ids", c_void_p),
+        ("req_lut", c_void_p), ("req_lut_len", c_int64), ("slot_ctx", c_void_p),
+        ("owner", c_void_p), ("kvb", c_int64), ("validate", c_int32), ("_pad0", c_int32),
+        ("plan", c_void_p), ("plan_cap", c_int64), ("records", c_void_p),
+        ("in_units", c_int64 * TPR_MAX_GPUS), ("out_units", c_int64 * TPR_MAX_GPUS),
+        ("n_plan", c_int64), ("total_units", c_int64),
+        ("d_xfers", c_void_p), ("d_meta", c_void_p), ("xfers_cap", c_int64),
+        ("d_totals", c_void_p), ("d_work", c_void_p), ("work_cap", c_int64),
+        ("d_status", c_void_p),
+    ]
+
+
+TPR_ECAPACITY = -3
+
 _P64 = POINTER(c_int64)
 _P32 = POINTER(c_int32)
 
@@ -101,6 +118,10 @@ _SIGNATURES = {
     "tpr_kv_switch": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                 c_void_p]),
+    "tpr_switch_prepare": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int64,
+                                     POINTER(SwitchTablesC)]),
+    "tpr_kv_switch_layouts": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p,
+                                        c_int64, POINTER(SwitchTablesC), c_void_p]),
     "tpr_memcpy_h2d": (c_int32, [c_uint64, c_void_p, c_uint64, c_void_p]),
     "tpr_memcpy_d2h": (c_int32, [c_void_p, c_uint64, c_uint64, c_void_p]),
     "tpr_copy_prepare": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, _P64]),

@@ -96,20 +96,27 @@ class ReconfigurationExecutor:
         if self.time_kernels:
             for k in ("k1_start", "k1_end", "k2_start", "k2_end"):
                 ev[k] = torch.cuda.Event(enable_timing=True)
-        with nvtx("plan"):
-            plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
-        if self.handshake is not None:
-            with nvtx("handshake"):
-                self.handshake(plan)
         # one stream unless K1 and K2 overlap: no cross-stream event waits on
         # the (latency-bound) small-switch path
         ks = self.kv_stream if self.overlap else main
         if ks is not main:
             ks.wait_stream(main)
-        with nvtx("kv K3+K1"):
-            kv_stats = self.kv.migrate(
-                plan, stream=ks, validate=validate,
-                k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
+        if self.handshake is None and not self.time_kernels:
+            # plan + records + K3 + K1 in one native call
+            with nvtx("plan+kv K3+K1"):
+                plan, kv_stats = self.kv.switch_layouts(old_layouts, new_layouts, stream=ks,
+                                                        validate=validate)
+        else:
+            with nvtx("plan"):
+                plan = plan_repartition(old_layouts, new_layouts,
+                                        self.kv.kv.kv_bytes_per_token_per_head)
+            if self.handshake is not None:
+                with nvtx("handshake"):
+                    self.handshake(plan)
+            with nvtx("kv K3+K1"):
+                kv_stats = self.kv.migrate(
+                    plan, stream=ks, validate=validate,
+                    k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
         w_stats = None
         if self.weights is not None and new_weight_groups is not None:
             ws = self.w_stream if self.overlap else main

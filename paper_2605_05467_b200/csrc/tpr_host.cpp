@@ -186,6 +186,100 @@ int tpr_plan_repartition(int32_t n_old, const int64_t* old_count, const int32_t*
                         capacity, out, n_out);
 }
 
+// ---------------------------------------------------------------------------
+// One call per switch (tpr_switch_prepare / tpr_kv_switch_layouts): the
+// packed layouts are unpacked into the SoA that tpr_plan_repartition takes,
+// planned, turned into K3 records and checked against ring capacity. Every
+// failure the reference reports maps to TPR_ENOTFOUND: the caller's general
+// path (plan_repartition + migrate) then raises it with the reference text.
+// ---------------------------------------------------------------------------
+int tpr_switch_prepare(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                       const int64_t* L, int64_t len, tpr_switch_tables_t* t) {
+  using tpr::set_error;
+  if (!geo || !cl || !t || (len > 0 && !L)) return set_error(TPR_EINVAL, "bad tpr_switch_prepare arguments");
+  if (len < 2) return set_error(TPR_EINVAL, "layouts blob too short");
+  const int32_t H = geo->total_heads;
+  const int32_t n_slots = cl->n_gpus;
+  if (n_slots < 1 || n_slots > TPR_MAX_GPUS || H < 1) return set_error(TPR_EINVAL, "bad geometry");
+  thread_local std::vector<int64_t> cnt, req, ctx, gids, members[2];
+  thread_local std::vector<int32_t> goff, tp;
+  const int64_t n_old = L[0], n_new = L[1];
+  if (n_old < 0 || n_new < 0 || n_old + n_new > INT32_MAX) return set_error(TPR_EINVAL, "bad layout counts");
+  cnt.clear(), req.clear(), ctx.clear(), gids.clear(), goff.clear(), tp.clear();
+  members[0].clear(), members[1].clear();
+  int64_t pos = 2, n_old_req = 0;
+  for (int64_t j = 0; j < n_old + n_new; ++j) {
+    if (pos + 2 > len) return set_error(TPR_EINVAL, "layouts blob truncated");
+    const int64_t h = L[pos++], k = L[pos++];
+    if (h != H) return set_error(TPR_ENOTFOUND, "layout head count differs from the pools");
+    if (k < 1 || pos + k + 1 > len) return set_error(TPR_EINVAL, "layouts blob truncated");
+    goff.push_back((int32_t)gids.size());
+    tp.push_back((int32_t)k);
+    for (int64_t r = 0; r < k; ++r) {
+      gids.push_back(L[pos]);
+      members[j < n_old ? 0 : 1].push_back(L[pos]);
+      ++pos;
+    }
+    const int64_t c = L[pos++];
+    if (c < 0 || pos + 2 * c > len) return set_error(TPR_EINVAL, "layouts blob truncated");
+    cnt.push_back(c);
+    for (int64_t i = 0; i < c; ++i) {
+      req.push_back(L[pos++]);
+      ctx.push_back(L[pos++]);
+    }
+    if (j < n_old) n_old_req += c;
+  }
+  if (pos != len) return set_error(TPR_EINVAL, "layouts blob has trailing data");
+  for (auto& m : members) {  // "GPU sets differ" (migration.py:150-155)
+    std::sort(m.begin(), m.end());
+    m.erase(std::unique(m.begin(), m.end()), m.end());
+  }
+  if (members[0] != members[1]) return set_error(TPR_ENOTFOUND, "GPU sets differ");
+  const int64_t n_new_req = (int64_t)req.size() - n_old_req;
+  const int64_t need = std::max<int64_t>(n_new_req, 1) * H;
+  if (!t->plan || !t->records || t->plan_cap < need) {
+    t->n_plan = need;
+    return set_error(TPR_ECAPACITY, "plan capacity %lld < %lld", (long long)t->plan_cap,
+                     (long long)need);
+  }
+  int64_t n = 0;
+  int rc = tpr_plan_repartition(
+      (int32_t)n_old, cnt.data(), goff.data(), tp.data(), req.data(), ctx.data(), (int32_t)n_new,
+      cnt.data() + n_old, goff.data() + n_old, tp.data() + n_old, req.data() + n_old_req,
+      ctx.data() + n_old_req, gids.data(), H, t->kvb, t->plan_cap, t->plan, &n);
+  if (rc == TPR_ECAPACITY) {
+    t->n_plan = need;
+    return rc;
+  }
+  if (rc != TPR_OK) return set_error(TPR_ENOTFOUND, "plan needs the general path");
+  t->n_plan = n;
+  rc = tpr_kv_records(t->plan, n, t->gpu_lut, t->gpu_lut_len, t->gpu_ids, n_slots, t->req_lut,
+                      t->req_lut_len, t->slot_ctx, t->owner, geo->n_req_slots, H,
+                      geo->block_tokens, t->kvb, t->validate, t->records, t->in_units,
+                      t->out_units, &t->total_units);
+  if (rc != TPR_OK) return set_error(TPR_ENOTFOUND, "records need the general path");
+  for (int s = 0; s < n_slots; ++s)  // capacity (kvcache._check_capacity)
+    if (t->in_units[s] > cl->ring_tail[s] - cl->ring_head[s])
+      return set_error(TPR_ENOTFOUND, "slot %d out of KV units", s);
+  return TPR_OK;
+}
+
+int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                          const int64_t* L, int64_t len, tpr_switch_tables_t* t, void* stream) {
+  int rc = tpr_switch_prepare(geo, cl, L, len, t);
+  if (rc != TPR_OK) return rc;
+  const int64_t n = t->n_plan, units = t->total_units;
+  if (n == 0) return TPR_OK;
+  if (n > t->xfers_cap || units > t->work_cap || !t->d_xfers || !t->d_meta || !t->d_totals ||
+      !t->d_status || (units > 0 && !t->d_work))
+    return tpr::set_error(TPR_ECAPACITY, "device scratch too small: %lld transfers, %lld units",
+                          (long long)n, (long long)units);
+  rc = tpr_kv_switch(geo, cl, t->records, t->d_xfers, (int32_t)n, -1, t->d_meta, t->d_totals,
+                     units, t->d_work, t->d_status, stream);
+  if (rc != TPR_OK) return rc;
+  return tpr_kv_apply_owner(t->records, n, t->owner, geo->total_heads);
+}
+
 int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads) {
   if (n < 0 || (n > 0 && (!records || !owner)) || total_heads < 1)
     return tpr::set_error(TPR_EINVAL, "bad tpr_kv_apply_owner arguments");

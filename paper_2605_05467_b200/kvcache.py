@@ -36,7 +36,8 @@ import torch
 
 from . import _native
 from .geometry import KvGeometry
-from .migration import BYTES, DST, HI, LO, REQ, SRC, KvLayout, MigrationError, MigrationPlan
+from .migration import (BYTES, DST, HI, LO, REQ, SRC, KvLayout, MigrationError, MigrationPlan,
+                        pack_layouts, plan_repartition)
 
 _LUT_MAX = 1 << 24  # ids below this use dense lookup tables, others a dict
 
@@ -544,6 +545,88 @@ class PagedKvCluster:
             in_units={self.gpu_ids[s]: int(v) for s, v in enumerate(in_u) if v},
             out_units={self.gpu_ids[s]: int(v) for s, v in enumerate(out_u) if v},
         )
+
+    def _switch_tables(self, validate: bool) -> _native.SwitchTablesC:
+        """The cached tpr_switch_tables_t of this cluster (lookup tables, host
+        outputs, device scratch); pointers refreshed when a table grows."""
+        t = self.__dict__.get("_swt")
+        if t is None or self.__dict__.get("_swt_lut") is not self._req_lut:
+            t = self._swt = _native.SwitchTablesC()
+            self._swt_lut = self._req_lut
+            t.gpu_lut = self._gpu_lut.ctypes.data
+            t.gpu_lut_len = len(self._gpu_lut)
+            t.gpu_ids = self._gpu_ids_arr.ctypes.data
+            t.req_lut = self._req_lut.ctypes.data
+            t.req_lut_len = len(self._req_lut)
+            t.slot_ctx = self.slot_ctx.ctypes.data
+            t.owner = self.owner.ctypes.data
+            t.kvb = self.kv.kv_bytes_per_token_per_head
+            t.d_totals = self._totals.data_ptr()
+            t.d_status = self.status.data_ptr()
+            self._swt_plan = np.empty((0, 6), np.int64)
+        t.validate = int(validate)
+        return t
+
+    def switch_layouts(self, old_layouts, new_layouts, stream: torch.cuda.Stream | None = None,
+                       validate: bool = True, handshake_ms: float = 0.0):
+        """``plan_repartition(old, new)`` + ``migrate(plan)`` in one native call
+        (``tpr_kv_switch_layouts``): plan, records, capacity check, K3 + K1 and
+        the placement update. Returns (MigrationPlan, MigrationStats) equal to
+        the two-step path's. Anything the reference reports as an error, a
+        repeated old request id or an id outside the lookup tables goes through
+        the two-step path, which raises the reference's error."""
+        stream = stream or self._default_stream
+        if self._gpu_lut is None or not self._single_device:
+            return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms)
+        blob = pack_layouts(old_layouts, new_layouts)
+        t = self._switch_tables(validate)
+        lib = _native.load()
+        cl = self._cluster_c()
+        addr = blob.buffer_info()[0]
+        for _ in range(3):  # grow-and-retry when a buffer is too small
+            rows = self._swt_plan
+            h_ptr, raw = self._staging.acquire(max(len(rows), 1) * 24)
+            t.plan, t.plan_cap, t.records = rows.ctypes.data, len(rows), h_ptr
+            t.d_xfers = self._xf.get(max(len(rows), 1) * 6, stream).data_ptr()
+            t.d_meta = self._meta.get(max(len(rows), 1) * 4, stream).data_ptr()
+            t.xfers_cap = len(rows)
+            work = self._work.t
+            t.d_work, t.work_cap = work.data_ptr(), work.numel() // 4
+            rc = lib.tpr_kv_switch_layouts(ctypes.byref(self._geo), ctypes.byref(cl), addr,
+                                           len(blob), ctypes.byref(t), stream.cuda_stream)
+            if rc != _native.TPR_ECAPACITY:
+                break
+            if t.n_plan > len(rows):
+                self._swt_plan = np.empty((max(t.n_plan, 2 * len(rows)), 6), np.int64)
+            if t.total_units > t.work_cap:
+                self._work.get(t.total_units * 4, stream)
+        if rc == _native.TPR_ENOTFOUND:
+            return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms)
+        if rc != 0:
+            raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
+        n = t.n_plan
+        plan = MigrationPlan.from_array(self._swt_plan[:n].copy(), handshake_ms=handshake_ms)
+        if n == 0:
+            return plan, MigrationStats(0, 0, 0, {}, {})
+        self._staging.fence(stream)
+        in_u, out_u = t.in_units, t.out_units
+        ids = self.gpu_ids
+        in_d, out_d = {}, {}
+        for s_ in range(self.n_gpus):
+            a, b = in_u[s_], out_u[s_]
+            self.ring_head[s_] += a
+            self.ring_tail[s_] += b
+            if a:
+                in_d[ids[s_]] = a
+            if b:
+                out_d[ids[s_]] = b
+        return plan, MigrationStats(transfers=n, units=t.total_units, bytes=plan.total_bytes,
+                                    in_units=in_d, out_units=out_d)
+
+    def _switch_general(self, old_layouts, new_layouts, stream, validate, handshake_ms):
+        plan = plan_repartition(old_layouts, new_layouts, self.kv.kv_bytes_per_token_per_head,
+                                handshake_ms=handshake_ms)
+        return plan, self.migrate(plan, stream=stream, validate=validate)
 
     # ------------------------------------------------------------ inspection
     def placement(self) -> dict:

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import math
 import threading
+from array import array as _array
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -85,6 +86,21 @@ class KvLayout:
             out = (np.zeros(0, np.int64), np.zeros(0, np.int64))
         if isinstance(self.requests, tuple):
             self.__dict__["_req_arrays"] = out  # frozen: bypass __setattr__
+        return out
+
+    def packed(self) -> tuple[int, ...]:
+        """(total_heads, tp, *group, count, id0, ctx0, id1, ctx1, ...): this
+        layout as ``tpr_switch_prepare`` reads it, cached when immutable."""
+        cached = self.__dict__.get("_packed")
+        if cached is not None:
+            return cached
+        flat = [self.total_heads, self.tp, *self.group, len(self.requests)]
+        for rid, ctx in self.requests:
+            flat.append(rid)
+            flat.append(ctx)
+        out = tuple(map(int, flat))
+        if isinstance(self.requests, tuple):
+            self.__dict__["_packed"] = out
         return out
 
 
@@ -321,6 +337,19 @@ def head_transfers_array(old: KvLayout, new: KvLayout, kvb: int) -> MigrationPla
     meta[0], meta[1], meta[2], meta[3] = off[0], tp[0], off[1], tp[1]
     return MigrationPlan.from_array(_call_planner(
         req, ctx, meta, np.asarray(table.ids, dtype=np.int64), old.total_heads, kvb))
+
+
+def pack_layouts(old_layouts, new_layouts):
+    """Old and new layouts as one int64 array for ``tpr_switch_prepare``
+    (include/tpr.h): n_old, n_new, then every layout's ``packed()``."""
+    if isinstance(new_layouts, KvLayout):
+        new_layouts = [new_layouts]
+    flat = [len(old_layouts), len(new_layouts)]
+    for lay in old_layouts:
+        flat.extend(lay.packed())
+    for lay in new_layouts:
+        flat.extend(lay.packed())
+    return _array("q", flat)
 
 
 def plan_repartition(old_layouts: list[KvLayout], new_layouts, kv_bytes_per_token_per_head: int,

@@ -141,6 +141,55 @@ def test_large_plan_takes_split_k3_and_matches_oracle():
     assert _native.kv_switch_launches(stats.units) == 3
 
 
+def test_one_call_switch_matches_two_step_path():
+    # PagedKvCluster.switch_layouts (tpr_kv_switch_layouts) vs plan_repartition
+    # + migrate on twin clusters: same plan, same pools / tables / rings
+    gpus = tuple(range(8))
+    rng = np.random.default_rng(5)
+    reqs = [(int(r), int(c)) for r, c in zip(rng.permutation(700)[:30], rng.integers(1, 260, 30))]
+    lay = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2, 4, 8)}
+    a = make(TINY, gpus, units=2048, reqs=32, blocks=20, seed=9)
+    b = make(TINY, gpus, units=2048, reqs=32, blocks=20, seed=9)
+    a.admit(lay[4], seed=3)
+    b.admit(lay[4], seed=3)
+    for x, y in ((4, 1), (1, 8), (8, 2), (2, 4)):
+        before = a.snapshot()
+        plan_a, st_a = a.switch_layouts(lay[x], lay[y])
+        plan_b = M.plan_repartition(lay[x], lay[y], TINY.kv_bytes_per_token_per_head)
+        st_b = b.migrate(plan_b)
+        assert np.array_equal(plan_a.as_array(), plan_b.as_array())
+        assert (st_a.units, st_a.bytes, st_a.in_units, st_a.out_units) == \
+            (st_b.units, st_b.bytes, st_b.in_units, st_b.out_units)
+        sa, sb = a.snapshot(), b.snapshot()
+        for k in ("pool", "block_table", "ring"):
+            assert all(np.array_equal(u, v) for u, v in zip(sa[k], sb[k])), k
+        assert (sa["ring_head"], sa["ring_tail"]) == (sb["ring_head"], sb["ring_tail"])
+        rec = b.records(plan_b, validate=False)
+        want = check.expected_after(a, before, rec)
+        assert not any(check.compare(sa, want).values())
+        assert np.array_equal(a.owner, b.owner)
+    assert int(a.status.item()) == 0
+
+
+def test_one_call_switch_raises_reference_errors():
+    gpus = (0, 1, 2, 3)
+    reqs = [(1, 50), (2, 70)]
+    c = make(TINY, gpus, units=64, reqs=4, blocks=8)
+    tp2 = workloads.round_robin(workloads.tp_groups(gpus, 2), reqs, 8)
+    c.admit(tp2, seed=1)
+    snap = c.snapshot()
+    with pytest.raises(M.MigrationError, match="GPU sets differ"):
+        c.switch_layouts(tp2, [M.KvLayout((0, 1), 2, 8, tuple(reqs))])
+    with pytest.raises(M.MigrationError, match="context length changed"):
+        c.switch_layouts(tp2, [M.KvLayout(gpus, 4, 8, ((1, 50), (2, 71)))])
+    onto0 = [M.KvLayout((0,), 1, 8, tuple(reqs))] + [M.KvLayout((g,), 1, 8, ()) for g in gpus[1:]]
+    with pytest.raises(M.MigrationError, match="KV units needed"):
+        c.switch_layouts(tp2, onto0)  # GPU0 needs 56 units, 48 are free
+    after = c.snapshot()
+    for k in ("pool", "block_table", "ring"):  # failed switches changed nothing
+        assert all(np.array_equal(u, v) for u, v in zip(snap[k], after[k])), k
+
+
 def test_engine_path_disjoint_groups():
     # prefill->decode handoff style: head_transfers between disjoint groups
     gpus = (0, 1, 2, 3, 4, 5)
