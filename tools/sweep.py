@@ -99,27 +99,35 @@ def main():
             cluster.admit(la, seed=n)
             fwd = M.plan_repartition(la, lb, kv.kv_bytes_per_token_per_head)
             back = M.plan_repartition(lb, la, kv.kv_bytes_per_token_per_head)
-            for p in (fwd, back):  # warm-up, leaves the cluster in layout A
-                cluster.migrate(p, validate=False)
+            for x, y in ((la, lb), (lb, la)):  # warm-up, leaves the cluster in layout A
+                cluster.switch_layouts(x, y, stream=stream, validate=False)
             torch.cuda.synchronize()
             dev_ms, host_ms, exec_ms, plan_ms = [], [], [], []
             for r in range(args.reps):
-                p = fwd if r % 2 == 0 else back
-                e0, ep, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                a_b = (la, lb) if r % 2 == 0 else (lb, la)
+                t0 = time.perf_counter()  # the planner alone (host), for the split
+                M.plan_repartition(*a_b, kv.kv_bytes_per_token_per_head)
+                plan_ms.append((time.perf_counter() - t0) * 1e3)
+                # the switch as the executor runs it: one native call (plan,
+                # records, K3, K1); e0 -> e1 includes the host's planning
+                # time, during which the GPU idles
+                e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
                 t0 = time.perf_counter()
                 e0.record(stream)
-                plan = M.plan_repartition(*((la, lb) if r % 2 == 0 else (lb, la)),
-                                          kv.kv_bytes_per_token_per_head)
-                plan_ms.append((time.perf_counter() - t0) * 1e3)
-                ep.record(stream)
-                cluster.migrate(plan, validate=False)
+                cluster.switch_layouts(*a_b, stream=stream, validate=False)
                 e1.record(stream)
                 e1.synchronize()
                 host_ms.append((time.perf_counter() - t0) * 1e3)
                 dev_ms.append(e0.elapsed_time(e1))
-                exec_ms.append(ep.elapsed_time(e1))
-            if args.reps % 2:
-                cluster.migrate(back, validate=False)
+            for r in range(args.reps, 2 * args.reps):  # device work alone: stream held
+                a_b = (la, lb) if r % 2 == 0 else (lb, la)  # while the host enqueues
+                e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                torch.cuda._sleep(400_000)
+                e0.record(stream)
+                cluster.switch_layouts(*a_b, stream=stream, validate=False)
+                e1.record(stream)
+                e1.synchronize()
+                exec_ms.append(e0.elapsed_time(e1))
             k1_ms = []
             for r in range(2 * args.k1_reps):  # fwd/back pairs: ends in layout A
                 k0, k1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
@@ -141,7 +149,7 @@ def main():
                 "device_ms": d, "host_ms": float(np.median(host_ms)),
                 "gbs": nbytes / (d * 1e-3) / 1e9 if d > 0 else None,
                 "hbm_frac": (2 * nbytes / (peak * 1e9)) / (d * 1e-3) if d > 0 else None,
-                # without the host planning the GPU idles through
+                # the planner alone on the host; the switch's device work alone
                 "plan_host_ms": float(np.median(plan_ms)), "exec_device_ms": x,
                 "exec_hbm_frac": (2 * nbytes / (peak * 1e9)) / (x * 1e-3) if x > 0 else None,
                 "k1_ms": float(np.median(k1_ms)) if k1_ms else None,
