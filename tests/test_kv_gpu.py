@@ -161,7 +161,7 @@ def test_one_call_switch_matches_two_step_path():
         assert (st_a.units, st_a.bytes, st_a.in_units, st_a.out_units) == \
             (st_b.units, st_b.bytes, st_b.in_units, st_b.out_units)
         sa, sb = a.snapshot(), b.snapshot()
-        for k in ("pool", "block_table", "ring"):
+        for k in ("pools", "block_tables", "rings"):
             assert all(np.array_equal(u, v) for u, v in zip(sa[k], sb[k])), k
         assert (sa["ring_head"], sa["ring_tail"]) == (sb["ring_head"], sb["ring_tail"])
         rec = b.records(plan_b, validate=False)
@@ -186,8 +186,9 @@ def test_one_call_switch_raises_reference_errors():
     with pytest.raises(M.MigrationError, match="KV units needed"):
         c.switch_layouts(tp2, onto0)  # GPU0 needs 56 units, 48 are free
     after = c.snapshot()
-    for k in ("pool", "block_table", "ring"):  # failed switches changed nothing
+    for k in ("pools", "block_tables", "rings"):  # failed switches changed nothing
         assert all(np.array_equal(u, v) for u, v in zip(snap[k], after[k])), k
+    assert (snap["ring_head"], snap["ring_tail"]) == (after["ring_head"], after["ring_tail"])
 
 
 def test_engine_path_disjoint_groups():
