@@ -108,7 +108,9 @@ int tpr_get_copy_engine(void);
  * environment variables in brackets):
  *   "k3_fuse_units" [TPR_K3_FUSE_UNITS, 4096]: plans up to this many units
  *                   run K3 as one fused CTA (scan + remap), 0 = never;
- *   "pdl"           [TPR_PDL, 1]: programmatic dependent launch of K3b / K1;
+ *   "pdl"           [TPR_PDL, 1]: programmatic dependent launch of K3b / K1:
+ *                   0 never, 1 plans up to k3_fuse_units (a large K1 whose
+ *                   CTAs start early leaves a tail), 2 every plan;
  *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place.
  * tpr_get_tuning returns the current value, -1 for an unknown key. */
 int tpr_set_tuning(const char* key, int64_t value);

@@ -144,6 +144,16 @@ cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_
 namespace tpr {
 bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
 
+// PDL pays for small plans only (its launch overlap is worth a few us). For a
+// large K1 it costs ~2.5% (tools/e2e_paths.py: 0.3 ms on the cfg2 switch):
+// CTAs that become resident while K3 still runs start their static share of
+// the pages late, which leaves a tail. Large plans launch K1 normally.
+// knob "pdl": 0 off, 1 plans up to k3_fuse_units (default), 2 every plan
+bool pdl_for(int64_t n_units) {
+  const int64_t v = knob(g_pdl, "TPR_PDL", 1);
+  return v >= 2 || (v == 1 && n_units <= k3_fuse_units());
+}
+
 int64_t k3_fuse_units() {
   // one 1024-thread CTA expands up to 4 units per thread faster than a second
   // launch + dependency gap (measured, profiles/README.md)
@@ -190,7 +200,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   if (!key) return fail(TPR_EINVAL, "null tuning key");
   if (value < 0) return fail(TPR_EINVAL, "tuning value must be >= 0");
   if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
-  else if (!strcmp(key, "pdl")) g_pdl.store(value != 0);
+  else if (!strcmp(key, "pdl")) g_pdl.store(value > 2 ? 2 : value);
   else if (!strcmp(key, "zero_copy")) g_zero_copy.store(value != 0);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
@@ -199,7 +209,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
 int64_t tpr_get_tuning(const char* key) {
   if (!key) return -1;
   if (!strcmp(key, "k3_fuse_units")) return tpr::k3_fuse_units();
-  if (!strcmp(key, "pdl")) return tpr::pdl_enabled() ? 1 : 0;
+  if (!strcmp(key, "pdl")) return knob(g_pdl, "TPR_PDL", 1);
   if (!strcmp(key, "zero_copy")) return knob(g_zero_copy, "TPR_ZERO_COPY", 1);
   return -1;
 }
@@ -316,7 +326,7 @@ int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, con
   if (n_units < 0) return fail(TPR_EINVAL, "n_units < 0");
   if (n_units > 0 && !d_work) return fail(TPR_EINVAL, "null work list");
   cudaError_t e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units,
-                         static_cast<cudaStream_t>(stream), tpr::pdl_enabled());
+                         static_cast<cudaStream_t>(stream), tpr::pdl_for(n_units));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_migrate launch");
 }
 
@@ -352,7 +362,7 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, cons
                      reinterpret_cast<int4*>(d_work), nullptr, d_status, st);
   if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
   e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st,
-             tpr::pdl_enabled());
+             tpr::pdl_for(n_units));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_switch K1");
 }
 

@@ -42,6 +42,7 @@ int sm_count();
 // CTA (TPR_K3_FUSE_UNITS, 0 = never).
 bool pdl_enabled();
 int64_t k3_fuse_units();
+bool pdl_for(int64_t n_units);  // pdl_enabled() for plans up to k3_fuse_units()
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute when `pdl`.
 template <typename... KArgs, typename... Args>

@@ -566,7 +566,6 @@ cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
   if (threads > kScanThreads) threads = kScanThreads;
   if (threads < 32) threads = 32;
   if (n_hint <= 0) n_hint = 1;
-  const bool pdl = pdl_enabled();
   if (n_hint <= k3_fuse_units()) {
     // small plan: one CTA scans and expands (one launch instead of two)
     int ft = threads;
@@ -582,7 +581,7 @@ cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
   int64_t blocks = (n_hint + 255) / 256;
   const int64_t max_blocks = (int64_t)sm_count() * 8;
   if (blocks > max_blocks) blocks = max_blocks;
-  return launch_ex(tpr_k3_remap, dim3((unsigned)blocks), dim3(256), 0, st, pdl,
+  return launch_ex(tpr_k3_remap, dim3((unsigned)blocks), dim3(256), 0, st, pdl_for(n_hint),
                    (const int32_t*)xf, n, (const int64_t*)meta, (const int64_t*)totals, geo, cl,
                    work, work_ext, status);
 }

@@ -93,8 +93,8 @@ def test_chain_of_switches_and_back():
 
 LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
     "split_plain_h2d": dict(k3_fuse_units=0, pdl=0, zero_copy=0),
-    "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=1, zero_copy=1),
-    "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=1, zero_copy=1),
+    "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=2, zero_copy=1),
+    "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=2, zero_copy=1),
     "fused_plain_h2d": dict(k3_fuse_units=1 << 30, pdl=0, zero_copy=0),
 }
 
