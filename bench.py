@@ -181,7 +181,7 @@ def capacity_units(w, kv) -> dict:
     return {g: n + 64 for g, n in peak.items()}
 
 
-def setup_ours(w, device, overlap=None, weights_mode="sharded"):
+def setup_ours(w, device, overlap=None, weights_mode="sharded", fragmented=True):
     import torch
     from paper_2605_05467_b200.controller import ReconfigurationExecutor
     from paper_2605_05467_b200.kvcache import PagedKvCluster
@@ -191,7 +191,7 @@ def setup_ours(w, device, overlap=None, weights_mode="sharded"):
     max_ctx = max(c for _, c in w.requests)
     cluster = PagedKvCluster(kv, w.gpus, units_per_gpu=capacity_units(w, kv),
                              max_requests=len(w.requests), max_blocks=kv.blocks(max_ctx),
-                             device=device, fragmented=True, seed=0)
+                             device=device, fragmented=fragmented, seed=0)
     cluster.admit(w.old, seed=1234)
     store = None
     if w.old_weight_groups is not None:
@@ -576,6 +576,9 @@ def main():
                     help="K1/K2 copy engine (default: the library default)")
     ap.add_argument("--overlap", choices=("auto", "on", "off"), default="auto",
                     help="K1 || K2 on two streams (auto: only across devices)")
+    ap.add_argument("--pool-layout", choices=("fragmented", "contiguous"), default="fragmented",
+                    help="free-ring order of the KV pools: a random permutation (PAPER.md:342) "
+                         "or ascending")
     ap.add_argument("--weights-mode", choices=("sharded", "full_copy_per_gpu"), default="sharded",
                     help="weight storage (weight_memory modes): sharded moves missing slices, "
                          "full_copy_per_gpu (the paper's design) switches by views only")
@@ -621,7 +624,7 @@ def main():
             dist.barrier()
 
     ex = setup_ours(w, device, overlap={"auto": None, "on": True, "off": False}[args.overlap],
-                    weights_mode=args.weights_mode)
+                    weights_mode=args.weights_mode, fragmented=args.pool_layout == "fragmented")
     fwd = True
     for _ in range(max(args.warmup, 1)):
         one_switch(ex, w, fwd, sync=True)
@@ -729,7 +732,7 @@ def main():
             "seqs": len(w.requests), "ctx": w.requests[0][1],
             "switch": "alternating forward/reverse, full stop-and-migrate (plan+K3+K1+K2)",
             "k1_k2_overlap": ex.overlap, "copy_engine": _engine_name(),
-            "weights_mode": args.weights_mode,
+            "weights_mode": args.weights_mode, "pool_layout": args.pool_layout,
             "kv_bytes_per_step": kv_per_step, "weight_bytes_per_step": w_bytes / args.steps,
             "weights_note": weights_note(w, w_bytes),
             "l2": "inputs larger than L2 (>= 24 GiB moved per step)",
