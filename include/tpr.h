@@ -111,7 +111,10 @@ int tpr_get_copy_engine(void);
  *   "pdl"           [TPR_PDL, 1]: programmatic dependent launch of K3b / K1:
  *                   0 never, 1 plans up to k3_fuse_units (a large K1 whose
  *                   CTAs start early leaves a tail), 2 every plan;
- *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place.
+ *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place;
+ *   "tensor_partial" [TPR_TENSOR_PARTIAL, 1]: K1 (TMA engine) moves partial
+ *                   pages as TMA tensor boxes (token x planes) instead of
+ *                   one short copy per plane.
  * tpr_get_tuning returns the current value, -1 for an unknown key. */
 int tpr_set_tuning(const char* key, int64_t value);
 int64_t tpr_get_tuning(const char* key);

@@ -8,6 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <string>
 
 #include "tpr.h"
@@ -89,10 +92,12 @@ int cluster_params(const tpr_kv_cluster_t* cl, const tpr_kv_geometry_t* geo,
 // selectable (tpr_set_copy_engine) for comparison.
 std::atomic<int> g_engine{TPR_ENGINE_BULK};
 
-cudaError_t run_k1(const tpr::KvCopyParams& p, const tpr::KvClusterParams& cl, const int4* work,
-                   int64_t n, cudaStream_t st, bool pdl) {
-  return g_engine.load() == TPR_ENGINE_BULK ? tpr::launch_k1_bulk(p, cl, work, n, st, pdl)
-                                            : tpr::launch_k1(p, cl, work, n, st, pdl);
+cudaError_t run_k1(const tpr_kv_geometry_t* geo, int n_gpus, const tpr::KvCopyParams& p,
+                   const tpr::KvClusterParams& cl, const int4* work, int64_t n, cudaStream_t st,
+                   bool pdl) {
+  return g_engine.load() == TPR_ENGINE_BULK
+             ? tpr::launch_k1_bulk(p, cl, work, n, st, pdl, geo, n_gpus)
+             : tpr::launch_k1(p, cl, work, n, st, pdl);
 }
 
 // Records in caller memory the device can read directly: pinned (page-locked)
@@ -102,7 +107,7 @@ int64_t env_i64(const char* name, int64_t dflt);
 
 // Launch-path knobs (process-wide): initialised from the environment, changed
 // at run time with tpr_set_tuning (tests cover every combination).
-std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1};
+std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1}, g_tensor{-1};
 
 int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
   int64_t v = k.load(std::memory_order_relaxed);
@@ -148,6 +153,70 @@ bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
 // large K1 it costs ~2.5% (tools/e2e_paths.py: 0.3 ms on the cfg2 switch):
 // CTAs that become resident while K3 still runs start their static share of
 // the pages late, which leaves a tail. Large plans launch K1 normally.
+bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) != 0; }
+
+// ---------------------------------------------------------------------------
+// TMA tensor maps of the KV pools (K1 partial pages, tpr_internal.h).
+// ---------------------------------------------------------------------------
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<EncodeTiled>(f);
+  }();
+  return fn;
+}
+
+struct MapKey {
+  uint64_t pool;
+  int64_t units;
+  int32_t tok_bytes, block_tokens, rows, r_box;
+  bool operator==(const MapKey& o) const {
+    return pool == o.pool && units == o.units && tok_bytes == o.tok_bytes &&
+           block_tokens == o.block_tokens && rows == o.rows && r_box == o.r_box;
+  }
+};
+
+// one encoded map per pool, reused across switches (encoding costs ~us)
+bool pool_map(const MapKey& k, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::vector<std::pair<MapKey, CUtensorMap>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cache)
+    if (e.first == k) {
+      *out = e.second;
+      return true;
+    }
+  EncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(k.tok_bytes / 8), (cuuint64_t)k.block_tokens,
+                              (cuuint64_t)k.units * (cuuint64_t)k.rows};
+  const cuuint64_t strides[2] = {(cuuint64_t)k.tok_bytes,
+                                 (cuuint64_t)k.tok_bytes * (cuuint64_t)k.block_tokens};
+  const cuuint32_t box[3] = {(cuuint32_t)(k.tok_bytes / 8), 1u, (cuuint32_t)k.r_box};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUtensorMap m;
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, reinterpret_cast<void*>(k.pool), dims, strides,
+          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (cache.size() >= 256) cache.erase(cache.begin());
+  cache.emplace_back(k, m);
+  *out = m;
+  return true;
+}
+
 // knob "pdl": 0 off, 1 plans up to k3_fuse_units (default), 2 every plan
 bool pdl_for(int64_t n_units) {
   const int64_t v = knob(g_pdl, "TPR_PDL", 1);
@@ -181,6 +250,33 @@ int sm_count() {
   }
   return cache[dev];
 }
+
+void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
+                    uint32_t piece_bytes, KvTensorMaps* out) {
+  out->enabled = 0;
+  const int32_t tok = geo.head_dim * geo.dtype_bytes;
+  const int32_t rows = 2 * geo.layers;
+  if (!tensor_partial_enabled() || tok % 16 || tok / 8 > 256 || geo.block_tokens > 256 ||
+      n_gpus < 1 || n_gpus > TPR_MAX_GPUS)
+    return;
+  // planes per tensor copy: the largest divisor of rows with <= 256 planes
+  // whose box fits one ring stage
+  int32_t r_box = 0;
+  for (int32_t r = rows < 256 ? rows : 256; r >= 1; --r)
+    if (rows % r == 0 && (int64_t)r * tok <= (int64_t)piece_bytes) {
+      r_box = r;
+      break;
+    }
+  if (r_box == 0 || (int64_t)r_box * tok % 128) return;
+  for (int g = 0; g < n_gpus; ++g) {
+    if (cl.pool[g] % 16) return;
+    MapKey k{cl.pool[g], cl.units[g], tok, geo.block_tokens, rows, r_box};
+    if (!pool_map(k, &out->map[g])) return;
+  }
+  out->r_box = r_box;
+  out->n_pb = rows / r_box;
+  out->enabled = 1;
+}
 }  // namespace tpr
 
 extern "C" {
@@ -202,6 +298,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
   else if (!strcmp(key, "pdl")) g_pdl.store(value > 2 ? 2 : value);
   else if (!strcmp(key, "zero_copy")) g_zero_copy.store(value != 0);
+  else if (!strcmp(key, "tensor_partial")) g_tensor.store(value != 0);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
 }
@@ -211,6 +308,7 @@ int64_t tpr_get_tuning(const char* key) {
   if (!strcmp(key, "k3_fuse_units")) return tpr::k3_fuse_units();
   if (!strcmp(key, "pdl")) return knob(g_pdl, "TPR_PDL", 1);
   if (!strcmp(key, "zero_copy")) return knob(g_zero_copy, "TPR_ZERO_COPY", 1);
+  if (!strcmp(key, "tensor_partial")) return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1);
   return -1;
 }
 
@@ -325,7 +423,7 @@ int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, con
   if ((rc = cluster_params(cl, geo, &cp))) return rc;
   if (n_units < 0) return fail(TPR_EINVAL, "n_units < 0");
   if (n_units > 0 && !d_work) return fail(TPR_EINVAL, "null work list");
-  cudaError_t e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units,
+  cudaError_t e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units,
                          static_cast<cudaStream_t>(stream), tpr::pdl_for(n_units));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_migrate launch");
 }
@@ -361,7 +459,7 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, cons
   e = tpr::launch_k3(*geo, cp, xin, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
                      reinterpret_cast<int4*>(d_work), nullptr, d_status, st);
   if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
-  e = run_k1(copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st,
+  e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st,
              tpr::pdl_for(n_units));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_switch K1");
 }

@@ -20,7 +20,7 @@
 
 namespace tpr {
 
-constexpr int kMaxStages = 16;  // shared-memory ring: stages x piece bytes (runtime)
+constexpr int kMaxStages = 8;  // shared-memory ring: stages x piece bytes (runtime)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -68,26 +68,62 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// TMA tensor copies (3-D, no swizzle) through a CUtensorMap kernel parameter.
+__device__ __forceinline__ void tensor_load(uint32_t dst_smem, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(dst_smem),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tensor_store(const CUtensorMap* map, int32_t c0, int32_t c1,
+                                             int32_t c2, uint32_t src_smem) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(src_smem)
+      : "memory");
+}
+
+// One copy the pipeline moves through a stage: a linear byte range (map < 0)
+// or a TMA tensor box of the source / destination pool maps.
+struct Copy {
+  const char* src;
+  char* dst;
+  uint32_t nb;
+  int32_t smap, dmap;  // tensor map index (GPU slot) or -1 for a linear copy
+  int32_t c1, sc2, dc2;  // tensor coordinates: token, first plane (src / dst)
+};
+
 // ---- piece sources ---------------------------------------------------------
 
-// K1: the CTA's work items (grid-stride) -> pieces. A full page item is one
-// contiguous span cut into `piece`-byte pieces; a partial page item is one piece
-// per plane row (ntok valid tokens).
+// K1: the CTA's work items (grid-stride) -> copies. A full page item is one
+// contiguous span cut into `piece`-byte copies. A partial page item is either
+// one copy per plane row (ntok valid tokens each) or, with the pools' tensor
+// maps, one TMA box per (token, r_box planes): item g of the unit takes tokens
+// g, g + items_per_unit, ... (no strided short copies at all).
 struct KvPieces {
   const int4* work;
   int64_t n_items;
   KvCopyParams p;
-  const KvClusterParams* cl;  // the kernel's __grid_constant__ parameter
+  const KvClusterParams* cl;    // the kernel's __grid_constant__ parameter
+  const KvTensorMaps* tm;       // likewise (tm->enabled = 0: row copies)
   uint32_t piece;
   int64_t item;
-  // current item
+  // current item: linear rows ...
   const char* s;
   char* d;
   int64_t rows_left, row_bytes, pitch, off;
+  // ... or tensor boxes
+  int32_t t_src, t_dst, t_tok, t_ntok, t_step, t_pb, t_sc2, t_dc2;
+  bool tensor;
 
   __device__ void start(int64_t first) {
     item = first;
     rows_left = 0;
+    tensor = false;
   }
   __device__ bool load_item() {
     while (item < n_items) {
@@ -96,13 +132,26 @@ struct KvPieces {
       item += gridDim.x;
       const int4 w = work[u];
       const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
+      const int64_t nb = (int64_t)ntok * p.tok_bytes;
+      if (nb != p.pitch && tm->enabled) {  // partial page: tensor boxes
+        if (g >= ntok) continue;            // no token for this item slot
+        tensor = true;
+        t_src = src_slot;
+        t_dst = dst_slot;
+        t_tok = g;
+        t_ntok = ntok;
+        t_step = p.items_per_unit;
+        t_pb = 0;
+        t_sc2 = w.x * p.rows;
+        t_dc2 = w.y * p.rows;
+        return true;
+      }
       const int row0 = g * p.rows_per_item;
       const int nr = min(p.rows_per_item, p.rows - row0);
       s = reinterpret_cast<const char*>(cl->pool[src_slot]) + (int64_t)w.x * p.unit_bytes +
           (int64_t)row0 * p.pitch;
       d = reinterpret_cast<char*>(cl->pool[dst_slot]) + (int64_t)w.y * p.unit_bytes +
           (int64_t)row0 * p.pitch;
-      const int64_t nb = (int64_t)ntok * p.tok_bytes;
       if (nb == p.pitch) {  // contiguous planes
         rows_left = 1;
         row_bytes = nb * nr;
@@ -116,12 +165,33 @@ struct KvPieces {
     }
     return false;
   }
-  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes) {
-    if (rows_left == 0 && !load_item()) return false;
+  // The next copy: 1 = produced (a linear copy of at most avail_linear bytes,
+  // or one tensor box when it fits avail_box), 2 = the next copy is a box
+  // that does not fit this stage (nothing consumed), 0 = no work left.
+  __device__ int next(Copy& c, uint32_t avail_linear, uint32_t avail_box) {
+    if (!tensor && rows_left == 0 && !load_item()) return 0;
+    if (tensor) {
+      const uint32_t bb = (uint32_t)(tm->r_box * p.tok_bytes);
+      if (bb > avail_box) return 2;
+      c.smap = t_src;
+      c.dmap = t_dst;
+      c.c1 = t_tok;
+      c.sc2 = t_sc2 + t_pb * tm->r_box;
+      c.dc2 = t_dc2 + t_pb * tm->r_box;
+      c.nb = bb;
+      if (++t_pb == tm->n_pb) {
+        t_pb = 0;
+        t_tok += t_step;
+        if (t_tok >= t_ntok) tensor = false;
+      }
+      return 1;
+    }
+    const uint32_t max_bytes = avail_linear;
     const int64_t take = min((int64_t)max_bytes, row_bytes - off);
-    src = s + off;
-    dst = d + off;
-    nb = (uint32_t)take;
+    c.src = s + off;
+    c.dst = d + off;
+    c.nb = (uint32_t)take;
+    c.smap = c.dmap = -1;
     off += take;
     if (off == row_bytes) {
       off = 0;
@@ -129,7 +199,7 @@ struct KvPieces {
       d += pitch;
       --rows_left;
     }
-    return true;
+    return 1;
   }
 };
 
@@ -250,12 +320,13 @@ struct SegPieces {
     }
     return false;
   }
-  __device__ bool next(const char*& src, char*& dst, uint32_t& nb, uint32_t max_bytes) {
-    if (rows_left == 0 && !load_item()) return false;
+  __device__ int next(Copy& c, uint32_t max_bytes, uint32_t /*avail_box*/) {
+    if (rows_left == 0 && !load_item()) return 0;
     const int64_t take = min((int64_t)max_bytes, row_bytes - off);
-    src = s + off;
-    dst = d + off;
-    nb = (uint32_t)take;
+    c.src = s + off;
+    c.dst = d + off;
+    c.nb = (uint32_t)take;
+    c.smap = c.dmap = -1;
     off += take;
     if (off == row_bytes) {
       off = 0;
@@ -263,7 +334,7 @@ struct SegPieces {
       d += dp;
       --rows_left;
     }
-    return true;
+    return 1;
   }
 };
 
@@ -271,18 +342,23 @@ constexpr int kMaxSub = 16;  // copies packed into one shared-memory stage
 
 // One elected thread runs the pipeline. A stage is `piece` bytes of shared
 // memory filled with up to kMaxSub consecutive copies (one 32 KiB page chunk,
-// or many short rows of partial pages / row-parallel weight slices). The
-// stage's loads all complete on one mbarrier; its stores form one bulk group,
-// so small copies still keep a full stage of bytes in flight.
+// many short rows of partial pages / row-parallel weight slices, or TMA
+// tensor boxes of partial pages, 128-byte aligned). The stage's loads all
+// complete on one mbarrier; its stores form one bulk group, so small copies
+// still keep a full stage of bytes in flight. `tm`: the pools' tensor maps
+// (K1), nullptr for K2.
 template <class Source>
-__device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
+__device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
+                                              const KvTensorMaps* tm) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[kMaxStages];
   __shared__ char* pdst[kMaxStages][kMaxSub];
   __shared__ uint32_t pnb[kMaxStages][kMaxSub];
   __shared__ uint32_t poff[kMaxStages][kMaxSub];
+  __shared__ int32_t pdmap[kMaxStages][kMaxSub];  // -1: linear store
+  __shared__ int32_t pc1[kMaxStages][kMaxSub];
+  __shared__ int32_t pdc2[kMaxStages][kMaxSub];
   __shared__ int pcnt[kMaxStages];
-  __shared__ const char* psrc[kMaxSub];  // sources of the stage being filled
   if (threadIdx.x != 0) return;
   const uint32_t piece = src_it.piece;
   const int lookahead = stages - 2;  // => the refilled stage's last store may still be pending
@@ -291,53 +367,70 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
   const uint32_t base = smem_u32(smem);
   int64_t issued = 0, stored = 0;
   bool more = true;
+  Copy cs[kMaxSub];  // the stage being filled (sources)
   auto issue = [&]() {
     const int t = (int)(issued % stages);
-    const char* s;
-    char* d;
-    uint32_t nb;
-    if (!src_it.next(s, d, nb, piece)) {
+    if (src_it.next(cs[0], piece, piece) != 1) {
       more = false;
       return;
     }
     if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
-    if (nb == piece) {  // fast path: one copy fills the stage (full-page chunks)
+    const uint32_t sbase = base + (uint32_t)t * piece;
+    if (cs[0].smap < 0 && cs[0].nb == piece) {  // fast path: one copy fills the stage
       pcnt[t] = 1;
-      pdst[t][0] = d;
-      pnb[t][0] = nb;
+      pdst[t][0] = cs[0].dst;
+      pnb[t][0] = piece;
       poff[t][0] = 0;
-      bulk_load(base + (uint32_t)t * piece, s, nb, &bar[t]);
+      pdmap[t][0] = -1;
+      bulk_load(sbase, cs[0].src, piece, &bar[t]);
       ++issued;
       return;
     }
-    psrc[0] = s;
-    pdst[t][0] = d;
-    pnb[t][0] = nb;
-    poff[t][0] = 0;
-    uint32_t used = nb;
+    uint32_t off[kMaxSub];
+    off[0] = 0;
+    uint32_t used = cs[0].nb, tx = cs[0].nb;
     int n = 1;
-    while (n < kMaxSub && piece - used >= 1024) {  // pack further short copies
-      if (!src_it.next(s, d, nb, piece - used)) {
+    while (n < kMaxSub) {  // pack further copies
+      const uint32_t aligned = (used + 127u) & ~127u;
+      const uint32_t avail_box = aligned <= piece ? piece - aligned : 0;
+      if (piece - used < 1024 && avail_box == 0) break;
+      const int r = src_it.next(cs[n], piece - used >= 1024 ? piece - used : 0, avail_box);
+      if (r == 0) {
         more = false;
         break;
       }
-      psrc[n] = s;
-      pdst[t][n] = d;
-      pnb[t][n] = nb;
-      poff[t][n] = used;
-      used += nb;
+      if (r == 2) break;  // a tensor box that needs the next stage
+      if (cs[n].smap >= 0) {
+        off[n] = aligned;
+        used = aligned + cs[n].nb;
+      } else {
+        if (cs[n].nb == 0) break;
+        off[n] = used;
+        used += cs[n].nb;
+      }
+      tx += cs[n].nb;
       ++n;
     }
     pcnt[t] = n;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[t])),
-                 "r"(used)
+                 "r"(tx)
                  : "memory");
     for (int i = 0; i < n; ++i) {
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              base + (uint32_t)t * piece + poff[t][i]),
-          "l"(psrc[i]), "r"(pnb[t][i]), "r"(smem_u32(&bar[t]))
-          : "memory");
+      const Copy& c = cs[i];
+      pdst[t][i] = c.dst;
+      pnb[t][i] = c.nb;
+      poff[t][i] = off[i];
+      pdmap[t][i] = c.dmap;
+      pc1[t][i] = c.c1;
+      pdc2[t][i] = c.dc2;
+      if (c.smap >= 0)
+        tensor_load(sbase + off[i], &tm->map[c.smap], 0, c.c1, c.sc2, &bar[t]);
+      else
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                sbase + off[i]),
+            "l"(c.src), "r"(c.nb), "r"(smem_u32(&bar[t]))
+            : "memory");
     }
     ++issued;
   };
@@ -346,10 +439,15 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
     if (more) issue();
     const int t = (int)(stored % stages);
     bar_wait(&bar[t], (uint32_t)((stored / stages) & 1));
-    for (int i = 0; i < pcnt[t]; ++i)
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pdst[t][i]),
-                   "r"(base + (uint32_t)t * piece + poff[t][i]), "r"(pnb[t][i])
-                   : "memory");
+    const uint32_t sbase = base + (uint32_t)t * piece;
+    for (int i = 0; i < pcnt[t]; ++i) {
+      if (pdmap[t][i] >= 0)
+        tensor_store(&tm->map[pdmap[t][i]], 0, pc1[t][i], pdc2[t][i], sbase + poff[t][i]);
+      else
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pdst[t][i]),
+                     "r"(sbase + poff[t][i]), "r"(pnb[t][i])
+                     : "memory");
+    }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     ++stored;
   }
@@ -358,7 +456,8 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages) {
 
 __global__ void __launch_bounds__(32)
     tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
-                           const __grid_constant__ KvClusterParams cl, int32_t stages,
+                           const __grid_constant__ KvClusterParams cl,
+                           const __grid_constant__ KvTensorMaps tm, int32_t stages,
                            uint32_t piece) {
   if (threadIdx.x != 0) return;
   pdl_wait();  // K3's work list (launched with programmatic serialization)
@@ -367,9 +466,10 @@ __global__ void __launch_bounds__(32)
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
   it.cl = &cl;
+  it.tm = &tm;
   it.piece = piece;
   it.start(blockIdx.x);
-  bulk_pipeline(it, stages);
+  bulk_pipeline(it, stages, &tm);
 }
 
 __global__ void __launch_bounds__(32)
@@ -386,7 +486,7 @@ __global__ void __launch_bounds__(32)
   it.chunk = chunk;
   it.piece = piece;
   it.start(blockIdx.x);
-  bulk_pipeline(it, stages);
+  bulk_pipeline(it, stages, nullptr);
 }
 
 // Ring shape per kernel (shared memory = stages x piece per CTA). Measured on
@@ -458,13 +558,17 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items) {
 }
 
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
-                           int64_t n_units, cudaStream_t st, bool pdl) {
+                           int64_t n_units, cudaStream_t st, bool pdl,
+                           const tpr_kv_geometry_t* geo, int n_gpus) {
   if (n_units <= 0) return cudaSuccess;
   const BulkConfig& c = k1_config();
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
                              n_units * p.items_per_unit);
+  KvTensorMaps tm;
+  tm.enabled = 0;
+  if (geo) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
   return launch_ex(tpr_k1_kv_migrate_bulk, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl,
-                   work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece);
+                   work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece);
 }
 
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,

@@ -1,6 +1,7 @@
 // Internal interfaces between the C-ABI layer (tpr_api.cpp) and the kernels.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (encoded through cudaGetDriverEntryPoint, no -lcuda)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -34,6 +35,26 @@ struct KvCopyParams {
   int32_t rows_per_item;  // planes per K1 work item
   int32_t items_per_unit;
 };
+
+// TMA tensor maps of the KV pools, one per GPU slot, for the partial pages of
+// K1 (bulk engine). A pool is viewed as a 3-D tensor of 8-byte elements
+//   d0 = tok_bytes / 8 (one token of one plane), d1 = block_tokens, d2 = planes
+// (units x rows), and one box is {one token} x {r_box planes}: the valid
+// tokens of a partial page move as ntok x (rows / r_box) tensor copies of
+// r_box x tok_bytes bytes instead of `rows` short row copies.
+struct KvTensorMaps {
+  CUtensorMap map[TPR_MAX_GPUS];  // 64-byte aligned (CUtensorMap is)
+  int32_t enabled;                // 0: partial pages use row copies
+  int32_t r_box;                  // planes per tensor copy (divides rows)
+  int32_t n_pb;                   // rows / r_box
+  int32_t _pad;
+};
+
+// Tensor maps for the pools of `cl` (cached per pool); out->enabled = 0 when
+// the geometry does not fit TMA's limits or the driver entry point is missing.
+void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
+                    uint32_t piece_bytes, KvTensorMaps* out);
+bool tensor_partial_enabled();
 
 int sm_count();
 
@@ -74,7 +95,8 @@ cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t
                       int64_t n_items, int64_t chunk, cudaStream_t st);
 // TMA bulk-copy engine variants (tpr_bulk.cu)
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
-                           int64_t n_units, cudaStream_t st, bool pdl);
+                           int64_t n_units, cudaStream_t st, bool pdl,
+                           const tpr_kv_geometry_t* geo, int n_gpus);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

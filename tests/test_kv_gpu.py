@@ -92,10 +92,10 @@ def test_chain_of_switches_and_back():
 
 
 LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
-    "split_plain_h2d": dict(k3_fuse_units=0, pdl=0, zero_copy=0),
-    "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=2, zero_copy=1),
-    "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=2, zero_copy=1),
-    "fused_plain_h2d": dict(k3_fuse_units=1 << 30, pdl=0, zero_copy=0),
+    "split_plain_h2d_rows": dict(k3_fuse_units=0, pdl=0, zero_copy=0, tensor_partial=0),
+    "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=2, zero_copy=1, tensor_partial=1),
+    "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=2, zero_copy=1, tensor_partial=1),
+    "fused_plain_h2d_rows": dict(k3_fuse_units=1 << 30, pdl=0, zero_copy=0, tensor_partial=0),
 }
 
 

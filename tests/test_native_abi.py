@@ -37,6 +37,8 @@ def test_tuning_knobs_roundtrip():
         assert lib.tpr_set_tuning(b"nope", 1) == -1 and b"unknown tuning key" in lib.tpr_last_error()
         assert lib.tpr_set_tuning(b"pdl", -1) == -1
         assert lib.tpr_get_tuning(b"nope") == -1
+        _native.set_tuning("tensor_partial", 0)
+        assert _native.get_tuning("tensor_partial") == 0
     finally:
         for k, v in saved.items():
             _native.set_tuning(k, v)
