@@ -342,12 +342,17 @@ constexpr int kMaxSub = 16;  // copies packed into one shared-memory stage
 
 // One elected thread runs the pipeline. A stage is `piece` bytes of shared
 // memory filled with up to kMaxSub consecutive copies (one 32 KiB page chunk,
-// many short rows of partial pages / row-parallel weight slices, or TMA
-// tensor boxes of partial pages, 128-byte aligned). The stage's loads all
-// complete on one mbarrier; its stores form one bulk group, so small copies
-// still keep a full stage of bytes in flight. `tm`: the pools' tensor maps
-// (K1), nullptr for K2.
-template <class Source>
+// many short rows of partial pages / row-parallel weight slices, or -- K1 with
+// kTensor -- TMA tensor boxes of partial pages, 128-byte aligned). The
+// stage's loads all complete on one mbarrier; its stores form one bulk group,
+// so small copies still keep a full stage of bytes in flight.
+//
+// The issuing thread is the throughput limit for short copies, so the per-copy
+// path stays in registers: each load is issued as soon as its copy is produced
+// and the stage's single arrive.expect_tx follows the loads (the mbarrier
+// tx-count may go transiently negative; the phase cannot complete before the
+// arrival). K2 instantiates kTensor = false: no tensor bookkeeping at all.
+template <bool kTensor, class Source>
 __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
                                               const KvTensorMaps* tm) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -355,9 +360,9 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
   __shared__ char* pdst[kMaxStages][kMaxSub];
   __shared__ uint32_t pnb[kMaxStages][kMaxSub];
   __shared__ uint32_t poff[kMaxStages][kMaxSub];
-  __shared__ int32_t pdmap[kMaxStages][kMaxSub];  // -1: linear store
-  __shared__ int32_t pc1[kMaxStages][kMaxSub];
-  __shared__ int32_t pdc2[kMaxStages][kMaxSub];
+  __shared__ int32_t pdmap[kTensor ? kMaxStages : 1][kMaxSub];  // -1: linear store
+  __shared__ int32_t pc1[kTensor ? kMaxStages : 1][kMaxSub];
+  __shared__ int32_t pdc2[kTensor ? kMaxStages : 1][kMaxSub];
   __shared__ int pcnt[kMaxStages];
   if (threadIdx.x != 0) return;
   const uint32_t piece = src_it.piece;
@@ -367,71 +372,56 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
   const uint32_t base = smem_u32(smem);
   int64_t issued = 0, stored = 0;
   bool more = true;
-  Copy cs[kMaxSub];  // the stage being filled (sources)
   auto issue = [&]() {
     const int t = (int)(issued % stages);
-    if (src_it.next(cs[0], piece, piece) != 1) {
+    Copy c;
+    if (src_it.next(c, piece, piece) != 1) {
       more = false;
       return;
     }
     if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
     const uint32_t sbase = base + (uint32_t)t * piece;
-    if (cs[0].smap < 0 && cs[0].nb == piece) {  // fast path: one copy fills the stage
-      pcnt[t] = 1;
-      pdst[t][0] = cs[0].dst;
-      pnb[t][0] = piece;
-      poff[t][0] = 0;
-      pdmap[t][0] = -1;
-      bulk_load(sbase, cs[0].src, piece, &bar[t]);
-      ++issued;
-      return;
-    }
-    uint32_t off[kMaxSub];
-    off[0] = 0;
-    uint32_t used = cs[0].nb, tx = cs[0].nb;
-    int n = 1;
-    while (n < kMaxSub) {  // pack further copies
+    uint32_t used = 0, tx = 0;
+    int n = 0;
+    while (true) {
+      uint32_t off = used;
+      if (kTensor && c.smap >= 0) {
+        off = (used + 127u) & ~127u;
+        tensor_load(sbase + off, &tm->map[c.smap], 0, c.c1, c.sc2, &bar[t]);
+        pdmap[t][n] = c.dmap;
+        pc1[t][n] = c.c1;
+        pdc2[t][n] = c.dc2;
+      } else {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                sbase + off),
+            "l"(c.src), "r"(c.nb), "r"(smem_u32(&bar[t]))
+            : "memory");
+        if (kTensor) pdmap[t][n] = -1;
+      }
+      pdst[t][n] = c.dst;
+      pnb[t][n] = c.nb;
+      poff[t][n] = off;
+      used = off + c.nb;
+      tx += c.nb;
+      ++n;
+      // pack a further copy: a linear one needs >= 1 KiB left, a box its size
+      if (n == kMaxSub) break;
       const uint32_t aligned = (used + 127u) & ~127u;
-      const uint32_t avail_box = aligned <= piece ? piece - aligned : 0;
-      if (piece - used < 1024 && avail_box == 0) break;
-      const int r = src_it.next(cs[n], piece - used >= 1024 ? piece - used : 0, avail_box);
+      const uint32_t avail_box = (kTensor && aligned <= piece) ? piece - aligned : 0;
+      const uint32_t avail_lin = piece - used >= 1024 ? piece - used : 0;
+      if (avail_lin == 0 && avail_box == 0) break;
+      const int r = src_it.next(c, avail_lin, avail_box);
       if (r == 0) {
         more = false;
         break;
       }
-      if (r == 2) break;  // a tensor box that needs the next stage
-      if (cs[n].smap >= 0) {
-        off[n] = aligned;
-        used = aligned + cs[n].nb;
-      } else {
-        if (cs[n].nb == 0) break;
-        off[n] = used;
-        used += cs[n].nb;
-      }
-      tx += cs[n].nb;
-      ++n;
+      if (r == 2 || c.nb == 0) break;  // the next copy needs a fresh stage
     }
     pcnt[t] = n;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[t])),
                  "r"(tx)
                  : "memory");
-    for (int i = 0; i < n; ++i) {
-      const Copy& c = cs[i];
-      pdst[t][i] = c.dst;
-      pnb[t][i] = c.nb;
-      poff[t][i] = off[i];
-      pdmap[t][i] = c.dmap;
-      pc1[t][i] = c.c1;
-      pdc2[t][i] = c.dc2;
-      if (c.smap >= 0)
-        tensor_load(sbase + off[i], &tm->map[c.smap], 0, c.c1, c.sc2, &bar[t]);
-      else
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                sbase + off[i]),
-            "l"(c.src), "r"(c.nb), "r"(smem_u32(&bar[t]))
-            : "memory");
-    }
     ++issued;
   };
   while (more && issued < lookahead) issue();
@@ -441,7 +431,7 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
     bar_wait(&bar[t], (uint32_t)((stored / stages) & 1));
     const uint32_t sbase = base + (uint32_t)t * piece;
     for (int i = 0; i < pcnt[t]; ++i) {
-      if (pdmap[t][i] >= 0)
+      if (kTensor && pdmap[t][i] >= 0)
         tensor_store(&tm->map[pdmap[t][i]], 0, pc1[t][i], pdc2[t][i], sbase + poff[t][i]);
       else
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pdst[t][i]),
@@ -469,7 +459,7 @@ __global__ void __launch_bounds__(32)
   it.tm = &tm;
   it.piece = piece;
   it.start(blockIdx.x);
-  bulk_pipeline(it, stages, &tm);
+  bulk_pipeline<true>(it, stages, &tm);
 }
 
 __global__ void __launch_bounds__(32)
@@ -486,7 +476,7 @@ __global__ void __launch_bounds__(32)
   it.chunk = chunk;
   it.piece = piece;
   it.start(blockIdx.x);
-  bulk_pipeline(it, stages, nullptr);
+  bulk_pipeline<false>(it, stages, nullptr);
 }
 
 // Ring shape per kernel (shared memory = stages x piece per CTA). Measured on
