@@ -381,6 +381,16 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
     }
     if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
     const uint32_t sbase = base + (uint32_t)t * piece;
+    if (c.smap < 0 && c.nb == piece) {  // fast path: one copy fills the stage (full pages)
+      pcnt[t] = 1;
+      pdst[t][0] = c.dst;
+      pnb[t][0] = piece;
+      poff[t][0] = 0;
+      if (kTensor) pdmap[t][0] = -1;
+      bulk_load(sbase, c.src, piece, &bar[t]);
+      ++issued;
+      return;
+    }
     uint32_t used = 0, tx = 0;
     int n = 0;
     while (true) {
