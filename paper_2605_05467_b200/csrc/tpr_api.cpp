@@ -92,12 +92,20 @@ int cluster_params(const tpr_kv_cluster_t* cl, const tpr_kv_geometry_t* geo,
 // selectable (tpr_set_copy_engine) for comparison.
 std::atomic<int> g_engine{TPR_ENGINE_BULK};
 
+// partial: the plan may contain partial pages (context not a multiple of the
+// page size); only then does K1 need the pools' tensor maps
 cudaError_t run_k1(const tpr_kv_geometry_t* geo, int n_gpus, const tpr::KvCopyParams& p,
                    const tpr::KvClusterParams& cl, const int4* work, int64_t n, cudaStream_t st,
-                   bool pdl) {
+                   bool pdl, bool partial = true) {
   return g_engine.load() == TPR_ENGINE_BULK
-             ? tpr::launch_k1_bulk(p, cl, work, n, st, pdl, geo, n_gpus)
+             ? tpr::launch_k1_bulk(p, cl, work, n, st, pdl, geo, n_gpus, partial)
              : tpr::launch_k1(p, cl, work, n, st, pdl);
+}
+
+bool any_partial(const int32_t* rec, int32_t n, int32_t block_tokens) {
+  for (int32_t t = 0; t < n; ++t)
+    if (rec[t * TPR_XFER_FIELDS + 5] % block_tokens) return true;
+  return false;
 }
 
 // Records in caller memory the device can read directly: pinned (page-locked)
@@ -460,7 +468,8 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, cons
                      reinterpret_cast<int4*>(d_work), nullptr, d_status, st);
   if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
   e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st,
-             tpr::pdl_for(n_units));
+             tpr::pdl_for(n_units),
+             h_xfers ? any_partial(h_xfers, n_xfers, geo->block_tokens) : true);
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_switch K1");
 }
 

@@ -104,6 +104,7 @@ struct Copy {
 // one copy per plane row (ntok valid tokens each) or, with the pools' tensor
 // maps, one TMA box per (token, r_box planes): item g of the unit takes tokens
 // g, g + items_per_unit, ... (no strided short copies at all).
+template <bool kTensor>
 struct KvPieces {
   const int4* work;
   int64_t n_items;
@@ -133,7 +134,7 @@ struct KvPieces {
       const int4 w = work[u];
       const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
       const int64_t nb = (int64_t)ntok * p.tok_bytes;
-      if (nb != p.pitch && tm->enabled) {  // partial page: tensor boxes
+      if (kTensor && nb != p.pitch) {  // partial page: tensor boxes
         if (g >= ntok) continue;            // no token for this item slot
         tensor = true;
         t_src = src_slot;
@@ -169,8 +170,8 @@ struct KvPieces {
   // or one tensor box when it fits avail_box), 2 = the next copy is a box
   // that does not fit this stage (nothing consumed), 0 = no work left.
   __device__ int next(Copy& c, uint32_t avail_linear, uint32_t avail_box) {
-    if (!tensor && rows_left == 0 && !load_item()) return 0;
-    if (tensor) {
+    if (!(kTensor && tensor) && rows_left == 0 && !load_item()) return 0;
+    if (kTensor && tensor) {
       const uint32_t bb = (uint32_t)(tm->r_box * p.tok_bytes);
       if (bb > avail_box) return 2;
       c.smap = t_src;
@@ -454,14 +455,33 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
   bulk_wait_all();
 }
 
+// K1 with partial pages as row copies (every page full: no tensor maps needed)
 __global__ void __launch_bounds__(32)
     tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
-                           const __grid_constant__ KvClusterParams cl,
-                           const __grid_constant__ KvTensorMaps tm, int32_t stages,
+                           const __grid_constant__ KvClusterParams cl, int32_t stages,
                            uint32_t piece) {
   if (threadIdx.x != 0) return;
   pdl_wait();  // K3's work list (launched with programmatic serialization)
-  KvPieces it;
+  KvPieces<false> it;
+  it.work = work;
+  it.n_items = n_units * p.items_per_unit;
+  it.p = p;
+  it.cl = &cl;
+  it.tm = nullptr;
+  it.piece = piece;
+  it.start(blockIdx.x);
+  bulk_pipeline<false>(it, stages, nullptr);
+}
+
+// K1 with partial pages as TMA tensor boxes of the pools' tensor maps
+__global__ void __launch_bounds__(32)
+    tpr_k1_kv_migrate_tma(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
+                          const __grid_constant__ KvClusterParams cl,
+                          const __grid_constant__ KvTensorMaps tm, int32_t stages,
+                          uint32_t piece) {
+  if (threadIdx.x != 0) return;
+  pdl_wait();
+  KvPieces<true> it;
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
@@ -559,16 +579,22 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items) {
 
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            int64_t n_units, cudaStream_t st, bool pdl,
-                           const tpr_kv_geometry_t* geo, int n_gpus) {
+                           const tpr_kv_geometry_t* geo, int n_gpus, bool partial) {
   if (n_units <= 0) return cudaSuccess;
   const BulkConfig& c = k1_config();
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
-                             n_units * p.items_per_unit);
   KvTensorMaps tm;
   tm.enabled = 0;
-  if (geo) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
+  if (geo && partial) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
+  if (tm.enabled) {
+    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma), c,
+                               n_units * p.items_per_unit);
+    return launch_ex(tpr_k1_kv_migrate_tma, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl,
+                     work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece);
+  }
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
+                             n_units * p.items_per_unit);
   return launch_ex(tpr_k1_kv_migrate_bulk, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl,
-                   work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece);
+                   work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece);
 }
 
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,

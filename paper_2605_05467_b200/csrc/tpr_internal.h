@@ -96,7 +96,7 @@ cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t
 // TMA bulk-copy engine variants (tpr_bulk.cu)
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            int64_t n_units, cudaStream_t st, bool pdl,
-                           const tpr_kv_geometry_t* geo, int n_gpus);
+                           const tpr_kv_geometry_t* geo, int n_gpus, bool partial);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
