@@ -114,7 +114,8 @@ int tpr_get_copy_engine(void);
  *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place;
  *   "tensor_partial" [TPR_TENSOR_PARTIAL, 1]: K1 (TMA engine) moves partial
  *                   pages as TMA tensor boxes (token x planes) instead of
- *                   one short copy per plane.
+ *                   one short copy per plane: 0 never, 1 when a page of the
+ *                   plan is partial, 2 the tensor kernel for every plan.
  * tpr_get_tuning returns the current value, -1 for an unknown key. */
 int tpr_set_tuning(const char* key, int64_t value);
 int64_t tpr_get_tuning(const char* key);
@@ -170,6 +171,12 @@ int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
 /* Copies the valid tokens of every work unit from pool[src] to pool[dst]. */
 int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* d_work, int64_t n_units, void* stream);
+/* tpr_kv_migrate with flags: TPR_MIGRATE_FULL_PAGES = the caller knows every
+ * page of the plan is full (all context lengths are multiples of the page
+ * size), so K1 needs no tensor maps for partial pages (the lean kernel). */
+#define TPR_MIGRATE_FULL_PAGES 1
+int tpr_kv_migrate_ex(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                      const int32_t* d_work, int64_t n_units, int32_t flags, void* stream);
 
 /* ---- switch bookkeeping (host) ----------------------------------------- */
 /* Plan rows -> K3 records, per-GPU-slot unit deltas and the plan checks of

@@ -27,7 +27,7 @@ TPR_ENOTFOUND = -4  # an id outside the caller's lookup tables (use the Python m
 EXPORTS = (
     "tpr_set_copy_engine", "tpr_get_copy_engine", "tpr_set_tuning", "tpr_get_tuning",
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads", "tpr_plan_repartition",
-    "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
+    "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_migrate_ex", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
     "tpr_switch_prepare", "tpr_kv_switch_layouts",
     "tpr_memcpy_h2d", "tpr_memcpy_d2h",
     "tpr_copy_prepare", "tpr_weight_reshard",
@@ -89,6 +89,7 @@ class SwitchTablesC(Structure):
 
 
 TPR_ECAPACITY = -3
+TPR_MIGRATE_FULL_PAGES = 1
 
 _P64 = POINTER(c_int64)
 _P32 = POINTER(c_int32)
@@ -111,6 +112,8 @@ _SIGNATURES = {
                                c_void_p, c_void_p]),
     "tpr_kv_migrate": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int64,
                                  c_void_p]),
+    "tpr_kv_migrate_ex": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_int64,
+                                    c_int32, c_void_p]),
     "tpr_kv_records": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int32, c_void_p,
                                  c_int64, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64,
                                  c_int32, c_void_p, c_void_p, c_void_p, _P64]),

@@ -161,7 +161,10 @@ bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
 // large K1 it costs ~2.5% (tools/e2e_paths.py: 0.3 ms on the cfg2 switch):
 // CTAs that become resident while K3 still runs start their static share of
 // the pages late, which leaves a tail. Large plans launch K1 normally.
+// knob "tensor_partial": 0 row copies, 1 tensor boxes when a page is partial
+// (default), 2 the tensor kernel for every plan (A/B measurements)
 bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) != 0; }
+bool tensor_kernel_always() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) >= 2; }
 
 // ---------------------------------------------------------------------------
 // TMA tensor maps of the KV pools (K1 partial pages, tpr_internal.h).
@@ -306,7 +309,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
   else if (!strcmp(key, "pdl")) g_pdl.store(value > 2 ? 2 : value);
   else if (!strcmp(key, "zero_copy")) g_zero_copy.store(value != 0);
-  else if (!strcmp(key, "tensor_partial")) g_tensor.store(value != 0);
+  else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
 }
@@ -423,17 +426,23 @@ int tpr_kv_remap(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_remap launch");
 }
 
-int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const int32_t* d_work,
-                   int64_t n_units, void* stream) {
+int tpr_kv_migrate_ex(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                      const int32_t* d_work, int64_t n_units, int32_t flags, void* stream) {
   int rc = check_geometry(geo);
   if (rc) return rc;
   tpr::KvClusterParams cp;
   if ((rc = cluster_params(cl, geo, &cp))) return rc;
   if (n_units < 0) return fail(TPR_EINVAL, "n_units < 0");
   if (n_units > 0 && !d_work) return fail(TPR_EINVAL, "null work list");
-  cudaError_t e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units,
-                         static_cast<cudaStream_t>(stream), tpr::pdl_for(n_units));
+  cudaError_t e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
+                         n_units, static_cast<cudaStream_t>(stream), tpr::pdl_for(n_units),
+                         !(flags & TPR_MIGRATE_FULL_PAGES));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_migrate launch");
+}
+
+int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const int32_t* d_work,
+                   int64_t n_units, void* stream) {
+  return tpr_kv_migrate_ex(geo, cl, d_work, n_units, 0, stream);
 }
 
 int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, const int32_t* h_xfers,

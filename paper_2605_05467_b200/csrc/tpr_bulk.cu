@@ -584,7 +584,7 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
   const BulkConfig& c = k1_config();
   KvTensorMaps tm;
   tm.enabled = 0;
-  if (geo && partial) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
+  if (geo && (partial || tensor_kernel_always())) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
   if (tm.enabled) {
     const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma), c,
                                n_units * p.items_per_unit);

@@ -55,6 +55,7 @@ struct KvTensorMaps {
 void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
                     uint32_t piece_bytes, KvTensorMaps* out);
 bool tensor_partial_enabled();
+bool tensor_kernel_always();
 
 int sm_count();
 

@@ -299,9 +299,11 @@ class DistributedKvCluster:
             cl = self._run_k3(rec, self.slot, n, want_ext=False)
             if k1_events:
                 k1_events[0].record(self.stream)
+            full = not (rec[:, 5] % self.kv.block_tokens).any()
             with torch.cuda.device(self.device):
-                _native.call("tpr_kv_migrate", ctypes.byref(self._geo), ctypes.byref(cl),
-                             self._work.data_ptr(), n, self.stream.cuda_stream)
+                _native.call("tpr_kv_migrate_ex", ctypes.byref(self._geo), ctypes.byref(cl),
+                             self._work.data_ptr(), n, _native.TPR_MIGRATE_FULL_PAGES if full else 0,
+                             self.stream.cuda_stream)
             if k1_events:
                 k1_events[1].record(self.stream)
         return rec, in_u, out_u, n

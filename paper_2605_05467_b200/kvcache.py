@@ -528,8 +528,10 @@ class PagedKvCluster:
                              total, d_work.data_ptr(), None, self.status.data_ptr(),
                              stream.cuda_stream)
             k1_events[0].record(stream)
-            _native.call("tpr_kv_migrate", ctypes.byref(self._geo), ctypes.byref(cl),
-                         d_work.data_ptr(), total, stream.cuda_stream)
+            full = not (xf32[:, 5] % self.kv.block_tokens).any()
+            _native.call("tpr_kv_migrate_ex", ctypes.byref(self._geo), ctypes.byref(cl),
+                         d_work.data_ptr(), total,
+                         _native.TPR_MIGRATE_FULL_PAGES if full else 0, stream.cuda_stream)
             k1_events[1].record(stream)
         else:
             _native.call("tpr_kv_switch", ctypes.byref(self._geo), ctypes.byref(cl), h_ptr,
