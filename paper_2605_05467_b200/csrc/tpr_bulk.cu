@@ -455,13 +455,137 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
   bulk_wait_all();
 }
 
+// Warp-specialised variant (64 threads): lane 0 of warp 0 produces (packs
+// copies, issues the loads), lane 0 of warp 1 consumes (issues the stores).
+// full[t] completes when stage t's loads have landed (tx bytes); empty[t] when
+// its stores have finished reading shared memory. The two issue streams no
+// longer serialise in one thread.
+__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <bool kTensor, class Source>
+__device__ __forceinline__ void bulk_pipeline_ws(Source& src_it, int stages,
+                                                 const KvTensorMaps* tm) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t empty[kMaxStages];
+  __shared__ char* pdst[kMaxStages][kMaxSub];
+  __shared__ uint32_t pnb[kMaxStages][kMaxSub];
+  __shared__ uint32_t poff[kMaxStages][kMaxSub];
+  __shared__ int32_t pdmap[kTensor ? kMaxStages : 1][kMaxSub];
+  __shared__ int32_t pc1[kTensor ? kMaxStages : 1][kMaxSub];
+  __shared__ int32_t pdc2[kTensor ? kMaxStages : 1][kMaxSub];
+  __shared__ int pcnt[kMaxStages];
+  const uint32_t piece = src_it.piece;
+  const uint32_t base = smem_u32(smem);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      bar_init(&full[s]);
+      bar_init(&empty[s]);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // ---------------------------------------- producer
+    pdl_wait();
+    src_it.start(blockIdx.x);
+    bool more = true;
+    for (int64_t k = 0;; ++k) {
+      const int t = (int)(k % stages);
+      if (k >= stages) bar_wait(&empty[t], (uint32_t)(((k / stages) - 1) & 1));
+      Copy c;
+      if (!more || src_it.next(c, piece, piece) != 1) {
+        pcnt[t] = -1;  // end of work
+        bar_arrive(&full[t]);
+        break;
+      }
+      const uint32_t sbase = base + (uint32_t)t * piece;
+      if (c.smap < 0 && c.nb == piece) {  // one copy fills the stage (full pages)
+        pcnt[t] = 1;
+        pdst[t][0] = c.dst;
+        pnb[t][0] = piece;
+        poff[t][0] = 0;
+        if (kTensor) pdmap[t][0] = -1;
+        bulk_load(sbase, c.src, piece, &full[t]);
+        continue;
+      }
+      uint32_t used = 0, tx = 0;
+      int n = 0;
+      while (true) {
+        uint32_t off = used;
+        if (kTensor && c.smap >= 0) {
+          off = (used + 127u) & ~127u;
+          tensor_load(sbase + off, &tm->map[c.smap], 0, c.c1, c.sc2, &full[t]);
+          pdmap[t][n] = c.dmap;
+          pc1[t][n] = c.c1;
+          pdc2[t][n] = c.dc2;
+        } else {
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  sbase + off),
+              "l"(c.src), "r"(c.nb), "r"(smem_u32(&full[t]))
+              : "memory");
+          if (kTensor) pdmap[t][n] = -1;
+        }
+        pdst[t][n] = c.dst;
+        pnb[t][n] = c.nb;
+        poff[t][n] = off;
+        used = off + c.nb;
+        tx += c.nb;
+        ++n;
+        if (n == kMaxSub) break;
+        const uint32_t aligned = (used + 127u) & ~127u;
+        const uint32_t avail_box = (kTensor && aligned <= piece) ? piece - aligned : 0;
+        const uint32_t avail_lin = piece - used >= 1024 ? piece - used : 0;
+        if (avail_lin == 0 && avail_box == 0) break;
+        const int r = src_it.next(c, avail_lin, avail_box);
+        if (r == 0) {
+          more = false;
+          break;
+        }
+        if (r == 2 || c.nb == 0) break;
+      }
+      pcnt[t] = n;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_u32(&full[t])),
+                   "r"(tx)
+                   : "memory");
+    }
+  } else if (threadIdx.x == 32) {  // ------------------------------- consumer
+    int64_t k = 0;
+    for (;; ++k) {
+      const int t = (int)(k % stages);
+      bar_wait(&full[t], (uint32_t)((k / stages) & 1));
+      const int n = pcnt[t];
+      if (n < 0) break;
+      const uint32_t sbase = base + (uint32_t)t * piece;
+      for (int i = 0; i < n; ++i) {
+        if (kTensor && pdmap[t][i] >= 0)
+          tensor_store(&tm->map[pdmap[t][i]], 0, pc1[t][i], pdc2[t][i], sbase + poff[t][i]);
+        else
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                           pdst[t][i]),
+                       "r"(sbase + poff[t][i]), "r"(pnb[t][i])
+                       : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (k >= 1) {  // stage k-1's stores have read shared memory: hand it back
+        bulk_wait_read_1();
+        bar_arrive(&empty[(k - 1) % stages]);
+      }
+    }
+    bulk_wait_all();  // every store has landed before the CTA exits
+  }
+}
+
 // K1 with partial pages as row copies (every page full: no tensor maps needed)
-__global__ void __launch_bounds__(32)
+template <bool kWS>
+__global__ void __launch_bounds__(64)
     tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
                            const __grid_constant__ KvClusterParams cl, int32_t stages,
                            uint32_t piece) {
-  if (threadIdx.x != 0) return;
-  pdl_wait();  // K3's work list (launched with programmatic serialization)
   KvPieces<false> it;
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
@@ -469,18 +593,23 @@ __global__ void __launch_bounds__(32)
   it.cl = &cl;
   it.tm = nullptr;
   it.piece = piece;
+  if (kWS) {
+    bulk_pipeline_ws<false>(it, stages, nullptr);
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  pdl_wait();  // K3's work list (launched with programmatic serialization)
   it.start(blockIdx.x);
   bulk_pipeline<false>(it, stages, nullptr);
 }
 
 // K1 with partial pages as TMA tensor boxes of the pools' tensor maps
-__global__ void __launch_bounds__(32)
+template <bool kWS>
+__global__ void __launch_bounds__(64)
     tpr_k1_kv_migrate_tma(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
                           const __grid_constant__ KvClusterParams cl,
                           const __grid_constant__ KvTensorMaps tm, int32_t stages,
                           uint32_t piece) {
-  if (threadIdx.x != 0) return;
-  pdl_wait();
   KvPieces<true> it;
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
@@ -488,15 +617,21 @@ __global__ void __launch_bounds__(32)
   it.cl = &cl;
   it.tm = &tm;
   it.piece = piece;
+  if (kWS) {
+    bulk_pipeline_ws<true>(it, stages, &tm);
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  pdl_wait();
   it.start(blockIdx.x);
   bulk_pipeline<true>(it, stages, &tm);
 }
 
-__global__ void __launch_bounds__(32)
+template <bool kWS>
+__global__ void __launch_bounds__(64)
     tpr_k2_copy_segments_bulk(const tpr_copy_seg_t* __restrict__ segs,
                               const int64_t* __restrict__ prefix, int32_t n_segs, int64_t n_items,
                               int64_t chunk, int64_t* claim, int32_t stages, uint32_t piece) {
-  if (threadIdx.x != 0) return;  // one issuing thread: start() claims work
   SegPieces it;
   it.segs = segs;
   it.prefix = prefix;
@@ -505,6 +640,11 @@ __global__ void __launch_bounds__(32)
   it.n_items = n_items;
   it.chunk = chunk;
   it.piece = piece;
+  if (kWS) {
+    bulk_pipeline_ws<false>(it, stages, nullptr);  // the producer's start() claims work
+    return;
+  }
+  if (threadIdx.x != 0) return;  // one issuing thread: start() claims work
   it.start(blockIdx.x);
   bulk_pipeline<false>(it, stages, nullptr);
 }
@@ -549,7 +689,7 @@ static const BulkConfig& k2_config() {
   return c;
 }
 
-static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items) {
+static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items, int threads) {
   // attribute + occupancy per (kernel, device) are fixed: set/query once (the
   // occupancy query costs microseconds of host time per small switch)
   static thread_local const void* done_fn[8] = {nullptr};
@@ -562,7 +702,7 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items) {
     if (done_fn[i] == fn && done_dev[i] == dev) per_sm = done_occ[i];
   if (per_sm == 0) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, c.smem());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, c.smem());
     if (per_sm < 1) per_sm = 1;
     for (int i = 0; i < 8; ++i)
       if (done_fn[i] == nullptr) {
@@ -577,6 +717,25 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items) {
   return grid < 1 ? 1 : (int)grid;
 }
 
+// Warp-specialised pipelines (producer + consumer warps): TPR_BULK_WS / the
+// "bulk_ws" knob (0 = one issuing thread per CTA).
+template <bool kWS>
+static cudaError_t k1_launch(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
+                             int64_t n_units, cudaStream_t st, bool pdl, const KvTensorMaps& tm,
+                             const BulkConfig& c) {
+  const int threads = kWS ? 64 : 32;
+  if (tm.enabled) {
+    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma<kWS>), c,
+                               n_units * p.items_per_unit, threads);
+    return launch_ex(tpr_k1_kv_migrate_tma<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
+                     pdl, work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece);
+  }
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk<kWS>), c,
+                             n_units * p.items_per_unit, threads);
+  return launch_ex(tpr_k1_kv_migrate_bulk<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
+                   pdl, work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece);
+}
+
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            int64_t n_units, cudaStream_t st, bool pdl,
                            const tpr_kv_geometry_t* geo, int n_gpus, bool partial) {
@@ -585,16 +744,8 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
   KvTensorMaps tm;
   tm.enabled = 0;
   if (geo && (partial || tensor_kernel_always())) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
-  if (tm.enabled) {
-    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma), c,
-                               n_units * p.items_per_unit);
-    return launch_ex(tpr_k1_kv_migrate_tma, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl,
-                     work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece);
-  }
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
-                             n_units * p.items_per_unit);
-  return launch_ex(tpr_k1_kv_migrate_bulk, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl,
-                   work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece);
+  return bulk_ws() ? k1_launch<true>(p, cl, work, n_units, st, pdl, tm, c)
+                   : k1_launch<false>(p, cl, work, n_units, st, pdl, tm, c);
 }
 
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
@@ -603,9 +754,17 @@ cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, in
   const BulkConfig& c = k2_config();
   // dynamic claims hand out kClaimBatch items per CTA and batch
   const int64_t units = claim ? (n_items + kClaimBatch - 1) / kClaimBatch : n_items;
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk), c, units);
-  tpr_k2_copy_segments_bulk<<<grid, 32, c.smem(), st>>>(segs, prefix, n_segs, n_items, chunk,
-                                                         claim, c.stages, c.piece);
+  if (bulk_ws()) {
+    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk<true>), c,
+                               units, 64);
+    tpr_k2_copy_segments_bulk<true><<<grid, 64, c.smem(), st>>>(segs, prefix, n_segs, n_items,
+                                                                chunk, claim, c.stages, c.piece);
+    return cudaGetLastError();
+  }
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk<false>), c,
+                             units, 32);
+  tpr_k2_copy_segments_bulk<false><<<grid, 32, c.smem(), st>>>(segs, prefix, n_segs, n_items,
+                                                               chunk, claim, c.stages, c.piece);
   return cudaGetLastError();
 }
 

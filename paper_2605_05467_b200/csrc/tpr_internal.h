@@ -56,6 +56,7 @@ void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int
                     uint32_t piece_bytes, KvTensorMaps* out);
 bool tensor_partial_enabled();
 bool tensor_kernel_always();
+bool bulk_ws();  // warp-specialised bulk pipelines (producer + consumer warps)
 
 int sm_count();
 

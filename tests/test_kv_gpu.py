@@ -96,6 +96,8 @@ LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
     "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=2, zero_copy=1, tensor_partial=1),
     "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=2, zero_copy=1, tensor_partial=1),
     "fused_plain_h2d_rows": dict(k3_fuse_units=1 << 30, pdl=0, zero_copy=0, tensor_partial=0),
+    "ws_tensor": dict(bulk_ws=1, tensor_partial=1),
+    "ws_rows": dict(bulk_ws=1, tensor_partial=0, pdl=2),
 }
 
 

@@ -1,8 +1,10 @@
-# same-box A/B of K1/K2 (bench cfg2): session-start code (exp_old worktree, if
-# present) vs the current lean and forced-tensor K1 kernels
+# same-box A/B of K1/K2 (bench cfg2) and the trace sweep's K1: session-start
+# code (exp_old worktree, if present), current default, warp-specialised
 set -x
 for i in 1 2; do
   [ -d exp_old ] && (cd exp_old && timeout 400 python bench.py --no-cpu --no-e2e --steps 20 > ../gpurun_out/ab_old_$i.json 2>&1)
   timeout 400 python bench.py --no-cpu --no-e2e --steps 20 > gpurun_out/ab_new_$i.json 2>&1
-  TPR_TENSOR_PARTIAL=2 timeout 400 python bench.py --no-cpu --no-e2e --steps 20 > gpurun_out/ab_tensor_$i.json 2>&1
+  TPR_BULK_WS=1 timeout 400 python bench.py --no-cpu --no-e2e --steps 20 > gpurun_out/ab_ws_$i.json 2>&1
 done
+timeout 600 python tools/sweep.py --modes trace --max-seqs 1 --reps 2 --out gpurun_out/ab_sweep_new.jsonl > /dev/null 2>&1
+TPR_BULK_WS=1 timeout 600 python tools/sweep.py --modes trace --max-seqs 1 --reps 2 --out gpurun_out/ab_sweep_ws.jsonl > /dev/null 2>&1
