@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--cpu-max-seqs", type=int, default=8)
     ap.add_argument("--modes", default="fixed4096,trace")
+    ap.add_argument("--only", default="", help="comma list of tp_old:tp_new:seqs points")
     ap.add_argument("--k1-reps", type=int, default=2,
                     help="extra switches timed with events around K1 alone (k1_ms)")
     args = ap.parse_args()
@@ -59,6 +60,7 @@ def main():
     trace = json.load(gzip.open(ROOT / "tests" / "golden" / "reference_golden.json.gz", "rt"))["bursty_trace"]
     trace_ctx = [p + o // 2 for p, o in trace]
     params = M.CostModelParams()
+    only = {tuple(int(v) for v in x.split(":")) for x in args.only.split(",") if x}
     out = open(args.out, "w")
     stream = torch.cuda.current_stream()
 
@@ -78,7 +80,7 @@ def main():
                 if a == b:
                     continue
                 for n in (1, 2, 4, 8, 16, 32, 64, 128, 256):
-                    if n > top:
+                    if n > top or (only and (a, b, n) not in only):
                         continue
                     ctxs = [4096] * n if mode == "fixed4096" else trace_ctx[:n]
                     reqs = [(i, c) for i, c in enumerate(ctxs)]
