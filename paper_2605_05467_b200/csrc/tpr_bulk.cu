@@ -382,7 +382,11 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
     }
     if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
     const uint32_t sbase = base + (uint32_t)t * piece;
-    if (c.smap < 0 && c.nb == piece) {  // fast path: one copy fills the stage (full pages)
+    // Fast path: one copy fills the stage (full pages), expect_tx before the
+    // load. Measured on one box (profiles/ab/r01_fastpath_*): +1.4% for the
+    // lean K1 on full pages, but -4..-14% for the tensor K1 on mixed plans
+    // (trace contexts), which runs at the copy peak without it.
+    if (!kTensor && c.nb == piece) {
       pcnt[t] = 1;
       pdst[t][0] = c.dst;
       pnb[t][0] = piece;
@@ -502,7 +506,7 @@ __device__ __forceinline__ void bulk_pipeline_ws(Source& src_it, int stages,
         break;
       }
       const uint32_t sbase = base + (uint32_t)t * piece;
-      if (c.smap < 0 && c.nb == piece) {  // one copy fills the stage (full pages)
+      if (!kTensor && c.nb == piece) {  // one copy fills the stage (lean kernels only)
         pcnt[t] = 1;
         pdst[t][0] = c.dst;
         pnb[t][0] = piece;
@@ -740,6 +744,7 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
                            int64_t n_units, cudaStream_t st, bool pdl,
                            const tpr_kv_geometry_t* geo, int n_gpus, bool partial) {
   if (n_units <= 0) return cudaSuccess;
+
   const BulkConfig& c = k1_config();
   KvTensorMaps tm;
   tm.enabled = 0;

@@ -97,6 +97,9 @@ def main():
             max_ctx, max_n = max(max_ctx, max(ctxs)), max(max_n, n)
         cluster = PagedKvCluster(kv, gpus, units_per_gpu=units + 256, max_requests=max_n,
                                  max_blocks=kv.blocks(max_ctx), fragmented=True, seed=0)
+        # touch every pool page once: first writes to fresh cudaMalloc memory
+        # are slower, and which points would pay for them depends on the order
+        cluster.fill_garbage(seed=1)
         for a, b, n, ctxs, reqs, la, lb in points(mode):
             cluster.admit(la, seed=n)
             fwd = M.plan_repartition(la, lb, kv.kv_bytes_per_token_per_head)
