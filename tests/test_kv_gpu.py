@@ -320,6 +320,32 @@ def test_cfg1_full_size_bit_exact():
     assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
 
 
+@pytest.mark.parametrize("model", ["8b", "70b"])
+@pytest.mark.parametrize("tensor_partial", [0, 1])
+def test_llama_geometry_ragged_bit_exact(model, tensor_partial):
+    # real page geometry (8B: 64 planes = one 16 KiB tensor box per token;
+    # 70B: 160 planes = two 20 KiB boxes per token) with partial last pages,
+    # tensor boxes vs row copies, against the C oracle
+    from paper_2605_05467_b200 import _native
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B, LLAMA_3_1_70B
+    kv = (LLAMA_3_1_8B if model == "8b" else LLAMA_3_1_70B).kv
+    saved = _native.get_tuning("tensor_partial")
+    _native.set_tuning("tensor_partial", tensor_partial)
+    try:
+        gpus = (0, 1, 2, 3)
+        reqs = [(0, 1), (1, 17), (2, 47), (3, 64), (4, 95)]  # 1 token .. 15 valid tokens
+        lay = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2, 4)}
+        c = make(kv, gpus, units=96, reqs=6, blocks=6, fragmented=True, seed=4)
+        c.admit(lay[1], seed=6)
+        for a, b in ((1, 4), (4, 2), (2, 1)):
+            plan = M.plan_repartition(lay[a], lay[b], kv.kv_bytes_per_token_per_head)
+            migrate_and_compare(c, plan)
+        v = c.verify(seed=6)
+        assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+    finally:
+        _native.set_tuning("tensor_partial", saved)
+
+
 @pytest.mark.slow
 def test_cfg4_70b_32k_full_size_property():
     # BASELINE configs[3]: Llama-3.1-70B TP4 <-> TP8, 8 x 32768 tokens, 640 KiB pages;
