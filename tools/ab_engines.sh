@@ -1,3 +1,4 @@
+# usage: git worktree add exp_old <commit> && (cd exp_old && python -m paper_2605_05467_b200.build); bash tools/ab_engines.sh
 # same-box A/B of K1/K2 (bench cfg2) and the trace sweep's K1: session-start
 # code (exp_old worktree, if present), current default, warp-specialised
 set -x
