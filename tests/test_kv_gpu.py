@@ -143,6 +143,24 @@ def test_large_plan_takes_split_k3_and_matches_oracle():
     assert _native.kv_switch_launches(stats.units) == 3
 
 
+@pytest.mark.parametrize("tp_old,tp_new", [(16, 1), (1, 16), (4, 16), (16, 2)])
+def test_sixteen_slots_bit_exact(tp_old, tp_new):
+    # TPR_MAX_GPUS = 16 slots (16 KV heads so TP16 is a valid KvLayout)
+    kv = geometry.KvGeometry(layers=1, head_dim=32, total_heads=16)
+    gpus = tuple(range(100, 116))
+    rng = np.random.default_rng(tp_old * 100 + tp_new)
+    reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 70, size=16))]
+    old = workloads.round_robin(workloads.tp_groups(gpus, tp_old), reqs, 16)
+    new = workloads.round_robin(workloads.tp_groups(gpus, tp_new), reqs, 16)
+    c = make(kv, gpus, units=256, reqs=16, blocks=8, seed=1)
+    c.admit(old, seed=2)
+    plan, stats = c.switch_layouts(old, new)
+    assert np.array_equal(plan.as_array(), M.plan_repartition(old, new, kv.kv_bytes_per_token_per_head).as_array())
+    assert c.placement() == M.layout_placement(new)
+    v = c.verify(seed=2)
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
+
+
 def test_one_call_switch_matches_two_step_path():
     # PagedKvCluster.switch_layouts (tpr_kv_switch_layouts) vs plan_repartition
     # + migrate on twin clusters: same plan, same pools / tables / rings
