@@ -201,6 +201,17 @@ def setup_ours(w, device, overlap=None, weights_mode="sharded", fragmented=True)
     return ReconfigurationExecutor(cluster, store, time_kernels=True, overlap=overlap)
 
 
+def k1_kernel_name(w) -> str:
+    """The K1 kernel this workload launches (bulk engine): the lean kernel when
+    every context is a whole number of pages, else the tensor-box kernel."""
+    from paper_2605_05467_b200 import _native
+    if _native.copy_engine() != "bulk":
+        return "tpr_k1_kv_migrate<8> (vector engine)"
+    B = w.model.kv.block_tokens
+    full = all(c % B == 0 for _, c in w.requests)
+    return "tpr_k1_kv_migrate_bulk<0>" if full else "tpr_k1_kv_migrate_tma<0>"
+
+
 def weights_note(w, w_bytes) -> str:
     if w.old_weight_groups is None:
         if w.model.name.endswith("70B"):
@@ -739,7 +750,7 @@ def main():
             "parallelism": "replicas" if world > 1 else "1 GPU, logical ranks",
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic, "kernel": "tpr_k1_kv_migrate",
+                     "frac": achieved / hbm, "traffic": traffic, "kernel": k1_kernel_name(w),
                      "k1_ms": k1_avg, "k2_ms": float(np.mean(k2_ms)) if k2_ms else None,
                      "peak_source": hbm_src,
                      # the whole switch (K3 + K1 + K2 + gaps): all bytes read + written
