@@ -221,7 +221,7 @@ typedef struct tpr_switch_tables {
   int32_t* owner;          /* [request slot][H] -> gpu slot; updated          */
   int64_t kvb;             /* kv_bytes_per_token_per_head                      */
   int32_t validate;        /* as tpr_kv_records                                */
-  int32_t _pad0;
+  int32_t mode;            /* TPR_SWITCH_REPARTITION / TPR_SWITCH_HEAD_TRANSFERS */
   int64_t* plan;           /* out: int64 [plan_cap][6], the MigrationPlan SoA  */
   int64_t plan_cap;
   int32_t* records;        /* out: int32 [plan_cap][6] K3 records (pinned)     */
@@ -237,6 +237,16 @@ typedef struct tpr_switch_tables {
   int64_t work_cap;
   int32_t* d_status;       /* device int32                                     */
 } tpr_switch_tables_t;
+
+/* tpr_switch_tables_t.mode: the planner of the switch.
+ *   TPR_SWITCH_REPARTITION     plan_repartition(old layouts, new layouts)
+ *                              (migration.py:137-189): equal GPU sets, the new
+ *                              layouts carry exactly the old requests;
+ *   TPR_SWITCH_HEAD_TRANSFERS  head_transfers(old, new) (migration.py:101-134):
+ *                              one old and one new layout, any GPU sets (the
+ *                              engine's prefill->decode handoff, engine.py:571-589). */
+#define TPR_SWITCH_REPARTITION 0
+#define TPR_SWITCH_HEAD_TRANSFERS 1
 
 /* The host half of a switch, no device work (plan_repartition,
  * migration.py:137-189, then tpr_kv_records and the capacity check).

@@ -78,7 +78,7 @@ class SwitchTablesC(Structure):
     _fields_ = [
         ("gpu_lut", c_void_p), ("gpu_lut_len", c_int64), ("gpu_ids", c_void_p),
         ("req_lut", c_void_p), ("req_lut_len", c_int64), ("slot_ctx", c_void_p),
-        ("owner", c_void_p), ("kvb", c_int64), ("validate", c_int32), ("_pad0", c_int32),
+        ("owner", c_void_p), ("kvb", c_int64), ("validate", c_int32), ("mode", c_int32),
         ("plan", c_void_p), ("plan_cap", c_int64), ("records", c_void_p),
         ("in_units", c_int64 * TPR_MAX_GPUS), ("out_units", c_int64 * TPR_MAX_GPUS),
         ("n_plan", c_int64), ("total_units", c_int64),
@@ -90,6 +90,8 @@ class SwitchTablesC(Structure):
 
 TPR_ECAPACITY = -3
 TPR_MIGRATE_FULL_PAGES = 1
+TPR_SWITCH_REPARTITION = 0
+TPR_SWITCH_HEAD_TRANSFERS = 1
 
 _P64 = POINTER(c_int64)
 _P32 = POINTER(c_int32)

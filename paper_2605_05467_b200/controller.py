@@ -21,7 +21,7 @@ import torch
 
 from . import _native
 from .kvcache import MigrationStats, PagedKvCluster
-from .migration import KvLayout, MigrationPlan, head_transfers_array, plan_repartition
+from .migration import KvLayout, MigrationPlan, plan_repartition
 from .tracing import nvtx
 from .weights import ReshardStats, ShardedWeightStore
 
@@ -144,11 +144,11 @@ class ReconfigurationExecutor:
         main = torch.cuda.current_stream(self.device)
         ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
         ev["start"].record(main)
-        plan = head_transfers_array(prefill, decode, self.kv.kv.kv_bytes_per_token_per_head)
         ks = self.kv_stream if self.overlap else main
         if ks is not main:
             ks.wait_event(ev["start"])
-        stats = self.kv.migrate(plan, stream=ks)
+        # head_transfers + records + K3 + K1 in one native call
+        plan, stats = self.kv.switch_layouts(prefill, decode, stream=ks, planner="head_transfers")
         if ks is not main:
             main.wait_stream(ks)
         res = SwitchResult(plan=plan, kv=stats, weights=None, events=ev)

@@ -234,19 +234,42 @@ int tpr_switch_prepare(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
     std::sort(m.begin(), m.end());
     m.erase(std::unique(m.begin(), m.end()), m.end());
   }
-  if (members[0] != members[1]) return set_error(TPR_ENOTFOUND, "GPU sets differ");
-  const int64_t n_new_req = (int64_t)req.size() - n_old_req;
-  const int64_t need = std::max<int64_t>(n_new_req, 1) * H;
+  const bool heads_mode = t->mode == TPR_SWITCH_HEAD_TRANSFERS;
+  if (heads_mode && (n_old != 1 || n_new != 1))
+    return set_error(TPR_EINVAL, "head_transfers mode takes one old and one new layout");
+  if (!heads_mode && members[0] != members[1])  // plan_repartition only (migration.py:150-155)
+    return set_error(TPR_ENOTFOUND, "GPU sets differ");
+  const int64_t n_plan_req = heads_mode ? n_old_req : (int64_t)req.size() - n_old_req;
+  const int64_t need = std::max<int64_t>(n_plan_req, 1) * H;
   if (!t->plan || !t->records || t->plan_cap < need) {
     t->n_plan = need;
     return set_error(TPR_ECAPACITY, "plan capacity %lld < %lld", (long long)t->plan_cap,
                      (long long)need);
   }
   int64_t n = 0;
-  int rc = tpr_plan_repartition(
-      (int32_t)n_old, cnt.data(), goff.data(), tp.data(), req.data(), ctx.data(), (int32_t)n_new,
-      cnt.data() + n_old, goff.data() + n_old, tp.data() + n_old, req.data() + n_old_req,
-      ctx.data() + n_old_req, gids.data(), H, t->kvb, t->plan_cap, t->plan, &n);
+  int rc;
+  if (heads_mode) {
+    // head_transfers(old, new) (migration.py:101-134): the old layout's
+    // requests in order, from its group to the new group (any GPU sets)
+    thread_local std::vector<int32_t> meta;
+    meta.resize(4 * (size_t)n_old_req);
+    for (int64_t i = 0; i < n_old_req; ++i) {
+      meta[i] = goff[0];
+      meta[n_old_req + i] = tp[0];
+      meta[2 * n_old_req + i] = goff[1];
+      meta[3 * n_old_req + i] = tp[1];
+    }
+    rc = n_old_req == 0 ? TPR_OK
+                        : tpr_plan_heads((int32_t)n_old_req, req.data(), ctx.data(), meta.data(),
+                                         meta.data() + n_old_req, meta.data() + 2 * n_old_req,
+                                         meta.data() + 3 * n_old_req, gids.data(), H, t->kvb,
+                                         t->plan_cap, t->plan, &n);
+  } else {
+    rc = tpr_plan_repartition(
+        (int32_t)n_old, cnt.data(), goff.data(), tp.data(), req.data(), ctx.data(), (int32_t)n_new,
+        cnt.data() + n_old, goff.data() + n_old, tp.data() + n_old, req.data() + n_old_req,
+        ctx.data() + n_old_req, gids.data(), H, t->kvb, t->plan_cap, t->plan, &n);
+  }
   if (rc == TPR_ECAPACITY) {
     t->n_plan = need;
     return rc;

@@ -37,7 +37,7 @@ import torch
 from . import _native
 from .geometry import KvGeometry
 from .migration import (BYTES, DST, HI, LO, REQ, SRC, KvLayout, MigrationError, MigrationPlan,
-                        pack_layouts, plan_repartition)
+                        head_transfers_array, pack_layouts, plan_repartition)
 
 _LUT_MAX = 1 << 24  # ids below this use dense lookup tables, others a dict
 
@@ -570,18 +570,29 @@ class PagedKvCluster:
         return t
 
     def switch_layouts(self, old_layouts, new_layouts, stream: torch.cuda.Stream | None = None,
-                       validate: bool = True, handshake_ms: float = 0.0):
+                       validate: bool = True, handshake_ms: float = 0.0,
+                       planner: str = "repartition"):
         """``plan_repartition(old, new)`` + ``migrate(plan)`` in one native call
         (``tpr_kv_switch_layouts``): plan, records, capacity check, K3 + K1 and
         the placement update. Returns (MigrationPlan, MigrationStats) equal to
         the two-step path's. Anything the reference reports as an error, a
         repeated old request id or an id outside the lookup tables goes through
-        the two-step path, which raises the reference's error."""
+        the two-step path, which raises the reference's error.
+
+        ``planner="head_transfers"``: one old and one new layout planned with
+        ``head_transfers`` (any GPU sets: the prefill->decode handoff)."""
         stream = stream or self._default_stream
+        if planner not in ("repartition", "head_transfers"):
+            raise MigrationError(f"unknown planner {planner!r}")
+        heads = planner == "head_transfers"
+        if heads:
+            old_layouts, new_layouts = [old_layouts], [new_layouts]
         if self._gpu_lut is None or not self._single_device:
-            return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms)
+            return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
+                                        heads)
         blob = pack_layouts(old_layouts, new_layouts)
         t = self._switch_tables(validate)
+        t.mode = _native.TPR_SWITCH_HEAD_TRANSFERS if heads else _native.TPR_SWITCH_REPARTITION
         lib = _native.load()
         cl = self._cluster_c()
         addr = blob.buffer_info()[0]
@@ -603,7 +614,8 @@ class PagedKvCluster:
             if t.total_units > t.work_cap:
                 self._work.get(t.total_units * 4, stream)
         if rc == _native.TPR_ENOTFOUND:
-            return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms)
+            return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
+                                        heads)
         if rc != 0:
             raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
         n = t.n_plan
@@ -625,9 +637,13 @@ class PagedKvCluster:
         return plan, MigrationStats(transfers=n, units=t.total_units, bytes=plan.total_bytes,
                                     in_units=in_d, out_units=out_d)
 
-    def _switch_general(self, old_layouts, new_layouts, stream, validate, handshake_ms):
-        plan = plan_repartition(old_layouts, new_layouts, self.kv.kv_bytes_per_token_per_head,
-                                handshake_ms=handshake_ms)
+    def _switch_general(self, old_layouts, new_layouts, stream, validate, handshake_ms,
+                        heads: bool = False):
+        kvb = self.kv.kv_bytes_per_token_per_head
+        if heads:
+            plan = head_transfers_array(old_layouts[0], new_layouts[0], kvb)
+        else:
+            plan = plan_repartition(old_layouts, new_layouts, kvb, handshake_ms=handshake_ms)
         return plan, self.migrate(plan, stream=stream, validate=validate)
 
     # ------------------------------------------------------------ inspection

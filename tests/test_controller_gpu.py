@@ -55,6 +55,32 @@ def test_prefill_decode_handoff():
     assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
 
 
+@pytest.mark.parametrize("src,dst", [((0, 1), (2, 3, 4, 5)), ((2,), (3,)), ((0, 1, 2, 3), (4, 5)),
+                                     ((4, 5), (5, 4))])
+def test_handoff_one_call_matches_two_step(src, dst):
+    # head_transfers + K3 + K1 in one native call vs head_transfers_array +
+    # migrate, on twin clusters: same plan and identical pools / tables / rings
+    import numpy as np
+    gpus = (0, 1, 2, 3, 4, 5)
+    reqs = ((1, 100), (2, 33), (3, 16))
+    pre = M.KvLayout(src, len(src), 8, reqs)
+    dec = M.KvLayout(dst, len(dst), 8, reqs)
+    a = PagedKvCluster(KV, gpus, units_per_gpu=256, max_requests=8, max_blocks=16, fragmented=True)
+    b = PagedKvCluster(KV, gpus, units_per_gpu=256, max_requests=8, max_blocks=16, fragmented=True)
+    for c in (a, b):
+        c.fill_garbage(seed=5)
+        c.admit([pre], seed=8)
+    plan_a, st_a = a.switch_layouts(pre, dec, planner="head_transfers")
+    plan_b = M.head_transfers_array(pre, dec, KV.kv_bytes_per_token_per_head)
+    st_b = b.migrate(plan_b)
+    assert np.array_equal(plan_a.as_array(), plan_b.as_array())
+    assert (st_a.units, st_a.bytes) == (st_b.units, st_b.bytes)
+    sa, sb = a.snapshot(), b.snapshot()
+    for k in ("pools", "block_tables", "rings"):
+        assert all(np.array_equal(u, v) for u, v in zip(sa[k], sb[k])), k
+    assert a.placement() == M.layout_placement(dec) == b.placement()
+
+
 def test_capacity_admission_evicts_best_effort():
     gpus = (0, 1, 2, 3)
     kv = PagedKvCluster(KV, gpus, units_per_gpu={0: 128, 1: 128, 2: 64, 3: 64}, max_requests=8,

@@ -42,8 +42,9 @@ class Tables:
         self.plan = np.zeros((max_req * KV.total_heads, 6), np.int64)
         self.rec = np.zeros((max_req * KV.total_heads, 6), np.int32)
 
-    def prepare(self, old, new, validate=True):
+    def prepare(self, old, new, validate=True, mode=0):
         t = _native.SwitchTablesC()
+        t.mode = mode
         t.gpu_lut, t.gpu_lut_len = self.gpu_lut.ctypes.data, len(self.gpu_lut)
         t.gpu_ids = self.ids.ctypes.data
         t.req_lut, t.req_lut_len = self.req_lut.ctypes.data, len(self.req_lut)
@@ -130,3 +131,29 @@ def test_packed_layout_is_cached_and_exact():
     assert lay.packed() is lay.packed()
     blob = M.pack_layouts([lay], lay)
     assert list(blob) == [1, 1, *lay.packed(), *lay.packed()]
+
+
+@pytest.mark.parametrize("src,dst", [((0, 1), (4, 5, 6, 7)), ((2,), (3,)), ((0, 1, 2, 3), (4, 5)),
+                                     ((4, 5), (5, 4))])
+def test_head_transfers_mode_matches_reference_planner(src, dst):
+    # the engine's handoff path: head_transfers between arbitrary groups
+    # (engine.py:571-589, migration.py:101-134), incl. disjoint GPU sets
+    gpus = tuple(range(8))
+    reqs = ((11, 70), (12, 16), (13, 1))
+    old = M.KvLayout(src, len(src), 8, reqs)
+    new = M.KvLayout(dst, len(dst), 8, reqs)
+    tab = Tables(gpus, [old])
+    rc, t = tab.prepare([old], [new], mode=_native.TPR_SWITCH_HEAD_TRANSFERS)
+    assert rc == 0, _native.load().tpr_last_error()
+    want = M.head_transfers_array(old, new, KVB).as_array()
+    assert t.n_plan == len(want) and np.array_equal(tab.plan[: t.n_plan], want)
+    assert np.array_equal(tab.rec[: t.n_plan], expected_records(tab, want))
+
+
+def test_head_transfers_mode_takes_one_layout_each():
+    gpus = (0, 1)
+    a = M.KvLayout((0,), 1, 8, ((1, 5),))
+    b = M.KvLayout((1,), 1, 8, ((1, 5),))
+    tab = Tables(gpus, [a])
+    rc, _ = tab.prepare([a, b], [b], mode=_native.TPR_SWITCH_HEAD_TRANSFERS)
+    assert rc == -1
