@@ -142,7 +142,8 @@ class ReconfigurationExecutor:
         exactly what runs here, through K3 + K1."""
         t0 = time.perf_counter()
         main = torch.cuda.current_stream(self.device)
-        ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
+        ev = ({"start": self._ev_sync[0], "end": self._ev_sync[1]} if sync else
+              {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")})
         ev["start"].record(main)
         ks = self.kv_stream if self.overlap else main
         if ks is not main:

@@ -43,7 +43,7 @@ CASES = (  # (name, slots, tp_old, tp_new, seqs, ctx)
 def main():
     import torch
 
-    from paper_2605_05467_b200 import _native, workloads
+    from paper_2605_05467_b200 import _native, migration as M, workloads
     from paper_2605_05467_b200.controller import ReconfigurationExecutor
     from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
     from paper_2605_05467_b200.kvcache import PagedKvCluster
@@ -100,6 +100,33 @@ def main():
                "device_us": float(np.median(dev_us)), "k1_roof_us": roof,
                "sync_hbm_frac": roof / float(np.median(sync_us)),
                "device_hbm_frac": roof / float(np.median(dev_us)), "bit_exact_property": ok}
+        print(json.dumps(row), flush=True)
+        if out:
+            out.write(json.dumps(row) + "\n")
+        del ex, cl
+        torch.cuda.empty_cache()
+    # prefill -> decode handoffs (disjoint groups, head_transfers): the most
+    # frequent small transfer of a disaggregated deployment
+    for name, src, dst, ctx in (("handoff 1 seq x 463 TP2(0,1)->TP4(2..5)", (0, 1), (2, 3, 4, 5), 463),
+                                ("handoff 1 seq x 4096 TP1(0)->TP1(1)", (0,), (1,), 4096)):
+        gpus = tuple(range(6))
+        pre = M.KvLayout(src, len(src), kv.total_heads, ((0, ctx),))
+        dec = M.KvLayout(dst, len(dst), kv.total_heads, ((0, ctx),))
+        cl = PagedKvCluster(kv, gpus, units_per_gpu=2 * kv.total_heads * kv.blocks(ctx) + 64,
+                            max_requests=1, max_blocks=kv.blocks(ctx), fragmented=True, seed=0)
+        cl.admit([pre], seed=5)
+        ex = ReconfigurationExecutor(cl)
+        sync_us, nbytes = [], 0
+        for i in range(args.reps + 20):
+            r = ex.handoff(*((pre, dec) if i % 2 == 0 else (dec, pre)))
+            if i >= 20:
+                sync_us.append(r.host_ms * 1e3)
+            nbytes = r.kv.bytes
+        v = cl.verify(seed=5)
+        roof = 2 * nbytes / (peak * 1e9) * 1e6
+        row = {"case": name, "env": env, "bytes": nbytes, "sync_us": float(np.median(sync_us)),
+               "k1_roof_us": roof, "sync_hbm_frac": roof / float(np.median(sync_us)),
+               "bit_exact_property": v["placement_errors"] == 0 and v["word_mismatches"] == 0}
         print(json.dumps(row), flush=True)
         if out:
             out.write(json.dumps(row) + "\n")
