@@ -341,83 +341,67 @@ struct SegPieces {
 
 constexpr int kMaxSub = 16;  // copies packed into one shared-memory stage
 
-// One elected thread runs the pipeline. A stage is `piece` bytes of shared
+// The shared-memory ring's per-stage copy descriptors, and the two halves of
+// moving one stage: fill() packs copies into stage t and issues their loads,
+// store() issues the stage's stores. A stage is `piece` bytes of shared
 // memory filled with up to kMaxSub consecutive copies (one 32 KiB page chunk,
-// many short rows of partial pages / row-parallel weight slices, or -- K1 with
-// kTensor -- TMA tensor boxes of partial pages, 128-byte aligned). The
-// stage's loads all complete on one mbarrier; its stores form one bulk group,
-// so small copies still keep a full stage of bytes in flight.
+// many short rows of row-parallel weight slices, or -- K1 with kTensor -- TMA
+// tensor boxes of partial pages, 128-byte aligned). The stage's loads all
+// complete on one mbarrier; its stores form one bulk group, so small copies
+// still keep a full stage of bytes in flight.
 //
 // The issuing thread is the throughput limit for short copies, so the per-copy
-// path stays in registers: each load is issued as soon as its copy is produced
-// and the stage's single arrive.expect_tx follows the loads (the mbarrier
-// tx-count may go transiently negative; the phase cannot complete before the
-// arrival). K2 instantiates kTensor = false: no tensor bookkeeping at all.
-template <bool kTensor, class Source>
-__device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
-                                              const KvTensorMaps* tm) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar[kMaxStages];
-  __shared__ char* pdst[kMaxStages][kMaxSub];
-  __shared__ uint32_t pnb[kMaxStages][kMaxSub];
-  __shared__ uint32_t poff[kMaxStages][kMaxSub];
-  __shared__ int32_t pdmap[kTensor ? kMaxStages : 1][kMaxSub];  // -1: linear store
-  __shared__ int32_t pc1[kTensor ? kMaxStages : 1][kMaxSub];
-  __shared__ int32_t pdc2[kTensor ? kMaxStages : 1][kMaxSub];
-  __shared__ int pcnt[kMaxStages];
-  if (threadIdx.x != 0) return;
-  const uint32_t piece = src_it.piece;
-  const int lookahead = stages - 2;  // => the refilled stage's last store may still be pending
-  for (int s = 0; s < stages; ++s) bar_init(&bar[s]);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  const uint32_t base = smem_u32(smem);
-  int64_t issued = 0, stored = 0;
-  bool more = true;
-  auto issue = [&]() {
-    const int t = (int)(issued % stages);
-    Copy c;
-    if (src_it.next(c, piece, piece) != 1) {
-      more = false;
-      return;
+// path stays in registers and each load is issued as soon as its copy is
+// produced; the stage's single arrive.expect_tx follows (the tx-count may go
+// transiently negative; the phase cannot complete before the arrival). Only
+// the lean pipelines (no tensor boxes) take the fast path for a full linear
+// stage, expect_tx before the load: that order is +1.4% on full pages but
+// costs 4-20% when tensor-box stages use it or mix with it.
+template <bool kTensor>
+struct StageRing {
+  char* dst[kMaxStages][kMaxSub];
+  uint32_t nb[kMaxStages][kMaxSub];
+  uint32_t off[kMaxStages][kMaxSub];
+  int32_t dmap[kTensor ? kMaxStages : 1][kMaxSub];  // -1: linear store
+  int32_t c1[kTensor ? kMaxStages : 1][kMaxSub];
+  int32_t dc2[kTensor ? kMaxStages : 1][kMaxSub];
+  int cnt[kMaxStages];  // -1: end of work (warp-specialised pipeline)
+
+  // Stage t from its first copy `c` on; false when the source ran dry.
+  template <class Source>
+  __device__ __forceinline__ bool fill(Source& src_it, Copy& c, int t, uint32_t sbase,
+                                       uint32_t piece, uint64_t* bar, const KvTensorMaps* tm) {
+    if (!kTensor && c.nb == piece) {  // fast path: one linear copy fills the stage
+      cnt[t] = 1;
+      dst[t][0] = c.dst;
+      nb[t][0] = piece;
+      off[t][0] = 0;
+      bulk_load(sbase, c.src, piece, bar);
+      return true;
     }
-    if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
-    const uint32_t sbase = base + (uint32_t)t * piece;
-    // Fast path: one copy fills the stage (full pages), expect_tx before the
-    // load. Measured on one box (profiles/ab/r01_fastpath_*): +1.4% for the
-    // lean K1 on full pages, but -4..-14% for the tensor K1 on mixed plans
-    // (trace contexts), which runs at the copy peak without it.
-    if (!kTensor && c.nb == piece) {
-      pcnt[t] = 1;
-      pdst[t][0] = c.dst;
-      pnb[t][0] = piece;
-      poff[t][0] = 0;
-      if (kTensor) pdmap[t][0] = -1;
-      bulk_load(sbase, c.src, piece, &bar[t]);
-      ++issued;
-      return;
-    }
+    bool more = true;
     uint32_t used = 0, tx = 0;
     int n = 0;
     while (true) {
-      uint32_t off = used;
+      uint32_t o = used;
       if (kTensor && c.smap >= 0) {
-        off = (used + 127u) & ~127u;
-        tensor_load(sbase + off, &tm->map[c.smap], 0, c.c1, c.sc2, &bar[t]);
-        pdmap[t][n] = c.dmap;
-        pc1[t][n] = c.c1;
-        pdc2[t][n] = c.dc2;
+        o = (used + 127u) & ~127u;
+        tensor_load(sbase + o, &tm->map[c.smap], 0, c.c1, c.sc2, bar);
+        dmap[t][n] = c.dmap;
+        c1[t][n] = c.c1;
+        dc2[t][n] = c.dc2;
       } else {
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                sbase + off),
-            "l"(c.src), "r"(c.nb), "r"(smem_u32(&bar[t]))
+                sbase + o),
+            "l"(c.src), "r"(c.nb), "r"(smem_u32(bar))
             : "memory");
-        if (kTensor) pdmap[t][n] = -1;
+        if (kTensor) dmap[t][n] = -1;
       }
-      pdst[t][n] = c.dst;
-      pnb[t][n] = c.nb;
-      poff[t][n] = off;
-      used = off + c.nb;
+      dst[t][n] = c.dst;
+      nb[t][n] = c.nb;
+      off[t][n] = o;
+      used = o + c.nb;
       tx += c.nb;
       ++n;
       // pack a further copy: a linear one needs >= 1 KiB left, a box its size
@@ -433,10 +417,51 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
       }
       if (r == 2 || c.nb == 0) break;  // the next copy needs a fresh stage
     }
-    pcnt[t] = n;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[t])),
+    cnt[t] = n;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(tx)
                  : "memory");
+    return more;
+  }
+
+  __device__ __forceinline__ void store(int t, uint32_t sbase, const KvTensorMaps* tm) {
+    for (int i = 0; i < cnt[t]; ++i) {
+      if (kTensor && dmap[t][i] >= 0)
+        tensor_store(&tm->map[dmap[t][i]], 0, c1[t][i], dc2[t][i], sbase + off[t][i]);
+      else
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[t][i]),
+                     "r"(sbase + off[t][i]), "r"(nb[t][i])
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+};
+
+// One elected thread issues every load and store (lookahead L = S - 2 stages:
+// the refilled stage's last store may still be reading shared memory).
+template <bool kTensor, class Source>
+__device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
+                                              const KvTensorMaps* tm) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar[kMaxStages];
+  __shared__ StageRing<kTensor> ring;
+  if (threadIdx.x != 0) return;
+  const uint32_t piece = src_it.piece;
+  const int lookahead = stages - 2;
+  for (int s = 0; s < stages; ++s) bar_init(&bar[s]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint32_t base = smem_u32(smem);
+  int64_t issued = 0, stored = 0;
+  bool more = true;
+  auto issue = [&]() {
+    const int t = (int)(issued % stages);
+    Copy c;
+    if (src_it.next(c, piece, piece) != 1) {
+      more = false;
+      return;
+    }
+    if (issued >= stages) bulk_wait_read_1();  // stores of stage issued-S done reading
+    more = ring.fill(src_it, c, t, base + (uint32_t)t * piece, piece, &bar[t], tm);
     ++issued;
   };
   while (more && issued < lookahead) issue();
@@ -444,16 +469,7 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
     if (more) issue();
     const int t = (int)(stored % stages);
     bar_wait(&bar[t], (uint32_t)((stored / stages) & 1));
-    const uint32_t sbase = base + (uint32_t)t * piece;
-    for (int i = 0; i < pcnt[t]; ++i) {
-      if (kTensor && pdmap[t][i] >= 0)
-        tensor_store(&tm->map[pdmap[t][i]], 0, pc1[t][i], pdc2[t][i], sbase + poff[t][i]);
-      else
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pdst[t][i]),
-                     "r"(sbase + poff[t][i]), "r"(pnb[t][i])
-                     : "memory");
-    }
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    ring.store(t, base + (uint32_t)t * piece, tm);
     ++stored;
   }
   bulk_wait_all();
@@ -474,13 +490,7 @@ __device__ __forceinline__ void bulk_pipeline_ws(Source& src_it, int stages,
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t empty[kMaxStages];
-  __shared__ char* pdst[kMaxStages][kMaxSub];
-  __shared__ uint32_t pnb[kMaxStages][kMaxSub];
-  __shared__ uint32_t poff[kMaxStages][kMaxSub];
-  __shared__ int32_t pdmap[kTensor ? kMaxStages : 1][kMaxSub];
-  __shared__ int32_t pc1[kTensor ? kMaxStages : 1][kMaxSub];
-  __shared__ int32_t pdc2[kTensor ? kMaxStages : 1][kMaxSub];
-  __shared__ int pcnt[kMaxStages];
+  __shared__ StageRing<kTensor> ring;
   const uint32_t piece = src_it.piece;
   const uint32_t base = smem_u32(smem);
   if (threadIdx.x == 0) {
@@ -501,80 +511,18 @@ __device__ __forceinline__ void bulk_pipeline_ws(Source& src_it, int stages,
       if (k >= stages) bar_wait(&empty[t], (uint32_t)(((k / stages) - 1) & 1));
       Copy c;
       if (!more || src_it.next(c, piece, piece) != 1) {
-        pcnt[t] = -1;  // end of work
+        ring.cnt[t] = -1;  // end of work
         bar_arrive(&full[t]);
         break;
       }
-      const uint32_t sbase = base + (uint32_t)t * piece;
-      if (!kTensor && c.nb == piece) {  // one copy fills the stage (lean kernels only)
-        pcnt[t] = 1;
-        pdst[t][0] = c.dst;
-        pnb[t][0] = piece;
-        poff[t][0] = 0;
-        if (kTensor) pdmap[t][0] = -1;
-        bulk_load(sbase, c.src, piece, &full[t]);
-        continue;
-      }
-      uint32_t used = 0, tx = 0;
-      int n = 0;
-      while (true) {
-        uint32_t off = used;
-        if (kTensor && c.smap >= 0) {
-          off = (used + 127u) & ~127u;
-          tensor_load(sbase + off, &tm->map[c.smap], 0, c.c1, c.sc2, &full[t]);
-          pdmap[t][n] = c.dmap;
-          pc1[t][n] = c.c1;
-          pdc2[t][n] = c.dc2;
-        } else {
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  sbase + off),
-              "l"(c.src), "r"(c.nb), "r"(smem_u32(&full[t]))
-              : "memory");
-          if (kTensor) pdmap[t][n] = -1;
-        }
-        pdst[t][n] = c.dst;
-        pnb[t][n] = c.nb;
-        poff[t][n] = off;
-        used = off + c.nb;
-        tx += c.nb;
-        ++n;
-        if (n == kMaxSub) break;
-        const uint32_t aligned = (used + 127u) & ~127u;
-        const uint32_t avail_box = (kTensor && aligned <= piece) ? piece - aligned : 0;
-        const uint32_t avail_lin = piece - used >= 1024 ? piece - used : 0;
-        if (avail_lin == 0 && avail_box == 0) break;
-        const int r = src_it.next(c, avail_lin, avail_box);
-        if (r == 0) {
-          more = false;
-          break;
-        }
-        if (r == 2 || c.nb == 0) break;
-      }
-      pcnt[t] = n;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       smem_u32(&full[t])),
-                   "r"(tx)
-                   : "memory");
+      more = ring.fill(src_it, c, t, base + (uint32_t)t * piece, piece, &full[t], tm);
     }
   } else if (threadIdx.x == 32) {  // ------------------------------- consumer
-    int64_t k = 0;
-    for (;; ++k) {
+    for (int64_t k = 0;; ++k) {
       const int t = (int)(k % stages);
       bar_wait(&full[t], (uint32_t)((k / stages) & 1));
-      const int n = pcnt[t];
-      if (n < 0) break;
-      const uint32_t sbase = base + (uint32_t)t * piece;
-      for (int i = 0; i < n; ++i) {
-        if (kTensor && pdmap[t][i] >= 0)
-          tensor_store(&tm->map[pdmap[t][i]], 0, pc1[t][i], pdc2[t][i], sbase + poff[t][i]);
-        else
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                           pdst[t][i]),
-                       "r"(sbase + poff[t][i]), "r"(pnb[t][i])
-                       : "memory");
-      }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (ring.cnt[t] < 0) break;
+      ring.store(t, base + (uint32_t)t * piece, tm);
       if (k >= 1) {  // stage k-1's stores have read shared memory: hand it back
         bulk_wait_read_1();
         bar_arrive(&empty[(k - 1) % stages]);
