@@ -416,21 +416,24 @@ def distributed_workload(world: int, seqs: int | None):
                                      f"{seqs or 16 * world}x4096 KV+weights, {world} GPUs")
 
 
-NVLINK_GBS = 900.0  # NVLink 5, per direction per GPU (B200 HGX through NVSwitch)
+# NVLink roofline denominator: the measured peer copy per direction per GPU
+# (B200_PROFILING.md; 900 GB/s nominal NVLink 5, for context)
+NVLINK_GBS = 770.0
 
 
 def link_roofline(own_gpus: bool, egress: dict, ingress: dict, total_bytes: int, ms: float,
                   hbm: float, hbm_src: str, k1_ms: float) -> dict:
     """Roofline of a multi-process switch. With a GPU per rank the bound is the
-    busiest NVLink direction: t_roof = max_g max(E_g, I_g) / 900 GB/s (SURVEY
-    §8d); ``achieved`` is that GPU's bytes over the measured time. With ranks
-    sharing one device every byte is an HBM read + write."""
+    busiest NVLink direction: t_roof = max_g max(E_g, I_g) / 770 GB/s, the
+    measured peer copy (SURVEY §8d with B200_PROFILING.md's denominator);
+    ``achieved`` is that GPU's bytes over the measured time. With ranks sharing
+    one device every byte is an HBM read + write."""
     if own_gpus:
         busiest = max(max(egress.values()), max(ingress.values()))
         achieved = busiest / (ms * 1e-3) / 1e9
         return {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_GBS, "unit": "GB/s",
                 "frac": achieved / NVLINK_GBS, "traffic": None, "kernel": "tpr_k1_kv_migrate",
-                "peak_source": "nominal NVLink 5 per direction (no multi-GPU box to measure on)",
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)",
                 "busiest_gpu_bytes": busiest, "k1_ms_rank0": k1_ms}
     achieved = 2 * total_bytes / (ms * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
