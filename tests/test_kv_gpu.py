@@ -191,6 +191,22 @@ def test_one_call_switch_matches_two_step_path():
     assert int(a.status.item()) == 0
 
 
+def test_one_call_switch_edge_cases():
+    gpus = (0, 1, 2, 3)
+    reqs = ((1, 0), (2, 16), (3, 5))  # zero-context, one full page, one partial page
+    tp2 = workloads.round_robin(workloads.tp_groups(gpus, 2), list(reqs), 8)
+    tp4 = workloads.round_robin(workloads.tp_groups(gpus, 4), list(reqs), 8)
+    c = make(TINY, gpus, units=64, reqs=4, blocks=4)
+    c.admit(tp2, seed=1)
+    plan, st = c.switch_layouts(tp2, tp2)  # identity: empty plan, nothing launched
+    assert len(plan) == 0 and st.units == 0
+    plan, st = c.switch_layouts(tp2, tp4)
+    assert plan.total_bytes == M.plan_repartition(tp2, tp4, TINY.kv_bytes_per_token_per_head).total_bytes
+    assert c.placement() == M.layout_placement(tp4)
+    v = c.verify()
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
+
+
 def test_one_call_switch_raises_reference_errors():
     gpus = (0, 1, 2, 3)
     reqs = [(1, 50), (2, 70)]
