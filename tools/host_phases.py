@@ -1,7 +1,14 @@
-"""Per-phase host cost of a small switch (cfg1 shape), median over N."""
+"""Per-phase host cost of a small switch through the one-call path
+(PagedKvCluster.switch_layouts), median over N. The switch is enqueued only
+(no sync inside the timed phases); every 16 switches the stream is drained.
+
+    python tools/host_phases.py [--config 0] [--n 400]
+"""
 
 from __future__ import annotations
 
+import argparse
+import ctypes
 import sys
 import time
 from pathlib import Path
@@ -12,48 +19,69 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
-def main(n=400):
-    import ctypes
-
+def main():
     import torch
 
     import bench
     from paper_2605_05467_b200 import _native, migration as M, workloads
     from paper_2605_05467_b200.kvcache import PagedKvCluster
 
-    w = workloads.config(0)
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=0)
+    ap.add_argument("--n", type=int, default=400)
+    args = ap.parse_args()
+    w = workloads.config(args.config, weights=False) if args.config else workloads.config(0)
     kv = w.model.kv
     c = PagedKvCluster(kv, w.gpus, units_per_gpu=bench.capacity_units(w, kv),
-                       max_requests=len(w.requests), max_blocks=kv.blocks(512))
+                       max_requests=len(w.requests),
+                       max_blocks=kv.blocks(max(x for _, x in w.requests)))
     c.admit(w.old)
-    st = torch.cuda.Stream()
-    t = {k: [] for k in ("plan", "records", "reserve", "stage", "native", "owner", "total")}
-    for i in range(n):
+    st = torch.cuda.current_stream()
+    for i in range(20):
+        c.switch_layouts(*((w.old, w.new) if i % 2 == 0 else (w.new, w.old)), stream=st)
+    st.synchronize()
+    lib = _native.load()
+    t = {k: [] for k in ("pack", "tables+staging", "native", "post", "total", "switch_layouts")}
+    for i in range(args.n):
         a, b = (w.old, w.new) if i % 2 == 0 else (w.new, w.old)
         t0 = time.perf_counter()
-        plan = M.plan_repartition(a, b, kv.kv_bytes_per_token_per_head)
+        blob = M.pack_layouts(a, b)
         t1 = time.perf_counter()
-        xf = c.records(plan, validate=False)
-        t2 = time.perf_counter()
-        total, in_u, out_u = c._reserve(xf)
-        t3 = time.perf_counter()
+        tab = c._switch_tables(False)
+        tab.mode = _native.TPR_SWITCH_REPARTITION
+        rows = c._swt_plan
+        h_ptr, _ = c._staging.acquire(max(len(rows), 1) * 24)
+        tab.plan, tab.plan_cap, tab.records = rows.ctypes.data, len(rows), h_ptr
+        tab.d_xfers = c._xf.get(max(len(rows), 1) * 6, st).data_ptr()
+        tab.d_meta = c._meta.get(max(len(rows), 1) * 4, st).data_ptr()
+        tab.xfers_cap = len(rows)
+        work = c._work.t
+        tab.d_work, tab.work_cap = work.data_ptr(), work.numel() // 4
         cl = c._cluster_c()
-        d_xf = c._xf.get(len(xf) * 6, st)
-        d_meta = c._meta.get(len(xf) * 4, st)
-        d_work = c._work.get(total * 4, st)
-        h = c._staging.stage(xf.astype(np.int32))
-        t4 = time.perf_counter()
-        _native.call("tpr_kv_switch", ctypes.byref(c._geo), ctypes.byref(cl), h, d_xf.data_ptr(),
-                     len(xf), -1, d_meta.data_ptr(), c._totals.data_ptr(), total, d_work.data_ptr(),
-                     c.status.data_ptr(), st.cuda_stream)
+        t2 = time.perf_counter()
+        rc = lib.tpr_kv_switch_layouts(ctypes.byref(c._geo), ctypes.byref(cl),
+                                       blob.buffer_info()[0], len(blob), ctypes.byref(tab),
+                                       st.cuda_stream)
+        t3 = time.perf_counter()
+        assert rc == 0, rc
+        n = tab.n_plan
+        plan = M.MigrationPlan.from_array(rows[:n].copy())
         c._staging.fence(st)
-        t5 = time.perf_counter()
-        c._commit(in_u, out_u)
-        for s, d, r, lo, hi, _ in xf.tolist():
-            c.owner[r, lo:hi] = d
-        t6 = time.perf_counter()
-        for k, (x, y) in zip(t, ((t0, t1), (t1, t2), (t2, t3), (t3, t4), (t4, t5), (t5, t6), (t0, t6))):
+        for s_ in range(c.n_gpus):
+            c.ring_head[s_] += tab.in_units[s_]
+            c.ring_tail[s_] += tab.out_units[s_]
+        _ = plan.total_bytes
+        t4 = time.perf_counter()
+        for k, (x, y) in zip(t, ((t0, t1), (t1, t2), (t2, t3), (t3, t4), (t0, t4))):
             t[k].append((y - x) * 1e6)
+        if i % 16 == 15:
+            st.synchronize()
+    st.synchronize()
+    for i in range(args.n):  # the public call, for comparison
+        a, b = (w.old, w.new) if i % 2 == 0 else (w.new, w.old)
+        t0 = time.perf_counter()
+        c.switch_layouts(a, b, stream=st, validate=False)
+        t["switch_layouts"].append((time.perf_counter() - t0) * 1e6)
         if i % 16 == 15:
             st.synchronize()
     st.synchronize()
