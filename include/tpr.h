@@ -236,6 +236,7 @@ typedef struct tpr_switch_tables {
   int32_t* d_work;         /* device int32x4 [work_cap]                        */
   int64_t work_cap;
   int32_t* d_status;       /* device int32                                     */
+  int64_t plan_bytes;      /* out: the plan's total bytes (MigrationPlan.total_bytes) */
 } tpr_switch_tables_t;
 
 /* tpr_switch_tables_t.mode: the planner of the switch.

@@ -276,6 +276,9 @@ int tpr_switch_prepare(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
   }
   if (rc != TPR_OK) return set_error(TPR_ENOTFOUND, "plan needs the general path");
   t->n_plan = n;
+  int64_t plan_bytes = 0;
+  for (int64_t i = 0; i < n; ++i) plan_bytes += t->plan[i * 6 + 5];
+  t->plan_bytes = plan_bytes;
   rc = tpr_kv_records(t->plan, n, t->gpu_lut, t->gpu_lut_len, t->gpu_ids, n_slots, t->req_lut,
                       t->req_lut_len, t->slot_ctx, t->owner, geo->n_req_slots, H,
                       geo->block_tokens, t->kvb, t->validate, t->records, t->in_units,

@@ -634,7 +634,7 @@ class PagedKvCluster:
                 in_d[ids[s_]] = a
             if b:
                 out_d[ids[s_]] = b
-        return plan, MigrationStats(transfers=n, units=t.total_units, bytes=plan.total_bytes,
+        return plan, MigrationStats(transfers=n, units=t.total_units, bytes=t.plan_bytes,
                                     in_units=in_d, out_units=out_d)
 
     def _switch_general(self, old_layouts, new_layouts, stream, validate, handshake_ms,

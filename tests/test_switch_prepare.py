@@ -79,6 +79,7 @@ def test_prepare_matches_two_step_path(a, b):
     assert t.n_plan == len(want)
     assert np.array_equal(tab.plan[: t.n_plan], want)
     assert np.array_equal(tab.rec[: t.n_plan], expected_records(tab, want))
+    assert t.plan_bytes == int(want[:, 5].sum())
     units = [(hi - lo) * KV.blocks(c) for _, _, _, lo, hi, c in expected_records(tab, want).tolist()]
     assert t.total_units == sum(units)
     for s, g in enumerate(gpus):
@@ -123,6 +124,12 @@ def test_plan_capacity_is_reported():
     tab.plan = np.zeros((2, 6), np.int64)
     rc, t = tab.prepare(old, new)
     assert rc == _native.TPR_ECAPACITY and t.n_plan == len(reqs) * 8
+
+
+def test_struct_size_matches_header():
+    # tpr_switch_tables_t (include/tpr.h), 432 bytes: 19 pointer/int64 fields, two
+    # int32, two [TPR_MAX_GPUS] int64 arrays and plan_bytes
+    assert ctypes.sizeof(_native.SwitchTablesC) == 20 * 8 + 2 * 4 + 2 * 8 * _native.TPR_MAX_GPUS + 8
 
 
 def test_packed_layout_is_cached_and_exact():
