@@ -22,6 +22,7 @@ import torch
 from . import _native
 from .kvcache import MigrationStats, PagedKvCluster
 from .migration import KvLayout, MigrationPlan, plan_repartition
+from .placement import reuse_layouts
 from .tracing import nvtx
 from .weights import ReshardStats, ShardedWeightStore
 
@@ -35,6 +36,7 @@ class SwitchResult:
     device_ms: float = 0.0      # CUDA-event time of the whole switch (only when synced)
     status: int = 0             # K3 status bits (0 = every head was where the plan said)
     events: dict = field(default_factory=dict)
+    new_layouts: list | None = None  # the layouts the switch realised (reuse_order may reorder ranks)
 
     @property
     def bytes(self) -> int:
@@ -81,13 +83,25 @@ class ReconfigurationExecutor:
     def switch(self, old_layouts: list[KvLayout], new_layouts: list[KvLayout],
                new_weight_groups=None, parked=(), sync: bool = True,
                validate: bool = True, stream: torch.cuda.Stream | None = None,
-               trim: bool = False) -> SwitchResult:
+               trim: bool = False, reuse_order: bool = False) -> SwitchResult:
         """Stop-and-migrate TP switch. With ``sync`` the call returns after the
         switch completed on the device and reports measured latencies; without
         it, work is only enqueued and ``stream`` (default: the device's default
         stream) waits for it. ``trim`` compacts GPUs whose resident weight
-        slices exceed their new shard (ShardedWeightStore.reshard)."""
+        slices exceed their new shard (ShardedWeightStore.reshard).
+        ``reuse_order`` re-ranks every new group to keep the most KV in place
+        (placement.reuse_layouts); the realised layouts are in
+        ``SwitchResult.new_layouts``. It changes the plan the reference would
+        produce, so it is off by default. Weight groups follow the new ranks."""
         t0 = time.perf_counter()
+        if isinstance(new_layouts, KvLayout):
+            new_layouts = [new_layouts]
+        if reuse_order:
+            new_layouts = reuse_layouts(old_layouts, new_layouts,
+                                        self.kv.kv.kv_bytes_per_token_per_head)
+            if new_weight_groups is not None:  # a weight group follows its KV group's ranks
+                ranked = {frozenset(lay.group): lay.group for lay in new_layouts}
+                new_weight_groups = [ranked.get(frozenset(g), tuple(g)) for g in new_weight_groups]
         main = stream or self.main_stream
         ev = {}
         if sync:
@@ -130,7 +144,8 @@ class ReconfigurationExecutor:
                 main.wait_stream(ws)
         if ks is not main:
             main.wait_stream(ks)
-        res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev)
+        res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev,
+                           new_layouts=list(new_layouts))
         return self._finish(res, main, t0) if sync else res
 
     def handoff(self, prefill: KvLayout, decode: KvLayout, sync: bool = True) -> SwitchResult:

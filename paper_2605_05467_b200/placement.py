@@ -63,6 +63,21 @@ def reuse_rank_order(old_layouts: Sequence[KvLayout], new_gpus: Sequence[int], k
     return tuple(new_gpus) if base >= best else tuple(order)
 
 
+def reuse_layouts(old_layouts: Sequence[KvLayout], new_layouts: Sequence[KvLayout],
+                  kvb: int) -> list[KvLayout]:
+    """``new_layouts`` with every group's rank order replaced by
+    ``reuse_rank_order`` over the old placement of that group's requests (the
+    same GPUs, requests and TP degree; only which rank each GPU is changes)."""
+    out = []
+    for lay in new_layouts:
+        rid = {r for r, _ in lay.requests}
+        sub = [KvLayout(o.group, o.tp, o.total_heads,
+                        tuple((r, c) for r, c in o.requests if r in rid)) for o in old_layouts]
+        order = reuse_rank_order(sub, lay.group, kvb) if lay.requests else tuple(lay.group)
+        out.append(KvLayout(tuple(order), lay.tp, lay.total_heads, lay.requests))
+    return out
+
+
 @dataclass
 class Arrival:
     request_id: int

@@ -81,6 +81,32 @@ def test_handoff_one_call_matches_two_step(src, dst):
     assert a.placement() == M.layout_placement(dec) == b.placement()
 
 
+def test_switch_with_reuse_order_moves_less_and_stays_exact():
+    # TP4 -> TP8 re-ranked keeps half the KV in place (vs 1/8)
+    gpus = tuple(range(8))
+    reqs = [(i, 5 + 11 * i) for i in range(16)]
+    tp4 = workloads.round_robin(workloads.tp_groups(gpus, 4), reqs, 8)
+    tp8 = workloads.round_robin(workloads.tp_groups(gpus, 8), reqs, 8)
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=1024, max_requests=16, max_blocks=16, fragmented=True)
+    kv.admit(tp4, seed=3)
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load(workloads.tp_groups(gpus, 4))
+    ex = ReconfigurationExecutor(kv, store)
+    canonical = M.plan_repartition(tp4, tp8, KV.kv_bytes_per_token_per_head)
+    res = ex.switch(tp4, tp8, new_weight_groups=workloads.tp_groups(gpus, 8), reuse_order=True)
+    assert res.status == 0
+    assert res.kv.bytes < canonical.total_bytes
+    new = res.new_layouts
+    assert sorted(r for lay in new for r, _ in lay.requests) == sorted(r for r, _ in reqs)
+    assert kv.placement() == M.layout_placement(new)
+    v = kv.verify(seed=3)
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+    assert store.verify() == 0
+    back = ex.switch(new, tp4, new_weight_groups=workloads.tp_groups(gpus, 4))  # and back
+    assert back.status == 0 and kv.placement() == M.layout_placement(tp4)
+    store.finish()
+
+
 def test_capacity_admission_evicts_best_effort():
     gpus = (0, 1, 2, 3)
     kv = PagedKvCluster(KV, gpus, units_per_gpu={0: 128, 1: 128, 2: 64, 3: 64}, max_requests=8,
