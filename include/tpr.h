@@ -12,11 +12,16 @@
  *                            executed on device: block-table remap + free-ring
  *                            allocation by warp-level prefix sums
  *   tpr_kv_migrate  (K1)  -> the Transfer list (migration.py:50-57) executed:
- *                            paged-KV head-shard movement, 16-B vectorised
- *                            loads/stores straight into the destination pool
- *                            (a peer mapping when the destination is another GPU)
+ *                            paged-KV head-shard movement, TMA bulk copies (or
+ *                            16-B vectorised loads/stores) straight into the
+ *                            destination pool (a peer mapping when the destination
+ *                            is another GPU); partial pages as TMA tensor boxes
  *   tpr_weight_reshard (K2)-> migration.py:295-306 weight_memory("sharded", tp)
  *                            volumes realised: fetch only missing shard slices
+ *   tpr_kv_switch_layouts -> migration.py:137-189 plan_repartition (or :101-134
+ *                            head_transfers) + apply_plan (:192-207) in one call:
+ *                            plan, records, capacity, K3 + K1, placement; the hook
+ *                            engine.py:571-609 would call per reconfiguration
  *
  * Conventions: every call returns 0 on success and a negative tpr_status code on
  * failure; tpr_last_error() returns a thread-local message. Device pointers are
