@@ -34,7 +34,8 @@ import torch.distributed as dist
 from . import _native
 from .geometry import MAX_TP, KvGeometry, ModelGeometry
 from .kvcache import MigrationStats, _PinnedStaging
-from .migration import BYTES, KvLayout, MigrationError, MigrationPlan, plan_repartition
+from .migration import (BYTES, KvLayout, MigrationError, MigrationPlan, pack_layouts,
+                        plan_repartition)
 from .weights import ReshardStats, ShardedWeightStore, groups_ranges
 
 
@@ -179,6 +180,16 @@ class DistributedKvCluster:
         self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
                                         H, self.max_blocks, self.max_requests, self.n_units)
         self._staging = _PinnedStaging()
+        # id -> slot lookup tables for the native switch bookkeeping
+        ids = np.asarray(self.gpu_ids, dtype=np.int64)
+        self._gpu_ids_arr = ids
+        self._gpu_lut = None
+        if ids.min() >= 0 and ids.max() < (1 << 24):
+            self._gpu_lut = np.full(int(ids.max()) + 1, -1, dtype=np.int64)
+            self._gpu_lut[ids] = np.arange(len(ids))
+        self._req_lut = np.full(1024, -1, dtype=np.int64)
+        self._swt = None
+        self._plan_rows = np.empty((0, 6), np.int64)
         self._xf = torch.empty(0, dtype=torch.int32, device=self.device)
         self._meta = torch.empty(0, dtype=torch.int64, device=self.device)
         self._totals = torch.zeros(_native.TPR_TOTALS_LEN, dtype=torch.int64, device=self.device)
@@ -249,6 +260,7 @@ class DistributedKvCluster:
         self._free_req_slots = free
         for rid, rs, ctx, runs in new:
             self.req_slot[rid] = rs
+            self._set_req_lut(rid, rs)
             self.slot_ctx[rs] = ctx
             for s, lo, hi in runs:
                 self.owner[rs, lo:hi] = s
@@ -265,6 +277,105 @@ class DistributedKvCluster:
         self.stream.synchronize()
         dist.barrier(group=self.group)
         return n
+
+    def _set_req_lut(self, rid: int, slot: int) -> None:
+        if 0 <= rid < (1 << 24):
+            if rid >= len(self._req_lut):
+                grown = np.full(max(rid + 1, 2 * len(self._req_lut)), -1, dtype=np.int64)
+                grown[: len(self._req_lut)] = self._req_lut
+                self._req_lut = grown
+                self._swt = None
+            self._req_lut[rid] = slot
+
+    def _prepare(self, old_layouts, new_layouts):
+        """The host half of the switch in libtpr (``tpr_switch_prepare``: plan,
+        records, capacity check), identical on every rank. None when the
+        switch needs the Python path (every error the reference reports)."""
+        if self._gpu_lut is None:
+            return None
+        t = self._swt
+        if t is None:
+            t = self._swt = _native.SwitchTablesC()
+            t.gpu_lut, t.gpu_lut_len = self._gpu_lut.ctypes.data, len(self._gpu_lut)
+            t.gpu_ids = self._gpu_ids_arr.ctypes.data
+            t.req_lut, t.req_lut_len = self._req_lut.ctypes.data, len(self._req_lut)
+            t.slot_ctx, t.owner = self.slot_ctx.ctypes.data, self.owner.ctypes.data
+            t.kvb = self.kv.kv_bytes_per_token_per_head
+            t.validate, t.mode = 1, _native.TPR_SWITCH_REPARTITION
+        blob = pack_layouts(old_layouts, new_layouts)
+        cl = self._cluster_c()
+        lib = _native.load()
+        for _ in range(2):
+            rows = self._plan_rows
+            h_ptr, raw = self._staging.acquire(max(len(rows), 1) * 24)
+            t.plan, t.plan_cap, t.records = rows.ctypes.data, len(rows), h_ptr
+            rc = lib.tpr_switch_prepare(ctypes.byref(self._geo), ctypes.byref(cl),
+                                        blob.buffer_info()[0], len(blob), ctypes.byref(t))
+            if rc != _native.TPR_ECAPACITY:
+                break
+            self._plan_rows = np.empty((max(t.n_plan, 2 * len(rows)), 6), np.int64)
+        if rc == _native.TPR_ENOTFOUND:
+            return None
+        if rc != 0:
+            raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
+        n = t.n_plan
+        rec32 = raw.view(np.int32)[: n * 6].reshape(n, 6)
+        plan = MigrationPlan.from_array(self._plan_rows[:n].copy())
+        in_u = np.array(t.in_units[: self.world], np.int64)
+        out_u = np.array(t.out_units[: self.world], np.int64)
+        return plan, h_ptr, rec32.astype(np.int64), in_u, out_u
+
+    def launch_layouts(self, old_layouts, new_layouts, k1_events=None,
+                       host_handshake: bool = True):
+        """``plan_repartition`` + ``launch`` with the host half in libtpr; the
+        pushes of this rank go out through ``tpr_kv_switch`` (records read
+        zero-copy, K3 with filter_src = this slot, K1). Returns (plan, pending)."""
+        prep = self._prepare(old_layouts, new_layouts)
+        if prep is None:
+            plan = plan_repartition(old_layouts, new_layouts, self.kv.kv_bytes_per_token_per_head)
+            return plan, self.launch(plan, k1_events, host_handshake)
+        plan, h_ptr, rec, in_u, out_u = prep
+        if host_handshake:
+            handshake(rec, self.ring_head, self.ring_tail, self.group)  # also the start barrier
+        n = int(out_u[self.slot])  # units this slot pushes
+        if n and k1_events:  # K1 alone between events: the split path
+            self._staging.fence(self.stream)
+            cl = self._run_k3(rec, self.slot, n, want_ext=False)
+            k1_events[0].record(self.stream)
+            self._k1(cl, n, rec)
+            k1_events[1].record(self.stream)
+        elif n:
+            st = self.stream
+            grow = lambda t_, k: t_ if t_.numel() >= k else torch.empty(  # noqa: E731
+                max(k, 2 * t_.numel()), dtype=t_.dtype, device=self.device)
+            with torch.cuda.stream(st):
+                self._xf = grow(self._xf, len(rec) * 6)
+                self._meta = grow(self._meta, len(rec) * 4)
+                self._work = grow(self._work, n * 4)
+            cl = self._cluster_c()
+            with torch.cuda.device(self.device):
+                _native.call("tpr_kv_switch", ctypes.byref(self._geo), ctypes.byref(cl), h_ptr,
+                             self._xf.data_ptr(), len(rec), self.slot, self._meta.data_ptr(),
+                             self._totals.data_ptr(), n, self._work.data_ptr(),
+                             self.status.data_ptr(), st.cuda_stream)
+            self._staging.fence(st)
+        else:
+            self._staging.fence(self.stream)
+        return plan, (rec, in_u, out_u, n)
+
+    def _k1(self, cl, n: int, rec: np.ndarray) -> None:
+        full = not (rec[:, 5] % self.kv.block_tokens).any()
+        with torch.cuda.device(self.device):
+            _native.call("tpr_kv_migrate_ex", ctypes.byref(self._geo), ctypes.byref(cl),
+                         self._work.data_ptr(), n, _native.TPR_MIGRATE_FULL_PAGES if full else 0,
+                         self.stream.cuda_stream)
+
+    def migrate_layouts(self, old_layouts, new_layouts) -> tuple:
+        """Collective ``launch_layouts`` + barrier + ``finish``: (plan, stats)."""
+        plan, pending = self.launch_layouts(old_layouts, new_layouts)
+        self.stream.synchronize()
+        dist.barrier(group=self.group)
+        return plan, self.finish(plan, pending)
 
     def records(self, plan: MigrationPlan) -> np.ndarray:
         arr = plan.as_array()
@@ -299,11 +410,7 @@ class DistributedKvCluster:
             cl = self._run_k3(rec, self.slot, n, want_ext=False)
             if k1_events:
                 k1_events[0].record(self.stream)
-            full = not (rec[:, 5] % self.kv.block_tokens).any()
-            with torch.cuda.device(self.device):
-                _native.call("tpr_kv_migrate_ex", ctypes.byref(self._geo), ctypes.byref(cl),
-                             self._work.data_ptr(), n, _native.TPR_MIGRATE_FULL_PAGES if full else 0,
-                             self.stream.cuda_stream)
+            self._k1(cl, n, rec)
             if k1_events:
                 k1_events[1].record(self.stream)
         return rec, in_u, out_u, n
@@ -560,19 +667,24 @@ class DistributedExecutor:
         import time
         t0 = time.perf_counter()
         self.n += 1
-        plan = plan_repartition(old_layouts, new_layouts, self.kv.kv.kv_bytes_per_token_per_head)
         kst = self.kv.stream
         wst = self.weights.stream if self.weights is not None else None
-        if self.barrier is None:
-            kv_pending = self.kv.launch(plan, k1_events)
+        start = None
+        if self.barrier is None:  # host handshake = the start barrier
+            plan, kv_pending = self.kv.launch_layouts(old_layouts, new_layouts, k1_events)
         else:
-            if self.check_every and self.n % self.check_every == 0:
-                handshake(self.kv.records(plan), self.kv.ring_head, self.kv.ring_tail, self.kv.group)
             self.barrier(kst)  # every rank is here: peers' pools / tables / rings are quiescent
-            kv_pending = self.kv.launch(plan, k1_events, host_handshake=False)
+            start = torch.cuda.Event()
+            start.record(kst)
+            check = bool(self.check_every and self.n % self.check_every == 0)
+            plan, kv_pending = self.kv.launch_layouts(old_layouts, new_layouts, k1_events,
+                                                      host_handshake=check)
         w_pending = None
         if self.weights is not None and new_weight_groups is not None:
-            wst.wait_stream(kst)
+            # K2 pulls only need the start barrier: it runs alongside K3 + K1
+            # (KV pushes use egress links, weight pulls ingress)
+            if start is not None:
+                wst.wait_event(start)
             w_pending = self.weights.launch(new_weight_groups, parked, k2_events)
         if self.barrier is None:
             kst.synchronize()

@@ -88,7 +88,11 @@ def _gpu_worker(rank, world, path, outdir, q):
             np.savez(os.path.join(outdir, f"before_{i}_{rank}.npz"), **c.snapshot())
             plan = M.plan_repartition(lays[a], lays[b], kv.kv_bytes_per_token_per_head)
             np.save(os.path.join(outdir, f"rec_{i}.npy"), c.records(plan))
-            c.migrate(plan)
+            if i % 2:  # the native host half (tpr_switch_prepare) + zero-copy tpr_kv_switch
+                got, _ = c.migrate_layouts(lays[a], lays[b])
+                assert np.array_equal(got.as_array(), plan.as_array())
+            else:
+                c.migrate(plan)
             np.savez(os.path.join(outdir, f"after_{i}_{rank}.npz"), **c.snapshot())
         v = c.verify()
         c.close()
