@@ -40,8 +40,8 @@ def same_state(a, b):
             and a["ring_head"] == b["ring_head"] and a["ring_tail"] == b["ring_tail"])
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2])
-def test_random_walk(seed):
+@pytest.mark.parametrize("seed,one_call", [(0, False), (1, False), (2, False), (3, True), (4, True)])
+def test_random_walk(seed, one_call):
     rng = np.random.default_rng(seed)
     c = PagedKvCluster(KV, GPUS, units_per_gpu=128, max_requests=24, max_blocks=32,
                        fragmented=True, seed=seed)
@@ -90,7 +90,11 @@ def test_random_walk(seed):
                 new = layouts(random_groups(rng), resident, rng)
                 plan = M.plan_repartition(cur, new, KV.kv_bytes_per_token_per_head)
                 rec = c.records(plan)
-                c.migrate(plan)
+                if one_call:  # tpr_kv_switch_layouts (general path on any reference error)
+                    got, _ = c.switch_layouts(cur, new)
+                    assert np.array_equal(got.as_array(), plan.as_array())
+                else:
+                    c.migrate(plan)
                 want = check.expected_after(c, before, rec)
                 diff = check.compare(c.snapshot(), want)
                 assert not any(diff.values()), (step, diff)
