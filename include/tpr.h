@@ -242,6 +242,9 @@ typedef struct tpr_switch_tables {
   int64_t work_cap;
   int32_t* d_status;       /* device int32                                     */
   int64_t plan_bytes;      /* out: the plan's total bytes (MigrationPlan.total_bytes) */
+  int32_t* h_status;       /* nullable pinned host int32: the status word is mirrored
+                              there on the stream (fused K3 store or a 4-byte D2H),
+                              so a synchronous caller needs no separate read-back */
 } tpr_switch_tables_t;
 
 /* tpr_switch_tables_t.mode: the planner of the switch.

@@ -69,13 +69,16 @@ class ReconfigurationExecutor:
         self._ev_sync = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 
     def _finish(self, res: SwitchResult, main: torch.cuda.Stream, t0: float) -> SwitchResult:
-        """Synchronous tail: the step's result (K3's status word) read back D2H,
-        then the host waits for the end event."""
-        _native.call("tpr_memcpy_d2h", self._status_host.data_ptr(), self.kv.status.data_ptr(), 4,
-                     main.cuda_stream)
+        """Synchronous tail: the step's result (K3's status word) read back,
+        then the host waits for the end event. After the one-call switch the
+        word is already mirrored into pinned memory on the stream."""
+        mirrored = self.kv.status_mirrored
+        if not mirrored:
+            _native.call("tpr_memcpy_d2h", self._status_host.data_ptr(), self.kv.status.data_ptr(),
+                         4, main.cuda_stream)
         res.events["end"].record(main)
         res.events["end"].synchronize()
-        res.status = int(self._status_host[0])
+        res.status = int((self.kv.status_host if mirrored else self._status_host)[0])
         res.host_ms = (time.perf_counter() - t0) * 1e3
         res.device_ms = res.events["start"].elapsed_time(res.events["end"])
         return res

@@ -289,6 +289,55 @@ void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int
   out->n_pb = rows / r_box;
   out->enabled = 1;
 }
+
+int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                   const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
+                   int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
+                   int32_t* d_status, void* stream, int32_t* status_mirror) {
+  int rc = check_geometry(geo);
+  if (rc) return rc;
+  KvClusterParams cp;
+  if ((rc = cluster_params(cl, geo, &cp))) return rc;
+  if (n_xfers < 0 || n_units < 0) return fail(TPR_EINVAL, "negative sizes");
+  if (n_xfers == 0 && !status_mirror) return TPR_OK;
+  if (!d_status || (n_xfers > 0 && (!d_xfers || !d_meta || !d_totals)) || (n_units > 0 && !d_work))
+    return fail(TPR_EINVAL, "null device buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  bool mirrored = false;
+  if (n_xfers > 0 && n_units > 0) {
+    // records K3 reads: pinned host records in place (zero-copy), else an
+    // H2D copy into d_xfers first
+    const int32_t* xin = d_xfers;
+    if (h_xfers) {
+      const int32_t* mapped = device_view(h_xfers);
+      if (mapped) {
+        xin = mapped;
+      } else {
+        e = cudaMemcpyAsync(d_xfers, h_xfers, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n_xfers,
+                            cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch H2D");
+      }
+    }
+    e = launch_k3(*geo, cp, xin, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
+                  reinterpret_cast<int4*>(d_work), nullptr, d_status, st, status_mirror, &mirrored);
+    if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
+    e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
+               n_units, st, pdl_for(n_units),
+               h_xfers ? any_partial(h_xfers, n_xfers, geo->block_tokens) : true);
+    if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K1");
+  } else if (h_xfers && n_xfers > 0) {
+    // nothing to allocate or move: the records still land in d_xfers
+    e = cudaMemcpyAsync(d_xfers, h_xfers, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n_xfers,
+                        cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch H2D");
+  }
+  if (status_mirror && !mirrored) {
+    e = cudaMemcpyAsync(status_mirror, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch status D2H");
+  }
+  return TPR_OK;
+}
 }  // namespace tpr
 
 extern "C" {
@@ -452,37 +501,8 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl, cons
                   int32_t* d_xfers, int32_t n_xfers, int32_t filter_src, int64_t* d_meta,
                   int64_t* d_totals, int64_t n_units, int32_t* d_work, int32_t* d_status,
                   void* stream) {
-  int rc = check_geometry(geo);
-  if (rc) return rc;
-  tpr::KvClusterParams cp;
-  if ((rc = cluster_params(cl, geo, &cp))) return rc;
-  if (n_xfers < 0 || n_units < 0) return fail(TPR_EINVAL, "negative sizes");
-  if (n_xfers == 0) return TPR_OK;
-  if (!d_xfers || !d_meta || !d_totals || !d_status || (n_units > 0 && !d_work))
-    return fail(TPR_EINVAL, "null device buffer");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  // records K3 reads: pinned host records in place (zero-copy), else an H2D
-  // copy into d_xfers first
-  const int32_t* xin = d_xfers;
-  if (h_xfers) {
-    const int32_t* mapped = n_units > 0 ? device_view(h_xfers) : nullptr;
-    if (mapped) {
-      xin = mapped;
-    } else {
-      e = cudaMemcpyAsync(d_xfers, h_xfers, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n_xfers,
-                          cudaMemcpyHostToDevice, st);
-      if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch H2D");
-    }
-  }
-  if (n_units == 0) return TPR_OK;
-  e = tpr::launch_k3(*geo, cp, xin, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
-                     reinterpret_cast<int4*>(d_work), nullptr, d_status, st);
-  if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
-  e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work), n_units, st,
-             tpr::pdl_for(n_units),
-             h_xfers ? any_partial(h_xfers, n_xfers, geo->block_tokens) : true);
-  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_kv_switch K1");
+  return tpr::kv_switch_impl(geo, cl, h_xfers, d_xfers, n_xfers, filter_src, d_meta, d_totals,
+                             n_units, d_work, d_status, stream, nullptr);
 }
 
 int tpr_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, void* stream) {

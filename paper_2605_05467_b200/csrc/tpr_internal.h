@@ -65,7 +65,14 @@ int sm_count();
 // CTA (TPR_K3_FUSE_UNITS, 0 = never).
 bool pdl_enabled();
 int64_t k3_fuse_units();
-bool pdl_for(int64_t n_units);  // pdl_enabled() for plans up to k3_fuse_units()
+bool pdl_for(int64_t n_units);
+
+// tpr_kv_switch with an optional pinned host mirror of the status word, kept
+// current on the stream (fused K3 store, else a 4-byte D2H after K1)
+int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
+                   const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
+                   int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
+                   int32_t* d_status, void* stream, int32_t* status_mirror);  // pdl_enabled() for plans up to k3_fuse_units()
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute when `pdl`.
 template <typename... KArgs, typename... Args>
@@ -86,10 +93,13 @@ cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
 
 // xf_in: records as the caller holds them (device memory, or mapped pinned
 // host memory read zero-copy); xf: the device copy K3b reads (may equal xf_in).
+// status_mirror (nullable, pinned host memory): the fused K3 stores the status
+// word there at its end; *mirrored tells whether it did (the split K3 does not).
 cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
                       const int32_t* xf_in, int32_t* xf, int32_t n, int32_t filter,
                       int64_t* meta, int64_t* totals, int64_t n_hint, int4* work,
-                      int4* work_ext, int32_t* status, cudaStream_t st);
+                      int4* work_ext, int32_t* status, cudaStream_t st,
+                      int32_t* status_mirror = nullptr, bool* mirrored = nullptr);
 // pdl: launched right behind K3 on the same stream (waits for it on device)
 cudaError_t launch_k1(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                       int64_t n_units, cudaStream_t st, bool pdl);

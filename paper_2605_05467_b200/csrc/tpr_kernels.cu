@@ -282,11 +282,16 @@ __global__ void __launch_bounds__(kScanThreads)
     tpr_k3_fused(const int32_t* xf_in, int32_t* xf, int32_t n,
                  int32_t filter, int64_t* __restrict__ meta, int64_t* __restrict__ totals,
                  tpr_kv_geometry_t geo, KvClusterParams cl, int4* __restrict__ work,
-                 int4* __restrict__ work_ext, int32_t* __restrict__ status) {
+                 int4* __restrict__ work_ext, int32_t* __restrict__ status,
+                 int32_t* status_mirror) {
   pdl_trigger();
   k3_scan_body(xf_in, xf, n, geo.block_tokens, filter, meta, totals);
   __syncthreads();
   k3_remap_body(xf, n, meta, totals[0], geo, cl, work, work_ext, status, threadIdx.x, blockDim.x);
+  if (status_mirror != nullptr) {  // the status word, straight into pinned host memory
+    __syncthreads();                // every thread's atomicOr has landed
+    if (threadIdx.x == 0) *reinterpret_cast<volatile int32_t*>(status_mirror) = atomicOr(status, 0);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -561,7 +566,9 @@ static int copy_grid(const void* fn, int threads, int64_t want_warps) {
 cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
                       const int32_t* xf_in, int32_t* xf, int32_t n, int32_t filter,
                       int64_t* meta, int64_t* totals, int64_t n_hint, int4* work,
-                      int4* work_ext, int32_t* status, cudaStream_t st) {
+                      int4* work_ext, int32_t* status, cudaStream_t st, int32_t* status_mirror,
+                      bool* mirrored) {
+  if (mirrored) *mirrored = false;
   int threads = ((n + 31) / 32) * 32;
   if (threads > kScanThreads) threads = kScanThreads;
   if (threads < 32) threads = 32;
@@ -572,7 +579,8 @@ cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
     const int64_t want = ((n_hint + 31) / 32) * 32;
     if (want > ft) ft = (int)(want < kScanThreads ? want : kScanThreads);
     tpr_k3_fused<<<1, ft, 0, st>>>(xf_in, xf, n, filter, meta, totals, geo, cl, work, work_ext,
-                                   status);
+                                   status, status_mirror);
+    if (mirrored) *mirrored = status_mirror != nullptr;
     return cudaGetLastError();
   }
   tpr_k3_scan<<<1, threads, 0, st>>>(xf_in, xf, n, geo.block_tokens, filter, meta, totals);

@@ -179,6 +179,10 @@ class PagedKvCluster:
         self._work_ext = _Scratch(torch.int32, self.home)
         self._totals = torch.zeros(_native.TPR_TOTALS_LEN, dtype=torch.int64, device=self.home)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.home)
+        # pinned host mirror of the status word, kept current by the one-call
+        # switch on its stream (no separate read-back for a synchronous caller)
+        self.status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self.status_mirrored = False  # the last switch_layouts refreshed status_host
         self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
                                         H, self.max_blocks, self.max_requests, self.n_units)
         self._cl = _native.KvClusterC()
@@ -497,6 +501,7 @@ class PagedKvCluster:
         splits the fused call in two so the events can sit between them).
         """
         stream = stream or self._default_stream
+        self.status_mirrored = False  # this path leaves status_host stale
         arr = plan.as_array()
         n = len(arr)
         if n == 0:
@@ -565,6 +570,7 @@ class PagedKvCluster:
             t.kvb = self.kv.kv_bytes_per_token_per_head
             t.d_totals = self._totals.data_ptr()
             t.d_status = self.status.data_ptr()
+            t.h_status = self.status_host.data_ptr()
             self._swt_plan = np.empty((0, 6), np.int64)
         t.validate = int(validate)
         return t
@@ -582,6 +588,7 @@ class PagedKvCluster:
         ``planner="head_transfers"``: one old and one new layout planned with
         ``head_transfers`` (any GPU sets: the prefill->decode handoff)."""
         stream = stream or self._default_stream
+        self.status_mirrored = False
         if planner not in ("repartition", "head_transfers"):
             raise MigrationError(f"unknown planner {planner!r}")
         heads = planner == "head_transfers"
@@ -619,6 +626,7 @@ class PagedKvCluster:
         if rc != 0:
             raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
         n = t.n_plan
+        self.status_mirrored = True
         plan = MigrationPlan.from_array(self._swt_plan[:n].copy(), handshake_ms=handshake_ms)
         if n == 0:
             return plan, MigrationStats(0, 0, 0, {}, {})
