@@ -315,6 +315,32 @@ def test_wrong_source_flagged_on_device_without_host_validation():
     assert int(c.status.item()) & 1
 
 
+def test_status_mirror_reports_device_errors():
+    # the one-call switch mirrors K3's status word into pinned host memory; a
+    # synchronous executor reads it from there (fused K3 store or D2H)
+    from paper_2605_05467_b200.controller import ReconfigurationExecutor
+    for fuse in (1 << 30, 0):
+        from paper_2605_05467_b200 import _native
+        saved = _native.get_tuning("k3_fuse_units")
+        _native.set_tuning("k3_fuse_units", fuse)
+        try:
+            c = make(TINY, (0, 1))
+            c.admit([M.KvLayout((0,), 1, 8, ((0, 10),))], seed=1)
+            ex = ReconfigurationExecutor(c)
+            ok = ex.switch([M.KvLayout((0,), 1, 8, ((0, 10),)), M.KvLayout((1,), 1, 8, ())],
+                           [M.KvLayout((0, 1), 2, 8, ((0, 10),))], validate=False)
+            assert ok.status == 0 and c.status_mirrored
+            # claim every head sits on GPU 1 (heads 0-3 are on GPU 0): K3 flags the
+            # missing sources and the occupied destinations on the device
+            lie = [M.KvLayout((1,), 1, 8, ((0, 10),)), M.KvLayout((0,), 1, 8, ())]
+            bad = ex.switch(lie, [M.KvLayout((0, 1), 2, 8, ((0, 10),))], validate=False)
+            assert c.status_mirrored
+            assert bad.status & _native.TPR_STATUS_WRONG_SOURCE, bad.status
+            assert bad.status & _native.TPR_STATUS_DST_OCCUPIED, bad.status
+        finally:
+            _native.set_tuning("k3_fuse_units", saved)
+
+
 def test_capacity_error():
     c = make(TINY, (0, 1), units=16, reqs=4, blocks=8)
     c.admit([M.KvLayout((0,), 1, 8, ((0, 16),))], seed=1)  # 8 units on gpu 0
