@@ -117,6 +117,9 @@ int tpr_get_copy_engine(void);
  *                   0 never, 1 plans up to k3_fuse_units (a large K1 whose
  *                   CTAs start early leaves a tail), 2 every plan;
  *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place;
+ *   "k1_dynamic"    [TPR_K1_DYNAMIC, 0]: K1 CTAs claim batches of items from
+ *                   the counter after the work list instead of a static
+ *                   grid-stride share;
  *   "tensor_partial" [TPR_TENSOR_PARTIAL, 1]: K1 (TMA engine) moves partial
  *                   pages as TMA tensor boxes (token x planes) instead of
  *                   one short copy per plane: 0 never, 1 when a page of the
@@ -162,7 +165,8 @@ int tpr_plan_repartition(int32_t n_old, const int64_t* old_count, const int32_t*
  * processes every transfer (single-process, all pools visible); filter_src =
  * g processes only transfers leaving slot g (one process per GPU, push
  * model) while allocation offsets still follow the whole plan.
- * d_work: int32x4 [n_units] {src_unit, dst_unit, src|dst<<16, ntok};
+ * d_work: int32x4 [n_units + 1] {src_unit, dst_unit, src|dst<<16, ntok}; the
+ * extra last entry is K1's claim counter (K3 zeroes it; knob "k1_dynamic");
  * d_work_ext (nullable): int32x4 {req_slot, head, block, xfer}.
  * n_units_hint: host-computed number of units this caller processes (the
  * expand grid is sized from it). d_status: int32 (device), OR-ed status bits. */
@@ -238,7 +242,7 @@ typedef struct tpr_switch_tables {
   int64_t* d_meta;         /* device int64 [xfers_cap][4]                      */
   int64_t xfers_cap;
   int64_t* d_totals;       /* device int64 [TPR_TOTALS_LEN]                    */
-  int32_t* d_work;         /* device int32x4 [work_cap]                        */
+  int32_t* d_work;         /* device int32x4 [work_cap], >= units + 1          */
   int64_t work_cap;
   int32_t* d_status;       /* device int32                                     */
   int64_t plan_bytes;      /* out: the plan's total bytes (MigrationPlan.total_bytes) */

@@ -190,7 +190,7 @@ def k3_fuse_units() -> int:
     return int(load().tpr_get_tuning(b"k3_fuse_units"))
 
 
-TUNING_KEYS = ("k3_fuse_units", "pdl", "zero_copy", "tensor_partial", "bulk_ws")
+TUNING_KEYS = ("k3_fuse_units", "pdl", "zero_copy", "tensor_partial", "bulk_ws", "k1_dynamic")
 
 
 def set_tuning(key: str, value: int) -> None:

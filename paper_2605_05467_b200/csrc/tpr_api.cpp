@@ -115,7 +115,7 @@ int64_t env_i64(const char* name, int64_t dflt);
 
 // Launch-path knobs (process-wide): initialised from the environment, changed
 // at run time with tpr_set_tuning (tests cover every combination).
-std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1}, g_tensor{-1}, g_ws{-1};
+std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1}, g_tensor{-1}, g_ws{-1}, g_dyn{-1};
 
 int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
   int64_t v = k.load(std::memory_order_relaxed);
@@ -166,6 +166,7 @@ bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
 bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) != 0; }
 bool tensor_kernel_always() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) >= 2; }
 bool bulk_ws() { return knob(g_ws, "TPR_BULK_WS", 0) != 0; }
+bool k1_dynamic() { return knob(g_dyn, "TPR_K1_DYNAMIC", 0) != 0; }
 
 // ---------------------------------------------------------------------------
 // TMA tensor maps of the KV pools (K1 partial pages, tpr_internal.h).
@@ -361,6 +362,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   else if (!strcmp(key, "zero_copy")) g_zero_copy.store(value != 0);
   else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
   else if (!strcmp(key, "bulk_ws")) g_ws.store(value != 0);
+  else if (!strcmp(key, "k1_dynamic")) g_dyn.store(value != 0);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
 }
@@ -372,6 +374,7 @@ int64_t tpr_get_tuning(const char* key) {
   if (!strcmp(key, "zero_copy")) return knob(g_zero_copy, "TPR_ZERO_COPY", 1);
   if (!strcmp(key, "tensor_partial")) return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1);
   if (!strcmp(key, "bulk_ws")) return knob(g_ws, "TPR_BULK_WS", 0);
+  if (!strcmp(key, "k1_dynamic")) return knob(g_dyn, "TPR_K1_DYNAMIC", 0);
   return -1;
 }
 

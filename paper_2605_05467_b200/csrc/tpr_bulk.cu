@@ -104,6 +104,12 @@ struct Copy {
 // one copy per plane row (ntok valid tokens each) or, with the pools' tensor
 // maps, one TMA box per (token, r_box planes): item g of the unit takes tokens
 // g, g + items_per_unit, ... (no strided short copies at all).
+// K1 items are handed out statically (grid-stride) or, with a claim counter,
+// dynamically in batches of kK1ClaimBatch consecutive items claimed one batch
+// ahead: CTAs then stay on neighbouring items (a small, shared working set of
+// pages) and none drains late.
+constexpr int64_t kK1ClaimBatch = 8;
+
 template <bool kTensor>
 struct KvPieces {
   const int4* work;
@@ -113,6 +119,8 @@ struct KvPieces {
   const KvTensorMaps* tm;       // likewise (tm->enabled = 0: row copies)
   uint32_t piece;
   int64_t item;
+  unsigned long long* claim = nullptr;  // dynamic schedule (0 at kernel start)
+  int64_t item_end = 0, next_batch = 0;
   // current item: linear rows ...
   const char* s;
   char* d;
@@ -122,15 +130,37 @@ struct KvPieces {
   bool tensor;
 
   __device__ void start(int64_t first) {
-    item = first;
     rows_left = 0;
     tensor = false;
+    if (claim) {
+      item = first * kK1ClaimBatch;
+      item_end = min(item + kK1ClaimBatch, n_items);
+      next_batch = (int64_t)gridDim.x + (int64_t)atomicAdd(claim, 1ull);
+    } else {
+      item = first;
+    }
+  }
+  __device__ bool take(int64_t& k) {
+    if (!claim) {
+      if (item >= n_items) return false;
+      k = item;
+      item += gridDim.x;
+      return true;
+    }
+    if (item >= item_end) {
+      item = next_batch * kK1ClaimBatch;
+      if (item >= n_items) return false;
+      item_end = min(item + kK1ClaimBatch, n_items);
+      next_batch = (int64_t)gridDim.x + (int64_t)atomicAdd(claim, 1ull);
+    }
+    k = item++;
+    return true;
   }
   __device__ bool load_item() {
-    while (item < n_items) {
-      const int64_t u = item / p.items_per_unit;
-      const int g = (int)(item - u * p.items_per_unit);
-      item += gridDim.x;
+    int64_t it;
+    while (take(it)) {
+      const int64_t u = it / p.items_per_unit;
+      const int g = (int)(it - u * p.items_per_unit);
       const int4 w = work[u];
       const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
       const int64_t nb = (int64_t)ntok * p.tok_bytes;
@@ -537,8 +567,10 @@ template <bool kWS>
 __global__ void __launch_bounds__(64)
     tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
                            const __grid_constant__ KvClusterParams cl, int32_t stages,
-                           uint32_t piece) {
+                           uint32_t piece, int32_t dynamic) {
   KvPieces<false> it;
+  // the claim counter is the int4 slot after the work list (zeroed by K3)
+  if (dynamic) it.claim = reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
@@ -561,8 +593,9 @@ __global__ void __launch_bounds__(64)
     tpr_k1_kv_migrate_tma(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
                           const __grid_constant__ KvClusterParams cl,
                           const __grid_constant__ KvTensorMaps tm, int32_t stages,
-                          uint32_t piece) {
+                          uint32_t piece, int32_t dynamic) {
   KvPieces<true> it;
+  if (dynamic) it.claim = reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
@@ -669,6 +702,11 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items, int thr
   return grid < 1 ? 1 : (int)grid;
 }
 
+// schedulable units of a K1 launch: items, or claim batches when dynamic
+static int64_t k1_grid_units(int64_t items) {
+  return k1_dynamic() ? (items + kK1ClaimBatch - 1) / kK1ClaimBatch : items;
+}
+
 // Warp-specialised pipelines (producer + consumer warps): TPR_BULK_WS / the
 // "bulk_ws" knob (0 = one issuing thread per CTA).
 template <bool kWS>
@@ -678,14 +716,16 @@ static cudaError_t k1_launch(const KvCopyParams& p, const KvClusterParams& cl, c
   const int threads = kWS ? 64 : 32;
   if (tm.enabled) {
     const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma<kWS>), c,
-                               n_units * p.items_per_unit, threads);
+                               k1_grid_units(n_units * p.items_per_unit), threads);
     return launch_ex(tpr_k1_kv_migrate_tma<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
-                     pdl, work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece);
+                     pdl, work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece,
+                     (int32_t)k1_dynamic());
   }
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk<kWS>), c,
-                             n_units * p.items_per_unit, threads);
+                             k1_grid_units(n_units * p.items_per_unit), threads);
   return launch_ex(tpr_k1_kv_migrate_bulk<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
-                   pdl, work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece);
+                   pdl, work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece,
+                   (int32_t)k1_dynamic());
 }
 
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

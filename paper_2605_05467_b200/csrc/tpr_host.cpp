@@ -295,7 +295,7 @@ int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* 
   int rc = tpr_switch_prepare(geo, cl, L, len, t);
   if (rc != TPR_OK) return rc;
   const int64_t n = t->n_plan, units = t->total_units;
-  if (n > 0 && (n > t->xfers_cap || units > t->work_cap || !t->d_xfers || !t->d_meta ||
+  if (n > 0 && (n > t->xfers_cap || units + 1 > t->work_cap || !t->d_xfers || !t->d_meta ||
                 !t->d_totals || !t->d_status || (units > 0 && !t->d_work)))
     return tpr::set_error(TPR_ECAPACITY, "device scratch too small: %lld transfers, %lld units",
                           (long long)n, (long long)units);

@@ -57,6 +57,7 @@ void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int
 bool tensor_partial_enabled();
 bool tensor_kernel_always();
 bool bulk_ws();  // warp-specialised bulk pipelines (producer + consumer warps)
+bool k1_dynamic();  // K1 claims item batches from a counter after the work list
 
 int sm_count();
 

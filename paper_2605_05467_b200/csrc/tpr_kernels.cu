@@ -223,6 +223,9 @@ __device__ __forceinline__ void k3_remap_body(const int32_t* __restrict__ xf, in
                                               int32_t* __restrict__ status, int64_t first,
                                               int64_t stride) {
   const int H = geo.total_heads, B = geo.block_tokens, MB = geo.max_blocks;
+  // the int4 slot after the work list is K1's claim counter: zero it here, in
+  // the kernel that K1 waits for
+  if (first == 0) work[n_mine] = make_int4(0, 0, 0, 0);
   for (int64_t i = first; i < n_mine; i += stride) {
     // upper_bound(mine_off, i) - 1
     int lo = 0, hi = n;

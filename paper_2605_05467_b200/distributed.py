@@ -215,7 +215,7 @@ class DistributedKvCluster:
         with torch.cuda.stream(st):
             self._xf = grow(self._xf, len(rec) * 6)
             self._meta = grow(self._meta, len(rec) * 4)
-            self._work = grow(self._work, max(n_mine, 1) * 4)
+            self._work = grow(self._work, (n_mine + 1) * 4)  # + K1 claim slot
             if want_ext:
                 self._work_ext = grow(self._work_ext, max(n_mine, 1) * 4)
             self._staging.upload(rec.astype(np.int32), self._xf, st)
@@ -351,7 +351,7 @@ class DistributedKvCluster:
             with torch.cuda.stream(st):
                 self._xf = grow(self._xf, len(rec) * 6)
                 self._meta = grow(self._meta, len(rec) * 4)
-                self._work = grow(self._work, n * 4)
+                self._work = grow(self._work, (n + 1) * 4)  # + K1 claim slot
             cl = self._cluster_c()
             with torch.cuda.device(self.device):
                 _native.call("tpr_kv_switch", ctypes.byref(self._geo), ctypes.byref(cl), h_ptr,

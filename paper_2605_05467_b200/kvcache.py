@@ -309,7 +309,7 @@ class PagedKvCluster:
         n = len(xf)
         d_xf = self._xf.get(n * 6, stream)
         self._staging.upload(xf.astype(np.int32), d_xf, stream)
-        d_work = self._work.get(total * 4, stream)
+        d_work = self._work.get((total + 1) * 4, stream)  # + K1 claim slot
         d_ext = self._work_ext.get(total * 4, stream) if want_ext else None
         cl = self._cluster_c()
         _native.call(
@@ -522,7 +522,7 @@ class PagedKvCluster:
         cl = self._cluster_c()
         d_xf = self._xf.get(n * 6, stream)
         d_meta = self._meta.get(n * 4, stream)
-        d_work = self._work.get(max(total, 1) * 4, stream)
+        d_work = self._work.get((total + 1) * 4, stream)  # + K1 claim slot
         if k1_events:
             _native.call("tpr_kv_switch", ctypes.byref(self._geo), ctypes.byref(cl), h_ptr,
                          d_xf.data_ptr(), n, -1, d_meta.data_ptr(), self._totals.data_ptr(), 0,
@@ -618,8 +618,8 @@ class PagedKvCluster:
                 break
             if t.n_plan > len(rows):
                 self._swt_plan = np.empty((max(t.n_plan, 2 * len(rows)), 6), np.int64)
-            if t.total_units > t.work_cap:
-                self._work.get(t.total_units * 4, stream)
+            if t.total_units + 1 > t.work_cap:
+                self._work.get((t.total_units + 1) * 4, stream)
         if rc == _native.TPR_ENOTFOUND:
             return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
                                         heads)

@@ -98,6 +98,9 @@ LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
     "fused_plain_h2d_rows": dict(k3_fuse_units=1 << 30, pdl=0, zero_copy=0, tensor_partial=0),
     "ws_tensor": dict(bulk_ws=1, tensor_partial=1),
     "ws_rows": dict(bulk_ws=1, tensor_partial=0, pdl=2),
+    "dynamic_split_tensor": dict(k1_dynamic=1, k3_fuse_units=0, tensor_partial=1),
+    "dynamic_fused_rows_pdl": dict(k1_dynamic=1, k3_fuse_units=1 << 30, tensor_partial=0, pdl=2),
+    "dynamic_ws": dict(k1_dynamic=1, bulk_ws=1),
 }
 
 
