@@ -166,7 +166,7 @@ bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
 bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) != 0; }
 bool tensor_kernel_always() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) >= 2; }
 bool bulk_ws() { return knob(g_ws, "TPR_BULK_WS", 0) != 0; }
-bool k1_dynamic() { return knob(g_dyn, "TPR_K1_DYNAMIC", 0) != 0; }
+bool k1_dynamic() { return knob(g_dyn, "TPR_K1_DYNAMIC", 1) != 0; }
 
 // ---------------------------------------------------------------------------
 // TMA tensor maps of the KV pools (K1 partial pages, tpr_internal.h).
@@ -374,7 +374,7 @@ int64_t tpr_get_tuning(const char* key) {
   if (!strcmp(key, "zero_copy")) return knob(g_zero_copy, "TPR_ZERO_COPY", 1);
   if (!strcmp(key, "tensor_partial")) return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1);
   if (!strcmp(key, "bulk_ws")) return knob(g_ws, "TPR_BULK_WS", 0);
-  if (!strcmp(key, "k1_dynamic")) return knob(g_dyn, "TPR_K1_DYNAMIC", 0);
+  if (!strcmp(key, "k1_dynamic")) return knob(g_dyn, "TPR_K1_DYNAMIC", 1);
   return -1;
 }
 
