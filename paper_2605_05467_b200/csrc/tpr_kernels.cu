@@ -304,27 +304,51 @@ __global__ void __launch_bounds__(kScanThreads)
 // Persistent grid, warp-independent items, no block-level synchronisation.
 // ---------------------------------------------------------------------------
 template <int kUnroll>
+__device__ __forceinline__ void k1_vector_item(const int4* __restrict__ work, int64_t item,
+                                               const KvCopyParams& p, const KvClusterParams& cl,
+                                               unsigned lane) {
+  const int64_t u = item / p.items_per_unit;
+  const int g = (int)(item - u * p.items_per_unit);
+  const int4 w = work[u];
+  const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
+  const int row0 = g * p.rows_per_item;
+  const int nr = min(p.rows_per_item, p.rows - row0);
+  const char* s = reinterpret_cast<const char*>(cl.pool[src_slot]) + (int64_t)w.x * p.unit_bytes +
+                  (int64_t)row0 * p.pitch;
+  char* d = reinterpret_cast<char*>(cl.pool[dst_slot]) + (int64_t)w.y * p.unit_bytes +
+            (int64_t)row0 * p.pitch;
+  warp_copy2d<kUnroll>(s, d, (uint32_t)nr, (uint32_t)(ntok * p.tok_bytes), p.pitch, p.pitch, lane);
+}
+
+// dynamic: warps claim batches of kVecClaimBatch items from the counter after
+// the work list (zeroed by K3), so warps stay on neighbouring items
+constexpr int64_t kVecClaimBatch = 4;
+
+template <int kUnroll>
 __global__ void __launch_bounds__(kCopyThreads)
     tpr_k1_kv_migrate(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
-                      KvClusterParams cl) {
+                      KvClusterParams cl, int32_t dynamic) {
   pdl_wait();  // K3's work list (launched with programmatic serialization)
   const unsigned lane = threadIdx.x & 31u;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_items = n_units * p.items_per_unit;
-  for (int64_t item = gwarp; item < n_items; item += nwarps) {
-    const int64_t u = item / p.items_per_unit;
-    const int g = (int)(item - u * p.items_per_unit);
-    const int4 w = work[u];
-    const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
-    const int row0 = g * p.rows_per_item;
-    const int nr = min(p.rows_per_item, p.rows - row0);
-    const char* s = reinterpret_cast<const char*>(cl.pool[src_slot]) +
-                    (int64_t)w.x * p.unit_bytes + (int64_t)row0 * p.pitch;
-    char* d = reinterpret_cast<char*>(cl.pool[dst_slot]) + (int64_t)w.y * p.unit_bytes +
-              (int64_t)row0 * p.pitch;
-    warp_copy2d<kUnroll>(s, d, (uint32_t)nr, (uint32_t)(ntok * p.tok_bytes), p.pitch, p.pitch,
-                         lane);
+  if (!dynamic) {
+    for (int64_t item = gwarp; item < n_items; item += nwarps)
+      k1_vector_item<kUnroll>(work, item, p, cl, lane);
+    return;
+  }
+  unsigned long long* claim =
+      reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
+  for (int64_t batch = gwarp;;) {
+    const int64_t first = batch * kVecClaimBatch;
+    if (first >= n_items) break;
+    unsigned long long nb = 0;  // the next batch, claimed one batch ahead
+    if (lane == 0) nb = atomicAdd(claim, 1ull);
+    nb = __shfl_sync(kFull, nb, 0);
+    const int64_t last = min(first + kVecClaimBatch, n_items);
+    for (int64_t item = first; item < last; ++item) k1_vector_item<kUnroll>(work, item, p, cl, lane);
+    batch = nwarps + (int64_t)nb;
   }
 }
 
@@ -601,9 +625,11 @@ cudaError_t launch_k1(const KvCopyParams& p, const KvClusterParams& cl, const in
                       int64_t n_units, cudaStream_t st, bool pdl) {
   if (n_units <= 0) return cudaSuccess;
   const void* fn = reinterpret_cast<const void*>(&tpr_k1_kv_migrate<kCopyUnroll>);
-  const int grid = copy_grid(fn, kCopyThreads, n_units * p.items_per_unit);
+  const bool dyn = k1_dynamic();
+  const int64_t items = n_units * p.items_per_unit;
+  const int grid = copy_grid(fn, kCopyThreads, dyn ? (items + kVecClaimBatch - 1) / kVecClaimBatch : items);
   return launch_ex(tpr_k1_kv_migrate<kCopyUnroll>, dim3(grid), dim3(kCopyThreads), 0, st, pdl,
-                   work, n_units, p, cl);
+                   work, n_units, p, cl, (int32_t)dyn);
 }
 
 cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
