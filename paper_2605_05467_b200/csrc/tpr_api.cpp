@@ -167,6 +167,12 @@ bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) !
 bool tensor_kernel_always() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) >= 2; }
 bool bulk_ws() { return knob(g_ws, "TPR_BULK_WS", 0) != 0; }
 bool k1_dynamic() { return knob(g_dyn, "TPR_K1_DYNAMIC", 1) != 0; }
+// knob "k1_dynamic": 0 static shares, 1 dynamic claims of 8 items (default),
+// n >= 2 dynamic claims of n items
+int k1_claim_batch() {
+  const int64_t v = knob(g_dyn, "TPR_K1_DYNAMIC", 1);
+  return v <= 0 ? 0 : v == 1 ? 8 : (int)(v > 4096 ? 4096 : v);
+}
 
 // ---------------------------------------------------------------------------
 // TMA tensor maps of the KV pools (K1 partial pages, tpr_internal.h).
@@ -362,7 +368,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   else if (!strcmp(key, "zero_copy")) g_zero_copy.store(value != 0);
   else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
   else if (!strcmp(key, "bulk_ws")) g_ws.store(value != 0);
-  else if (!strcmp(key, "k1_dynamic")) g_dyn.store(value != 0);
+  else if (!strcmp(key, "k1_dynamic")) g_dyn.store(value);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
 }

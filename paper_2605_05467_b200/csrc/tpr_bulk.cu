@@ -105,10 +105,9 @@ struct Copy {
 // maps, one TMA box per (token, r_box planes): item g of the unit takes tokens
 // g, g + items_per_unit, ... (no strided short copies at all).
 // K1 items are handed out statically (grid-stride) or, with a claim counter,
-// dynamically in batches of kK1ClaimBatch consecutive items claimed one batch
-// ahead: CTAs then stay on neighbouring items (a small, shared working set of
-// pages) and none drains late.
-constexpr int64_t kK1ClaimBatch = 8;
+// dynamically in batches of `batch` consecutive items (knob k1_dynamic; 8 by
+// default) claimed one batch ahead: CTAs then stay on neighbouring items (a
+// small, shared working set of pages) and none drains late.
 
 template <bool kTensor>
 struct KvPieces {
@@ -120,7 +119,7 @@ struct KvPieces {
   uint32_t piece;
   int64_t item;
   unsigned long long* claim = nullptr;  // dynamic schedule (0 at kernel start)
-  int64_t item_end = 0, next_batch = 0;
+  int64_t batch = 8, item_end = 0, next_batch = 0;
   // current item: linear rows ...
   const char* s;
   char* d;
@@ -133,8 +132,8 @@ struct KvPieces {
     rows_left = 0;
     tensor = false;
     if (claim) {
-      item = first * kK1ClaimBatch;
-      item_end = min(item + kK1ClaimBatch, n_items);
+      item = first * batch;
+      item_end = min(item + batch, n_items);
       next_batch = (int64_t)gridDim.x + (int64_t)atomicAdd(claim, 1ull);
     } else {
       item = first;
@@ -148,9 +147,9 @@ struct KvPieces {
       return true;
     }
     if (item >= item_end) {
-      item = next_batch * kK1ClaimBatch;
+      item = next_batch * batch;
       if (item >= n_items) return false;
-      item_end = min(item + kK1ClaimBatch, n_items);
+      item_end = min(item + batch, n_items);
       next_batch = (int64_t)gridDim.x + (int64_t)atomicAdd(claim, 1ull);
     }
     k = item++;
@@ -569,8 +568,12 @@ __global__ void __launch_bounds__(64)
                            const __grid_constant__ KvClusterParams cl, int32_t stages,
                            uint32_t piece, int32_t dynamic) {
   KvPieces<false> it;
-  // the claim counter is the int4 slot after the work list (zeroed by K3)
-  if (dynamic) it.claim = reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
+  // the claim counter is the int4 slot after the work list (zeroed by K3);
+  // `dynamic` = items per claim, 0 = static grid-stride shares
+  if (dynamic > 0) {
+    it.claim = reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
+    it.batch = dynamic;
+  }
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
@@ -595,7 +598,10 @@ __global__ void __launch_bounds__(64)
                           const __grid_constant__ KvTensorMaps tm, int32_t stages,
                           uint32_t piece, int32_t dynamic) {
   KvPieces<true> it;
-  if (dynamic) it.claim = reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
+  if (dynamic > 0) {
+    it.claim = reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
+    it.batch = dynamic;
+  }
   it.work = work;
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
@@ -704,7 +710,8 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items, int thr
 
 // schedulable units of a K1 launch: items, or claim batches when dynamic
 static int64_t k1_grid_units(int64_t items) {
-  return k1_dynamic() ? (items + kK1ClaimBatch - 1) / kK1ClaimBatch : items;
+  const int64_t b = k1_claim_batch();
+  return b > 0 ? (items + b - 1) / b : items;
 }
 
 // Warp-specialised pipelines (producer + consumer warps): TPR_BULK_WS / the
@@ -719,13 +726,13 @@ static cudaError_t k1_launch(const KvCopyParams& p, const KvClusterParams& cl, c
                                k1_grid_units(n_units * p.items_per_unit), threads);
     return launch_ex(tpr_k1_kv_migrate_tma<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
                      pdl, work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece,
-                     (int32_t)k1_dynamic());
+                     (int32_t)k1_claim_batch());
   }
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk<kWS>), c,
                              k1_grid_units(n_units * p.items_per_unit), threads);
   return launch_ex(tpr_k1_kv_migrate_bulk<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
                    pdl, work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece,
-                   (int32_t)k1_dynamic());
+                   (int32_t)k1_claim_batch());
 }
 
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

@@ -58,6 +58,7 @@ bool tensor_partial_enabled();
 bool tensor_kernel_always();
 bool bulk_ws();  // warp-specialised bulk pipelines (producer + consumer warps)
 bool k1_dynamic();  // K1 claims item batches from a counter after the work list
+int k1_claim_batch();  // items per claim, 0 = static shares
 
 int sm_count();
 
