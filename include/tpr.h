@@ -117,7 +117,7 @@ int tpr_get_copy_engine(void);
  *                   0 never, 1 plans up to k3_fuse_units (a large K1 whose
  *                   CTAs start early leaves a tail), 2 every plan;
  *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place;
- *   "k1_dynamic"    [TPR_K1_DYNAMIC, 1]: K1 CTAs claim batches of items (1: 8 per
+ *   "k1_dynamic"    [TPR_K1_DYNAMIC, 1]: K1 CTAs claim batches of items (1: 4 per
  *                   claim, n >= 2: n per claim, 0: static shares) from
  *                   the counter after the work list instead of a static
  *                   grid-stride share;

@@ -167,11 +167,12 @@ bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) !
 bool tensor_kernel_always() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) >= 2; }
 bool bulk_ws() { return knob(g_ws, "TPR_BULK_WS", 0) != 0; }
 bool k1_dynamic() { return knob(g_dyn, "TPR_K1_DYNAMIC", 1) != 0; }
-// knob "k1_dynamic": 0 static shares, 1 dynamic claims of 8 items (default),
+// knob "k1_dynamic": 0 static shares, 1 dynamic claims of 4 items (default;
+// profiles/ab/r01_claimbatch_*: 2 contends on the counter, 4-6 best),
 // n >= 2 dynamic claims of n items
 int k1_claim_batch() {
   const int64_t v = knob(g_dyn, "TPR_K1_DYNAMIC", 1);
-  return v <= 0 ? 0 : v == 1 ? 8 : (int)(v > 4096 ? 4096 : v);
+  return v <= 0 ? 0 : v == 1 ? 4 : (int)(v > 4096 ? 4096 : v);
 }
 
 // ---------------------------------------------------------------------------

@@ -105,7 +105,7 @@ struct Copy {
 // maps, one TMA box per (token, r_box planes): item g of the unit takes tokens
 // g, g + items_per_unit, ... (no strided short copies at all).
 // K1 items are handed out statically (grid-stride) or, with a claim counter,
-// dynamically in batches of `batch` consecutive items (knob k1_dynamic; 8 by
+// dynamically in batches of `batch` consecutive items (knob k1_dynamic; 4 by
 // default) claimed one batch ahead: CTAs then stay on neighbouring items (a
 // small, shared working set of pages) and none drains late.
 
@@ -119,7 +119,7 @@ struct KvPieces {
   uint32_t piece;
   int64_t item;
   unsigned long long* claim = nullptr;  // dynamic schedule (0 at kernel start)
-  int64_t batch = 8, item_end = 0, next_batch = 0;
+  int64_t batch = 4, item_end = 0, next_batch = 0;
   // current item: linear rows ...
   const char* s;
   char* d;
