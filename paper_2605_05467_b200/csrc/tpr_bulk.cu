@@ -709,8 +709,17 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items, int thr
 }
 
 // schedulable units of a K1 launch: items, or claim batches when dynamic
-static int64_t k1_grid_units(int64_t items) {
+// items per dynamic claim for a K1 of `items` items: 0 (static grid-stride
+// shares) below 32 items per SM, where a copy is too short to drift and every
+// CTA should start at once
+static int64_t k1_batch_for(int64_t items) {
   const int64_t b = k1_claim_batch();
+  return (b > 0 && items >= (int64_t)sm_count() * 32) ? b : 0;
+}
+
+// schedulable units of a K1 launch: items, or claim batches when dynamic
+static int64_t k1_grid_units(int64_t items) {
+  const int64_t b = k1_batch_for(items);
   return b > 0 ? (items + b - 1) / b : items;
 }
 
@@ -726,13 +735,13 @@ static cudaError_t k1_launch(const KvCopyParams& p, const KvClusterParams& cl, c
                                k1_grid_units(n_units * p.items_per_unit), threads);
     return launch_ex(tpr_k1_kv_migrate_tma<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
                      pdl, work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece,
-                     (int32_t)k1_claim_batch());
+                     (int32_t)k1_batch_for(n_units * p.items_per_unit));
   }
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk<kWS>), c,
                              k1_grid_units(n_units * p.items_per_unit), threads);
   return launch_ex(tpr_k1_kv_migrate_bulk<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
                    pdl, work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece,
-                   (int32_t)k1_claim_batch());
+                   (int32_t)k1_batch_for(n_units * p.items_per_unit));
 }
 
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
