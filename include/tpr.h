@@ -250,6 +250,7 @@ typedef struct tpr_switch_tables {
   int32_t* h_status;       /* nullable pinned host int32: the status word is mirrored
                               there on the stream (fused K3 store or a 4-byte D2H),
                               so a synchronous caller needs no separate read-back */
+  void* k1_events[2];      /* nullable cudaEvent_t pair recorded around K1 (timing) */
 } tpr_switch_tables_t;
 
 /* tpr_switch_tables_t.mode: the planner of the switch.

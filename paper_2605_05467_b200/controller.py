@@ -118,11 +118,13 @@ class ReconfigurationExecutor:
         ks = self.kv_stream if self.overlap else main
         if ks is not main:
             ks.wait_stream(main)
-        if self.handshake is None and not self.time_kernels:
-            # plan + records + K3 + K1 in one native call
+        if self.handshake is None:
+            # plan + records + K3 + K1 in one native call (K1 bracketed by events
+            # when the kernels are timed)
             with nvtx("plan+kv K3+K1"):
-                plan, kv_stats = self.kv.switch_layouts(old_layouts, new_layouts, stream=ks,
-                                                        validate=validate)
+                plan, kv_stats = self.kv.switch_layouts(
+                    old_layouts, new_layouts, stream=ks, validate=validate,
+                    k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
         else:
             with nvtx("plan"):
                 plan = plan_repartition(old_layouts, new_layouts,

@@ -301,7 +301,8 @@ void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int
 int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                    int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
-                   int32_t* d_status, void* stream, int32_t* status_mirror) {
+                   int32_t* d_status, void* stream, int32_t* status_mirror,
+                   void* const* k1_events) {
   int rc = check_geometry(geo);
   if (rc) return rc;
   KvClusterParams cp;
@@ -330,15 +331,25 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
     e = launch_k3(*geo, cp, xin, d_xfers, n_xfers, filter_src, d_meta, d_totals, n_units,
                   reinterpret_cast<int4*>(d_work), nullptr, d_status, st, status_mirror, &mirrored);
     if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K3");
+    const bool timed = k1_events && k1_events[0] && k1_events[1];
+    if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[0]), st)) != cudaSuccess)
+      return cuda_fail(e, "tpr_kv_switch K1 start event");
     e = run_k1(geo, cl->n_gpus, copy_params(geo), cp, reinterpret_cast<const int4*>(d_work),
-               n_units, st, pdl_for(n_units),
+               n_units, st, pdl_for(n_units) && !timed,
                h_xfers ? any_partial(h_xfers, n_xfers, geo->block_tokens) : true);
     if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch K1");
+    if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[1]), st)) != cudaSuccess)
+      return cuda_fail(e, "tpr_kv_switch K1 end event");
   } else if (h_xfers && n_xfers > 0) {
     // nothing to allocate or move: the records still land in d_xfers
     e = cudaMemcpyAsync(d_xfers, h_xfers, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n_xfers,
                         cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "tpr_kv_switch H2D");
+  }
+  if (k1_events && k1_events[0] && k1_events[1] && !(n_xfers > 0 && n_units > 0)) {
+    // no K1 this time: an empty, still-recorded interval
+    cudaEventRecord(static_cast<cudaEvent_t>(k1_events[0]), st);
+    cudaEventRecord(static_cast<cudaEvent_t>(k1_events[1]), st);
   }
   if (status_mirror && !mirrored) {
     e = cudaMemcpyAsync(status_mirror, d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st);

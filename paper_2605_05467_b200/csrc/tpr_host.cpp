@@ -301,7 +301,8 @@ int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* 
                           (long long)n, (long long)units);
   if (n == 0 && !t->h_status) return TPR_OK;
   rc = tpr::kv_switch_impl(geo, cl, t->records, t->d_xfers, (int32_t)n, -1, t->d_meta,
-                           t->d_totals, units, t->d_work, t->d_status, stream, t->h_status);
+                           t->d_totals, units, t->d_work, t->d_status, stream, t->h_status,
+                           t->k1_events);
   if (rc != TPR_OK) return rc;
   if (n == 0) return TPR_OK;
   return tpr_kv_apply_owner(t->records, n, t->owner, geo->total_heads);

@@ -71,10 +71,12 @@ bool pdl_for(int64_t n_units);
 
 // tpr_kv_switch with an optional pinned host mirror of the status word, kept
 // current on the stream (fused K3 store, else a 4-byte D2H after K1)
+// k1_events (nullable): cudaEvent_t pair recorded on the stream around K1.
 int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                    int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
-                   int32_t* d_status, void* stream, int32_t* status_mirror);  // pdl_enabled() for plans up to k3_fuse_units()
+                   int32_t* d_status, void* stream, int32_t* status_mirror,
+                   void* const* k1_events = nullptr);  // pdl_enabled() for plans up to k3_fuse_units()
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute when `pdl`.
 template <typename... KArgs, typename... Args>

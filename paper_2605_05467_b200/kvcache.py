@@ -577,7 +577,7 @@ class PagedKvCluster:
 
     def switch_layouts(self, old_layouts, new_layouts, stream: torch.cuda.Stream | None = None,
                        validate: bool = True, handshake_ms: float = 0.0,
-                       planner: str = "repartition"):
+                       planner: str = "repartition", k1_events: tuple | None = None):
         """``plan_repartition(old, new)`` + ``migrate(plan)`` in one native call
         (``tpr_kv_switch_layouts``): plan, records, capacity check, K3 + K1 and
         the placement update. Returns (MigrationPlan, MigrationStats) equal to
@@ -586,7 +586,8 @@ class PagedKvCluster:
         the two-step path, which raises the reference's error.
 
         ``planner="head_transfers"``: one old and one new layout planned with
-        ``head_transfers`` (any GPU sets: the prefill->decode handoff)."""
+        ``head_transfers`` (any GPU sets: the prefill->decode handoff).
+        ``k1_events``: (start, end) CUDA events recorded around K1."""
         stream = stream or self._default_stream
         self.status_mirrored = False
         if planner not in ("repartition", "head_transfers"):
@@ -600,6 +601,10 @@ class PagedKvCluster:
         blob = pack_layouts(old_layouts, new_layouts)
         t = self._switch_tables(validate)
         t.mode = _native.TPR_SWITCH_HEAD_TRANSFERS if heads else _native.TPR_SWITCH_REPARTITION
+        if k1_events:
+            t.k1_events[0], t.k1_events[1] = k1_events[0].cuda_event, k1_events[1].cuda_event
+        else:
+            t.k1_events[0] = t.k1_events[1] = None
         lib = _native.load()
         cl = self._cluster_c()
         addr = blob.buffer_info()[0]
@@ -622,7 +627,7 @@ class PagedKvCluster:
                 self._work.get((t.total_units + 1) * 4, stream)
         if rc == _native.TPR_ENOTFOUND:
             return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
-                                        heads)
+                                        heads, k1_events)
         if rc != 0:
             raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
         n = t.n_plan
@@ -646,13 +651,13 @@ class PagedKvCluster:
                                     in_units=in_d, out_units=out_d)
 
     def _switch_general(self, old_layouts, new_layouts, stream, validate, handshake_ms,
-                        heads: bool = False):
+                        heads: bool = False, k1_events=None):
         kvb = self.kv.kv_bytes_per_token_per_head
         if heads:
             plan = head_transfers_array(old_layouts[0], new_layouts[0], kvb)
         else:
             plan = plan_repartition(old_layouts, new_layouts, kvb, handshake_ms=handshake_ms)
-        return plan, self.migrate(plan, stream=stream, validate=validate)
+        return plan, self.migrate(plan, stream=stream, validate=validate, k1_events=k1_events)
 
     # ------------------------------------------------------------ inspection
     def placement(self) -> dict:

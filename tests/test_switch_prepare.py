@@ -127,9 +127,9 @@ def test_plan_capacity_is_reported():
 
 
 def test_struct_size_matches_header():
-    # tpr_switch_tables_t (include/tpr.h), 440 bytes: 22 pointer/int64 fields, two
+    # tpr_switch_tables_t (include/tpr.h), 456 bytes: 24 pointer/int64 fields, two
     # int32 and two [TPR_MAX_GPUS] int64 arrays
-    assert ctypes.sizeof(_native.SwitchTablesC) == 22 * 8 + 2 * 4 + 2 * 8 * _native.TPR_MAX_GPUS
+    assert ctypes.sizeof(_native.SwitchTablesC) == 24 * 8 + 2 * 4 + 2 * 8 * _native.TPR_MAX_GPUS
 
 
 def test_packed_layout_is_cached_and_exact():
