@@ -602,6 +602,8 @@ class PagedKvCluster:
         t = self._switch_tables(validate)
         t.mode = _native.TPR_SWITCH_HEAD_TRANSFERS if heads else _native.TPR_SWITCH_REPARTITION
         if k1_events:
+            for e in k1_events:  # torch creates the event on its first record; libtpr
+                e.record(stream)  # then re-records it around K1 on the same stream
             t.k1_events[0], t.k1_events[1] = k1_events[0].cuda_event, k1_events[1].cuda_event
         else:
             t.k1_events[0] = t.k1_events[1] = None
