@@ -157,10 +157,11 @@ cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_
 namespace tpr {
 bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
 
-// PDL pays for small plans only (its launch overlap is worth a few us). For a
-// large K1 it costs ~2.5% (tools/e2e_paths.py: 0.3 ms on the cfg2 switch):
-// CTAs that become resident while K3 still runs start their static share of
-// the pages late, which leaves a tail. Large plans launch K1 normally.
+// PDL pays for small plans (its launch overlap is worth a few us). Under the
+// static grid-stride schedule it cost ~2.5% on a large K1 (CTAs resident while
+// K3 still ran started their share late and left a tail); with dynamic claims
+// it is neutral there (profiles/ab/r01_pdl_dynamic_*). Large plans launch K1
+// normally.
 // knob "tensor_partial": 0 row copies, 1 tensor boxes when a page is partial
 // (default), 2 the tensor kernel for every plan (A/B measurements)
 bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) != 0; }
