@@ -51,6 +51,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--cases", type=int, default=len(CASES), help="run the first N switch cases")
+    ap.add_argument("--no-handoff", action="store_true")
     args = ap.parse_args()
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
@@ -59,7 +61,7 @@ def main():
     out = open(args.out, "a") if args.out else None
     torch.cuda.set_device(0)
     main_stream = torch.cuda.current_stream()
-    for name, slots, a, b, n, ctx in CASES:
+    for name, slots, a, b, n, ctx in CASES[:args.cases]:
         gpus = tuple(range(slots))
         reqs = [(i, ctx) for i in range(n)]
         la = workloads.round_robin(workloads.tp_groups(gpus, a), reqs, kv.total_heads)
@@ -107,8 +109,9 @@ def main():
         torch.cuda.empty_cache()
     # prefill -> decode handoffs (disjoint groups, head_transfers): the most
     # frequent small transfer of a disaggregated deployment
-    for name, src, dst, ctx in (("handoff 1 seq x 463 TP2(0,1)->TP4(2..5)", (0, 1), (2, 3, 4, 5), 463),
-                                ("handoff 1 seq x 4096 TP1(0)->TP1(1)", (0,), (1,), 4096)):
+    handoffs = (("handoff 1 seq x 463 TP2(0,1)->TP4(2..5)", (0, 1), (2, 3, 4, 5), 463),
+                ("handoff 1 seq x 4096 TP1(0)->TP1(1)", (0,), (1,), 4096))
+    for name, src, dst, ctx in () if args.no_handoff else handoffs:
         gpus = tuple(range(6))
         pre = M.KvLayout(src, len(src), kv.total_heads, ((0, ctx),))
         dec = M.KvLayout(dst, len(dst), kv.total_heads, ((0, ctx),))
