@@ -114,51 +114,65 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kKeys = TPR_MAX_GPUS + 1;  // key TPR_MAX_GPUS = "no gpu" sink
 
-__device__ __forceinline__ int64_t block_keyed_exclusive(int key, int64_t val,
-                                                         int64_t* s_tab,  // [warps][kKeys]
-                                                         int64_t* s_run)  // [kKeys]
-{
+// Three keyed exclusive scans in one pass (shared barriers; the 3 x kKeys
+// column scans over the warp table run in parallel).
+constexpr int kScans = 3;
+__device__ __forceinline__ void block_keyed_exclusive3(const int (&key)[kScans],
+                                                       const int64_t (&val)[kScans],
+                                                       int64_t* s_tab,  // [kScans][warps][kKeys]
+                                                       int64_t* s_run,  // [kScans][kKeys]
+                                                       int64_t (&out)[kScans]) {
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;  // sized to the plan: small plans scan with one warp
-  for (int i = threadIdx.x; i < nwarps * kKeys; i += blockDim.x) s_tab[i] = 0;
+  const int plane = nwarps * kKeys;
+  for (int i = threadIdx.x; i < kScans * plane; i += blockDim.x) s_tab[i] = 0;
   __syncthreads();
-  const unsigned peers = __match_any_sync(kFull, key);
-  const unsigned lower = peers & ((1u << lane) - 1u);
-  int64_t in_warp = 0;
+  int64_t in_warp[kScans];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int64_t vj = __shfl_sync(kFull, val, j);
-    if ((lower >> j) & 1u) in_warp += vj;
+  for (int s = 0; s < kScans; ++s) {
+    const unsigned peers = __match_any_sync(kFull, key[s]);
+    const unsigned lower = peers & ((1u << lane) - 1u);
+    int64_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t vj = __shfl_sync(kFull, val[s], j);
+      if ((lower >> j) & 1u) acc += vj;
+    }
+    in_warp[s] = acc;
+    if (lane == 31u - (unsigned)__clz(peers)) s_tab[s * plane + warp * kKeys + key[s]] = acc + val[s];
   }
-  if (lane == 31u - (unsigned)__clz(peers)) s_tab[warp * kKeys + key] = in_warp + val;
   __syncthreads();
-  if (threadIdx.x < kKeys) {
-    const int k = threadIdx.x;
-    int64_t run = s_run[k];
+  for (int c = threadIdx.x; c < kScans * kKeys; c += blockDim.x) {  // one-warp blocks loop
+    const int s = c / kKeys, k = c - s * kKeys;
+    int64_t* col = s_tab + s * plane + k;
+    int64_t run = s_run[c];
     for (int w = 0; w < nwarps; ++w) {
-      const int64_t t = s_tab[w * kKeys + k];
-      s_tab[w * kKeys + k] = run;
+      const int64_t t = col[w * kKeys];
+      col[w * kKeys] = run;
       run += t;
     }
-    s_run[k] = run;
+    s_run[c] = run;
   }
   __syncthreads();
-  const int64_t out = s_tab[warp * kKeys + key] + in_warp;
+#pragma unroll
+  for (int s = 0; s < kScans; ++s) out[s] = s_tab[s * plane + warp * kKeys + key[s]] + in_warp[s];
   __syncthreads();
-  return out;
 }
 
 // Scan body (one CTA). Records are read from `xf_in`, which may be the
 // caller's pinned host buffer (mapped: zero-copy over PCIe, no separate H2D
 // copy) and are written to `xf` (device) when the two differ.
-__device__ __forceinline__ void k3_scan_body(const int32_t* xf_in,  // may alias xf
+__device__ __forceinline__ int64_t k3_scan_body(const int32_t* xf_in,  // may alias xf
                                              int32_t* xf, int32_t n,
                                              int32_t block_tokens, int32_t filter,
                                              int64_t* __restrict__ meta,
-                                             int64_t* __restrict__ totals) {
-  __shared__ int64_t s_tab[kScanWarps * kKeys];
-  __shared__ int64_t s_run[3][kKeys];
-  for (int i = threadIdx.x; i < 3 * kKeys; i += blockDim.x) (&s_run[0][0])[i] = 0;
+                                             int64_t* __restrict__ totals,
+                                             int32_t* s_xf = nullptr,    // shared copies
+                                             int64_t* s_meta = nullptr)  // (fused K3, small n)
+{
+  __shared__ int64_t s_tab[kScans * kScanWarps * kKeys];
+  __shared__ int64_t s_run[kScans][kKeys];
+  for (int i = threadIdx.x; i < kScans * kKeys; i += blockDim.x) (&s_run[0][0])[i] = 0;
   __syncthreads();
   for (int base = 0; base < n; base += blockDim.x) {
     const int t = base + threadIdx.x;
@@ -174,6 +188,10 @@ __device__ __forceinline__ void k3_scan_body(const int32_t* xf_in,  // may alias
 #pragma unroll
         for (int f = 0; f < TPR_XFER_FIELDS; ++f) o[f] = r[f];
       }
+      if (s_xf != nullptr) {
+#pragma unroll
+        for (int f = 0; f < TPR_XFER_FIELDS; ++f) s_xf[t * TPR_XFER_FIELDS + f] = r[f];
+      }
       const int32_t ctx = r[5];
       const int64_t nblk = ctx > 0 ? (ctx + block_tokens - 1) / block_tokens : 0;
       units = (int64_t)(r[4] - r[3]) * nblk;
@@ -181,17 +199,25 @@ __device__ __forceinline__ void k3_scan_body(const int32_t* xf_in,  // may alias
       dst = r[1] >= 0 ? r[1] : TPR_MAX_GPUS;
       mine = (filter < 0 || r[0] == filter) ? units : 0;
     }
-    const int64_t mine_off = block_keyed_exclusive(0, mine, s_tab, s_run[0]);
-    const int64_t alloc_off =
-        block_keyed_exclusive(dst, dst < TPR_MAX_GPUS ? units : 0, s_tab, s_run[1]);
-    const int64_t rel_off =
-        block_keyed_exclusive(src, src < TPR_MAX_GPUS ? units : 0, s_tab, s_run[2]);
+    const int keys[kScans] = {0, dst, src};
+    const int64_t vals[kScans] = {mine, dst < TPR_MAX_GPUS ? units : 0,
+                                  src < TPR_MAX_GPUS ? units : 0};
+    int64_t offs[kScans];
+    block_keyed_exclusive3(keys, vals, s_tab, &s_run[0][0], offs);
+    const int64_t mine_off = offs[0], alloc_off = offs[1], rel_off = offs[2];
     if (t < n) {
       int64_t* m = meta + (int64_t)t * TPR_META_FIELDS;
       m[0] = mine_off;
       m[1] = alloc_off;
       m[2] = rel_off;
       m[3] = mine;
+      if (s_meta != nullptr) {
+        int64_t* sm = s_meta + t * TPR_META_FIELDS;
+        sm[0] = mine_off;
+        sm[1] = alloc_off;
+        sm[2] = rel_off;
+        sm[3] = mine;
+      }
     }
   }
   __syncthreads();
@@ -200,6 +226,7 @@ __device__ __forceinline__ void k3_scan_body(const int32_t* xf_in,  // may alias
     totals[1 + threadIdx.x] = s_run[1][threadIdx.x];
     totals[1 + TPR_MAX_GPUS + threadIdx.x] = s_run[2][threadIdx.x];
   }
+  return s_run[0][0];  // units this filter processes (every thread)
 }
 
 __global__ void __launch_bounds__(kScanThreads)
@@ -244,21 +271,26 @@ __device__ __forceinline__ void k3_remap_body(const int32_t* __restrict__ xf, in
     const int ntok = (b == nblk - 1) ? ctx - b * B : B;
     const int64_t bt_idx = ((int64_t)req * H + h) * MB + b;
 
-    int32_t src_unit = -1;
-    if (src >= 0) {
-      int32_t* bts = reinterpret_cast<int32_t*>(cl.block_table[src]);
-      src_unit = bts[bt_idx];
+    // All loads first, then the stores: the three reads are independent (an
+    // entry moves once per plan, and the released ring positions never overlap
+    // the allocated ones), so they cost one memory latency instead of three.
+    int32_t* bts = src >= 0 ? reinterpret_cast<int32_t*>(cl.block_table[src]) : nullptr;
+    int32_t* btd = dst >= 0 ? reinterpret_cast<int32_t*>(cl.block_table[dst]) : nullptr;
+    const int32_t src_unit = bts ? __ldcg(bts + bt_idx) : -1;
+    // dst == -1: release only (request finished or evicted)
+    const int32_t dst_unit =
+        btd ? __ldcg(reinterpret_cast<const int32_t*>(cl.free_ring[dst]) +
+                     (cl.ring_head[dst] + m[1] + local) % cl.units[dst])
+            : -1;
+    const int32_t dst_prev = btd ? __ldcg(btd + bt_idx) : -1;
+    if (bts) {
       if (src_unit < 0) atomicOr(status, TPR_STATUS_WRONG_SOURCE);
       bts[bt_idx] = -1;
       int32_t* ring_s = reinterpret_cast<int32_t*>(cl.free_ring[src]);
       ring_s[(cl.ring_tail[src] + m[2] + local) % cl.units[src]] = src_unit;
     }
-    int32_t dst_unit = -1;
-    if (dst >= 0) {  // dst == -1: release only (request finished or evicted)
-      const int32_t* ring_d = reinterpret_cast<const int32_t*>(cl.free_ring[dst]);
-      dst_unit = ring_d[(cl.ring_head[dst] + m[1] + local) % cl.units[dst]];
-      int32_t* btd = reinterpret_cast<int32_t*>(cl.block_table[dst]);
-      if (btd[bt_idx] >= 0) atomicOr(status, TPR_STATUS_DST_OCCUPIED);
+    if (btd) {
+      if (dst_prev >= 0) atomicOr(status, TPR_STATUS_DST_OCCUPIED);
       btd[bt_idx] = dst_unit;
     }
 
@@ -278,6 +310,8 @@ __global__ void __launch_bounds__(256)
                 (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
+constexpr int kFusedSmemXfers = 512;
+
 // K3 fused (small plans): one CTA scans, then the same CTA expands every unit.
 // Saves the second launch and its dependency gap; the scan's meta/totals are
 // re-read from L2 by the block that wrote them (visible after __syncthreads).
@@ -287,10 +321,17 @@ __global__ void __launch_bounds__(kScanThreads)
                  tpr_kv_geometry_t geo, KvClusterParams cl, int4* __restrict__ work,
                  int4* __restrict__ work_ext, int32_t* __restrict__ status,
                  int32_t* status_mirror) {
+  // up to kFusedSmemXfers records and their offsets stay in shared memory, so
+  // the per-unit binary search and record reads do not go to L2
+  __shared__ int32_t s_xf[kFusedSmemXfers * TPR_XFER_FIELDS];
+  __shared__ int64_t s_meta[kFusedSmemXfers * TPR_META_FIELDS];
+  const bool in_smem = n <= kFusedSmemXfers;
   pdl_trigger();
-  k3_scan_body(xf_in, xf, n, geo.block_tokens, filter, meta, totals);
+  const int64_t n_mine = k3_scan_body(xf_in, xf, n, geo.block_tokens, filter, meta, totals,
+                                      in_smem ? s_xf : nullptr, in_smem ? s_meta : nullptr);
   __syncthreads();
-  k3_remap_body(xf, n, meta, totals[0], geo, cl, work, work_ext, status, threadIdx.x, blockDim.x);
+  k3_remap_body(in_smem ? s_xf : xf, n, in_smem ? s_meta : meta, n_mine, geo, cl, work,
+                work_ext, status, threadIdx.x, blockDim.x);
   if (status_mirror != nullptr) {  // the status word, straight into pinned host memory
     __syncthreads();                // every thread's atomicOr has landed
     if (threadIdx.x == 0) *reinterpret_cast<volatile int32_t*>(status_mirror) = atomicOr(status, 0);
