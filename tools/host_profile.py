@@ -1,0 +1,72 @@
+"""cProfile of the public small-switch call (ReconfigurationExecutor.switch,
+1 seq x 463 tokens TP1->TP2, enqueue only): where the host microseconds go.
+
+    python tools/host_profile.py [--n 3000]
+"""
+
+from __future__ import annotations
+
+import argparse
+import cProfile
+import io
+import pstats
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+
+    from paper_2605_05467_b200 import workloads
+    from paper_2605_05467_b200.controller import ReconfigurationExecutor
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
+    from paper_2605_05467_b200.kvcache import PagedKvCluster
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=3000)
+    args = ap.parse_args()
+    kv = LLAMA_3_1_8B.kv
+    gpus, ctx = (0, 1), 463
+    reqs = [(0, ctx)]
+    la = workloads.round_robin(workloads.tp_groups(gpus, 1), reqs, kv.total_heads)
+    lb = workloads.round_robin(workloads.tp_groups(gpus, 2), reqs, kv.total_heads)
+    cl = PagedKvCluster(kv, gpus, units_per_gpu=2 * kv.total_heads * kv.blocks(ctx) + 64,
+                        max_requests=1, max_blocks=kv.blocks(ctx), fragmented=True, seed=0)
+    cl.admit(la, seed=5)
+    ex = ReconfigurationExecutor(cl)
+
+    def run(n, sync):
+        for i in range(n):
+            ex.switch(*((la, lb) if i % 2 == 0 else (lb, la)), validate=False, sync=sync)
+            if not sync and i % 16 == 15:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+
+    run(200, False)
+    for sync in (False, True):
+        t = []
+        for i in range(args.n):
+            t0 = time.perf_counter()
+            ex.switch(*((la, lb) if i % 2 == 0 else (lb, la)), validate=False, sync=sync)
+            t.append(time.perf_counter() - t0)
+            if not sync and i % 16 == 15:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        print(f"switch(sync={sync}) median {np.median(t) * 1e6:.1f} us", flush=True)
+    pr = cProfile.Profile()
+    pr.enable()
+    run(args.n, False)
+    pr.disable()
+    s = io.StringIO()
+    pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(30)
+    print(s.getvalue())
+
+
+if __name__ == "__main__":
+    main()
