@@ -146,6 +146,28 @@ def test_large_plan_takes_split_k3_and_matches_oracle():
     assert _native.kv_switch_launches(stats.units) == 3
 
 
+@pytest.mark.parametrize("n_reqs", [1, 31, 512, 513, 900])
+def test_fused_k3_record_counts_bit_exact(n_reqs):
+    # fused K3 (<= k3_fuse_units pages) keeps up to 512 records in shared
+    # memory and reads larger plans from global: both sides of the boundary,
+    # one-warp blocks included, through the one-call and the two-step path
+    from paper_2605_05467_b200 import _native
+    gpus = (0, 1)
+    reqs = [(i, 16) for i in range(n_reqs)]  # one page per head: TP1 -> TP2 = 1 transfer, 4 pages
+    lay = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2)}
+    c = make(TINY, gpus, units=8 * n_reqs + 64, reqs=n_reqs, blocks=1, seed=n_reqs)
+    c.admit(lay[1], seed=4)
+    plan = M.plan_repartition(lay[1], lay[2], TINY.kv_bytes_per_token_per_head)
+    stats = migrate_and_compare(c, plan)
+    assert stats.transfers == n_reqs and stats.units <= _native.k3_fuse_units()
+    assert _native.kv_switch_launches(stats.units) == 2
+    before = c.snapshot()
+    plan_b, st = c.switch_layouts(lay[2], lay[1])
+    want = check.expected_after(c, before, c.records(plan_b, validate=False))
+    assert not any(check.compare(c.snapshot(), want).values())
+    assert c.placement() == M.layout_placement(lay[1]) and int(c.status.item()) == 0
+
+
 @pytest.mark.parametrize("tp_old,tp_new", [(16, 1), (1, 16), (4, 16), (16, 2)])
 def test_sixteen_slots_bit_exact(tp_old, tp_new):
     # TPR_MAX_GPUS = 16 slots (16 KV heads so TP16 is a valid KvLayout)
