@@ -675,33 +675,49 @@ static const BulkConfig& k1_config() {
   static BulkConfig c = parse_bulk("TPR_BULK_K1", BulkConfig{6, 32768});
   return c;
 }
+// Short K1s (up to 24 items per SM, ~110 MiB) finish sooner with more,
+// shallower rings: 3 x 32 KiB (2 CTAs/SM) moves one-sequence switches 5-19%
+// faster, while 6 x 32 KiB stays ahead from cfg1 (4096 items, 27.7 per SM) up
+// (profiles/ab/r01_k1small_*).
+static const BulkConfig& k1_small_config() {
+  static BulkConfig c = parse_bulk("TPR_BULK_K1_SMALL", BulkConfig{3, 32768});
+  return c;
+}
+static int64_t k1_small_items() {
+  static const int64_t v = [] {
+    const char* e = getenv("TPR_K1_SMALL_ITEMS_PER_SM");
+    return (int64_t)(e ? atoll(e) : 24) * sm_count();
+  }();
+  return v;
+}
 static const BulkConfig& k2_config() {
   static BulkConfig c = parse_bulk("TPR_BULK_K2", BulkConfig{3, 32768});
   return c;
 }
 
 static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items, int threads) {
-  // attribute + occupancy per (kernel, device) are fixed: set/query once (the
-  // occupancy query costs microseconds of host time per small switch)
-  static thread_local const void* done_fn[8] = {nullptr};
-  static thread_local int done_dev[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
-  static thread_local int done_occ[8] = {0};
+  // attribute + occupancy per (kernel, device, ring size) are fixed: set/query
+  // once (the occupancy query costs microseconds of host time per small switch)
+  struct Entry {
+    const void* fn;
+    int dev, smem, occ;
+  };
+  static thread_local Entry done[16];
+  static thread_local int n_done = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   int per_sm = 0;
-  for (int i = 0; i < 8; ++i)
-    if (done_fn[i] == fn && done_dev[i] == dev) per_sm = done_occ[i];
+  for (int i = 0; i < n_done; ++i)
+    if (done[i].fn == fn && done[i].dev == dev && done[i].smem == c.smem()) per_sm = done[i].occ;
   if (per_sm == 0) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem());
+    // the attribute is an upper bound: keep the largest ring this kernel uses
+    int attr = c.smem();
+    for (int i = 0; i < n_done; ++i)
+      if (done[i].fn == fn && done[i].dev == dev && done[i].smem > attr) attr = done[i].smem;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, attr);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, c.smem());
     if (per_sm < 1) per_sm = 1;
-    for (int i = 0; i < 8; ++i)
-      if (done_fn[i] == nullptr) {
-        done_fn[i] = fn;
-        done_dev[i] = dev;
-        done_occ[i] = per_sm;
-        break;
-      }
+    if (n_done < 16) done[n_done++] = Entry{fn, dev, c.smem(), per_sm};
   }
   int64_t grid = (int64_t)sm_count() * per_sm;
   if (items < grid) grid = items;
@@ -749,7 +765,8 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
                            const tpr_kv_geometry_t* geo, int n_gpus, bool partial) {
   if (n_units <= 0) return cudaSuccess;
 
-  const BulkConfig& c = k1_config();
+  const BulkConfig& c = n_units * p.items_per_unit <= k1_small_items() ? k1_small_config()
+                                                                        : k1_config();
   KvTensorMaps tm;
   tm.enabled = 0;
   if (geo && (partial || tensor_kernel_always())) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
