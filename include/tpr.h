@@ -114,8 +114,8 @@ int tpr_get_copy_engine(void);
  *   "k3_fuse_units" [TPR_K3_FUSE_UNITS, 4096]: plans up to this many units
  *                   run K3 as one fused CTA (scan + remap), 0 = never;
  *   "pdl"           [TPR_PDL, 1]: programmatic dependent launch of K3b / K1:
- *                   0 never, 1 plans up to k3_fuse_units (a large K1 whose
- *                   CTAs start early leaves a tail), 2 every plan;
+ *                   0 never, 1 plans up to k3_fuse_units, 2 every plan
+ *                   (neutral on large plans with dynamic claims);
  *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place;
  *   "k1_dynamic"    [TPR_K1_DYNAMIC, 1]: K1 CTAs claim batches of items (1: 4 per
  *                   claim, n >= 2: n per claim, 0: static shares) from
@@ -125,7 +125,10 @@ int tpr_get_copy_engine(void);
  *                   pages as TMA tensor boxes (token x planes) instead of
  *                   one short copy per plane: 0 never, 1 when a page of the
  *                   plan is partial, 2 the tensor kernel for every plan.
- * tpr_get_tuning returns the current value, -1 for an unknown key. */
+ * tpr_get_tuning returns the current value, -1 for an unknown key.
+ * Read once from the environment (TMA engine ring shapes, "<stages>x<bytes>"):
+ *   TPR_BULK_K1 [6x32768], TPR_BULK_K2 [3x32768], TPR_BULK_K1_SMALL [3x32768]
+ *   for K1s of at most TPR_K1_SMALL_ITEMS_PER_SM [24] items per SM. */
 int tpr_set_tuning(const char* key, int64_t value);
 int64_t tpr_get_tuning(const char* key);
 int tpr_version(void);
