@@ -108,7 +108,9 @@ def main():
                 cluster.switch_layouts(x, y, stream=stream, validate=False)
             torch.cuda.synchronize()
             dev_ms, host_ms, exec_ms, plan_ms = [], [], [], []
-            for r in range(args.reps):
+            # short switches are host/latency-bound and jittery: more repetitions
+            reps = args.reps if fwd.total_bytes >= (256 << 20) else max(args.reps, 24)
+            for r in range(reps):
                 a_b = (la, lb) if r % 2 == 0 else (lb, la)
                 t0 = time.perf_counter()  # the planner alone (host), for the split
                 M.plan_repartition(*a_b, kv.kv_bytes_per_token_per_head)
@@ -124,7 +126,7 @@ def main():
                 e1.synchronize()
                 host_ms.append((time.perf_counter() - t0) * 1e3)
                 dev_ms.append(e0.elapsed_time(e1))
-            for r in range(args.reps, 2 * args.reps):  # device work alone: stream held
+            for r in range(reps, 2 * reps):  # device work alone: stream held
                 a_b = (la, lb) if r % 2 == 0 else (lb, la)  # while the host enqueues
                 e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
                 torch.cuda._sleep(400_000)
