@@ -117,6 +117,8 @@ int tpr_get_copy_engine(void);
  *                   0 never, 1 plans up to k3_fuse_units, 2 every plan
  *                   (neutral on large plans with dynamic claims);
  *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place;
+ *   "bulk_ws"       [TPR_BULK_WS, 0]: TMA engine with a producer and a consumer
+ *                   warp per CTA instead of one issuing thread;
  *   "k1_dynamic"    [TPR_K1_DYNAMIC, 1]: K1 CTAs claim batches of items (1: 4 per
  *                   claim, n >= 2: n per claim, 0: static shares) from
  *                   the counter after the work list instead of a static
