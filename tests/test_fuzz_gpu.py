@@ -4,6 +4,8 @@ partitions of 8 GPU slots (mixed TP levels in one config), with pools small
 enough that capacity errors happen. A rejected operation must leave device
 state untouched."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -40,7 +42,13 @@ def same_state(a, b):
             and a["ring_head"] == b["ring_head"] and a["ring_tail"] == b["ring_tail"])
 
 
-@pytest.mark.parametrize("seed,one_call", [(0, False), (1, False), (2, False), (3, True), (4, True)])
+# TPR_FUZZ_SEEDS=n widens the campaign to n seeds (alternating launch paths)
+_N = int(os.environ.get("TPR_FUZZ_SEEDS", "5"))
+SEEDS = [(0, False), (1, False), (2, False), (3, True), (4, True)] + \
+    [(s, s % 2 == 1) for s in range(5, _N)]
+
+
+@pytest.mark.parametrize("seed,one_call", SEEDS)
 def test_random_walk(seed, one_call):
     rng = np.random.default_rng(seed)
     c = PagedKvCluster(KV, GPUS, units_per_gpu=128, max_requests=24, max_blocks=32,
