@@ -115,4 +115,6 @@ def test_random_walk(seed, one_call):
         v = c.verify(seed=7)
         assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0, (step, v)
         assert c.placement() == M.layout_placement(cur)
-    assert stats["switch"] >= 5 and stats["admit"] >= 3, stats
+    if seed < 5:  # the fixed seeds are chosen to cover every operation; a wider
+        # campaign (TPR_FUZZ_SEEDS) checks correctness only: some walks mostly hit capacity
+        assert stats["switch"] >= 5 and stats["admit"] >= 3, stats
