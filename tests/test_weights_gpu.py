@@ -189,3 +189,31 @@ def test_llama8b_tp2_tp4_full_size():
     assert s.remote_bytes == 2 * split // 4 and s.views == 2
     assert store.verify() == 0
     store.finish()
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TPR_FUZZ_SEEDS", "4"))))
+def test_random_reshard_walk(seed):
+    # random partitions of 8 GPUs into groups of mixed TP degree, in random
+    # rank order, with and without trim: after every reshard each GPU's shard
+    # equals the oracle's slice of the matrix reassembled from the old shards
+    rng = np.random.default_rng(seed)
+    gpus = tuple(range(8))
+
+    def random_groups():
+        perm = [int(g) for g in rng.permutation(gpus)]
+        out, i = [], 0
+        while i < 8:
+            s = int(rng.choice([x for x in (1, 2, 4, 8) if i + x <= 8]))
+            out.append(tuple(perm[i:i + s]))
+            i += s
+        return out
+
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load(random_groups())
+    for step in range(8):
+        pieces = host_pieces(store)
+        groups = random_groups()
+        store.reshard(groups, trim=bool(rng.integers(2)))
+        torch.cuda.synchronize()
+        check_against_oracle(store, pieces, groups)
+        assert store.verify() == 0, step
