@@ -144,3 +144,49 @@ def test_measured_switch_cost_adapter():
     ms = cost(M.WARM, M.plan_repartition(old, new, KV.kv_bytes_per_token_per_head), M.CostModelParams())
     assert ms > 0
     assert kv.placement() == M.layout_placement(new)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TPR_FUZZ_SEEDS", "3"))))
+def test_random_switch_walk_kv_and_weights(seed):
+    # the executor between random partitions of 8 GPUs (mixed TP degrees,
+    # random rank order), requests redistributed at random, KV and weights in
+    # one switch, one or two streams: KV bit-exact vs the oracle replay,
+    # weights verified, placement = layout_placement(new)
+    import numpy as np
+    from test_weights_gpu import check_against_oracle, host_pieces
+    rng = np.random.default_rng(seed)
+    gpus = tuple(range(8))
+    reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 90, size=20))]
+
+    def random_layouts():
+        perm = [int(g) for g in rng.permutation(gpus)]
+        groups, i = [], 0
+        while i < 8:
+            s = int(rng.choice([x for x in (1, 2, 4, 8) if i + x <= 8]))
+            groups.append(tuple(perm[i:i + s]))
+            i += s
+        per = [[] for _ in groups]
+        for r in reqs:
+            per[int(rng.integers(len(groups)))].append(r)
+        return groups, [M.KvLayout(g, len(g), 8, tuple(p)) for g, p in zip(groups, per)]
+
+    groups, cur = random_layouts()
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=1024, max_requests=20, max_blocks=16, fragmented=True,
+                        seed=seed)
+    kv.admit(cur, seed=3)
+    store = ShardedWeightStore(MODEL, gpus)
+    store.load(groups)
+    ex = ReconfigurationExecutor(kv, store, overlap=bool(seed % 2))
+    for step in range(10):
+        groups, new = random_layouts()
+        before = kv.snapshot()
+        pieces = host_pieces(store)
+        plan = M.plan_repartition(cur, new, KV.kv_bytes_per_token_per_head)
+        rec = kv.records(plan, validate=False)
+        res = ex.switch(cur, new, new_weight_groups=groups, trim=bool(rng.integers(2)))
+        assert res.status == 0 and res.kv.bytes == plan.total_bytes, step
+        diff = check.compare(kv.snapshot(), check.expected_after(kv, before, rec))
+        assert not any(diff.values()), (step, diff)
+        check_against_oracle(store, pieces, groups)
+        assert store.verify() == 0 and kv.placement() == M.layout_placement(new)
+        cur = new
