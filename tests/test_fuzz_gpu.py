@@ -15,10 +15,12 @@ from paper_2605_05467_b200.kvcache import PagedKvCluster
 
 pytestmark = pytest.mark.gpu
 
-# TPR_FUZZ_GEOMETRY=8b runs the walks on Llama-3.1-8B pages (256 KiB, 64 planes,
-# partial pages as TMA tensor boxes) instead of the tiny default
-KV = (geometry.LLAMA_3_1_8B.kv if os.environ.get("TPR_FUZZ_GEOMETRY") == "8b" else
-      geometry.KvGeometry(layers=1, head_dim=16, total_heads=8, block_tokens=4))
+# TPR_FUZZ_GEOMETRY=8b|70b runs the walks on Llama-3.1 pages (8B: 256 KiB, 64
+# planes; 70B: 640 KiB, 160 planes; partial pages as TMA tensor boxes) instead
+# of the tiny default
+KV = {"8b": geometry.LLAMA_3_1_8B.kv, "70b": geometry.LLAMA_3_1_70B.kv}.get(
+    os.environ.get("TPR_FUZZ_GEOMETRY", ""),
+    geometry.KvGeometry(layers=1, head_dim=16, total_heads=8, block_tokens=4))
 GPUS = tuple(range(8))
 
 
