@@ -13,7 +13,7 @@ import sys
 from pathlib import Path
 
 T = sys.argv[1]
-R = Path("/root/repo")
+R = Path(__file__).resolve().parent.parent
 G = R / "gpurun_out"
 P = R / "profiles"
 
