@@ -195,7 +195,10 @@ def setup_ours(w, device, overlap=None, weights_mode="sharded", fragmented=True)
     cluster.admit(w.old, seed=1234)
     store = None
     if w.old_weight_groups is not None:
-        store = ShardedWeightStore(w.model, w.gpus, device=device, mode=weights_mode)
+        # every GPU's arena window holds its largest shard of the workload, so
+        # growing shards fetch only their missing slices, in place
+        store = ShardedWeightStore(w.model, w.gpus, device=device, mode=weights_mode,
+                                   max_slices=cpu_windows(w))
         store.load(w.old_weight_groups)
     torch.cuda.synchronize()
     return ReconfigurationExecutor(cluster, store, time_kernels=True, overlap=overlap)
@@ -239,23 +242,47 @@ def one_switch(ex, w, forward: bool, sync: bool):
 # CPU reference path (oracle restatement; test infrastructure)
 # ---------------------------------------------------------------------------
 
+def reference_planner():
+    """The reference's own ``tpsim.migration`` from ``baseline/_ref`` (the
+    unmodified reference, installed by build() from /root/reference), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "tpsim" / "migration.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import tpsim.migration as RM  # noqa: N813
+    return RM
+
+
 class CpuReference:
-    """The reference's CPU path restated: pure-Python planner (as the
-    reference's plan_repartition) + C restatement of page movement and weight
-    slicing on host memory, all host threads. Bounded sample of the workload."""
+    """The reference's CPU path for one switch of the workload, on host memory:
+
+    * the plan from the reference's OWN planner, ``tpsim.migration.
+      plan_repartition`` of the unmodified reference (baseline/_ref; the
+      restatement oracle/plan_oracle.py only when it is absent), timed apart
+      as ``planner_ms``;
+    * page movement and weight slicing: the reference has no KV or weight bytes,
+      so these run as the C restatement (oracle/kvmove.c), all host threads.
+
+    ``sample_seqs`` < all runs a bounded sample (the same share of every weight
+    slice) when the full workload does not fit the host's free memory."""
 
     def __init__(self, w, sample_seqs: int, threads: int):
         from oracle import kvmove, plan_oracle
-        from paper_2605_05467_b200 import workloads
         self.kvmove, self.po = kvmove, plan_oracle
         kvmove.build()
+        self.RM = reference_planner()
         self.threads = threads
         reqs = w.requests[:sample_seqs]
         groups_old = [lay.group for lay in w.old]
         groups_new = [lay.group for lay in w.new]
         H = w.model.n_kv_heads
-        self.old = [(g, H, r) for g, r in zip(groups_old, _rr(groups_old, reqs))]
-        self.new = [(g, H, r) for g, r in zip(groups_new, _rr(groups_new, reqs))]
+        self.H = H
+        self.old = [(g, H, r) for g, r in zip(groups_old, _split(w.old, reqs))]
+        self.new = [(g, H, r) for g, r in zip(groups_new, _split(w.new, reqs))]
+        if self.RM is not None:
+            mk = lambda lays: [self.RM.KvLayout(tuple(g), len(g), H, tuple(r)) for g, _, r in lays]
+            self.ref_old, self.ref_new = mk(self.old), mk(self.new)
         kv = w.model.kv
         self.kv = kv
         self.kvb = kv.kv_bytes_per_token_per_head
@@ -263,19 +290,12 @@ class CpuReference:
         self.rslot = {rid: i for i, (rid, _) in enumerate(reqs)}
         self.ctx = dict(reqs)
         max_blocks = max(kv.blocks(c) for _, c in reqs)
-        need = {g: 0 for g in w.gpus}
-        for lays in (self.old, self.new):
-            for grp, _, rr in lays:
-                per = H // len(grp)
-                for _, c in rr:
-                    for gg in grp:
-                        need[gg] += per * kv.blocks(c)
-        units = [need[g] + 16 for g in w.gpus]
+        units = cpu_units(w, reqs)
         self.geo = dict(layers=kv.layers, head_dim=kv.head_dim, dtype_bytes=kv.dtype_bytes,
                         block_tokens=kv.block_tokens, total_heads=H, max_blocks=max_blocks,
                         n_req_slots=len(reqs), n_units=max(units))
         n = len(w.gpus)
-        self.pools = [np.ones(u * kv.unit_bytes, np.uint8) for u in units]
+        self.pools = [kvmove.filled(u * kv.unit_bytes, 1, threads) for u in units]
         self.tables = [np.full(len(reqs) * H * max_blocks, -1, np.int32) for _ in range(n)]
         rng = np.random.default_rng(0)
         self.rings = [rng.permutation(u).astype(np.int32) for u in units]
@@ -288,19 +308,25 @@ class CpuReference:
                 for r, g in enumerate(grp):
                     adm.append((-1, self.slot[g], self.rslot[rid], r * per, (r + 1) * per, c))
         self._exec(np.asarray(adm, np.int64))
-        # weights: the same 1/`frac` share of every slice copy as the GPU arm
+        # weights: every GPU holds whole slices (one host buffer per slice, the
+        # `frac` share of its bytes); a switch fetches exactly the slices the
+        # GPU arm's K2 fetches (cpu_weight_moves), copied from a holder
         self.frac = sample_seqs / len(w.requests)
-        self.w = w
         self.wbytes_slice = None
         if w.old_weight_groups is not None:
             from paper_2605_05467_b200.weights import groups_ranges
-            split = [m for m in w.model.matrices if m.split != "rep"]
-            per_slice = sum((m.rows * m.cols) // 8 for m in split) * w.model.dtype_bytes
-            self.wbytes_slice = max(int(per_slice * self.frac) // 64 * 64, 64)
-            self.ranges = {True: groups_ranges(w.new_weight_groups), False: groups_ranges(w.old_weight_groups)}
-            self.res = dict(groups_ranges(w.old_weight_groups))
-            self.arena = {g: np.ones((b - a) * self.wbytes_slice, np.uint8) for g, (a, b) in self.res.items()}
+            self.wbytes_slice = cpu_slice_bytes(w, self.frac)
+            self.ranges = {True: groups_ranges(w.new_weight_groups),
+                           False: groups_ranges(w.old_weight_groups)}
+            self.trim = {True: False, False: w.trim_on_reverse}
+            self.parked = {True: set(w.parked), False: set()}
+            m = cpu_windows(w)
+            old = self.ranges[False]
+            self.win = {g: _window(*old[g], m[g]) for g in w.gpus}
+            self.held = {g: {sl: kvmove.filled(self.wbytes_slice, 1, threads)
+                             for sl in range(*old[g])} for g in w.gpus}
         self.fwd = True
+        self.planner_s = 0.0
 
     def _exec(self, rec):
         n, status, self.head, self.tail = self.kvmove.kv_migrate(
@@ -308,43 +334,120 @@ class CpuReference:
         assert status == 0
         return n
 
+    def plan(self):
+        """(src, dst, request, lo, hi, bytes) rows of this step's switch, from the
+        reference's plan_repartition (timed)."""
+        t0 = time.perf_counter()
+        if self.RM is not None:
+            src, dst = (self.ref_old, self.ref_new) if self.fwd else (self.ref_new, self.ref_old)
+            plan = self.RM.plan_repartition(src, dst, self.kvb)
+            moves = [(t.src_gpu, t.dst_gpu, t.request_id, t.head_lo, t.head_hi, t.bytes)
+                     for t in plan.transfers]
+        else:
+            src, dst = (self.old, self.new) if self.fwd else (self.new, self.old)
+            moves = self.po.plan(src, dst, self.kvb)
+        self.planner_s += time.perf_counter() - t0
+        return moves
+
     def step(self) -> int:
         """One switch of the sample; returns bytes moved."""
-        src, dst = (self.old, self.new) if self.fwd else (self.new, self.old)
-        moves = self.po.plan(src, dst, self.kvb)
+        moves = self.plan()
         rec = np.array([(self.slot[s], self.slot[d], self.rslot[r], lo, hi, self.ctx[r])
                         for s, d, r, lo, hi, _ in moves], np.int64).reshape(-1, 6)
         self._exec(rec)
         moved = sum(m[5] for m in moves)
         if self.wbytes_slice:
-            moved += self._weights(self.ranges[self.fwd])
+            moved += self._weights(self.fwd)
         self.fwd = not self.fwd
         return moved
 
-    def _weights(self, act) -> int:
-        blocks, moved, new_arena = [], 0, {}
-        for g, (x, y) in act.items():
-            a, b = self.res[g]
-            if a <= x and y <= b:
-                continue
-            buf = np.empty((y - x) * self.wbytes_slice, np.uint8)
-            for s in range(x, y):
-                if a <= s < b:
-                    h, ha = g, a
-                else:
-                    h = next(k for k, (p, q) in self.res.items() if p <= s < q and k != g)
-                    ha = self.res[h][0]
-                blocks.append((buf, (s - x) * self.wbytes_slice, self.arena[h],
-                               (s - ha) * self.wbytes_slice, 1, self.wbytes_slice,
-                               self.wbytes_slice, self.wbytes_slice))
-                moved += self.wbytes_slice
-            new_arena[g] = (buf, (x, y))
+    def _weights(self, fwd: bool) -> int:
+        moves, self.win, keep = cpu_weight_step(self.held, self.win, self.ranges[fwd],
+                                                self.parked[fwd], self.trim[fwd])
+        blocks, new = [], {}
+        for g, sl, h in moves:
+            buf = np.empty(self.wbytes_slice, np.uint8)
+            new.setdefault(g, {})[sl] = buf
+            blocks.append((buf, 0, self.held[h][sl], 0, 1, self.wbytes_slice, self.wbytes_slice,
+                           self.wbytes_slice))
         if blocks:
             self.kvmove.copy_blocks(blocks, self.threads)
-        for g, (buf, r) in new_arena.items():
-            self.arena[g] = buf
-            self.res[g] = r
-        return moved
+        for g in self.held:
+            self.held[g] = {sl: b for sl, b in self.held[g].items() if sl in keep[g]}
+            self.held[g].update(new.get(g, {}))
+        return len(moves) * self.wbytes_slice
+
+
+def cpu_windows(w) -> dict:
+    """Arena window (slices) of every GPU: the largest shard it takes in the
+    workload (the bench's max_slices for the GPU arm)."""
+    from paper_2605_05467_b200.weights import groups_ranges
+    out = {g: 1 for g in w.gpus}
+    for groups in (w.old_weight_groups, w.new_weight_groups):
+        for g, (a, b) in groups_ranges(groups).items():
+            out[g] = max(out[g], b - a)
+    return out
+
+
+def _window(x: int, y: int, m: int):
+    m = max(m, y - x)
+    return (x // m) * m, m
+
+
+def cpu_weight_step(held: dict, win: dict, act: dict, parked: set, trim: bool):
+    """The slice-level rules of ShardedWeightStore.plan restated on host slice
+    buffers: a shard inside its GPU's window keeps every held slice (only the
+    shard's with ``trim``), one that leaves it starts a new window; every
+    missing slice of the new shard is fetched from the least-loaded holder.
+    Returns (moves [(gpu, slice, holder)], new windows, kept slices)."""
+    order = list(held)
+    egress = {g: 0 for g in order}
+    moves, keep, new_win = [], {}, dict(win)
+    for g in order:
+        if g in parked or g not in act:
+            keep[g] = set(held[g])
+            continue
+        x, y = act[g]
+        w0, m = win[g]
+        if w0 <= x and y <= w0 + m:
+            keep[g] = (set(range(x, y)) & set(held[g])) if trim else set(held[g])
+        else:
+            new_win[g] = _window(x, y, m)
+            keep[g] = set(range(x, y)) & set(held[g])
+        for sl in range(x, y):
+            if sl in held[g]:
+                continue
+            h = min((k for k in order if k != g and sl in held[k]),
+                    key=lambda k: (egress[k], order.index(k)))
+            egress[h] += 1
+            moves.append((g, sl, h))
+    return moves, new_win, keep
+
+
+def cpu_slice_bytes(w, frac: float) -> int:
+    split = [m for m in w.model.matrices if m.split != "rep"]
+    per_slice = sum((m.rows * m.cols) // 8 for m in split) * w.model.dtype_bytes
+    return max(int(per_slice * frac) // 64 * 64, 64)
+
+
+def cpu_units(w, reqs) -> list:
+    """Pool units per slot for the CPU sample: resident + incoming at the peak
+    of either switch direction (bench.capacity_units on the sample)."""
+    H = w.model.n_kv_heads
+    kv = w.model.kv
+    rid = {r for r, _ in reqs}
+    from paper_2605_05467_b200.migration import KvLayout
+    sub = lambda lays: [KvLayout(l.group, l.tp, H, tuple(r for r in l.requests if r[0] in rid))
+                        for l in lays]
+    ws = type(w)(w.name, w.model, w.gpus, sub(w.old), sub(w.new), None, None)
+    cap = capacity_units(ws, kv)
+    return [cap[g] for g in w.gpus]
+
+
+def _split(layouts, reqs):
+    """The sample's requests, grouped like ``layouts``."""
+    rid = {r for r, _ in reqs}
+    return [[r for r in lay.requests if r[0] in rid] for lay in layouts]
 
 
 def _rr(groups, reqs):
@@ -371,34 +474,57 @@ def cpu_model() -> str:
     return "unknown"
 
 
-CPU_SAMPLE_KV_BYTES = 4 << 30  # resident KV of the CPU sample (host RAM bound)
+def cpu_host_bytes(w, n_seqs: int) -> int:
+    """Host bytes the CPU arm holds for ``n_seqs`` of the workload: KV pools at
+    their peak plus the weight slices of the largest shards (whole model at
+    most)."""
+    reqs = w.requests[:n_seqs]
+    kv = sum(cpu_units(w, reqs)) * w.model.kv.unit_bytes
+    if w.old_weight_groups is None:
+        return kv
+    frac = n_seqs / len(w.requests)
+    m = cpu_windows(w)
+    return kv + int(sum(min(2 * x, 8) for x in m.values()) * cpu_slice_bytes(w, frac))
 
 
-def cpu_sample_seqs(w, requested: int) -> int:
-    """At most `requested` sequences and at most ~4 GiB of resident KV."""
-    kvb = w.model.kv.kv_bytes_per_token_per_head * w.model.n_kv_heads
-    per_seq = max(kvb * c for _, c in w.requests)
-    return max(1, min(requested, len(w.requests), CPU_SAMPLE_KV_BYTES // per_seq))
+def cpu_sample_seqs(w, requested: int | None, budget_frac: float = 0.45) -> int:
+    """The whole workload (``requested`` None) when it fits ``budget_frac`` of
+    the host's available memory, else the largest sample that does."""
+    import psutil
+    n = len(w.requests) if not requested else min(requested, len(w.requests))
+    budget = psutil.virtual_memory().available * budget_frac
+    while n > 1 and cpu_host_bytes(w, n) > budget:
+        n = max(1, int(n * budget / cpu_host_bytes(w, n)) if n > 8 else n - 1)
+    return n
 
 
-def run_cpu_reference(w, steps: int, warmup: int, sample_seqs: int, min_seconds: float = 0.0):
-    """Time the CPU restatement: `steps` switches of the sample, continuing
-    until at least `min_seconds` of CPU work have been timed."""
+def run_cpu_reference(w, steps: int, warmup: int, sample_seqs: int | None = None,
+                      min_seconds: float = 0.0):
+    """Time the reference's CPU path: `steps` switches of the workload (or of a
+    sample when the host cannot hold it), continuing until at least
+    `min_seconds` of CPU work have been timed."""
     sample_seqs = cpu_sample_seqs(w, sample_seqs)
     threads = cpu_threads()
     ref = CpuReference(w, sample_seqs, threads)
     for _ in range(warmup):
         ref.step()
+    ref.planner_s = 0.0
     t0 = time.perf_counter()
     moved = done = 0
     while done < steps or time.perf_counter() - t0 < min_seconds:
         moved += ref.step()
         done += 1
     dt = time.perf_counter() - t0
+    full = sample_seqs == len(w.requests)
+    what = "the whole workload" if full else (
+        f"{sample_seqs} of {len(w.requests)} seqs (+ the same share of every weight slice)")
+    planner = ("reference tpsim.migration.plan_repartition (baseline/_ref, unmodified)"
+               if ref.RM is not None else "restatement oracle/plan_oracle.py")
     return {"value": moved / dt / 1e9, "ms_per_step": dt / done * 1e3, "bytes": moved,
-            "threads": threads, "seconds": dt,
-            "sample": f"{sample_seqs} of {len(w.requests)} seqs (+ the same share of every "
-                      f"weight slice copy), {done} alternating switches, {dt:.1f} s timed"}
+            "threads": threads, "seconds": dt, "same_config": full,
+            "planner": planner, "planner_ms": ref.planner_s / done * 1e3,
+            "sample": f"{what}, {done} alternating switches, {dt:.1f} s timed; plan: {planner}, "
+                      "pages + weight slices: oracle/kvmove.c on all host threads"}
 
 
 # ---------------------------------------------------------------------------
@@ -456,12 +582,9 @@ def run_distributed(args, w, rank: int, world: int, local: int):
     # NCCL carries the control plane (IPC-handle exchange, optional handshake)
     # when every rank has its own GPU; ranks that share a device use gloo
     backend = "nccl" if n_dev >= world else "gloo"
-    if n_dev >= world and not args.engine:
-        # TMA bulk copies into/out of peer mappings over NVLink have not been
-        # validated on multi-GPU hardware yet (every box here has one GPU);
-        # across devices use the 16-B vector engine, which is plain ld/st
-        from paper_2605_05467_b200 import _native
-        _native.set_copy_engine("vector")
+    # libtpr picks the copy engine per pointer: peer pools / arenas on other
+    # GPUs take the 16-byte vector engine (the TMA engine is validated on local
+    # HBM only), so no override is needed here
     dist.init_process_group(backend, timeout=datetime.timedelta(minutes=10),
                             **({"device_id": device} if backend == "nccl" else {}))
     kv = w.model.kv
@@ -471,8 +594,7 @@ def run_distributed(args, w, rank: int, world: int, local: int):
                               max_requests=len(w.requests), max_blocks=kv.blocks(max_ctx),
                               device=device, fragmented=True, seed=rank)
     cl.admit(w.old, seed=1234)
-    slices = max(8 // len(g) for g in (w.old_weight_groups or [()]) + (w.new_weight_groups or [()]) if g)
-    ws = DistributedWeightStore(w.model, w.gpus, device=device, max_slices=slices)
+    ws = DistributedWeightStore(w.model, w.gpus, device=device, max_slices=cpu_windows(w))
     ws.load(w.old_weight_groups)
     # ranks sharing one device are time-sliced, so a spinning device barrier
     # would wait for a context switch; use the host barrier there
@@ -523,7 +645,7 @@ def run_distributed(args, w, rank: int, world: int, local: int):
             # this rank's kernels: 2 device barriers, K3 (+ K1) over its pushes, K2 pull
             launches += (2 if ex.barrier is not None else 0) + _native.kv_switch_launches(ks.units) \
                 + (1 if wst and wst.segments else 0)
-            h2d += len(plan) * 24 + (wst.segments * 72 + 8 if wst and wst.segments else 0)
+            h2d += plan.n_transfers * 24 + (wst.segments * 72 + 8 if wst and wst.segments else 0)
         wall = time.perf_counter() - t0
         clk.stop()
         dist.barrier()
@@ -573,6 +695,116 @@ def run_distributed(args, w, rank: int, world: int, local: int):
 # main
 # ---------------------------------------------------------------------------
 
+def measure_single(args, w, device, cpu: bool, e2e_on: bool = True) -> dict:
+    """One GPU, logical ranks: the device-timed switches, the end-to-end public
+    call, the full-size correctness property and (``cpu``) the reference's CPU
+    path on the same workload. Returns the JSON fields."""
+    import torch
+    from paper_2605_05467_b200 import _native
+    from paper_2605_05467_b200.controller import host_to_device_bytes
+
+    ex = setup_ours(w, device, overlap={"auto": None, "on": True, "off": False}[args.overlap],
+                    weights_mode=args.weights_mode, fragmented=args.pool_layout == "fragmented")
+    fwd = True
+    for _ in range(max(args.warmup, 1)):
+        one_switch(ex, w, fwd, sync=True)
+        fwd = not fwd
+
+    # ---- device-timed region: K switches enqueued back to back --------------
+    main_stream = torch.cuda.current_stream(device)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(device.index if device.index is not None else 0) as clk:
+        torch.cuda.synchronize()
+        clk.start()
+        start.record(main_stream)
+        for _ in range(args.steps):
+            results.append(one_switch(ex, w, fwd, sync=False))
+            fwd = not fwd
+        end.record(main_stream)
+        torch.cuda.synchronize()
+        clk.stop()
+    ms = start.elapsed_time(end)
+    kv_bytes = sum(r.kv.bytes for r in results)
+    w_bytes = sum(r.weights.bytes for r in results if r.weights)
+    w_local = sum(r.weights.local_bytes for r in results if r.weights)
+    total_bytes = kv_bytes + w_bytes
+    k1_ms = [r.events["k1_start"].elapsed_time(r.events["k1_end"]) for r in results]
+    k2_ms = [r.events["k2_start"].elapsed_time(r.events["k2_end"]) for r in results
+             if r.weights is not None and r.weights.segments]
+    launches = sum(_native.kv_switch_launches(r.kv.units)
+                   + (1 if r.weights is not None and r.weights.segments else 0) for r in results)
+    status = int(ex.kv.status.item())
+
+    # ---- end to end through the public API (host layouts -> device -> status) --
+    e2e = None
+    if e2e_on:
+        torch.cuda.synchronize()
+        ex.time_kernels = False  # the production call: plan + K3 + K1 in one native call
+        t0 = time.perf_counter()
+        eb, h2d = 0, 0
+        for _ in range(args.steps):
+            r = one_switch(ex, w, fwd, sync=True)
+            fwd = not fwd
+            eb += r.bytes
+            h2d += host_to_device_bytes(r.plan, r.weights)
+            status |= r.status
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": eb / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s / args.steps * 1e3,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": 4}
+
+    # ---- after the timed regions: full-size correctness of the final state ----
+    # every owned page carries its placement-invariant pattern, every block-table
+    # entry realises the host placement, every weight shard equals its slice
+    vkv = ex.kv.verify()
+    vw = ex.weights.verify() if ex.weights is not None else 0
+    bit_exact = (vkv["placement_errors"] == 0 and vkv["word_mismatches"] == 0
+                 and vkv["status"] == 0 and vw == 0 and status == 0)
+    overlap = ex.overlap
+    del ex, results
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+
+    hbm, hbm_src = peaks()
+    k1_avg = float(np.mean(k1_ms))
+    kv_per_step = kv_bytes / args.steps
+    achieved = 2 * kv_per_step / (k1_avg * 1e-3) / 1e9  # HBM read + write GB/s
+    # DRAM bytes of one K1 launch of this workload from this round's ncu --set
+    # full capture (tools/ncu_traffic.py writes the file from the raw CSV)
+    traffic = None
+    prof = ROOT / "profiles" / "k1_traffic.json"
+    if prof.exists():
+        try:
+            tj = json.loads(prof.read_text())
+            if tj.get("workload") == w.name:
+                traffic = tj.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    cpu = None
+    if cpu:
+        r = run_cpu_reference(w, 2, 1, args.cpu_sample_seqs, min_seconds=args.cpu_seconds)
+        cpu = {"value": r["value"], "unit": "GB/s", "cores": r["threads"], "kind": "port",
+               "sample": r["sample"], "cpu": cpu_model(), "ms_per_step": r["ms_per_step"],
+               "same_config": r["same_config"], "planner": r["planner"],
+               "planner_ms": r["planner_ms"]}
+    return {
+        "ms": ms, "value": total_bytes / (ms * 1e-3) / 1e9, "kv_per_step": kv_per_step,
+        "w_per_step": w_bytes / args.steps, "w_local_per_step": w_local / args.steps,
+        "w_bytes": w_bytes, "overlap": overlap,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "kernel": k1_kernel_name(w),
+                     "k1_ms": k1_avg, "k2_ms": float(np.mean(k2_ms)) if k2_ms else None,
+                     "peak_source": hbm_src,
+                     # the whole switch (K3 + K1 + K2 + gaps): all bytes read + written
+                     "step_achieved": 2 * total_bytes / args.steps / (ms / args.steps * 1e-3) / 1e9,
+                     "step_frac": 2 * total_bytes / (ms * 1e-3) / 1e9 / hbm},
+        "cpu_baseline": cpu, "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
+        "status": status, "bit_exact_property": bit_exact, "pages_verified": vkv["pages_checked"],
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -581,11 +813,15 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, default=1, help="BASELINE configs[] index (0-based)")
     ap.add_argument("--seqs", type=int, default=None)
-    ap.add_argument("--cpu-sample-seqs", type=int, default=8)
+    ap.add_argument("--cpu-sample-seqs", type=int, default=None,
+                    help="sequences of the CPU arm (default: the whole workload if the host "
+                         "memory holds it)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum timed CPU work of the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-headline", action="store_true",
+                    help="skip the north-star headline (Llama-3.1-8B 8 x 32768 TP2<->TP4)")
     ap.add_argument("--engine", choices=("vector", "bulk"), default=None,
                     help="K1/K2 copy engine (default: the library default)")
     ap.add_argument("--overlap", choices=("auto", "on", "off"), default="auto",
@@ -609,15 +845,17 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        r = run_cpu_reference(w, args.steps, args.warmup, min(args.cpu_sample_seqs, len(w.requests)))
+        r = run_cpu_reference(w, args.steps, args.warmup, args.cpu_sample_seqs)
         line = {
             "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": w.name, "cpu_sample": r["sample"]},
+            "config": {"workload": w.name, "cpu_sample": r["sample"],
+                       "same_config": r["same_config"]},
             "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["threads"],
-                             "kind": "port", "sample": r["sample"], "cpu": cpu_model()},
+                             "kind": "port", "sample": r["sample"], "cpu": cpu_model(),
+                             "planner": r["planner"], "planner_ms": r["planner_ms"]},
             "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
@@ -625,149 +863,55 @@ def main():
         return
 
     import torch
-    import torch.distributed as dist
 
     if world > 1:
         run_distributed(args, w, rank, world, local)
         return
     device = torch.device("cuda", 0)
     torch.cuda.set_device(device)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    ex = setup_ours(w, device, overlap={"auto": None, "on": True, "off": False}[args.overlap],
-                    weights_mode=args.weights_mode, fragmented=args.pool_layout == "fragmented")
-    fwd = True
-    for _ in range(max(args.warmup, 1)):
-        one_switch(ex, w, fwd, sync=True)
-        fwd = not fwd
-
-    # ---- device-timed region: K switches enqueued back to back --------------
-    main_stream = torch.cuda.current_stream(device)
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    results = []
-    with ClockSampler(device.index if device.index is not None else 0) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        clk.start()
-        start.record(main_stream)
-        for _ in range(args.steps):
-            results.append(one_switch(ex, w, fwd, sync=False))
-            fwd = not fwd
-        end.record(main_stream)
-        torch.cuda.synchronize()
-        clk.stop()
-        barrier()
-    ms = start.elapsed_time(end)
-    if world > 1:
-        t = torch.tensor([ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    kv_bytes = sum(r.kv.bytes for r in results)
-    w_bytes = sum(r.weights.bytes for r in results if r.weights)
-    total_bytes = kv_bytes + w_bytes
-    k1_ms = [r.events["k1_start"].elapsed_time(r.events["k1_end"]) for r in results]
-    k2_ms = [r.events["k2_start"].elapsed_time(r.events["k2_end"]) for r in results
-             if r.weights is not None and r.weights.segments]
-    from paper_2605_05467_b200 import _native
-    launches = sum(_native.kv_switch_launches(r.kv.units)
-                   + (1 if r.weights is not None and r.weights.segments else 0) for r in results)
-    status = int(ex.kv.status.item())
-
-    # ---- end to end through the public API (host layouts -> device -> status) --
-    e2e = None
-    if not args.no_e2e:
-        from paper_2605_05467_b200.controller import host_to_device_bytes
-        barrier()
-        torch.cuda.synchronize()
-        ex.time_kernels = False  # the production call: plan + K3 + K1 in one native call
-        t0 = time.perf_counter()
-        eb, h2d = 0, 0
-        for _ in range(args.steps):
-            r = one_switch(ex, w, fwd, sync=True)
-            fwd = not fwd
-            eb += r.bytes
-            h2d += host_to_device_bytes(r.plan, r.weights)
-            status |= r.status
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], device=device, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = {"value": eb * world / e2e_s / 1e9, "unit": "GB/s",
-               "ms_per_step": e2e_s / args.steps * 1e3,
-               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": 4}
-
-    # ---- after the timed regions: full-size correctness of the final state ----
-    # every owned page carries its placement-invariant pattern, every block-table
-    # entry realises the host placement, every weight shard equals its slice
-    vkv = ex.kv.verify()
-    vw = ex.weights.verify() if ex.weights is not None else 0
-    bit_exact = (vkv["placement_errors"] == 0 and vkv["word_mismatches"] == 0
-                 and vkv["status"] == 0 and vw == 0 and status == 0)
-
-    if world > 1:
-        dist.destroy_process_group()
-    if rank != 0:
-        return
-
-    hbm, hbm_src = peaks()
+    m = measure_single(args, w, device, cpu=not args.no_cpu, e2e_on=not args.no_e2e)
     copy_peak = copy_peak_in_run(device)
-    k1_avg = float(np.mean(k1_ms))
-    kv_per_step = kv_bytes / args.steps
-    achieved = 2 * kv_per_step / (k1_avg * 1e-3) / 1e9  # HBM read + write GB/s
-    traffic = None
-    prof = ROOT / "profiles" / "k1_traffic.json"
-    if prof.exists():
-        try:
-            tj = json.loads(prof.read_text())
-            # DRAM bytes of the captured launch: only valid for that workload
-            if tj.get("workload") == w.name:
-                traffic = tj.get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
-    cpu = None
-    if not args.no_cpu:
-        r = run_cpu_reference(w, 2, 1, min(args.cpu_sample_seqs, len(w.requests)),
-                              min_seconds=args.cpu_seconds)
-        cpu = {"value": r["value"], "unit": "GB/s", "cores": r["threads"], "kind": "port",
-               "sample": r["sample"], "cpu": cpu_model()}
-    value = total_bytes * world / (ms * 1e-3) / 1e9
+    m["roofline"]["copy_peak_in_run"] = copy_peak
+    m["roofline"]["frac_vs_copy_in_run"] = m["roofline"]["achieved"] / copy_peak
+    headline = None
+    if not args.no_headline and args.config != 4 and args.seqs is None:
+        # the north star's headline in the same run: Llama-3.1-8B at 32k context
+        wh = build_workload(4, None)
+        h = measure_single(args, wh, device, cpu=not args.no_cpu, e2e_on=True)
+        headline = {
+            "workload": wh.name, "ms_per_switch": h["ms"] / args.steps,
+            "e2e_ms_per_switch": h["e2e"]["ms_per_step"], "gbs": h["value"],
+            "e2e_gbs": h["e2e"]["value"], "kv_bytes_per_step": h["kv_per_step"],
+            "weight_bytes_per_step": h["w_per_step"], "k1_ms": h["roofline"]["k1_ms"],
+            "k1_frac": h["roofline"]["frac"], "step_frac": h["roofline"]["step_frac"],
+            "bit_exact_property": h["bit_exact_property"],
+            "cpu_ms_per_switch": h["cpu_baseline"]["ms_per_step"] if h["cpu_baseline"] else None,
+            "cpu_gbs": h["cpu_baseline"]["value"] if h["cpu_baseline"] else None,
+            "cpu_same_config": h["cpu_baseline"]["same_config"] if h["cpu_baseline"] else None,
+            "cpu_planner_ms": h["cpu_baseline"]["planner_ms"] if h["cpu_baseline"] else None,
+            "cpu_cores": h["cpu_baseline"]["cores"] if h["cpu_baseline"] else None,
+        }
     line = {
-        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "metric": METRIC, "value": m["value"], "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["ms"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
         "config": {
             "workload": w.name, "model": w.model.name, "logical_gpus_per_device": len(w.gpus),
             "seqs": len(w.requests), "ctx": w.requests[0][1],
             "switch": "alternating forward/reverse, full stop-and-migrate (plan+K3+K1+K2)",
-            "k1_k2_overlap": ex.overlap, "copy_engine": _engine_name(),
+            "k1_k2_overlap": m["overlap"], "copy_engine": _engine_name(),
             "weights_mode": args.weights_mode, "pool_layout": args.pool_layout,
-            "kv_bytes_per_step": kv_per_step, "weight_bytes_per_step": w_bytes / args.steps,
-            "weights_note": weights_note(w, w_bytes),
+            "kv_bytes_per_step": m["kv_per_step"], "weight_bytes_per_step": m["w_per_step"],
+            "weight_relayout_bytes_per_step": m["w_local_per_step"],
+            "weights_note": weights_note(w, m["w_bytes"]),
             "l2": "inputs larger than L2 (>= 24 GiB moved per step)",
-            "parallelism": "replicas" if world > 1 else "1 GPU, logical ranks",
+            "parallelism": "1 GPU, logical ranks",
         },
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic, "kernel": k1_kernel_name(w),
-                     "k1_ms": k1_avg, "k2_ms": float(np.mean(k2_ms)) if k2_ms else None,
-                     "peak_source": hbm_src,
-                     # the whole switch (K3 + K1 + K2 + gaps): all bytes read + written
-                     "step_achieved": 2 * total_bytes / args.steps / (ms / args.steps * 1e-3) / 1e9,
-                     "step_frac": 2 * total_bytes / (ms * 1e-3) / 1e9 / hbm,
-                     # the peak file's method (torch copy_, 2 GiB) re-measured in this run
-                     "copy_peak_in_run": copy_peak, "frac_vs_copy_in_run": achieved / copy_peak},
-        "cpu_baseline": cpu,
-        "clocks": clk.summary(),
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "status": status,
-        "bit_exact_property": bit_exact,
-        "pages_verified": vkv["pages_checked"],
+        "roofline": m["roofline"], "cpu_baseline": m["cpu_baseline"], "clocks": m["clocks"],
+        "e2e": m["e2e"], "gpu_launches": m["gpu_launches"], "status": m["status"],
+        "bit_exact_property": m["bit_exact_property"], "pages_verified": m["pages_verified"],
+        "headline": headline,
     }
     print(json.dumps(line))
 

@@ -53,9 +53,18 @@ enum tpr_status {
                        /* caller's general path, which resolves or raises */
 };
 
-/* Device-side status bits written by the K3 remap kernel (status word). */
-#define TPR_STATUS_WRONG_SOURCE 1 /* head not on src_gpu (migration.py:201-205) */
-#define TPR_STATUS_DST_OCCUPIED 2 /* destination block-table slot already set   */
+/* Device-side status bits written by the K3 remap kernel (status word). Each
+ * K3 call (tpr_kv_remap, tpr_kv_switch, tpr_kv_switch_layouts) first zeroes
+ * the word, so it reports that call only. A page with an error is not touched
+ * (its work item has ntok = 0 and K1 skips it); the ring positions the host
+ * counts are still written, so ring state stays defined (see tpr_kernels.cu
+ * k3_page and oracle/kvmove.c for the exact rules). */
+#define TPR_STATUS_WRONG_SOURCE 1  /* head not on src_gpu (migration.py:201-205) */
+#define TPR_STATUS_DST_OCCUPIED 2  /* destination block-table slot already set   */
+#define TPR_STATUS_OUT_OF_RANGE 8  /* request slot / head / page outside the
+                                      block table (context longer than max_blocks) */
+#define TPR_STATUS_RING_POISONED 16 /* a free-ring pop returned no valid unit (a
+                                      slot an earlier error left poisoned)        */
 
 /* Paged KV pool geometry. One pool unit = one KV head x one page of
  * `block_tokens` tokens x all layers x {K,V}, laid out [layer][kv][token][dim].
@@ -127,7 +136,13 @@ int tpr_get_copy_engine(void);
  *                   pages as TMA tensor boxes (token x planes) instead of
  *                   one short copy per plane: 0 never, 1 when a page of the
  *                   plan is partial, 2 the tensor kernel for every plan.
- * tpr_get_tuning returns the current value, -1 for an unknown key.
+ * tpr_get_tuning returns the current value, -1 for an unknown key. Two
+ * read-only keys report the engine the last K1 / K2 launch used
+ * ("k1_engine_last", "k2_engine_last": TPR_ENGINE_*, -1 before the first):
+ * the TMA engine runs only when every pool (K1) or segment address
+ * (tpr_weight_reshard_host) is the launching device's own HBM; peer mappings
+ * of another GPU take the vector engine, and no tensor map is ever encoded
+ * over a peer mapping.
  * Read once from the environment (TMA engine ring shapes, "<stages>x<bytes>"):
  *   TPR_BULK_K1 [6x32768], TPR_BULK_K2 [3x32768], TPR_BULK_K1_SMALL [3x32768]
  *   for K1s of at most TPR_K1_SMALL_ITEMS_PER_SM [24] items per SM. */
@@ -335,6 +350,18 @@ int tpr_weight_reshard(const tpr_copy_seg_t* d_segs, const int64_t* d_prefix,
                        int32_t n_segs, int64_t n_items, int64_t chunk_bytes,
                        int64_t* d_claim, void* stream);
 
+/* K2 in one call from host segments: `h_buf` (pinned host memory of
+ * tpr_reshard_buffer_bytes(n_segs) bytes) holds the n_segs segments; the call
+ * normalises them in place (tpr_copy_prepare), appends the item prefix and the
+ * claim counter, copies the buffer to `d_buf` on `stream` and launches K2.
+ * The copy engine follows the pointers: the TMA engine when every source and
+ * destination is the launching device's own HBM, the 16-byte vector engine when
+ * any is a peer mapping (another GPU). h_buf must stay untouched until the
+ * stream passes this call. *n_items_out (nullable) = work items launched. */
+size_t tpr_reshard_buffer_bytes(int32_t n_segs);
+int tpr_weight_reshard_host(tpr_copy_seg_t* h_buf, int32_t n_segs, int64_t chunk, uint64_t d_buf,
+                            uint64_t d_buf_bytes, int64_t* n_items_out, void* stream);
+
 /* ---- synthetic data + full-size property checks (device) --------------- */
 /* Pattern fill of every work unit's valid tokens in its destination pool
  * (typically the work list of an admission remap); the pattern is a function
@@ -388,7 +415,6 @@ int tpr_device_barrier(const uint64_t* peer_flags, int32_t rank, int32_t world, 
  * base, so its IPC handle maps exactly this buffer in a peer process. */
 int tpr_device_alloc(uint64_t bytes, uint64_t* dptr);
 int tpr_device_free(uint64_t dptr);
-int tpr_enable_peer(int32_t peer_device);
 int tpr_ipc_get_handle(uint64_t dptr, uint8_t* handle64);
 int tpr_ipc_open(const uint8_t* handle64, uint64_t* dptr);
 int tpr_ipc_close(uint64_t dptr);

@@ -36,7 +36,10 @@ typedef struct {
 } page_move;
 
 /* Returns number of page moves, or -1 on allocation failure. status |= 1 for
- * a head not on src, |= 2 for an occupied destination entry. */
+ * a head not on src, |= 2 for an occupied destination entry, |= 8 for a page
+ * outside the block table, |= 16 for a poisoned free-ring slot (the
+ * TPR_STATUS_* bits of include/tpr.h). pools == NULL replays block tables,
+ * free rings and ring counters only (no page bytes). */
 int64_t oracle_kv_migrate(const oracle_geo* g, uint8_t** pools, int32_t** tables, int32_t** rings,
                           const int64_t* ring_len, int64_t* ring_head, int64_t* ring_tail,
                           const int64_t* xf, int64_t n, int32_t n_threads, int32_t* status) {
@@ -58,19 +61,37 @@ int64_t oracle_kv_migrate(const oracle_geo* g, uint8_t** pools, int32_t** tables
     const int64_t pages = (ctx + B - 1) / B;
     for (int64_t h = r[3]; h < r[4]; ++h) {
       for (int64_t b = 0; b < pages; ++b) {
+        /* A page with an error is not touched (K1 skips it); the ring positions
+         * are still consumed: a missing source is pushed as -1 (a poisoned
+         * slot), a destination unit that cannot be placed leaks. */
+        const int in_range = h >= 0 && h < H && b < MB && req >= 0 && req < g->n_req_slots;
         const int64_t idx = (req * H + h) * MB + b;
         int32_t su = -1;
+        if (!in_range) *status |= 8;
         if (src >= 0) {
-          su = tables[src][idx];
-          if (su < 0) *status |= 1;
-          tables[src][idx] = -1;
+          if (in_range) {
+            su = tables[src][idx];
+            if (su < 0 || su >= ring_len[src]) {
+              *status |= 1;
+              su = -1;
+            }
+            tables[src][idx] = -1;
+          }
           rings[src][ring_tail[src]++ % ring_len[src]] = su;
         }
         int32_t du = -1;
         if (dst >= 0) { /* dst < 0: release only */
-          du = rings[dst][ring_head[dst]++ % ring_len[dst]];
-          if (tables[dst][idx] >= 0) *status |= 2;
-          tables[dst][idx] = du;
+          const int32_t v = rings[dst][ring_head[dst]++ % ring_len[dst]];
+          if (v < 0 || v >= ring_len[dst]) {
+            *status |= 16;
+          } else if (!in_range) {
+            /* leaked */
+          } else if (tables[dst][idx] >= 0) {
+            *status |= 2;
+          } else if (!(src >= 0 && su < 0)) {
+            tables[dst][idx] = v;
+            du = v;
+          }
         }
         mv[k].su = su;
         mv[k].du = du;
@@ -80,6 +101,10 @@ int64_t oracle_kv_migrate(const oracle_geo* g, uint8_t** pools, int32_t** tables
         ++k;
       }
     }
+  }
+  if (!pools) { /* tables-and-rings-only replay (full-size parity of K3) */
+    free(mv);
+    return total;
   }
 #ifdef _OPENMP
   if (n_threads > 0) omp_set_num_threads(n_threads);
@@ -140,4 +165,19 @@ int32_t oracle_max_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/* Threaded first touch of a host buffer (the CPU baseline's pools and arenas
+ * are page-faulted here, outside its timed region). */
+void oracle_fill(uint8_t* p, int64_t n, uint8_t v, int32_t n_threads) {
+  const int64_t piece = 1 << 22;
+  const int64_t tasks = (n + piece - 1) / piece;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel for schedule(static)
+#endif
+  for (int64_t t = 0; t < tasks; ++t) {
+    const int64_t off = t * piece;
+    memset(p + off, v, (size_t)(n - off < piece ? n - off : piece));
+  }
 }

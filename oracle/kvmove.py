@@ -52,11 +52,20 @@ def lib():
         _lib.oracle_copy_blocks.restype = None
         _lib.oracle_copy_blocks.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 6 + [ctypes.c_int32]
         _lib.oracle_max_threads.restype = ctypes.c_int32
+        _lib.oracle_fill.restype = None
+        _lib.oracle_fill.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint8, ctypes.c_int32]
     return _lib
 
 
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+def filled(nbytes: int, value: int = 1, n_threads: int = 0) -> np.ndarray:
+    """A uint8 host buffer of ``nbytes``, first-touched by all threads."""
+    a = np.empty(nbytes, np.uint8)
+    lib().oracle_fill(a.ctypes.data, nbytes, value, n_threads)
+    return a
 
 
 def _ptrs(arrs):
@@ -67,7 +76,8 @@ def kv_migrate(geo: dict, pools, tables, rings, ring_head, ring_tail, records: n
                n_threads: int = 0):
     """Execute int64 [n, 6] slot records (src, dst, req_slot, lo, hi, ctx) in place.
 
-    Mutates pools/tables/rings (numpy arrays) and returns
+    Mutates pools/tables/rings (numpy arrays; ``pools=None`` replays block
+    tables, free rings and ring counters only) and returns
     (pages moved, status bits, ring_head, ring_tail)."""
     g = OracleGeo(**geo)
     heads = np.asarray(ring_head, dtype=np.int64).copy()
@@ -75,7 +85,8 @@ def kv_migrate(geo: dict, pools, tables, rings, ring_head, ring_tail, records: n
     rec = np.ascontiguousarray(records, dtype=np.int64)
     status = ctypes.c_int32(0)
     lens = np.array([len(r) for r in rings], dtype=np.int64)  # a ring's length is its modulus
-    n = lib().oracle_kv_migrate(ctypes.byref(g), _ptrs(pools), _ptrs(tables), _ptrs(rings),
+    n = lib().oracle_kv_migrate(ctypes.byref(g), None if pools is None else _ptrs(pools),
+                                _ptrs(tables), _ptrs(rings),
                                 lens.ctypes.data, heads.ctypes.data, tails.ctypes.data,
                                 rec.ctypes.data, len(rec), n_threads, ctypes.byref(status))
     if n < 0:
@@ -110,20 +121,32 @@ def kv_migrate_py(geo: dict, pools, tables, rings, ring_head, ring_tail, records
         pages = -(-ctx // B)
         for h in range(lo, hi):
             for b in range(pages):
+                # the rules of tpr_kernels.cu k3_page / kvmove.c
+                ok = 0 <= h < H and b < MB and 0 <= req < geo["n_req_slots"]
+                status |= 0 if ok else 8
                 su = du = -1
                 if src >= 0:
-                    tb_s = tables[src].reshape(-1, H, MB)
-                    su = int(tb_s[req, h, b])
-                    status |= 1 if su < 0 else 0
-                    tb_s[req, h, b] = -1
+                    if ok:
+                        tb_s = tables[src].reshape(-1, H, MB)
+                        su = int(tb_s[req, h, b])
+                        if not 0 <= su < len(rings[src]):
+                            status |= 1
+                            su = -1
+                        tb_s[req, h, b] = -1
                     rings[src][tails[src] % len(rings[src])] = su
                     tails[src] += 1
                 if dst >= 0:
-                    tb_d = tables[dst].reshape(-1, H, MB)
-                    du = int(rings[dst][heads[dst] % len(rings[dst])])
+                    v = int(rings[dst][heads[dst] % len(rings[dst])])
                     heads[dst] += 1
-                    status |= 2 if tb_d[req, h, b] >= 0 else 0
-                    tb_d[req, h, b] = du
+                    if not 0 <= v < len(rings[dst]):
+                        status |= 16
+                    elif ok:
+                        tb_d = tables[dst].reshape(-1, H, MB)
+                        if tb_d[req, h, b] >= 0:
+                            status |= 2
+                        elif not (src >= 0 and su < 0):
+                            tb_d[req, h, b] = v
+                            du = v
                 ntok = ctx - b * B if b == pages - 1 else B
                 moves.append((su, du, src, dst, ntok))
     for su, du, src, dst, ntok in moves:

@@ -21,6 +21,8 @@ TPR_TOTALS_LEN = 1 + 2 * TPR_MAX_GPUS
 TPR_STATUS_WRONG_SOURCE = 1
 TPR_STATUS_DST_OCCUPIED = 2
 TPR_STATUS_BARRIER_TIMEOUT = 4
+TPR_STATUS_OUT_OF_RANGE = 8
+TPR_STATUS_RING_POISONED = 16
 TPR_ENOTFOUND = -4  # an id outside the caller's lookup tables (use the Python maps)
 
 # Every exported symbol of include/tpr.h; tests check the library exports all.
@@ -30,11 +32,10 @@ EXPORTS = (
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_migrate_ex", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
     "tpr_switch_prepare", "tpr_kv_switch_layouts",
     "tpr_memcpy_h2d", "tpr_memcpy_d2h",
-    "tpr_copy_prepare", "tpr_weight_reshard",
+    "tpr_copy_prepare", "tpr_weight_reshard", "tpr_reshard_buffer_bytes", "tpr_weight_reshard_host",
     "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
     "tpr_matrix_verify", "tpr_baseline_copy_pages", "tpr_device_barrier", "tpr_device_alloc",
     "tpr_device_free",
-    "tpr_enable_peer",
     "tpr_ipc_get_handle", "tpr_ipc_open", "tpr_ipc_close",
 )
 
@@ -133,6 +134,9 @@ _SIGNATURES = {
     "tpr_copy_prepare": (c_int32, [c_void_p, c_int32, c_int64, c_void_p, _P64]),
     "tpr_weight_reshard": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p,
                                      c_void_p]),
+    "tpr_reshard_buffer_bytes": (ctypes.c_size_t, [c_int32]),
+    "tpr_weight_reshard_host": (c_int32, [c_void_p, c_int32, c_int64, c_uint64, c_uint64, _P64,
+                                          c_void_p]),
     "tpr_kv_fill": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
                               c_int64, c_uint64, c_void_p]),
     "tpr_pool_fill": (c_int32, [POINTER(KvGeometryC), c_uint64, c_int32, c_uint64, c_void_p]),
@@ -148,7 +152,6 @@ _SIGNATURES = {
                                      c_void_p]),
     "tpr_device_alloc": (c_int32, [c_uint64, POINTER(c_uint64)]),
     "tpr_device_free": (c_int32, [c_uint64]),
-    "tpr_enable_peer": (c_int32, [c_int32]),
     "tpr_ipc_get_handle": (c_int32, [c_uint64, POINTER(c_uint8)]),
     "tpr_ipc_open": (c_int32, [POINTER(c_uint8), POINTER(c_uint64)]),
     "tpr_ipc_close": (c_int32, [c_uint64]),
@@ -215,6 +218,13 @@ def set_copy_engine(name: str) -> None:
     if name not in ENGINES:
         raise ValueError(f"unknown copy engine {name!r}; choose from {sorted(ENGINES)}")
     call("tpr_set_copy_engine", ENGINES[name])
+
+
+def last_engines() -> tuple[str | None, str | None]:
+    """The copy engine the last K1 and K2 launches used (None before the first)."""
+    names = {v: k for k, v in ENGINES.items()}
+    return tuple(names.get(int(load().tpr_get_tuning(k)))
+                 for k in (b"k1_engine_last", b"k2_engine_last"))
 
 
 def copy_engine() -> str:

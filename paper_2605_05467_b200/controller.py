@@ -195,7 +195,7 @@ def measured_switch_cost(executor: ReconfigurationExecutor):
 
 def host_to_device_bytes(plan: MigrationPlan, w: ReshardStats | None) -> int:
     """Bytes a switch uploads: transfer records + weight copy segments/prefix."""
-    n = len(plan)
+    n = plan.n_transfers
     segs = w.segments if w else 0
     return n * 6 * 4 + (segs * 64 + (segs + 1) * 8 if segs else 0)
 

@@ -91,15 +91,22 @@ int cluster_params(const tpr_kv_cluster_t* cl, const tpr_kv_geometry_t* geo,
 // issuing thread per CTA (profiles/README.md); the vector engine stays
 // selectable (tpr_set_copy_engine) for comparison.
 std::atomic<int> g_engine{TPR_ENGINE_BULK};
+// the engine the last K1 / K2 launch used (tpr_get_tuning "k1_engine_last" /
+// "k2_engine_last"; -1 before the first launch)
+std::atomic<int> g_k1_last{-1}, g_k2_last{-1};
 
 // partial: the plan may contain partial pages (context not a multiple of the
-// page size); only then does K1 need the pools' tensor maps
+// page size); only then does K1 need the pools' tensor maps. The TMA engine
+// runs only when every pool of the cluster is the launching device's own HBM
+// (tpr::all_local); a cluster with peer-mapped pools (one process per GPU,
+// pools on other GPUs) takes the 16-byte vector engine.
 cudaError_t run_k1(const tpr_kv_geometry_t* geo, int n_gpus, const tpr::KvCopyParams& p,
                    const tpr::KvClusterParams& cl, const int4* work, int64_t n, cudaStream_t st,
                    bool pdl, bool partial = true) {
-  return g_engine.load() == TPR_ENGINE_BULK
-             ? tpr::launch_k1_bulk(p, cl, work, n, st, pdl, geo, n_gpus, partial)
-             : tpr::launch_k1(p, cl, work, n, st, pdl);
+  const bool bulk = g_engine.load() == TPR_ENGINE_BULK && tpr::all_local(cl.pool, n_gpus);
+  g_k1_last.store(bulk ? TPR_ENGINE_BULK : TPR_ENGINE_VECTOR);
+  return bulk ? tpr::launch_k1_bulk(p, cl, work, n, st, pdl, geo, n_gpus, partial)
+              : tpr::launch_k1(p, cl, work, n, st, pdl);
 }
 
 bool any_partial(const int32_t* rec, int32_t n, int32_t block_tokens) {
@@ -145,11 +152,16 @@ int64_t env_i64(const char* name, int64_t dflt) {
   return (v && *v) ? strtoll(v, nullptr, 10) : dflt;
 }
 
+// local: every segment's source and destination is the launching device's
+// own HBM (tpr_weight_reshard_host checks; tpr_weight_reshard, which only sees
+// device-side segments, trusts the engine setting)
 cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
-                   int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st) {
-  return g_engine.load() == TPR_ENGINE_BULK
-             ? tpr::launch_k2_bulk(segs, prefix, n_segs, n_items, chunk, claim, st)
-             : tpr::launch_k2(segs, prefix, n_segs, n_items, chunk, st);
+                   int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st,
+                   bool local = true) {
+  const bool bulk = g_engine.load() == TPR_ENGINE_BULK && local;
+  g_k2_last.store(bulk ? TPR_ENGINE_BULK : TPR_ENGINE_VECTOR);
+  return bulk ? tpr::launch_k2_bulk(segs, prefix, n_segs, n_items, chunk, claim, st)
+              : tpr::launch_k2(segs, prefix, n_segs, n_items, chunk, st);
 }
 
 }  // namespace
@@ -258,6 +270,74 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+// ---------------------------------------------------------------------------
+// Pointer locality. The TMA engine (cp.async.bulk, tensor maps) is validated
+// on the launching device's own HBM only; addresses that belong to another
+// GPU (peer mappings over NVLink, CUDA-IPC handles of another device) are
+// moved with plain 16-byte loads/stores. The owning device of an address is
+// cached per allocation range (cuMemGetAddressRange), so a switch pays a few
+// range compares, not a driver query per pointer.
+// ---------------------------------------------------------------------------
+using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+GetRange range_fn() {
+  static GetRange fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<GetRange>(f);
+  }();
+  return fn;
+}
+
+struct DevRange {
+  uint64_t lo, hi;
+  int dev;
+};
+std::mutex g_range_mu;
+std::vector<DevRange> g_ranges;
+
+int ptr_device(uint64_t p) {
+  {
+    std::lock_guard<std::mutex> lock(g_range_mu);
+    for (const DevRange& r : g_ranges)
+      if (p >= r.lo && p < r.hi) return r.dev;
+  }
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, reinterpret_cast<const void*>(p)) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  const int dev = a.type == cudaMemoryTypeDevice ? a.device : -1;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  GetRange fn = range_fn();
+  if (dev >= 0 && fn && fn(&base, &size, (CUdeviceptr)p) == CUDA_SUCCESS && size > 0) {
+    std::lock_guard<std::mutex> lock(g_range_mu);
+    if (g_ranges.size() >= 4096) g_ranges.clear();
+    g_ranges.push_back(DevRange{(uint64_t)base, (uint64_t)base + size, dev});
+  }
+  return dev;
+}
+
+void forget_ranges() {
+  std::lock_guard<std::mutex> lock(g_range_mu);
+  g_ranges.clear();
+}
+
+bool all_local(const uint64_t* ptrs, int n) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int i = 0; i < n; ++i)
+    if (ptrs[i] && ptr_device(ptrs[i]) != cur) return false;
+  return true;
+}
+
 int sm_count() {
   static int cache[64] = {0};
   int dev = 0;
@@ -280,6 +360,7 @@ void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int
   if (!tensor_partial_enabled() || tok % 16 || tok / 8 > 256 || geo.block_tokens > 256 ||
       n_gpus < 1 || n_gpus > TPR_MAX_GPUS)
     return;
+  if (!all_local(cl.pool, n_gpus)) return;  // never a tensor map over a peer mapping
   // planes per tensor copy: the largest divisor of rows with <= 256 planes
   // whose box fits one ring stage
   int32_t r_box = 0;
@@ -394,6 +475,8 @@ int64_t tpr_get_tuning(const char* key) {
   if (!strcmp(key, "tensor_partial")) return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1);
   if (!strcmp(key, "bulk_ws")) return knob(g_ws, "TPR_BULK_WS", 0);
   if (!strcmp(key, "k1_dynamic")) return knob(g_dyn, "TPR_K1_DYNAMIC", 1);
+  if (!strcmp(key, "k1_engine_last")) return g_k1_last.load();
+  if (!strcmp(key, "k2_engine_last")) return g_k2_last.load();
   return -1;
 }
 
@@ -588,6 +671,43 @@ int tpr_weight_reshard(const tpr_copy_seg_t* d_segs, const int64_t* d_prefix, in
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_weight_reshard launch");
 }
 
+int tpr_weight_reshard_host(tpr_copy_seg_t* h_buf, int32_t n_segs, int64_t chunk, uint64_t d_buf,
+                            uint64_t d_buf_bytes, int64_t* n_items_out, void* stream) {
+  if (n_segs < 0 || (n_segs > 0 && (!h_buf || !d_buf))) return fail(TPR_EINVAL, "bad reshard arguments");
+  const size_t bytes = tpr_reshard_buffer_bytes(n_segs);
+  if (d_buf_bytes < bytes) return fail(TPR_ECAPACITY, "device buffer %llu < %llu bytes",
+                                       (unsigned long long)d_buf_bytes, (unsigned long long)bytes);
+  int64_t* prefix = reinterpret_cast<int64_t*>(h_buf + n_segs);
+  int64_t n_items = 0;
+  int rc = tpr_copy_prepare(h_buf, n_segs, chunk, prefix, &n_items);
+  if (rc) return rc;
+  prefix[n_segs + 1] = 0;  // the dynamic-claim counter, 0 when K2 starts
+  if (n_items_out) *n_items_out = n_items;
+  if (n_items == 0) return TPR_OK;
+  // TMA engine only when every byte K2 touches is this device's HBM
+  std::vector<uint64_t> ptrs;
+  ptrs.reserve(2 * (size_t)n_segs);
+  for (int32_t i = 0; i < n_segs; ++i) {
+    ptrs.push_back(h_buf[i].src);
+    ptrs.push_back(h_buf[i].dst);
+  }
+  const bool local = tpr::all_local(ptrs.data(), (int)ptrs.size());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(d_buf), h_buf, bytes,
+                                  cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "tpr_weight_reshard_host H2D");
+  const tpr_copy_seg_t* d_segs = reinterpret_cast<const tpr_copy_seg_t*>(d_buf);
+  const int64_t* d_prefix = reinterpret_cast<const int64_t*>(d_segs + n_segs);
+  e = run_k2(d_segs, d_prefix, n_segs, n_items, chunk, const_cast<int64_t*>(d_prefix) + n_segs + 1,
+             st, local);
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_weight_reshard_host launch");
+}
+
+size_t tpr_reshard_buffer_bytes(int32_t n_segs) {
+  return sizeof(tpr_copy_seg_t) * (size_t)(n_segs > 0 ? n_segs : 0) +
+         sizeof(int64_t) * (size_t)((n_segs > 0 ? n_segs : 0) + 2);
+}
+
 // ---------------------------------------------------------------------------
 // Synthetic data and checks
 // ---------------------------------------------------------------------------
@@ -712,17 +832,9 @@ int tpr_device_alloc(uint64_t bytes, uint64_t* dptr) {
 }
 
 int tpr_device_free(uint64_t dptr) {
+  tpr::forget_ranges();
   cudaError_t e = cudaFree(reinterpret_cast<void*>(dptr));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "cudaFree");
-}
-
-int tpr_enable_peer(int32_t peer) {
-  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
-  if (e == cudaErrorPeerAccessAlreadyEnabled) {
-    cudaGetLastError();
-    return TPR_OK;
-  }
-  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
 }
 
 int tpr_ipc_get_handle(uint64_t dptr, uint8_t* handle64) {
@@ -745,6 +857,7 @@ int tpr_ipc_open(const uint8_t* handle64, uint64_t* dptr) {
 }
 
 int tpr_ipc_close(uint64_t dptr) {
+  tpr::forget_ranges();
   cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(dptr));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }

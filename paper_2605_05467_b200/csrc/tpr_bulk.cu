@@ -162,6 +162,7 @@ struct KvPieces {
       const int g = (int)(it - u * p.items_per_unit);
       const int4 w = work[u];
       const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
+      if (w.x < 0 || w.y < 0 || ntok <= 0) continue;  // a page K3 refused (status word)
       const int64_t nb = (int64_t)ntok * p.tok_bytes;
       if (kTensor && nb != p.pitch) {  // partial page: tensor boxes
         if (g >= ntok) continue;            // no token for this item slot

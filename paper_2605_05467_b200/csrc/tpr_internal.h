@@ -62,6 +62,12 @@ int k1_claim_batch();  // items per claim, 0 = static shares
 
 int sm_count();
 
+// Device index owning a device address (-1: host / unknown), cached per
+// allocation range; all_local: every non-null pointer is on the current device.
+int ptr_device(uint64_t p);
+bool all_local(const uint64_t* ptrs, int n);
+void forget_ranges();
+
 // Programmatic dependent launch of K3b/K1 behind their producer (TPR_PDL=0
 // turns it off) and the plan size (units) up to which K3 runs as one fused
 // CTA (TPR_K3_FUSE_UNITS, 0 = never).

@@ -232,9 +232,70 @@ __device__ __forceinline__ int64_t k3_scan_body(const int32_t* xf_in,  // may al
 __global__ void __launch_bounds__(kScanThreads)
     tpr_k3_scan(const int32_t* xf_in, int32_t* xf, int32_t n,
                 int32_t block_tokens, int32_t filter, int64_t* __restrict__ meta,
-                int64_t* __restrict__ totals) {
+                int64_t* __restrict__ totals, int32_t* __restrict__ status) {
   pdl_trigger();  // the remap grid may get resident; it waits for this scan
+  // the status word reports this K3 call only (the remap grid sets bits after
+  // pdl_wait, i.e. after this store) -- unless a device barrier timed out into
+  // it: then the bit stays and the remap grid aborts (k3_remap_body)
+  if (threadIdx.x == 0 && !(*status & TPR_STATUS_BARRIER_TIMEOUT)) *status = 0;
   k3_scan_body(xf_in, xf, n, block_tokens, filter, meta, totals);
+}
+
+// ---------------------------------------------------------------------------
+// Bookkeeping of one page (req, h, b) moving src -> dst (either may be -1):
+// push the source unit at release position rel_pos of the source ring, pop the
+// destination unit at allocation position alloc_pos of the destination ring,
+// rewrite both block-table entries. Returns the work item
+// {src_unit, dst_unit, src | dst << 16, ntok}; a page that must not be touched
+// comes back with ntok = 0 (and the status word says why). The ring positions
+// the host counts are always written, so ring state stays defined after an
+// error: a missing source is pushed as -1 (a poisoned slot that a later pop
+// reports instead of using), a destination unit that cannot be placed leaks.
+// oracle/kvmove.c restates exactly these rules.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int4 k3_page(const KvClusterParams& cl, const tpr_kv_geometry_t& geo,
+                                        int src, int dst, int req, int h, int b, int ntok,
+                                        int64_t alloc_pos, int64_t rel_pos,
+                                        int32_t* __restrict__ status) {
+  const int H = geo.total_heads, MB = geo.max_blocks;
+  const bool in_range = h >= 0 && h < H && b >= 0 && b < MB && req >= 0 && req < geo.n_req_slots;
+  const int64_t bt_idx = ((int64_t)req * H + h) * MB + b;
+  // All loads first, then the stores: the three reads are independent (an
+  // entry moves once per plan, and the released ring positions never overlap
+  // the allocated ones), so they cost one memory latency instead of three.
+  int32_t* bts = (src >= 0 && in_range) ? reinterpret_cast<int32_t*>(cl.block_table[src]) : nullptr;
+  int32_t* btd = (dst >= 0 && in_range) ? reinterpret_cast<int32_t*>(cl.block_table[dst]) : nullptr;
+  int32_t src_unit = bts ? __ldcg(bts + bt_idx) : -1;
+  const int32_t popped =
+      dst >= 0 ? __ldcg(reinterpret_cast<const int32_t*>(cl.free_ring[dst]) +
+                        (cl.ring_head[dst] + alloc_pos) % cl.units[dst])
+               : -1;
+  const int32_t dst_prev = btd ? __ldcg(btd + bt_idx) : -1;
+  int bits = in_range ? 0 : TPR_STATUS_OUT_OF_RANGE;
+  if (src >= 0) {
+    if (in_range && (src_unit < 0 || src_unit >= cl.units[src])) {
+      bits |= TPR_STATUS_WRONG_SOURCE;
+      src_unit = -1;
+    }
+    if (bts) bts[bt_idx] = -1;
+    int32_t* ring_s = reinterpret_cast<int32_t*>(cl.free_ring[src]);
+    ring_s[(cl.ring_tail[src] + rel_pos) % cl.units[src]] = src_unit;
+  }
+  int32_t dst_unit = -1;
+  if (dst >= 0) {
+    if (popped < 0 || popped >= cl.units[dst]) bits |= TPR_STATUS_RING_POISONED;
+    else if (!in_range) {}  // leaked
+    else if (dst_prev >= 0) bits |= TPR_STATUS_DST_OCCUPIED;  // a live entry stays; popped leaks
+    else if (src >= 0 && src_unit < 0) {}  // nothing to place
+    else {
+      btd[bt_idx] = popped;
+      dst_unit = popped;
+    }
+  }
+  if (bits) atomicOr(status, bits);
+  const bool ok = dst_unit >= 0 && (src < 0 || src_unit >= 0);
+  return make_int4(src_unit, dst_unit, (src & 0xffff) | ((dst & 0xffff) << 16),
+                   ok || (dst < 0 && src_unit >= 0) ? ntok : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -248,11 +309,16 @@ __device__ __forceinline__ void k3_remap_body(const int32_t* __restrict__ xf, in
                                               const KvClusterParams& cl, int4* __restrict__ work,
                                               int4* __restrict__ work_ext,
                                               int32_t* __restrict__ status, int64_t first,
-                                              int64_t stride) {
-  const int H = geo.total_heads, B = geo.block_tokens, MB = geo.max_blocks;
+                                              int64_t stride, bool abort) {
+  const int B = geo.block_tokens;
   // the int4 slot after the work list is K1's claim counter: zero it here, in
   // the kernel that K1 waits for
   if (first == 0) work[n_mine] = make_int4(0, 0, 0, 0);
+  if (abort) {  // the start barrier timed out (a peer never arrived): touch no
+    // table, ring or pool; K1 skips every item
+    for (int64_t i = first; i < n_mine; i += stride) work[i] = make_int4(-1, -1, 0, 0);
+    return;
+  }
   for (int64_t i = first; i < n_mine; i += stride) {
     // upper_bound(mine_off, i) - 1
     int lo = 0, hi = n;
@@ -269,32 +335,7 @@ __device__ __forceinline__ void k3_remap_body(const int32_t* __restrict__ xf, in
     const int h = h_lo + (int)(local / nblk);
     const int b = (int)(local - (int64_t)(h - h_lo) * nblk);
     const int ntok = (b == nblk - 1) ? ctx - b * B : B;
-    const int64_t bt_idx = ((int64_t)req * H + h) * MB + b;
-
-    // All loads first, then the stores: the three reads are independent (an
-    // entry moves once per plan, and the released ring positions never overlap
-    // the allocated ones), so they cost one memory latency instead of three.
-    int32_t* bts = src >= 0 ? reinterpret_cast<int32_t*>(cl.block_table[src]) : nullptr;
-    int32_t* btd = dst >= 0 ? reinterpret_cast<int32_t*>(cl.block_table[dst]) : nullptr;
-    const int32_t src_unit = bts ? __ldcg(bts + bt_idx) : -1;
-    // dst == -1: release only (request finished or evicted)
-    const int32_t dst_unit =
-        btd ? __ldcg(reinterpret_cast<const int32_t*>(cl.free_ring[dst]) +
-                     (cl.ring_head[dst] + m[1] + local) % cl.units[dst])
-            : -1;
-    const int32_t dst_prev = btd ? __ldcg(btd + bt_idx) : -1;
-    if (bts) {
-      if (src_unit < 0) atomicOr(status, TPR_STATUS_WRONG_SOURCE);
-      bts[bt_idx] = -1;
-      int32_t* ring_s = reinterpret_cast<int32_t*>(cl.free_ring[src]);
-      ring_s[(cl.ring_tail[src] + m[2] + local) % cl.units[src]] = src_unit;
-    }
-    if (btd) {
-      if (dst_prev >= 0) atomicOr(status, TPR_STATUS_DST_OCCUPIED);
-      btd[bt_idx] = dst_unit;
-    }
-
-    work[i] = make_int4(src_unit, dst_unit, (src & 0xffff) | ((dst & 0xffff) << 16), ntok);
+    work[i] = k3_page(cl, geo, src, dst, req, h, b, ntok, m[1] + local, m[2] + local, status);
     if (work_ext != nullptr) work_ext[i] = make_int4(req, h, b, t);
   }
 }
@@ -306,8 +347,10 @@ __global__ void __launch_bounds__(256)
                  int32_t* __restrict__ status) {
   pdl_trigger();  // K1 may get resident; it waits for the whole remap grid
   pdl_wait();     // the scan's offsets
+  const bool abort = (__ldcg(status) & TPR_STATUS_BARRIER_TIMEOUT) != 0;
   k3_remap_body(xf, n, meta, totals[0], geo, cl, work, work_ext, status,
-                (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+                (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x,
+                abort);
 }
 
 constexpr int kFusedSmemXfers = 512;
@@ -325,13 +368,19 @@ __global__ void __launch_bounds__(kScanThreads)
   // the per-unit binary search and record reads do not go to L2
   __shared__ int32_t s_xf[kFusedSmemXfers * TPR_XFER_FIELDS];
   __shared__ int64_t s_meta[kFusedSmemXfers * TPR_META_FIELDS];
+  __shared__ int s_abort;
   const bool in_smem = n <= kFusedSmemXfers;
   pdl_trigger();
+  if (threadIdx.x == 0) {  // this call's bits only, unless a device barrier timed out into it
+    s_abort = (*status & TPR_STATUS_BARRIER_TIMEOUT) != 0;
+    if (!s_abort) *status = 0;
+  }
+  __syncthreads();
   const int64_t n_mine = k3_scan_body(xf_in, xf, n, geo.block_tokens, filter, meta, totals,
                                       in_smem ? s_xf : nullptr, in_smem ? s_meta : nullptr);
   __syncthreads();
   k3_remap_body(in_smem ? s_xf : xf, n, in_smem ? s_meta : meta, n_mine, geo, cl, work,
-                work_ext, status, threadIdx.x, blockDim.x);
+                work_ext, status, threadIdx.x, blockDim.x, s_abort != 0);
   if (status_mirror != nullptr) {  // the status word, straight into pinned host memory
     __syncthreads();                // every thread's atomicOr has landed
     if (threadIdx.x == 0) *reinterpret_cast<volatile int32_t*>(status_mirror) = atomicOr(status, 0);
@@ -352,6 +401,7 @@ __device__ __forceinline__ void k1_vector_item(const int4* __restrict__ work, in
   const int g = (int)(item - u * p.items_per_unit);
   const int4 w = work[u];
   const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
+  if (w.x < 0 || w.y < 0 || ntok <= 0) return;  // a page K3 refused (status word)
   const int row0 = g * p.rows_per_item;
   const int nr = min(p.rows_per_item, p.rows - row0);
   const char* s = reinterpret_cast<const char*>(cl.pool[src_slot]) + (int64_t)w.x * p.unit_bytes +
@@ -454,6 +504,7 @@ __global__ void __launch_bounds__(256)
     const int64_t u = item / p.rows;
     const int row = (int)(item - u * p.rows);
     const int4 w = work[u];
+    if (w.y < 0 || w.w <= 0) continue;  // a page K3 refused
     const int4 e = work_ext[u];
     const uint64_t key = tpr_page_key(seed, (uint32_t)e.x, (uint32_t)e.y, (uint32_t)e.z);
     char* pool = reinterpret_cast<char*>(cl.pool[(w.z >> 16) & 0xffff]);
@@ -651,7 +702,7 @@ cudaError_t launch_k3(const tpr_kv_geometry_t& geo, const KvClusterParams& cl,
     if (mirrored) *mirrored = status_mirror != nullptr;
     return cudaGetLastError();
   }
-  tpr_k3_scan<<<1, threads, 0, st>>>(xf_in, xf, n, geo.block_tokens, filter, meta, totals);
+  tpr_k3_scan<<<1, threads, 0, st>>>(xf_in, xf, n, geo.block_tokens, filter, meta, totals, status);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int64_t blocks = (n_hint + 255) / 256;

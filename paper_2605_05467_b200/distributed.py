@@ -36,7 +36,7 @@ from .geometry import MAX_TP, KvGeometry, ModelGeometry
 from .kvcache import MigrationStats, _PinnedStaging
 from .migration import (BYTES, KvLayout, MigrationError, MigrationPlan, pack_layouts,
                         plan_repartition)
-from .weights import ReshardStats, ShardedWeightStore, groups_ranges
+from .weights import ReshardStats, ShardedWeightStore, groups_ranges, window_for
 
 
 class _CudaArray:
@@ -244,13 +244,22 @@ class DistributedKvCluster:
         """Every rank calls with the same layouts; each allocates + fills its pages."""
         recs, new = [], []
         free = list(self._free_req_slots)
+        seen = set()
+        H = self.kv.total_heads
         for lay in layouts:
+            # the checks of PagedKvCluster.admit: K3 indexes block-table rows by
+            # (request slot, head, page), and these tables are mapped by peers
+            if lay.total_heads != H:
+                raise MigrationError("all layouts must share total_heads")
             hpr = lay.heads_per_rank
             for rid, ctx in lay.requests:
-                if rid in self.req_slot or any(rid == x[0] for x in new):
+                if rid in self.req_slot or rid in seen:
                     raise MigrationError(f"request {rid} already resident")
+                if self.kv.blocks(ctx) > self.max_blocks:
+                    raise MigrationError(f"request {rid}: {ctx} tokens exceed max_blocks")
                 if not free:
                     raise MigrationError("no free request slots")
+                seen.add(rid)
                 rs = free.pop()
                 runs = [(self.slot_of[g], r * hpr, (r + 1) * hpr) for r, g in enumerate(lay.group)]
                 new.append((rid, rs, int(ctx), runs))
@@ -440,6 +449,13 @@ class DistributedKvCluster:
         return {"placement_errors": c[0], "word_mismatches": c[1], "pages_checked": c[2],
                 "status": int(self.status.item())}
 
+    def tables_snapshot(self) -> dict:
+        """This slot's block table and free ring + all ring counters (no pool)."""
+        torch.cuda.synchronize(self.device)
+        return {"block_tables": [self.bt.tensor.view(torch.int32).cpu().numpy()],
+                "rings": [self.ring.tensor.view(torch.int32).cpu().numpy()],
+                "ring_head": list(self.ring_head), "ring_tail": list(self.ring_tail)}
+
     def snapshot(self) -> dict:
         torch.cuda.synchronize(self.device)
         return {"pool": self.pool.tensor.cpu().numpy(),
@@ -476,26 +492,27 @@ class _PeerPtr:
 class DistributedWeightStore(ShardedWeightStore):
     """The sharded weights of ONE GPU (this rank) + IPC views of its peers.
 
-    Each rank owns two arenas (double buffer) sized for ``max_slices`` slices.
-    Both are registered with every peer once. A reshard rebuilds a GPU's shard
-    into its idle arena by pulling slices from the peers' current arenas
-    (remote loads over NVLink, local ones from HBM). The pull uses the same
-    planner as the single-process store, so every rank computes the same
-    source choice and egress balance. After the barrier the GPUs that rebuilt
-    flip to the other arena; the old one stays readable until the next
-    reshard, which starts after a barrier."""
+    Each rank owns two slice-addressed arenas (double buffer) of ``max_slices``
+    slices (its window). Both are registered with every peer once. A reshard
+    uses the same planner as the single-process store, so every rank computes
+    the same plan, source choice and egress balance. A shard that grows inside
+    its window pulls only the missing slices from the peers' current arenas
+    straight into their positions of its CURRENT arena (remote loads over
+    NVLink; the resident slices are not touched, and peers may read them
+    meanwhile). A shard that leaves its window is rebuilt into the idle arena,
+    and the rank flips to it after the end barrier; the old one stays readable
+    until the next reshard, which starts after a barrier."""
 
     def __init__(self, model: ModelGeometry, gpu_ids, device: torch.device, group=None,
                  max_slices: int = MAX_TP, mode: str = "sharded"):
-        super().__init__(model, gpu_ids, device=device, mode=mode)
+        super().__init__(model, gpu_ids, device=device, mode=mode, max_slices=max_slices)
         self.group = group
         self.rank = dist.get_rank(group)
         if len(self.gpu_ids) != dist.get_world_size(group):
             raise MigrationError("one GPU per rank")
         self.me = self.gpu_ids[self.rank]
         self.device = torch.device(device)
-        self.max_slices = MAX_TP if mode == "full_copy_per_gpu" else int(max_slices)
-        cap = max(self.max_slices * self.bytes_per_slice, 16)
+        cap = max(self.max_slices[self.me] * self.bytes_per_slice, 16)
         self.bufs = [DeviceBuffer(cap, self.device), DeviceBuffer(cap, self.device)]
         handles = [b.handle() for b in self.bufs]
         allh = [None] * len(self.gpu_ids)
@@ -510,71 +527,62 @@ class DistributedWeightStore(ShardedWeightStore):
     def _views(self):
         arena = {}
         for g in self.gpu_ids:
-            a, b = self.resident[g]
             if g == self.me:
-                arena[g] = self.bufs[self.cur[g]].tensor[: (b - a) * self.bytes_per_slice]
+                arena[g] = self.bufs[self.cur[g]].tensor[: self.window[g][1] * self.bytes_per_slice]
             else:
                 arena[g] = _PeerPtr(self.peer_bufs[g][self.cur[g]])
         self.arena = arena
+
+    def _check_windows(self, windows) -> None:
+        for g, (_, m) in windows.items():
+            if m > self.max_slices[g]:
+                raise MigrationError(f"gpu {g}: shard exceeds max_slices={self.max_slices[g]}")
 
     def load(self, groups, stream=None) -> None:
         act = groups_ranges(groups)
         if set(act) != set(self.gpu_ids):
             raise MigrationError("groups must cover exactly the store's GPUs")
         for g in self.gpu_ids:
-            self.resident[g] = (0, MAX_TP) if self.mode == "full_copy_per_gpu" else act[g]
+            res = (0, MAX_TP) if self.mode == "full_copy_per_gpu" else act[g]
+            self.window[g] = window_for(*res, self.max_slices[g])
+            self.have[g] = frozenset(range(*res))
             self.active[g] = act[g]
-            if self.resident[g][1] - self.resident[g][0] > self.max_slices:
-                raise MigrationError(f"gpu {g}: shard exceeds max_slices={self.max_slices}")
+        self._check_windows(self.window)
         self._views()
         rep_bytes = sum(m.rows * m.cols for m in self.replicated) * self.model.dtype_bytes
         self.rep_arena = {self.me: torch.empty(max(rep_bytes, 16), dtype=torch.uint8, device=self.device)}
         st = stream or self.stream
         with torch.cuda.device(self.device):
-            self._fill(self.me, st)
+            self._fill(self.me, st, *((0, MAX_TP) if self.mode == "full_copy_per_gpu"
+                                      else act[self.me]))
         st.synchronize()
         dist.barrier(group=self.group)
 
     def launch(self, new_groups, parked=(), events=None):
         """Plan (same on every rank) and enqueue this rank's K2 pull."""
-        act, new_res, moves = self.plan(new_groups, parked)
-        for g in parked:
-            act[g] = new_res[g]
-        stats = ReshardStats(egress={g: 0 for g in self.gpu_ids}, ingress={g: 0 for g in self.gpu_ids})
-        for g in self.gpu_ids:
-            if not moves[g]:
-                stats.views += 1
-                continue
-            x, y = new_res[g]
-            if y - x > self.max_slices:
-                raise MigrationError(f"gpu {g}: shard exceeds max_slices={self.max_slices}")
-            for src, lo, hi in moves[g]:
-                nb = (hi - lo) * self.bytes_per_slice
-                if src == g:
-                    stats.local_bytes += nb
-                else:
-                    stats.remote_bytes += nb
-                    stats.egress[src] += nb
-                    stats.ingress[g] += nb
+        plan = self.plan(new_groups, parked)
+        self._check_windows(plan.window)
+        stats = self._stats(plan)
         if events:
             events[0].record(self.stream)
-        if moves[self.me]:
-            target = self.bufs[1 - self.cur[self.me]].tensor
-            seg = np.ascontiguousarray(self._segments(self.me, new_res, moves, target))
+        me = self.me
+        if plan.fetch[me] or plan.relayout[me]:
+            # in place: the current arena; a new window: the idle one
+            target = self.bufs[self.cur[me] ^ int(plan.relayout[me])].tensor
+            seg = np.ascontiguousarray(self._segments(me, plan, target))
             stats.segments = len(seg)
             self._launch(seg, self.device, self.stream)
         if events:
             events[1].record(self.stream)
-        return act, new_res, moves, stats
+        return plan, stats
 
     def finish(self, pending) -> ReshardStats:
-        """After the barrier: flip rebuilt GPUs to their new arena."""
-        act, new_res, moves, stats = pending
+        """After the barrier: flip GPUs that moved to a new window."""
+        plan, stats = pending
         for g in self.gpu_ids:
-            if moves[g]:
+            if plan.relayout[g]:
                 self.cur[g] ^= 1
-        self.resident = new_res
-        self.active = act
+        self.have, self.window, self.active = plan.have, plan.window, plan.active
         self._views()
         return stats
 
@@ -626,15 +634,22 @@ class DeviceBarrier:
         self.epoch = 0
         dist.barrier(group=group)
 
-    def __call__(self, stream: torch.cuda.Stream) -> None:
+    def __call__(self, stream: torch.cuda.Stream, status: torch.Tensor | None = None) -> None:
+        """Enqueue the barrier. A timeout ORs TPR_STATUS_BARRIER_TIMEOUT into
+        ``status`` (default: this barrier's own word). Passing the KV cluster's
+        status word makes the K3 that follows abort (no table, ring or pool is
+        touched, K1 skips every item) instead of writing into peers that never
+        arrived."""
         self.epoch += 1
+        st = self.status if status is None else status
         _native.call("tpr_device_barrier", self.ptrs, self.rank, self.world, self.epoch,
-                     self.timeout_ns, self.status.data_ptr(), stream.cuda_stream)
+                     self.timeout_ns, st.data_ptr(), stream.cuda_stream)
 
-    def check(self) -> None:
-        """Raise if a barrier gave up waiting (host sync on the status word)."""
-        if int(self.status.item()) & _native.TPR_STATUS_BARRIER_TIMEOUT:
-            raise MigrationError("device barrier timed out: a peer rank never arrived")
+    def check(self, *extra: torch.Tensor) -> None:
+        """Raise if a barrier gave up waiting (host sync on the status words)."""
+        for st in (self.status, *extra):
+            if int(st.item()) & _native.TPR_STATUS_BARRIER_TIMEOUT:
+                raise MigrationError("device barrier timed out: a peer rank never arrived")
 
     def close(self):
         dist.barrier(group=self.group)
@@ -655,16 +670,22 @@ class DistributedExecutor:
     (``check_every`` switches, 0 = never)."""
 
     def __init__(self, kv: DistributedKvCluster, weights: DistributedWeightStore | None = None,
-                 device_barrier: bool = True, check_every: int = 0):
+                 device_barrier: bool = True, check_every: int = 0,
+                 barrier_timeout_s: float = 30.0):
         self.kv = kv
         self.weights = weights
-        self.barrier = DeviceBarrier(kv.device, kv.group) if device_barrier else None
+        self.barrier = (DeviceBarrier(kv.device, kv.group, timeout_s=barrier_timeout_s)
+                        if device_barrier else None)
         self.check_every = check_every
         self.n = 0
+        self.broken = False
 
     def switch(self, old_layouts, new_layouts, new_weight_groups=None, parked=(),
                k1_events=None, k2_events=None):
         import time
+        if self.broken:
+            raise MigrationError("a device barrier timed out earlier: the barrier epochs and "
+                                 "ring counters of the ranks may disagree; rebuild the executor")
         t0 = time.perf_counter()
         self.n += 1
         kst = self.kv.stream
@@ -673,7 +694,9 @@ class DistributedExecutor:
         if self.barrier is None:  # host handshake = the start barrier
             plan, kv_pending = self.kv.launch_layouts(old_layouts, new_layouts, k1_events)
         else:
-            self.barrier(kst)  # every rank is here: peers' pools / tables / rings are quiescent
+            # every rank is here: peers' pools / tables / rings are quiescent. A
+            # timeout lands in the KV status word, so this rank's K3 + K1 abort
+            self.barrier(kst, self.kv.status)
             start = torch.cuda.Event()
             start.record(kst)
             check = bool(self.check_every and self.n % self.check_every == 0)
@@ -696,7 +719,11 @@ class DistributedExecutor:
                 kst.wait_stream(wst)
             self.barrier(kst)  # every rank's pushes and pulls have completed
             kst.synchronize()
-            self.barrier.check()
+            try:
+                self.barrier.check(self.kv.status)
+            except MigrationError:
+                self.broken = True
+                raise
         kv_stats = self.kv.finish(plan, kv_pending)
         w_stats = self.weights.finish(w_pending) if w_pending is not None else None
         return plan, kv_stats, w_stats, (time.perf_counter() - t0) * 1e3

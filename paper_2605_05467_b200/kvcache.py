@@ -694,6 +694,17 @@ class PagedKvCluster:
         out["status"] = int(self.status.item())
         return out
 
+    def tables_snapshot(self) -> dict:
+        """Host copies of block tables, rings and ring counters (no pools): the
+        K3 state at any size."""
+        torch.cuda.synchronize()
+        return {
+            "block_tables": [b.cpu().numpy() for b in self.block_tables],
+            "rings": [r.cpu().numpy() for r in self.rings],
+            "ring_head": list(self.ring_head),
+            "ring_tail": list(self.ring_tail),
+        }
+
     def snapshot(self) -> dict:
         """Host copies of pools, block tables, rings and ring counters."""
         torch.cuda.synchronize()

@@ -128,7 +128,7 @@ class MigrationPlan:
     objects.
     """
 
-    transfers: list[Transfer] = field(default_factory=list)
+    transfers: list[Transfer]
     handshake_ms: float = 0.0
     predicted_latency_ms: dict = field(default_factory=dict)
 
@@ -160,7 +160,11 @@ class MigrationPlan:
             self._arr = np.asarray(rows, dtype=np.int64).reshape(-1, 6)
         return self._arr
 
-    def __len__(self) -> int:
+    @property
+    def n_transfers(self) -> int:
+        """len(plan.transfers) without building Transfer objects. (The reference
+        dataclass defines no __len__, so neither does this one: an empty plan
+        stays truthy, as there.)"""
         return len(self._list) if self._list is not None else len(self._arr)
 
     @property
@@ -181,7 +185,7 @@ class MigrationPlan:
         return out
 
     def __repr__(self):
-        return (f"MigrationPlan(transfers=<{len(self)} transfers>, handshake_ms={self.handshake_ms}, "
+        return (f"MigrationPlan(transfers=<{self.n_transfers} transfers>, handshake_ms={self.handshake_ms}, "
                 f"predicted_latency_ms={self.predicted_latency_ms})")
 
 

@@ -12,14 +12,19 @@ time. This store realises both regimes on B200:
   TP-N group uses slices [r*8/N, (r+1)*8/N) -- the same contiguous 1/N that
   Megatron/SGLang give rank r, and for k/v the rows of exactly the KV heads
   that ``KvLayout`` puts on that rank (migration.py:27);
-* a GPU holds one *resident* slice range [a, b) of every matrix in one arena,
-  laid out matrix by matrix: column-parallel slices as contiguous rows,
-  row-parallel slices as a [rows, (b-a)*cols/8] block;
-* a reshard reuses resident slices in place -- if the new shard lies inside
-  the resident range the new shard is just a view (zero bytes moved) -- and
-  otherwise builds a new arena from local slices plus slices fetched from
-  peers that hold them (egress balanced across holders). That copy list is
-  executed by K2 (``tpr_weight_reshard``) as one batched 2-D strided copy.
+* a GPU's arena is slice-addressed: it holds one aligned *window* of
+  ``max_slices`` slices of every matrix, laid out matrix by matrix
+  (column-parallel: [window * rows/8, cols] rows; row-parallel: a
+  [rows, window * cols/8] block), and slice k sits at position k - base
+  whether or not the GPU holds it. A shard [x, y) inside the window is a
+  contiguous row range / a strided column block: a view the GEMMs read;
+* a reshard reuses resident slices in place: a shard that is resident is a
+  view (zero bytes); a shard that grows inside the window keeps its resident
+  slices where they are and K2 fetches only the missing slices into their
+  positions, from peers that hold them (egress balanced across holders). That
+  copy list is executed by K2 (``tpr_weight_reshard_host``) as one batched 2-D
+  strided copy. Only a shard that outgrows its window needs a new arena and a
+  local relayout copy (``ReshardStats.local_bytes``).
 
 ``mode="full_copy_per_gpu"`` makes every GPU resident on all 8 slices: every
 switch is then views only (the paper's zero-overhead weight switching).
@@ -44,10 +49,11 @@ CHUNK_BYTES = int(os.environ.get("TPR_K2_CHUNK", 32 * 1024))  # K2 work-item siz
 
 @dataclass
 class ReshardStats:
-    local_bytes: int = 0    # bytes copied from the GPU's own old arena
-    remote_bytes: int = 0   # bytes fetched from peers (NVLink in multi-GPU mode)
+    local_bytes: int = 0    # relayout copies inside a GPU (only when a shard outgrows its window)
+    remote_bytes: int = 0   # missing slices fetched from peers (NVLink in multi-GPU mode)
     segments: int = 0
     views: int = 0          # GPUs whose new shard is a view of resident slices
+    in_place: int = 0       # GPUs that grew their shard in place (fetches only)
     egress: dict = field(default_factory=dict)   # gpu -> bytes sent to peers
     ingress: dict = field(default_factory=dict)  # gpu -> bytes fetched
 
@@ -71,10 +77,41 @@ def groups_ranges(groups: Sequence[Sequence[int]]) -> dict[int, tuple[int, int]]
     return out
 
 
+def window_for(x: int, y: int, m: int) -> tuple[int, int]:
+    """The m-slice window (base, m) holding shard [x, y): shards are aligned to
+    their size (rank r of TP-N holds [r*8/N, (r+1)*8/N)), so with m a power of
+    two >= y - x the aligned window floor(x / m) * m contains the shard, and
+    two shards either share a window or are disjoint."""
+    m = max(m, y - x)
+    return (x // m) * m, m
+
+
+@dataclass
+class ReshardPlan:
+    """Host reshard plan (``ShardedWeightStore.plan``).
+
+    active[g] / have[g] / window[g]: the new shard, resident slices and arena
+    window of every GPU; fetch[g]: runs (src gpu, lo, hi) of missing slices;
+    relayout[g]: g needs a new arena (its shard left its window), and then
+    local[g] lists the resident slices copied into it."""
+
+    active: dict
+    have: dict
+    window: dict
+    fetch: dict
+    relayout: dict
+    local: dict
+
+
 class ShardedWeightStore:
     def __init__(self, model: ModelGeometry, gpu_ids: Sequence[int],
                  device: str | torch.device = "cuda", devices: dict | None = None,
-                 mode: str = "sharded"):
+                 mode: str = "sharded", max_slices=MAX_TP):
+        """``max_slices``: the window of every GPU's arena, in slices (an int for
+        all or {gpu: int}; a power of two dividing 8). An arena holds one window
+        of every matrix, slice-addressed, so a shard that grows inside its
+        window keeps its resident slices in place and only the missing slices
+        are fetched. Default: the whole matrix (never a relayout copy)."""
         if mode not in ("sharded", "full_copy_per_gpu"):
             raise MigrationError(f"unknown weight storage mode {mode!r}")
         _native.load()
@@ -83,6 +120,12 @@ class ShardedWeightStore:
         self.gpu_ids = tuple(gpu_ids)
         default = torch.device(device)
         self.device_of = {g: torch.device(devices[g]) if devices else default for g in self.gpu_ids}
+        ms = max_slices if isinstance(max_slices, dict) else {g: max_slices for g in self.gpu_ids}
+        self.max_slices = {g: MAX_TP if mode == "full_copy_per_gpu" else int(ms[g])
+                           for g in self.gpu_ids}
+        for g, m in self.max_slices.items():
+            if m < 1 or MAX_TP % m:
+                raise MigrationError(f"gpu {g}: max_slices={m} must divide {MAX_TP}")
         es = model.dtype_bytes
         self.split = [m for m in model.matrices if m.split != "rep"]
         self.replicated = [m for m in model.matrices if m.split == "rep"]
@@ -93,6 +136,9 @@ class ShardedWeightStore:
         self.slice_off = np.concatenate([[0], np.cumsum(self.slice_bytes)[:-1]]).astype(np.int64)
         self.bytes_per_slice = int(self.slice_bytes.sum())
         self.is_col = np.array([m.split == "col" for m in self.split])
+        # slice k of a matrix region starts at k * step: whole rows for a
+        # column-parallel matrix (contiguous), a column block for a row-parallel
+        # one (rows strided by window * step)
         self._step = np.where(self.is_col, self.slice_bytes,
                               np.array([m.cols // MAX_TP for m in self.split], np.int64) * es)
         self._seg_rows = np.where(self.is_col, 1, np.array([m.rows for m in self.split], np.int64))
@@ -100,11 +146,17 @@ class ShardedWeightStore:
         self.cols = np.array([m.cols for m in self.split], dtype=np.int64)
         self.index = {(m.name, m.layer): i for i, m in enumerate(self.split)}
         self.rep_index = {(m.name, m.layer): i for i, m in enumerate(self.replicated)}
-        self.resident: dict[int, tuple[int, int]] = {}
+        self.have: dict[int, frozenset] = {}
+        self.window: dict[int, tuple[int, int]] = {}
         self.active: dict[int, tuple[int, int]] = {}
         self.arena: dict[int, torch.Tensor] = {}
         self.rep_arena: dict[int, torch.Tensor] = {}
         self._segs_dev = {}  # device -> (pinned staging, device scratch) for K2 segments
+
+    @property
+    def resident(self) -> dict[int, tuple[int, int]]:
+        """[lo, hi) hull of every GPU's resident slices."""
+        return {g: (min(h), max(h) + 1) for g, h in self.have.items()}
 
     # ----------------------------------------------------------------- load
     def load(self, groups: Sequence[Sequence[int]], stream: torch.cuda.Stream | None = None) -> None:
@@ -115,30 +167,31 @@ class ShardedWeightStore:
         self.arena.clear()
         for g in self.gpu_ids:
             res = (0, MAX_TP) if self.mode == "full_copy_per_gpu" else act[g]
+            self.window[g] = window_for(*res, self.max_slices[g])
+            self.have[g] = frozenset(range(*res))
+            self.active[g] = act[g]
             dev = self.device_of[g]
             st = stream or torch.cuda.current_stream(dev)
-            self.arena[g] = torch.empty((res[1] - res[0]) * self.bytes_per_slice, dtype=torch.uint8,
+            self.arena[g] = torch.empty(self.window[g][1] * self.bytes_per_slice, dtype=torch.uint8,
                                         device=dev)
-            self.resident[g] = res
-            self.active[g] = act[g]
             rep_bytes = sum(m.rows * m.cols for m in self.replicated) * self.model.dtype_bytes
             self.rep_arena[g] = torch.empty(max(rep_bytes, 16), dtype=torch.uint8, device=dev)
             with torch.cuda.device(dev):
-                self._fill(g, st)
+                self._fill(g, st, *res)
 
-    def _fill(self, g: int, st: torch.cuda.Stream) -> None:
-        a, b = self.resident[g]
-        s = b - a
+    def _fill(self, g: int, st: torch.cuda.Stream, a: int, b: int) -> None:
+        """Synthetic content of slices [a, b) at their window positions."""
+        w0, m_ = self.window[g]
         es = self.model.dtype_bytes
         base = self.arena[g].data_ptr()
         for i, m in enumerate(self.split):
-            ptr = base + s * int(self.slice_off[i])
+            ptr = base + m_ * int(self.slice_off[i]) + (a - w0) * int(self._step[i])
             if m.split == "col":
-                rows = s * (m.rows // MAX_TP)
+                rows = (b - a) * (m.rows // MAX_TP)
                 args = (ptr, rows, m.cols, m.cols, a * (m.rows // MAX_TP), 0)
             else:
-                cols = s * (m.cols // MAX_TP)
-                args = (ptr, m.rows, cols, cols, 0, a * (m.cols // MAX_TP))
+                cps = m.cols // MAX_TP
+                args = (ptr, m.rows, (b - a) * cps, m_ * cps, 0, a * cps)
             _native.call("tpr_matrix_fill", *args, m.cols, m.key, es, st.cuda_stream)
         off = 0
         rbase = self.rep_arena[g].data_ptr()
@@ -148,8 +201,26 @@ class ShardedWeightStore:
             off += m.rows * m.cols * es
 
     # ---------------------------------------------------------------- views
+    def slices(self, gpu: int, name: str, layer: int, x: int, y: int) -> torch.Tensor:
+        """View of slices [x, y) of one matrix on ``gpu`` (all resident)."""
+        es = self.model.dtype_bytes
+        dtype = {1: torch.uint8, 2: torch.bfloat16, 4: torch.float32}[es]
+        i = self.index[(name, layer)]
+        m = self.split[i]
+        w0, m_ = self.window[gpu]
+        if not all(s in self.have[gpu] for s in range(x, y)):
+            raise MigrationError(f"gpu {gpu}: slices [{x}, {y}) of {name} are not resident")
+        lo = m_ * int(self.slice_off[i])
+        mat = self.arena[gpu][lo: lo + m_ * int(self.slice_bytes[i])].view(dtype)
+        if m.split == "col":
+            rps = m.rows // MAX_TP
+            return mat.view(m_ * rps, m.cols)[(x - w0) * rps:(y - w0) * rps]
+        cps = m.cols // MAX_TP
+        return mat.view(m.rows, m_ * cps)[:, (x - w0) * cps:(y - w0) * cps]
+
     def shard(self, gpu: int, name: str, layer: int = -1) -> torch.Tensor:
-        """The TP shard GPU ``gpu`` computes with (a view; never a copy)."""
+        """The TP shard GPU ``gpu`` computes with (a view; never a copy). A
+        row-parallel shard is a strided view (row pitch = the window)."""
         es = self.model.dtype_bytes
         dtype = {1: torch.uint8, 2: torch.bfloat16, 4: torch.float32}[es]
         if (name, layer) in self.rep_index:
@@ -158,109 +229,117 @@ class ShardedWeightStore:
                 off += m.rows * m.cols * es
             m = self.replicated[self.rep_index[(name, layer)]]
             return self.rep_arena[gpu][off: off + m.rows * m.cols * es].view(dtype).view(m.rows, m.cols)
-        i = self.index[(name, layer)]
-        m = self.split[i]
-        a, b = self.resident[gpu]
-        x, y = self.active[gpu]
-        s = b - a
-        lo = s * int(self.slice_off[i])
-        mat = self.arena[gpu][lo: lo + s * int(self.slice_bytes[i])].view(dtype)
-        if m.split == "col":
-            rps = m.rows // MAX_TP
-            return mat.view(s * rps, m.cols)[(x - a) * rps:(y - a) * rps]
-        cps = m.cols // MAX_TP
-        return mat.view(m.rows, s * cps)[:, (x - a) * cps:(y - a) * cps]
+        return self.slices(gpu, name, layer, *self.active[gpu])
 
     def memory_bytes(self, gpu: int) -> int:
-        a, b = self.resident[gpu]
-        return (b - a) * self.bytes_per_slice + self.rep_arena[gpu].numel()
+        return self.window[gpu][1] * self.bytes_per_slice + self.rep_arena[gpu].numel()
 
     # -------------------------------------------------------------- reshard
     def plan(self, new_groups: Sequence[Sequence[int]], parked: Sequence[int] = (),
-             trim: bool = False):
-        """Host reshard planner: new resident ranges, sources of missing slices.
+             trim: bool = False) -> ReshardPlan:
+        """Host reshard planner.
 
-        ``parked`` GPUs leave service (scale-in): they keep their resident
-        slices, which stay available as sources. ``trim`` shrinks a GPU whose
-        resident range is larger than its new shard to exactly that shard (a
-        local compaction copy that frees the extra slices, e.g. for KV pages);
-        without it the shard is a view and the extra slices stay resident for
-        reuse by a later switch. Returns (new_active,
-        new_resident, moves) where moves[g] is a list of (src_gpu, slice_lo,
-        slice_hi) runs building g's new arena (empty when the new shard is a
-        view of resident slices).
-        """
+        A GPU whose new shard is resident is a view (0 bytes). A shard that
+        grows inside its arena window keeps every resident slice in place and
+        fetches only the missing slices (weight_memory("sharded"),
+        migration.py:295-306: the new shard is full/tp, and what is already
+        there is not moved), from peers that hold them, balancing egress. A
+        shard that leaves its window (or outgrows it) gets a new arena: by the
+        alignment of shards it shares no slice with the old window unless it
+        outgrew it, and only then are resident slices copied (``local``).
+
+        ``parked`` GPUs leave service (scale-in) and keep their slices as
+        sources. ``trim`` drops every resident slice outside the new shard
+        (bookkeeping only: the arena keeps its window), so a later switch
+        fetches them again."""
         act = groups_ranges(new_groups)
         if set(act) | set(parked) != set(self.gpu_ids) or set(act) & set(parked):
             raise MigrationError("groups + parked GPUs must cover exactly the store's GPUs")
         egress = {g: 0 for g in self.gpu_ids}
-        new_res, moves = {}, {}
+        out = ReshardPlan(dict(act), {}, {}, {}, {}, {})
         for g in self.gpu_ids:
+            have, win = self.have[g], self.window[g]
+            out.fetch[g], out.local[g], out.relayout[g] = [], [], False
             if g in parked:
-                new_res[g] = self.resident[g]
-                moves[g] = []
+                out.active[g] = self.active[g]
+                out.have[g], out.window[g] = have, win
                 continue
             x, y = act[g]
-            a, b = self.resident[g]
-            if a <= x and y <= b and not (trim and (a, b) != (x, y)):
-                new_res[g] = (a, b)
-                moves[g] = []
-                continue
-            new_res[g] = (x, y)
+            shard = frozenset(range(x, y))
+            w0, m_ = win
+            if w0 <= x and y <= w0 + m_:
+                out.window[g] = win
+                out.have[g] = shard if trim else have | shard
+                missing = [s for s in range(x, y) if s not in have]
+            else:
+                out.window[g] = window_for(x, y, m_)
+                out.relayout[g] = True
+                out.have[g] = shard
+                out.local[g] = [s for s in range(x, y) if s in have]
+                missing = [s for s in range(x, y) if s not in have]
             runs = []
-            for sl in range(x, y):
-                if a <= sl < b:
-                    src = g
-                else:
-                    holders = [h for h in self.gpu_ids
-                               if h != g and self.resident[h][0] <= sl < self.resident[h][1]]
-                    if not holders:
-                        raise MigrationError(f"weight slice {sl} is resident nowhere")
-                    src = min(holders, key=lambda h: (egress[h], self.gpu_ids.index(h)))
-                    egress[src] += self.bytes_per_slice
+            for sl in missing:
+                holders = [h for h in self.gpu_ids if h != g and sl in self.have[h]]
+                if not holders:
+                    raise MigrationError(f"weight slice {sl} is resident nowhere")
+                src = min(holders, key=lambda h: (egress[h], self.gpu_ids.index(h)))
+                egress[src] += self.bytes_per_slice
                 if runs and runs[-1][0] == src and runs[-1][2] == sl:
                     runs[-1][2] = sl + 1
                 else:
                     runs.append([src, sl, sl + 1])
-            moves[g] = [tuple(r) for r in runs]
-        return act, new_res, moves
+            out.fetch[g] = [tuple(r) for r in runs]
+        return out
 
-    def _segments(self, g: int, new_res, moves, new_arena: torch.Tensor) -> np.ndarray:
-        """Copy segments (uint64/int64 x 8 per row, tpr_copy_seg_t layout)."""
-        x, y = new_res[g]
-        s_new = y - x
-        dbase = new_arena.data_ptr()
-        # Within a matrix region of an arena holding s slices, slice k starts at
-        # k * step: whole rows for column-parallel matrices (step = one slice,
-        # contiguous), a column block for row-parallel ones (step = cols/8
-        # elements, rows strided by s * step).
+    def _segments(self, g: int, plan: ReshardPlan, dst_arena, src_arena=None) -> np.ndarray:
+        """Copy segments into g's arena (uint64/int64 x 8 per row,
+        tpr_copy_seg_t layout): the fetched runs, plus the local relayout
+        copies from g's old arena."""
+        dw0, dm = plan.window[g]
+        dbase = dst_arena.data_ptr()
         step = self._step
-        runs = moves[g]
+        runs = list(plan.fetch[g])
+        runs += [(g, s, s + 1) for s in plan.local[g]]
         seg = np.zeros((len(runs), len(self.split), 8), dtype=np.int64)
         for i, (src, lo, hi) in enumerate(runs):
-            ha, hb = self.resident[src]
-            s_src = hb - ha
+            sw0, sm = self.window[src]
+            sbase = (src_arena if (src == g and src_arena is not None) else self.arena[src]).data_ptr()
             row_bytes = (hi - lo) * step
-            seg[i, :, 0] = self.arena[src].data_ptr() + s_src * self.slice_off + (lo - ha) * step
-            seg[i, :, 1] = dbase + s_new * self.slice_off + (lo - x) * step
+            seg[i, :, 0] = sbase + sm * self.slice_off + (lo - sw0) * step
+            seg[i, :, 1] = dbase + dm * self.slice_off + (lo - dw0) * step
             seg[i, :, 2] = self._seg_rows
             seg[i, :, 3] = row_bytes
-            seg[i, :, 4] = np.where(self.is_col, row_bytes, s_src * step)
-            seg[i, :, 5] = np.where(self.is_col, row_bytes, s_new * step)
+            seg[i, :, 4] = np.where(self.is_col, row_bytes, sm * step)
+            seg[i, :, 5] = np.where(self.is_col, row_bytes, dm * step)
         return seg.reshape(-1, 8)
+
+    def _stats(self, plan: ReshardPlan) -> ReshardStats:
+        stats = ReshardStats(egress={g: 0 for g in self.gpu_ids},
+                             ingress={g: 0 for g in self.gpu_ids})
+        for g in self.gpu_ids:
+            if not plan.fetch[g] and not plan.relayout[g]:
+                stats.views += 1
+                continue
+            if not plan.relayout[g]:
+                stats.in_place += 1
+            stats.local_bytes += len(plan.local[g]) * self.bytes_per_slice
+            for src, lo, hi in plan.fetch[g]:
+                nb = (hi - lo) * self.bytes_per_slice
+                stats.remote_bytes += nb
+                stats.egress[src] += nb
+                stats.ingress[g] += nb
+        return stats
 
     def reshard(self, new_groups: Sequence[Sequence[int]], stream: torch.cuda.Stream | None = None,
                 events: tuple | None = None, parked: Sequence[int] = (),
                 trim: bool = False) -> ReshardStats:
-        """Move to ``new_groups``: K2 copies for every GPU whose new shard is not
-        resident; views for the rest. Stream-ordered, no host sync: new arenas
-        are allocated and old ones released on ``stream`` (the caching
-        allocator reuses a block on the same stream only after the K2 that
-        last touched it), so the host may run ahead without holding memory."""
-        act, new_res, moves = self.plan(new_groups, parked, trim)
-        for g in parked:
-            act[g] = new_res[g]
-        stats = ReshardStats(egress={g: 0 for g in self.gpu_ids}, ingress={g: 0 for g in self.gpu_ids})
+        """Move to ``new_groups``: K2 fetches every GPU's missing slices into
+        their window positions (in place), views for the rest. Stream-ordered,
+        no host sync: a relayout arena is allocated and the old one released on
+        ``stream`` (the caching allocator reuses a block on the same stream only
+        after the K2 that last touched it), so the host may run ahead."""
+        plan = self.plan(new_groups, parked, trim)
+        stats = self._stats(plan)
         devs = {self.device_of[g] for g in self.gpu_ids}
         if len(devs) != 1:
             raise MigrationError("multi-device weight reshard goes through the distributed executor")
@@ -268,22 +347,14 @@ class ShardedWeightStore:
         stream = stream or torch.cuda.current_stream(dev)
         new_arena, segs = {}, []
         for g in self.gpu_ids:
-            if not moves[g]:
-                stats.views += 1
+            if not plan.fetch[g] and not plan.relayout[g]:
                 continue
-            x, y = new_res[g]
-            with torch.cuda.stream(stream):
-                new_arena[g] = torch.empty((y - x) * self.bytes_per_slice, dtype=torch.uint8,
-                                           device=dev)
-            segs.append(self._segments(g, new_res, moves, new_arena[g]))
-            for src, lo, hi in moves[g]:
-                nb = (hi - lo) * self.bytes_per_slice
-                if src == g:
-                    stats.local_bytes += nb
-                else:
-                    stats.remote_bytes += nb
-                    stats.egress[src] += nb
-                    stats.ingress[g] += nb
+            dst = self.arena[g]
+            if plan.relayout[g]:
+                with torch.cuda.stream(stream):
+                    dst = new_arena[g] = torch.empty(plan.window[g][1] * self.bytes_per_slice,
+                                                     dtype=torch.uint8, device=dev)
+            segs.append(self._segments(g, plan, dst))
         if events:
             events[0].record(stream)
         if segs:
@@ -296,8 +367,7 @@ class ShardedWeightStore:
             if self.arena[g].device == dev:
                 self.arena[g].record_stream(stream)
             self.arena[g] = t
-        self.resident = new_res
-        self.active = act
+        self.have, self.window, self.active = plan.have, plan.window, plan.active
         self._stream = stream
         return stats
 
@@ -307,22 +377,21 @@ class ShardedWeightStore:
         from .kvcache import _PinnedStaging, _Scratch
 
         n = len(seg)
-        # segments | prefix[n + 1] | dynamic-claim counter (uploaded as 0)
-        buf = np.empty(seg.size + n + 2, dtype=np.int64)
-        buf[: seg.size] = seg.reshape(-1)
-        buf[-1] = 0
-        n_items = ctypes.c_int64(0)
-        _native.call("tpr_copy_prepare", buf.ctypes.data, n, CHUNK_BYTES,
-                     buf.ctypes.data + seg.nbytes, ctypes.byref(n_items))
+        # segments | prefix[n + 1] | dynamic-claim counter, built in pinned
+        # memory; libtpr normalises them, uploads and launches K2 in one call
+        # (the copy engine follows the segment addresses: TMA on local HBM,
+        # 16-byte loads/stores when a slice comes from another GPU)
+        nbytes = int(_native.load().tpr_reshard_buffer_bytes(n))
         if dev not in self._segs_dev:
             self._segs_dev[dev] = (_PinnedStaging(), _Scratch(torch.int64, dev))
         staging, scratch = self._segs_dev[dev]
-        d = scratch.get(buf.size, stream)
+        h_ptr, raw = staging.acquire(nbytes)
+        raw.view(np.int64)[: seg.size] = seg.reshape(-1)
+        d = scratch.get(nbytes // 8, stream)
         with torch.cuda.device(dev):
-            staging.upload(buf, d, stream)
-            _native.call("tpr_weight_reshard", d.data_ptr(), d.data_ptr() + seg.nbytes, n,
-                         n_items.value, CHUNK_BYTES, d.data_ptr() + 8 * (buf.size - 1),
-                         stream.cuda_stream)
+            _native.call("tpr_weight_reshard_host", h_ptr, n, CHUNK_BYTES, d.data_ptr(),
+                         d.numel() * 8, None, stream.cuda_stream)
+        staging.fence(stream)
 
     def finish(self) -> None:
         """Wait for the last reshard's copies."""

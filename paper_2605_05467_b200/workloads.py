@@ -60,30 +60,34 @@ def transition(model, n_gpus, tp_old, tp_new, n_seqs, ctx, weights=True, name=No
 
 def config(idx: int, **kw) -> Workload:
     """BASELINE.json configs[idx] (0-based)."""
+    seqs, ctx = kw.get("seqs"), kw.get("ctx")
     if idx == 0:  # 8B TP1->TP2, 4 x 512, KV only
-        return transition(LLAMA_3_1_8B, 2, 1, 2, kw.get("seqs", 4), kw.get("ctx", 512),
-                          weights=False, name="cfg1 Llama-3.1-8B TP1->TP2 4x512 KV")
+        seqs, ctx = seqs or 4, ctx or 512
+        return transition(LLAMA_3_1_8B, 2, 1, 2, seqs, ctx, weights=False,
+                          name=f"cfg1 Llama-3.1-8B TP1->TP2 {seqs}x{ctx} KV")
     if idx == 1:  # 8B TP2->TP4, 64 x 4k + weights
-        return transition(LLAMA_3_1_8B, 4, 2, 4, kw.get("seqs", 64), kw.get("ctx", 4096),
-                          weights=kw.get("weights", True),
-                          name="cfg2 Llama-3.1-8B TP2->TP4 64x4096 KV+weights")
+        seqs, ctx = seqs or 64, ctx or 4096
+        w = kw.get("weights", True)
+        return transition(LLAMA_3_1_8B, 4, 2, 4, seqs, ctx, weights=w,
+                          name=f"cfg2 Llama-3.1-8B TP2->TP4 {seqs}x{ctx} KV" + ("+weights" if w else ""))
     if idx == 2:  # 8B TP8 -> TP1 on GPU0 (scale-in), 64 x 4k
         m = LLAMA_3_1_8B
         gpus = tuple(range(8))
-        reqs = [(i, kw.get("ctx", 4096)) for i in range(kw.get("seqs", 64))]
+        seqs, ctx = seqs or 64, ctx or 4096
+        reqs = [(i, ctx) for i in range(seqs)]
         old = [KvLayout(gpus, 8, m.n_kv_heads, tuple(reqs))]
         new = [KvLayout((0,), 1, m.n_kv_heads, tuple(reqs))] + [
             KvLayout((g,), 1, m.n_kv_heads, ()) for g in gpus[1:]]
         w = kw.get("weights", True)
-        return Workload("cfg3 Llama-3.1-8B TP8->TP1 consolidation 64x4096", m, gpus, old, new,
+        return Workload(f"cfg3 Llama-3.1-8B TP8->TP1 consolidation {seqs}x{ctx}", m, gpus, old, new,
                         [gpus] if w else None, [(0,)] if w else None, parked=gpus[1:],
                         trim_on_reverse=True)
     if idx == 3:  # 70B TP4 <-> TP8, 8 x 32k
-        return transition(LLAMA_3_1_70B, 8, 4, 8, kw.get("seqs", 8), kw.get("ctx", 32768),
-                          weights=kw.get("weights", False),
-                          name="cfg4 Llama-3.1-70B TP4->TP8 8x32768")
+        seqs, ctx = seqs or 8, ctx or 32768
+        return transition(LLAMA_3_1_70B, 8, 4, 8, seqs, ctx, weights=kw.get("weights", False),
+                          name=f"cfg4 Llama-3.1-70B TP4->TP8 {seqs}x{ctx}")
     if idx == 4:  # the north star's headline: Llama-3.1-8B at 32k context, TP2 <-> TP4 + weights
-        return transition(LLAMA_3_1_8B, 4, 2, 4, kw.get("seqs", 8), kw.get("ctx", 32768),
-                          weights=kw.get("weights", True),
-                          name="headline Llama-3.1-8B TP2->TP4 8x32768 KV+weights")
+        seqs, ctx = seqs or 8, ctx or 32768
+        return transition(LLAMA_3_1_8B, 4, 2, 4, seqs, ctx, weights=kw.get("weights", True),
+                          name=f"headline Llama-3.1-8B TP2->TP4 {seqs}x{ctx} KV+weights")
     raise ValueError(idx)

@@ -1,7 +1,10 @@
 """One process per GPU slot. CPU: the handshake and plan partition logic over
 gloo with world_size 2. GPU: the full push-model migration with 2 and 4
-processes sharing ONE B200 through CUDA IPC; pools, block tables and rings
-of all ranks together must equal the oracle's replay bit for bit."""
+processes through CUDA IPC; pools, block tables and rings of all ranks
+together must equal the oracle's replay bit for bit. Each rank takes GPU
+``rank % device_count``: one GPU per rank on a multi-GPU node (peer pools over
+NVLink, the copy engine libtpr picks for peer mappings), all ranks on one
+device otherwise (the gpurun boxes)."""
 
 import os
 import tempfile
@@ -17,6 +20,13 @@ from conftest import ROOT
 
 def _init(rank, world, path):
     dist.init_process_group("gloo", init_method=f"file://{path}", rank=rank, world_size=world)
+
+
+def _device(rank):
+    """This rank's GPU: its own when the node has one per rank, else shared."""
+    dev = torch.device("cuda", rank % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    return dev
 
 
 def _handshake_worker(rank, world, path, q):
@@ -74,14 +84,14 @@ def _gpu_worker(rank, world, path, outdir, q):
         from paper_2605_05467_b200 import geometry, migration as M, workloads
         from paper_2605_05467_b200.distributed import DistributedKvCluster
         _init(rank, world, path)
-        torch.cuda.set_device(0)
+        dev = _device(rank)
         kv = geometry.KvGeometry(layers=2, head_dim=32, total_heads=8)
         gpus = tuple(range(world))
         reqs = [(i, 5 + 29 * i) for i in range(7)]
         lays = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8)
                 for tp in (1, 2, 4) if tp <= world}
         c = DistributedKvCluster(kv, gpus, units_per_gpu=512, max_requests=8, max_blocks=16,
-                                 device=torch.device("cuda", 0), fragmented=True, seed=rank)
+                                 device=dev, fragmented=True, seed=rank)
         c.admit(lays[1], seed=17)
         seq = [1, world, 1] if world == 2 else [1, 2, 4, 2]
         for i, (a, b) in enumerate(zip(seq, seq[1:])):
@@ -95,6 +105,11 @@ def _gpu_worker(rank, world, path, outdir, q):
                 c.migrate(plan)
             np.savez(os.path.join(outdir, f"after_{i}_{rank}.npz"), **c.snapshot())
         v = c.verify()
+        from paper_2605_05467_b200 import _native
+        k1_engine, _ = _native.last_engines()
+        # peer pools on another GPU never take the TMA engine
+        if torch.cuda.device_count() >= world:
+            assert k1_engine == "vector", k1_engine
         c.close()
         dist.destroy_process_group()
         q.put((rank, v, len(seq) - 1))
@@ -111,13 +126,12 @@ def _exec_worker(rank, world, path, q, device_barrier=True):
         from paper_2605_05467_b200.distributed import (DistributedExecutor, DistributedKvCluster,
                                                        DistributedWeightStore)
         _init(rank, world, path)
-        torch.cuda.set_device(0)
+        dev = _device(rank)
         model = geometry.tiny_geometry()
         gpus = tuple(range(world))
         reqs = [(i, 9 + 17 * i) for i in range(6)]
         tps = [t for t in (1, 2, 4) if t <= world]
         lays = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in tps}
-        dev = torch.device("cuda", 0)
         kv = DistributedKvCluster(model.kv, gpus, units_per_gpu=512, max_requests=8, max_blocks=16,
                                   device=dev, fragmented=True, seed=rank)
         kv.admit(lays[1], seed=5)
@@ -149,8 +163,7 @@ def _barrier_timeout_worker(rank, world, path, q):
         from paper_2605_05467_b200.distributed import DeviceBarrier
         from paper_2605_05467_b200.migration import MigrationError
         _init(rank, world, path)
-        torch.cuda.set_device(0)
-        bar = DeviceBarrier(torch.device("cuda", 0), timeout_s=0.5)
+        bar = DeviceBarrier(_device(rank), timeout_s=0.5)
         st = torch.cuda.Stream()
         bar(st)                      # both ranks arrive: passes
         st.synchronize()
@@ -247,3 +260,61 @@ def test_multiprocess_push_migration_bit_exact(world):
                 live = np.arange(heads[r], tails[r]) % 512
                 assert np.array_equal(after[r]["ring"][live], rings[r][live]), (i, r)
                 assert list(after[r]["ring_head"]) == heads and list(after[r]["ring_tail"]) == tails
+
+
+def _abort_worker(rank, world, path, q):
+    import sys
+    sys.path.insert(0, str(ROOT))
+    try:
+        from paper_2605_05467_b200 import geometry, workloads
+        from paper_2605_05467_b200.distributed import DistributedExecutor, DistributedKvCluster
+        from paper_2605_05467_b200.migration import MigrationError
+        _init(rank, world, path)
+        dev = _device(rank)
+        kv = geometry.KvGeometry(layers=2, head_dim=32, total_heads=8)
+        gpus = (0, 1)
+        reqs = [(i, 20 + 9 * i) for i in range(4)]
+        lays = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2)}
+        c = DistributedKvCluster(kv, gpus, units_per_gpu=256, max_requests=4, max_blocks=8,
+                                 device=dev, fragmented=True, seed=rank)
+        c.admit(lays[1], seed=3)
+        ex = DistributedExecutor(c, device_barrier=True, barrier_timeout_s=0.5)
+        before = c.snapshot()
+        raised = None
+        if rank == 0:  # rank 1 never arrives: the start barrier times out, K3 + K1 abort
+            try:
+                ex.switch(lays[1], lays[2])
+                raised = False
+            except MigrationError:
+                raised = True
+            try:  # and the executor refuses further switches
+                ex.switch(lays[1], lays[2])
+                raised = False
+            except MigrationError as exc:
+                raised = raised and "rebuild" in str(exc)
+        dist.barrier()
+        after = c.snapshot()
+        same = all(np.array_equal(before[k], after[k]) for k in ("pool", "block_table", "ring"))
+        q.put((rank, raised, same))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc(), None))
+
+
+@pytest.mark.gpu
+def test_start_barrier_timeout_aborts_the_switch():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "store")
+        procs = [ctx.Process(target=_abort_worker, args=(r, 2, path, q), daemon=True)
+                 for r in range(2)]
+        for p in procs:
+            p.start()
+        res = sorted((q.get(timeout=180) for _ in procs), key=lambda x: x[0])
+        for p in procs:
+            p.join(timeout=60)
+    # no table, ring or pool byte changed on either rank
+    assert res == [(0, True, True), (1, None, True)], res

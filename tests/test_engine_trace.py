@@ -21,7 +21,7 @@ def test_plans_match_reference_engine():
     for e in doc["events"]:
         plan = R.plan_for(e, prof["kv_bytes_per_token_per_head"], prof["total_kv_heads"])
         assert plan.total_bytes == e["total_bytes"]
-        assert len(plan) == e["transfers"]
+        assert plan.n_transfers == e["transfers"]
         n_calls += len(e["calls"])
     assert n_calls == 75  # 75 head_transfers calls on demo.yaml
 

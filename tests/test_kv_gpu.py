@@ -224,7 +224,7 @@ def test_one_call_switch_edge_cases():
     c = make(TINY, gpus, units=64, reqs=4, blocks=4)
     c.admit(tp2, seed=1)
     plan, st = c.switch_layouts(tp2, tp2)  # identity: empty plan, nothing launched
-    assert len(plan) == 0 and st.units == 0
+    assert plan.n_transfers == 0 and st.units == 0
     plan, st = c.switch_layouts(tp2, tp4)
     assert plan.total_bytes == M.plan_repartition(tp2, tp4, TINY.kv_bytes_per_token_per_head).total_bytes
     assert c.placement() == M.layout_placement(tp4)
@@ -388,7 +388,7 @@ def test_zero_context_request_moves_nothing():
     new = M.KvLayout((0, 1), 2, 8, ((5, 0),))
     c.admit(old, seed=1)
     plan = M.plan_repartition(old, new, TINY.kv_bytes_per_token_per_head)
-    assert len(plan) == 1 and plan.total_bytes == 0
+    assert plan.n_transfers == 1 and plan.total_bytes == 0
     migrate_and_compare(c, plan)
 
 

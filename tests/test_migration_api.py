@@ -224,6 +224,11 @@ def test_plan_is_a_dataclass_like_the_reference():
     assert plan == M.MigrationPlan(list(plan.transfers), 0.5, {})
     for cls in (M.KvLayout, M.Transfer, M.CostModelParams):
         assert dataclasses.is_dataclass(cls)
+    # like the reference dataclass: `transfers` is required, an empty plan is truthy
+    with pytest.raises(TypeError):
+        M.MigrationPlan()
+    empty = M.plan_repartition([lay([1], 8, [(0, 10)])], [lay([1], 8, [(0, 10)])], 4096)
+    assert empty and empty.n_transfers == 0 and not hasattr(M.MigrationPlan, "__len__")
 
 
 def test_plan_mutation_keeps_array_in_sync():

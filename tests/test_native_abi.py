@@ -13,7 +13,7 @@ from paper_2605_05467_b200 import _native
 
 def declared_symbols():
     text = (ROOT / "include" / "tpr.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tpr_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(tpr_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -121,3 +121,50 @@ def test_weight_oracle_shards():
     assert seen.all() and np.array_equal(f, full)
     with pytest.raises(ValueError):
         W.assemble_full([(0, 0, full[:4]), (2, 0, full[:4])], 8, 8)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_c_and_python_oracles_agree_on_error_rules(seed):
+    # the K3 error rules (tpr_kernels.cu k3_page): a page with a missing source,
+    # an occupied destination, an index outside the table or a poisoned ring slot
+    # is not touched, and the ring positions are still consumed
+    rng = np.random.default_rng(100 + seed)
+    geo = dict(layers=1, head_dim=8, dtype_bytes=2, block_tokens=4, total_heads=4, max_blocks=3,
+               n_req_slots=3, n_units=24)
+    state = _random_cluster(rng, 3, geo, 24, 3)
+    a = [[x.copy() for x in part] if isinstance(part, list) and hasattr(part[0], "copy") else list(part)
+         for part in state]
+    b = [[x.copy() for x in part] if isinstance(part, list) and hasattr(part[0], "copy") else list(part)
+         for part in state]
+    statuses = set()
+    for _ in range(8):
+        n = int(rng.integers(1, 6))
+        rec = np.stack([rng.integers(-1, 3, n), rng.integers(-1, 3, n), rng.integers(0, 4, n),
+                        rng.integers(0, 3, n), rng.integers(3, 5, n), rng.integers(0, 16, n)], 1)
+        rec = rec.astype(np.int64)
+        ra = kvmove.kv_migrate(geo, a[0], a[1], a[2], a[3], a[4], rec, 1)
+        rb = kvmove.kv_migrate_py(geo, b[0], b[1], b[2], b[3], b[4], rec)
+        assert ra == rb
+        a[3], a[4] = ra[2], ra[3]
+        b[3], b[4] = rb[2], rb[3]
+        statuses.add(ra[1])
+        for x, y in zip(a[0] + a[1] + a[2], b[0] + b[1] + b[2]):
+            assert np.array_equal(x, y)
+    assert any(s & 1 for s in statuses) and any(s & 8 for s in statuses)
+
+
+def test_tables_only_replay_matches_full_replay():
+    rng = np.random.default_rng(7)
+    geo = dict(layers=1, head_dim=8, dtype_bytes=2, block_tokens=4, total_heads=4, max_blocks=8,
+               n_req_slots=4, n_units=64)
+    pools, tables, rings, h, t = _random_cluster(rng, 2, geo, 64, 4)
+    adm = np.array([(-1, r % 2, r, 0, 4, 5 + 7 * r) for r in range(4)], np.int64)
+    mv = np.array([(r % 2, 1 - r % 2, r, 0, 4, 5 + 7 * r) for r in range(4)], np.int64)
+    full = kvmove.kv_migrate(geo, pools, tables, rings, h, t, adm)
+    t2 = [x.copy() for x in tables]
+    r2 = [x.copy() for x in rings]
+    want = kvmove.kv_migrate(geo, pools, tables, rings, full[2], full[3], mv)
+    got = kvmove.kv_migrate(geo, None, t2, r2, full[2], full[3], mv)
+    assert got == want
+    for x, y in zip(tables + rings, t2 + r2):
+        assert np.array_equal(x, y)

@@ -22,15 +22,13 @@ def host_pieces(store):
     """{matrix index: [(row0, col0, ndarray)]} from every GPU's resident slices."""
     out = {}
     for g in store.gpu_ids:
-        a, b = store.resident[g]
-        saved = store.active[g]
-        store.active[g] = (a, b)
-        for i, m in enumerate(store.split):
-            v = store.shard(g, m.name, m.layer).cpu().view(torch.int16).numpy().view(np.uint16)
-            r0 = a * (m.rows // 8) if m.split == "col" else 0
-            c0 = a * (m.cols // 8) if m.split == "row" else 0
-            out.setdefault(i, []).append((r0, c0, v.copy()))
-        store.active[g] = saved
+        for a in sorted(store.have[g]):
+            for i, m in enumerate(store.split):
+                v = store.slices(g, m.name, m.layer, a, a + 1)
+                v = v.cpu().view(torch.int16).numpy().view(np.uint16)
+                r0 = a * (m.rows // 8) if m.split == "col" else 0
+                c0 = a * (m.cols // 8) if m.split == "row" else 0
+                out.setdefault(i, []).append((r0, c0, v.copy()))
     return out
 
 
@@ -61,28 +59,32 @@ def test_all_transitions_bit_exact(tp_old, tp_new):
     local, remote, views = expected_volume(workloads.tp_groups(gpus, tp_old), new_groups,
                                            store.bytes_per_slice)
     assert (stats.local_bytes, stats.remote_bytes, stats.views) == (local, remote, views)
-    # every rebuilt shard is exactly weight_memory("sharded", tp_new) of the
-    # split matrices (replicated norms never move)
+    # what a GPU fetches is its new shard, weight_memory("sharded", tp_new) of
+    # the split matrices (replicated norms never move), minus what it held
     rep = sum(m.rows * m.cols for m in store.replicated) * MODEL.dtype_bytes
     per_gpu = M.weight_memory("sharded", MODEL, tp=tp_new) * 1e9 - rep / tp_new
-    assert (stats.local_bytes + stats.remote_bytes) == pytest.approx((8 - views) * per_gpu)
+    old, new = groups_ranges(workloads.tp_groups(gpus, tp_old)), groups_ranges(new_groups)
+    held = sum(max(0, min(old[g][1], y) - max(old[g][0], x)) for g, (x, y) in new.items()
+               if not (old[g][0] <= x and y <= old[g][1]))
+    assert stats.local_bytes == 0
+    assert stats.remote_bytes == pytest.approx((8 - views) * per_gpu - held * store.bytes_per_slice)
     store.finish()
 
 
 def expected_volume(old_groups, new_groups, per_slice):
     """Independent count: a GPU whose new slice range lies inside its old one
-    is a view; otherwise it copies the overlap locally and fetches the rest."""
+    is a view; otherwise its resident slices stay in place (slice-addressed
+    arena) and exactly the missing ones are fetched -- no local copy."""
     old, new = groups_ranges(old_groups), groups_ranges(new_groups)
-    local = remote = views = 0
+    remote = views = 0
     for g, (x, y) in new.items():
         a, b = old[g]
         if a <= x and y <= b:
             views += 1
             continue
         inter = max(0, min(b, y) - max(a, x))
-        local += inter
         remote += (y - x) - inter
-    return local * per_slice, remote * per_slice, views
+    return 0, remote * per_slice, views
 
 
 def test_sequence_reuses_resident_slices():
@@ -101,19 +103,48 @@ def test_sequence_reuses_resident_slices():
     store.finish()
 
 
-def test_trim_compacts_and_stays_bit_exact():
+def test_trim_drops_slices_and_regrowth_fetches_them_in_place():
     gpus = (0, 1, 2, 3)
     store = ShardedWeightStore(MODEL, gpus)
     store.load(workloads.tp_groups(gpus, 4))
-    store.reshard(workloads.tp_groups(gpus, 1))          # every GPU gathers all 8 slices
+    grow = store.reshard(workloads.tp_groups(gpus, 1))   # every GPU gathers all 8 slices
+    assert grow.local_bytes == 0 and grow.remote_bytes == 4 * 6 * store.bytes_per_slice
+    assert grow.in_place == 4
     pieces = host_pieces(store)
     kept = store.reshard(workloads.tp_groups(gpus, 2))   # views: the full copy stays resident
     assert kept.views == 4 and kept.bytes == 0
-    trimmed = store.reshard(workloads.tp_groups(gpus, 2), trim=True)  # compact to TP2 halves
-    assert trimmed.remote_bytes == 0 and trimmed.local_bytes == 4 * 4 * store.bytes_per_slice
+    trimmed = store.reshard(workloads.tp_groups(gpus, 2), trim=True)  # drop to TP2 halves
+    assert trimmed.bytes == 0 and trimmed.views == 4
     assert store.resident == groups_ranges(workloads.tp_groups(gpus, 2))
     torch.cuda.synchronize()
     check_against_oracle(store, pieces, workloads.tp_groups(gpus, 2))
+    assert store.verify() == 0
+    regrow = store.reshard(workloads.tp_groups(gpus, 1))  # the dropped halves come back
+    assert regrow.local_bytes == 0 and regrow.remote_bytes == 4 * 4 * store.bytes_per_slice
+    torch.cuda.synchronize()
+    check_against_oracle(store, pieces, workloads.tp_groups(gpus, 1))
+    store.finish()
+
+
+def test_window_change_and_overflow():
+    # windows of 2 slices: TP4 -> TP4 in another rank order leaves the window
+    # (a new arena, everything fetched); TP4 -> TP2 outgrows it (the one case
+    # with a local relayout copy)
+    gpus = (0, 1, 2, 3)
+    store = ShardedWeightStore(MODEL, gpus, max_slices=2)
+    store.load(workloads.tp_groups(gpus, 4))
+    pieces = host_pieces(store)
+    s = store.reshard([(3, 2, 1, 0)])
+    torch.cuda.synchronize()
+    check_against_oracle(store, pieces, [(3, 2, 1, 0)])
+    assert s.local_bytes == 0 and s.remote_bytes == 4 * 2 * store.bytes_per_slice
+    assert store.window == {3: (0, 2), 2: (2, 2), 1: (4, 2), 0: (6, 2)}
+    s = store.reshard([(3, 2), (1, 0)])
+    torch.cuda.synchronize()
+    check_against_oracle(store, pieces, [(3, 2), (1, 0)])
+    # GPU3 and GPU0 keep 2 of their 4 new slices (copied into the larger
+    # arena), GPU2 and GPU1 hold none of theirs: 4 local + 12 fetched slices
+    assert s.local_bytes == 4 * store.bytes_per_slice and s.remote_bytes == 12 * store.bytes_per_slice
     assert store.verify() == 0
     store.finish()
 
@@ -172,7 +203,7 @@ def test_scale_in_parks_gpus():
     s = store.reshard([(0,)], parked=gpus[1:])
     torch.cuda.synchronize()
     split_bytes = sum(m.rows * m.cols for m in store.split) * MODEL.dtype_bytes
-    assert s.remote_bytes == 7 * split_bytes // 8 and s.local_bytes == split_bytes // 8
+    assert s.remote_bytes == 7 * split_bytes // 8 and s.local_bytes == 0
     assert store.verify() == 0
     # egress balanced: every parked GPU serves exactly its own slice
     assert sorted(v for g, v in s.egress.items() if g) == [split_bytes // 8] * 7

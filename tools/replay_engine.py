@@ -92,7 +92,7 @@ def replay(events, kv, gpus, verify=True, reps=3):
             ok = ok and c.placement() == want
         c.release([rid for _, _, rid, _ in e["calls"]])
         rows.append({"event": i, "t_sim_s": e["t"], "calls": len(e["calls"]),
-                     "transfers": len(plan), "bytes": plan.total_bytes,
+                     "transfers": plan.n_transfers, "bytes": plan.total_bytes,
                      "reference_plan_bytes": e["total_bytes"],
                      "reference_plan_transfers": e["transfers"],
                      "modeled_switch_cost_ms": e["modeled_switch_cost_ms"],
