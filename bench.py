@@ -476,18 +476,32 @@ def cpu_model() -> str:
 
 def cpu_host_bytes(w, n_seqs: int) -> int:
     """Host bytes the CPU arm holds for ``n_seqs`` of the workload: KV pools at
-    their peak plus the weight slices of the largest shards (whole model at
-    most)."""
+    their peak plus the weight slices at their peak over a few alternating
+    switches (held + fetched before the replaced ones are freed)."""
     reqs = w.requests[:n_seqs]
     kv = sum(cpu_units(w, reqs)) * w.model.kv.unit_bytes
     if w.old_weight_groups is None:
         return kv
-    frac = n_seqs / len(w.requests)
+    from paper_2605_05467_b200.weights import groups_ranges
     m = cpu_windows(w)
-    return kv + int(sum(min(2 * x, 8) for x in m.values()) * cpu_slice_bytes(w, frac))
+    ranges = {True: groups_ranges(w.new_weight_groups), False: groups_ranges(w.old_weight_groups)}
+    held = {g: dict.fromkeys(range(*ranges[False][g])) for g in w.gpus}
+    win = {g: _window(*ranges[False][g], m[g]) for g in w.gpus}
+    peak = sum(len(h) for h in held.values())
+    fwd = True
+    for _ in range(4):
+        moves, win, keep = cpu_weight_step(held, win, ranges[fwd], set(w.parked) if fwd else set(),
+                                           w.trim_on_reverse and not fwd)
+        peak = max(peak, sum(len(h) for h in held.values()) + len(moves))
+        for g in held:
+            held[g] = {sl: None for sl in held[g] if sl in keep[g]}
+        for g, sl, _ in moves:
+            held[g][sl] = None
+        fwd = not fwd
+    return kv + peak * cpu_slice_bytes(w, n_seqs / len(w.requests))
 
 
-def cpu_sample_seqs(w, requested: int | None, budget_frac: float = 0.45) -> int:
+def cpu_sample_seqs(w, requested: int | None, budget_frac: float = 0.6) -> int:
     """The whole workload (``requested`` None) when it fits ``budget_frac`` of
     the host's available memory, else the largest sample that does."""
     import psutil
@@ -643,7 +657,7 @@ def run_distributed(args, w, rank: int, world: int, local: int):
                     egress[g] += wst.egress.get(g, 0)
                     ingress[g] += wst.ingress.get(g, 0)
             # this rank's kernels: 2 device barriers, K3 (+ K1) over its pushes, K2 pull
-            launches += (2 if ex.barrier is not None else 0) + _native.kv_switch_launches(ks.units) \
+            launches += (2 if ex.barrier is not None else 0) + _native.kv_switch_launches(ks.units, ks.transfers) \
                 + (1 if wst and wst.segments else 0)
             h2d += plan.n_transfers * 24 + (wst.segments * 72 + 8 if wst and wst.segments else 0)
         wall = time.perf_counter() - t0
@@ -695,10 +709,10 @@ def run_distributed(args, w, rank: int, world: int, local: int):
 # main
 # ---------------------------------------------------------------------------
 
-def measure_single(args, w, device, cpu: bool, e2e_on: bool = True) -> dict:
+def measure_single(args, w, device, with_cpu: bool, e2e_on: bool = True) -> dict:
     """One GPU, logical ranks: the device-timed switches, the end-to-end public
     call, the full-size correctness property and (``cpu``) the reference's CPU
-    path on the same workload. Returns the JSON fields."""
+    path on the same workload (``with_cpu``). Returns the JSON fields."""
     import torch
     from paper_2605_05467_b200 import _native
     from paper_2605_05467_b200.controller import host_to_device_bytes
@@ -733,7 +747,7 @@ def measure_single(args, w, device, cpu: bool, e2e_on: bool = True) -> dict:
     k1_ms = [r.events["k1_start"].elapsed_time(r.events["k1_end"]) for r in results]
     k2_ms = [r.events["k2_start"].elapsed_time(r.events["k2_end"]) for r in results
              if r.weights is not None and r.weights.segments]
-    launches = sum(_native.kv_switch_launches(r.kv.units)
+    launches = sum(_native.kv_switch_launches(r.kv.units, r.kv.transfers)
                    + (1 if r.weights is not None and r.weights.segments else 0) for r in results)
     status = int(ex.kv.status.item())
 
@@ -783,7 +797,7 @@ def measure_single(args, w, device, cpu: bool, e2e_on: bool = True) -> dict:
         except (OSError, ValueError):
             traffic = None
     cpu = None
-    if cpu:
+    if with_cpu:
         r = run_cpu_reference(w, 2, 1, args.cpu_sample_seqs, min_seconds=args.cpu_seconds)
         cpu = {"value": r["value"], "unit": "GB/s", "cores": r["threads"], "kind": "port",
                "sample": r["sample"], "cpu": cpu_model(), "ms_per_step": r["ms_per_step"],
@@ -869,7 +883,7 @@ def main():
         return
     device = torch.device("cuda", 0)
     torch.cuda.set_device(device)
-    m = measure_single(args, w, device, cpu=not args.no_cpu, e2e_on=not args.no_e2e)
+    m = measure_single(args, w, device, with_cpu=not args.no_cpu, e2e_on=not args.no_e2e)
     copy_peak = copy_peak_in_run(device)
     m["roofline"]["copy_peak_in_run"] = copy_peak
     m["roofline"]["frac_vs_copy_in_run"] = m["roofline"]["achieved"] / copy_peak
@@ -877,7 +891,7 @@ def main():
     if not args.no_headline and args.config != 4 and args.seqs is None:
         # the north star's headline in the same run: Llama-3.1-8B at 32k context
         wh = build_workload(4, None)
-        h = measure_single(args, wh, device, cpu=not args.no_cpu, e2e_on=True)
+        h = measure_single(args, wh, device, with_cpu=not args.no_cpu, e2e_on=True)
         headline = {
             "workload": wh.name, "ms_per_switch": h["ms"] / args.steps,
             "e2e_ms_per_switch": h["e2e"]["ms_per_step"], "gbs": h["value"],

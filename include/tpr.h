@@ -107,8 +107,13 @@ typedef struct tpr_kv_cluster {
 #define TPR_META_FIELDS 4
 
 /* totals output of K3 (int64): [0] units processed by this caller,
- * [1+g] units allocated on slot g, [1+TPR_MAX_GPUS+g] units released on g. */
-#define TPR_TOTALS_LEN (1 + 2 * TPR_MAX_GPUS)
+ * [1+g] units allocated on slot g, [1+TPR_MAX_GPUS+g] units released on g;
+ * [TPR_TOTALS_K31_DONE], [TPR_TOTALS_K31_STATUS] are scratch words of the
+ * fused small-switch kernel. The caller zero-initialises d_totals once; the
+ * kernels leave the scratch words zero between calls. */
+#define TPR_TOTALS_K31_DONE (1 + 2 * TPR_MAX_GPUS)
+#define TPR_TOTALS_K31_STATUS (2 + 2 * TPR_MAX_GPUS)
+#define TPR_TOTALS_LEN (3 + 2 * TPR_MAX_GPUS)
 
 /* ---- host utilities -------------------------------------------------- */
 /* Copy engine of K1 and K2 (process-wide): TPR_ENGINE_BULK (default) = TMA
@@ -135,7 +140,13 @@ int tpr_get_copy_engine(void);
  *   "tensor_partial" [TPR_TENSOR_PARTIAL, 1]: K1 (TMA engine) moves partial
  *                   pages as TMA tensor boxes (token x planes) instead of
  *                   one short copy per plane: 0 never, 1 when a page of the
- *                   plan is partial, 2 the tensor kernel for every plan.
+ *                   plan is partial, 2 the tensor kernel for every plan;
+ *   "k31"           [TPR_K31, 1]: a plan of at most k3_fuse_units pages and 96
+ *                   transfers (host records, TMA engine, local pools) runs as
+ *                   ONE kernel, K31: every CTA redoes the keyed scan of the
+ *                   records (kernel parameters) and owns whole pages, doing
+ *                   their bookkeeping and their copy (ring TPR_BULK_K31
+ *                   [6x32768]). The fused path leaves d_xfers unfilled.
  * tpr_get_tuning returns the current value, -1 for an unknown key. Two
  * read-only keys report the engine the last K1 / K2 launch used
  * ("k1_engine_last", "k2_engine_last": TPR_ENGINE_*, -1 before the first):

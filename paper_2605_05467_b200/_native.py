@@ -17,7 +17,7 @@ TPR_ABI_VERSION = 1
 TPR_MAX_GPUS = 16
 TPR_XFER_FIELDS = 6
 TPR_META_FIELDS = 4
-TPR_TOTALS_LEN = 1 + 2 * TPR_MAX_GPUS
+TPR_TOTALS_LEN = 3 + 2 * TPR_MAX_GPUS  # + 2 scratch words of the fused small switch
 TPR_STATUS_WRONG_SOURCE = 1
 TPR_STATUS_DST_OCCUPIED = 2
 TPR_STATUS_BARRIER_TIMEOUT = 4
@@ -194,7 +194,7 @@ def k3_fuse_units() -> int:
     return int(load().tpr_get_tuning(b"k3_fuse_units"))
 
 
-TUNING_KEYS = ("k3_fuse_units", "pdl", "zero_copy", "tensor_partial", "bulk_ws", "k1_dynamic")
+TUNING_KEYS = ("k3_fuse_units", "pdl", "zero_copy", "tensor_partial", "bulk_ws", "k1_dynamic", "k31")
 
 
 def set_tuning(key: str, value: int) -> None:
@@ -206,11 +206,17 @@ def get_tuning(key: str) -> int:
     return int(load().tpr_get_tuning(key.encode()))
 
 
-def kv_switch_launches(units: int) -> int:
-    """Kernels one tpr_kv_switch launches: K3 (fused, or scan + remap) + K1."""
+def kv_switch_launches(units: int, n_transfers: int = 0) -> int:
+    """Kernels one tpr_kv_switch launches: K31 alone for a small plan (<=
+    k3_fuse_units pages, <= 96 transfers, TMA engine), else K3 (fused, or scan +
+    remap) + K1."""
     if units <= 0:
         return 0
-    return 2 if units <= k3_fuse_units() else 3
+    if units <= k3_fuse_units():
+        if 0 < n_transfers <= 96 and get_tuning("k31") and copy_engine() == "bulk":
+            return 1
+        return 2
+    return 3
 
 
 def set_copy_engine(name: str) -> None:

@@ -20,7 +20,8 @@ INCLUDE = ROOT / "include"
 LIB = PKG / "libtpr.so"
 
 SOURCES = [CSRC / "tpr_kernels.cu", CSRC / "tpr_bulk.cu", CSRC / "tpr_api.cpp", CSRC / "tpr_host.cpp"]
-HEADERS = [INCLUDE / "tpr.h", CSRC / "tpr_common.cuh", CSRC / "tpr_internal.h"]
+HEADERS = [INCLUDE / "tpr.h", CSRC / "tpr_common.cuh", CSRC / "tpr_internal.h",
+           CSRC / "tpr_k3page.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -122,7 +122,8 @@ int64_t env_i64(const char* name, int64_t dflt);
 
 // Launch-path knobs (process-wide): initialised from the environment, changed
 // at run time with tpr_set_tuning (tests cover every combination).
-std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1}, g_tensor{-1}, g_ws{-1}, g_dyn{-1};
+std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1}, g_tensor{-1}, g_ws{-1}, g_dyn{-1},
+    g_k31{-1};
 
 int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
   int64_t v = k.load(std::memory_order_relaxed);
@@ -132,6 +133,16 @@ int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
     k.store(v, std::memory_order_relaxed);
   }
   return v;
+}
+
+// pinned or pageable host memory (the CPU can read it); not device memory
+bool host_readable(const int32_t* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return true;  // unregistered host memory
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
 }
 
 const int32_t* device_view(const int32_t* h) {
@@ -396,6 +407,25 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   bool mirrored = false;
+  // small plans: the whole switch in one launch (K31), the records passed as
+  // kernel parameters -- needs host records, the TMA engine on local pools
+  if (n_xfers > 0 && n_units > 0 && h_xfers && n_xfers <= kK31Xfers && n_units <= k3_fuse_units() &&
+      knob(g_k31, "TPR_K31", 1) && g_engine.load() == TPR_ENGINE_BULK &&
+      all_local(cp.pool, cl->n_gpus) && host_readable(h_xfers)) {
+    const bool timed = k1_events && k1_events[0] && k1_events[1];
+    if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[0]), st)) != cudaSuccess)
+      return cuda_fail(e, "tpr_kv_switch K31 start event");
+    e = launch_k31(*geo, copy_params(geo), cp, h_xfers, n_xfers, filter_src, n_units, d_totals,
+                   d_status, status_mirror, st);
+    if (e == cudaSuccess) {
+      g_k1_last.store(TPR_ENGINE_BULK);
+      if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[1]), st)) != cudaSuccess)
+        return cuda_fail(e, "tpr_kv_switch K31 end event");
+      return TPR_OK;
+    }
+    if (e != cudaErrorNotSupported) return cuda_fail(e, "tpr_kv_switch K31");
+    cudaGetLastError();
+  }
   if (n_xfers > 0 && n_units > 0) {
     // records K3 reads: pinned host records in place (zero-copy), else an
     // H2D copy into d_xfers first
@@ -463,6 +493,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
   else if (!strcmp(key, "bulk_ws")) g_ws.store(value != 0);
   else if (!strcmp(key, "k1_dynamic")) g_dyn.store(value);
+  else if (!strcmp(key, "k31")) g_k31.store(value != 0);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
 }
@@ -475,6 +506,7 @@ int64_t tpr_get_tuning(const char* key) {
   if (!strcmp(key, "tensor_partial")) return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1);
   if (!strcmp(key, "bulk_ws")) return knob(g_ws, "TPR_BULK_WS", 0);
   if (!strcmp(key, "k1_dynamic")) return knob(g_dyn, "TPR_K1_DYNAMIC", 1);
+  if (!strcmp(key, "k31")) return knob(g_k31, "TPR_K31", 1);
   if (!strcmp(key, "k1_engine_last")) return g_k1_last.load();
   if (!strcmp(key, "k2_engine_last")) return g_k2_last.load();
   return -1;

@@ -13,10 +13,12 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "tpr.h"
 #include "tpr_common.cuh"
 #include "tpr_internal.h"
+#include "tpr_k3page.cuh"
 
 namespace tpr {
 
@@ -120,6 +122,7 @@ struct KvPieces {
   int64_t item;
   unsigned long long* claim = nullptr;  // dynamic schedule (0 at kernel start)
   int64_t batch = 4, item_end = 0, next_batch = 0;
+  int64_t stride = -1;  // static schedule step (-1: gridDim.x, grid-stride shares)
   // current item: linear rows ...
   const char* s;
   char* d;
@@ -137,13 +140,14 @@ struct KvPieces {
       next_batch = (int64_t)gridDim.x + (int64_t)atomicAdd(claim, 1ull);
     } else {
       item = first;
+      if (stride < 0) stride = gridDim.x;
     }
   }
   __device__ bool take(int64_t& k) {
     if (!claim) {
       if (item >= n_items) return false;
       k = item;
-      item += gridDim.x;
+      item += stride;
       return true;
     }
     if (item >= item_end) {
@@ -641,6 +645,125 @@ __global__ void __launch_bounds__(64)
   bulk_pipeline<false>(it, stages, nullptr);
 }
 
+// ---------------------------------------------------------------------------
+// K31: the whole switch of a small plan in ONE launch (K3 bookkeeping + K1
+// copy). The records ride in the kernel parameters (constant bank: every CTA
+// reads them without touching PCIe or L2). Every CTA redoes the keyed scan of
+// the plan (<= kK31Xfers records, one warp), then owns whole pages
+// p = blockIdx.x + j * gridDim.x: its lanes do those pages' block-table /
+// free-ring bookkeeping (k3_page, the same rules as K3), and its elected
+// thread moves them through the TMA ring. A page's bookkeeping and bytes stay
+// in one CTA, so no CTA ever waits for another (the source block-table entry
+// is read and cleared by the CTA that copies the page).
+//
+// The status word reports this call only: CTAs OR their bits into
+// totals[TPR_TOTALS_K31_STATUS]; the last CTA to finish (counter
+// totals[TPR_TOTALS_K31_DONE]) publishes them to *status (+ the pinned mirror)
+// and leaves both scratch words zero for the next launch. A device-barrier
+// timeout already in *status aborts the call (nothing is touched, the bit stays).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32)
+    tpr_k31_switch(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo, KvCopyParams p,
+                   const __grid_constant__ KvClusterParams cl, int64_t* __restrict__ totals,
+                   int32_t* __restrict__ status, int32_t* status_mirror, int32_t stages,
+                   uint32_t piece) {
+  __shared__ int64_t s_off[4][kK31Xfers];  // mine, alloc, release offsets; units
+  __shared__ int64_t s_carry[3][TPR_MAX_GPUS + 1];
+  __shared__ __align__(16) int4 s_work[kK31MaxPages];
+  const unsigned lane = threadIdx.x;
+  const int32_t st0 = __ldcg(status);
+  const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
+  const int n = rp.n, B = geo.block_tokens;
+  for (int i = lane; i < 3 * (TPR_MAX_GPUS + 1); i += 32) (&s_carry[0][0])[i] = 0;
+  __syncwarp();
+  // three keyed exclusive scans over the records, 32 at a time
+  for (int base = 0; base < n; base += 32) {
+    const int t = base + (int)lane;
+    int key[3] = {0, TPR_MAX_GPUS, TPR_MAX_GPUS};
+    int64_t val[3] = {0, 0, 0};
+    if (t < n) {
+      const int32_t* r = rp.rec[t];
+      const int64_t nblk = r[5] > 0 ? (r[5] + B - 1) / B : 0;
+      const int64_t u = (int64_t)(r[4] - r[3]) * nblk;
+      key[1] = r[1] >= 0 ? r[1] : TPR_MAX_GPUS;
+      key[2] = r[0] >= 0 ? r[0] : TPR_MAX_GPUS;
+      val[0] = (rp.filter < 0 || r[0] == rp.filter) ? u : 0;
+      val[1] = r[1] >= 0 ? u : 0;
+      val[2] = r[0] >= 0 ? u : 0;
+      s_off[3][t] = val[0];
+    }
+#pragma unroll
+    for (int sc = 0; sc < 3; ++sc) {
+      const unsigned peers = __match_any_sync(0xffffffffu, key[sc]);
+      const unsigned lower = peers & ((1u << lane) - 1u);
+      int64_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int64_t vj = __shfl_sync(0xffffffffu, val[sc], j);
+        if ((lower >> j) & 1u) acc += vj;
+      }
+      const int64_t carry = s_carry[sc][key[sc]];
+      if (t < n) s_off[sc][t] = carry + acc;
+      __syncwarp();
+      if (lane == 31u - (unsigned)__clz(peers)) s_carry[sc][key[sc]] = carry + acc + val[sc];
+      __syncwarp();
+    }
+  }
+  const int64_t n_mine = s_carry[0][0];
+  // this CTA's pages: bookkeeping, one lane per page
+  int n_pages = 0;
+  if (!abort && (int64_t)blockIdx.x < n_mine)
+    n_pages = (int)((n_mine - 1 - blockIdx.x) / gridDim.x) + 1;
+  int bits = 0;
+  for (int j = lane; j < n_pages; j += 32) {
+    const int64_t pg = blockIdx.x + (int64_t)j * gridDim.x;
+    int lo = 0, hi = n;  // upper_bound(mine offsets, pg) - 1
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[0][mid] <= pg) lo = mid; else hi = mid;
+    }
+    const int32_t* r = rp.rec[lo];
+    const int64_t local = pg - s_off[0][lo];
+    const int ctx = r[5], nblk = (ctx + B - 1) / B;
+    const int h = r[3] + (int)(local / nblk);
+    const int b = (int)(local - (int64_t)(h - r[3]) * nblk);
+    const int ntok = (b == nblk - 1) ? ctx - b * B : B;
+    s_work[j] = k3_page(cl, geo, r[0], r[1], r[2], h, b, ntok, s_off[1][lo] + local,
+                        s_off[2][lo] + local, bits);
+  }
+  bits = (int)__reduce_or_sync(0xffffffffu, (unsigned)bits);
+  __syncwarp();
+  if (lane == 0) {
+    if (bits) atomicOr(reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS),
+                       (unsigned long long)bits);
+    if (n_pages > 0) {
+      KvPieces<false> it;
+      it.work = s_work;
+      it.n_items = (int64_t)n_pages * p.items_per_unit;
+      it.p = p;
+      it.cl = &cl;
+      it.tm = nullptr;
+      it.piece = piece;
+      it.stride = 1;
+      it.start(0);
+      bulk_pipeline<false>(it, stages, nullptr);  // waits for its last store
+    }
+    // the last CTA publishes the status word and resets the scratch words
+    __threadfence();
+    unsigned long long* done = reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_DONE);
+    if (atomicAdd(done, 1ull) == gridDim.x - 1) {
+      __threadfence();
+      const int32_t acc = (int32_t)atomicExch(
+          reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS), 0ull);
+      const int32_t out = acc | (st0 & TPR_STATUS_BARRIER_TIMEOUT);
+      *status = out;
+      if (status_mirror) *reinterpret_cast<volatile int32_t*>(status_mirror) = out;
+      *done = 0ull;
+      if (!abort) totals[0] = n_mine;
+    }
+  }
+}
+
 // Ring shape per kernel (shared memory = stages x piece per CTA). Measured on
 // B200 (profiles/README.md): K1 streams whole 32 KiB page chunks and is
 // fastest with one CTA per SM and 32 KiB pieces (6 x 32 KiB = 192 KiB, at the
@@ -773,6 +896,29 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
   if (geo && (partial || tensor_kernel_always())) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
   return bulk_ws() ? k1_launch<true>(p, cl, work, n_units, st, pdl, tm, c)
                    : k1_launch<false>(p, cl, work, n_units, st, pdl, tm, c);
+}
+
+// K31 ring: one CTA per SM owning ~1-28 whole pages; TPR_BULK_K31 overrides
+static const BulkConfig& k31_config() {
+  static BulkConfig c = parse_bulk("TPR_BULK_K31", BulkConfig{6, 32768});
+  return c;
+}
+
+cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
+                       const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
+                       int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
+                       cudaStream_t st) {
+  if (n < 1 || n > kK31Xfers || n_units < 1) return cudaErrorNotSupported;
+  const BulkConfig& c = k31_config();
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k31_switch), c, n_units, 32);
+  if ((n_units + grid - 1) / grid > kK31MaxPages) return cudaErrorNotSupported;
+  K31Params rp;
+  memcpy(rp.rec, h_rec, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n);
+  rp.n = n;
+  rp.filter = filter;
+  tpr_k31_switch<<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, totals, status, status_mirror,
+                                                     c.stages, c.piece);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,

@@ -50,6 +50,15 @@ struct KvTensorMaps {
   int32_t _pad;
 };
 
+// K31 (fused small switch): the plan's records ride in the kernel parameters.
+constexpr int kK31Xfers = 96;      // records per fused launch (2304 B of parameters)
+constexpr int kK31MaxPages = 64;   // pages one CTA owns
+struct K31Params {
+  int32_t rec[kK31Xfers][TPR_XFER_FIELDS];
+  int32_t n;
+  int32_t filter;
+};
+
 // Tensor maps for the pools of `cl` (cached per pool); out->enabled = 0 when
 // the geometry does not fit TMA's limits or the driver entry point is missing.
 void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
@@ -119,6 +128,12 @@ cudaError_t launch_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                            int64_t n_units, cudaStream_t st, bool pdl,
                            const tpr_kv_geometry_t* geo, int n_gpus, bool partial);
+// K31: n_units pages, records from host memory (copied into the parameters);
+// returns cudaErrorNotSupported when the plan does not fit the fused path.
+cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
+                       const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
+                       int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
+                       cudaStream_t st);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

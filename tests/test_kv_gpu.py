@@ -92,6 +92,9 @@ def test_chain_of_switches_and_back():
 
 
 LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
+    "k31_one_launch": dict(k31=1, k3_fuse_units=1 << 30),
+    "k31_vector_engine_fallback": dict(k31=1, k3_fuse_units=1 << 30, engine="vector"),
+    "fused_k3_no_k31": dict(k31=0, k3_fuse_units=1 << 30, pdl=2, zero_copy=1, tensor_partial=1),
     "split_plain_h2d_rows": dict(k3_fuse_units=0, pdl=0, zero_copy=0, tensor_partial=0),
     "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=2, zero_copy=1, tensor_partial=1),
     "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=2, zero_copy=1, tensor_partial=1),
@@ -108,11 +111,16 @@ LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
 def launch_path(request):
     from paper_2605_05467_b200 import _native
     saved = {k: _native.get_tuning(k) for k in _native.TUNING_KEYS}
+    engine = _native.copy_engine()
     for k, v in LAUNCH_PATHS[request.param].items():
-        _native.set_tuning(k, v)
+        if k == "engine":
+            _native.set_copy_engine(v)
+        else:
+            _native.set_tuning(k, v)
     yield request.param
     for k, v in saved.items():
         _native.set_tuning(k, v)
+    _native.set_copy_engine(engine)
 
 
 @pytest.mark.parametrize("launch_path", sorted(LAUNCH_PATHS), indirect=True)
@@ -160,7 +168,7 @@ def test_fused_k3_record_counts_bit_exact(n_reqs):
     plan = M.plan_repartition(lay[1], lay[2], TINY.kv_bytes_per_token_per_head)
     stats = migrate_and_compare(c, plan)
     assert stats.transfers == n_reqs and stats.units <= _native.k3_fuse_units()
-    assert _native.kv_switch_launches(stats.units) == 2
+    assert _native.kv_switch_launches(stats.units, stats.transfers) == (1 if n_reqs <= 96 else 2)
     before = c.snapshot()
     plan_b, st = c.switch_layouts(lay[2], lay[1])
     want = check.expected_after(c, before, c.records(plan_b, validate=False))
@@ -468,3 +476,50 @@ def test_cfg2_full_size_property():
     assert v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
     assert v["pages_checked"] == 64 * 8 * 256
     assert c.placement() == M.layout_placement(w.new)
+
+
+@pytest.mark.parametrize("model", ["tiny", "8b"])
+@pytest.mark.parametrize("tp_old,tp_new", [(1, 2), (2, 1), (1, 8), (8, 1), (4, 8), (8, 2)])
+def test_k31_single_launch_bit_exact(model, tp_old, tp_new):
+    # small plans (<= 96 transfers, <= k3_fuse_units pages): the whole switch is
+    # one launch (K31: bookkeeping + TMA copy per CTA-owned page), with ragged
+    # contexts (partial pages as row copies) and 8 slots, against the oracle
+    from paper_2605_05467_b200 import _native
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
+    kv = TINY if model == "tiny" else LLAMA_3_1_8B.kv
+    gpus = tuple(range(8))
+    rng = np.random.default_rng(tp_old * 31 + tp_new)
+    reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 300, size=6))]
+    old = workloads.round_robin(workloads.tp_groups(gpus, tp_old), reqs, 8)
+    new = workloads.round_robin(workloads.tp_groups(gpus, tp_new), reqs, 8)
+    c = make(kv, gpus, units=160, reqs=8, blocks=20, fragmented=True, seed=tp_new)
+    c.admit(old, seed=5)
+    for a, b in ((old, new), (new, old)):
+        before = c.snapshot()
+        plan = M.plan_repartition(a, b, kv.kv_bytes_per_token_per_head)
+        rec = c.records(plan, validate=False)
+        got, st = c.switch_layouts(a, b)
+        assert _native.kv_switch_launches(st.units, st.transfers) == 1
+        want = check.expected_after(c, before, rec)
+        diff = check.compare(c.snapshot(), want)
+        assert not any(diff.values()), diff
+        assert int(c.status.item()) == 0 and c.status_host[0] == 0
+    v = c.verify(seed=5)
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+
+
+def test_k31_reports_errors_per_call():
+    # K31's status word is this call's bits only, also in the pinned mirror
+    from paper_2605_05467_b200.controller import ReconfigurationExecutor
+    c = make(TINY, (0, 1))
+    c.admit([M.KvLayout((0,), 1, 8, ((0, 10),))], seed=1)
+    ex = ReconfigurationExecutor(c)
+    lie = [M.KvLayout((1,), 1, 8, ((0, 10),)), M.KvLayout((0,), 1, 8, ())]
+    bad = ex.switch(lie, [M.KvLayout((0, 1), 2, 8, ((0, 10),))], validate=False)
+    assert bad.status & 1 and bad.status & 2
+    # the heads are now on GPU1 only as far as the host knows; a correct switch
+    # of another request reports a clean word
+    c.admit([M.KvLayout((0, 1), 2, 8, ((7, 33),))], seed=1)
+    ok = ex.switch([M.KvLayout((0, 1), 2, 8, ((7, 33),))],
+                   [M.KvLayout((1, 0), 2, 8, ((7, 33),))], validate=False)
+    assert ok.status == 0 and int(c.status.item()) == 0

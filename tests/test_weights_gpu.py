@@ -95,8 +95,10 @@ def test_sequence_reuses_resident_slices():
     assert fwd.remote_bytes == 2 * store.bytes_per_slice * 2 and fwd.local_bytes == 0
     assert fwd.views == 2
     pieces = host_pieces(store)
-    back = store.reshard(workloads.tp_groups(gpus, 2))  # GPU0, GPU3 still resident on halves
-    assert back.views == 2
+    # every GPU still holds its TP2 half: GPU0 / GPU3 kept theirs, GPU1 / GPU2
+    # grew in place (their halves stayed at their window positions)
+    back = store.reshard(workloads.tp_groups(gpus, 2))
+    assert back.views == 4 and back.bytes == 0
     torch.cuda.synchronize()
     check_against_oracle(store, pieces, workloads.tp_groups(gpus, 2))
     assert store.verify() == 0

@@ -56,7 +56,8 @@ def main():
     args = ap.parse_args()
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
-    env = {k: os.environ.get(k, "") for k in ("TPR_PDL", "TPR_K3_FUSE_UNITS", "TPR_ZERO_COPY")}
+    env = {k: os.environ.get(k, "") for k in ("TPR_PDL", "TPR_K3_FUSE_UNITS", "TPR_ZERO_COPY", "TPR_K31",
+                                              "TPR_BULK_K31")}
     kv = LLAMA_3_1_8B.kv
     out = open(args.out, "a") if args.out else None
     torch.cuda.set_device(0)
@@ -97,7 +98,7 @@ def main():
         ok = v["placement_errors"] == 0 and v["word_mismatches"] == 0 and v["status"] == 0
         roof = 2 * nbytes / (peak * 1e9) * 1e6
         row = {"case": name, "env": env, "bytes": nbytes,
-               "launches": _native.kv_switch_launches(r.kv.units), "units": r.kv.units,
+               "launches": _native.kv_switch_launches(r.kv.units, r.kv.transfers), "units": r.kv.units,
                "sync_us": float(np.median(sync_us)), "enqueue_us": float(np.median(enq_us)),
                "device_us": float(np.median(dev_us)), "k1_roof_us": roof,
                "sync_hbm_frac": roof / float(np.median(sync_us)),
