@@ -492,7 +492,7 @@ def test_k31_single_launch_bit_exact(model, tp_old, tp_new):
     reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 300, size=6))]
     old = workloads.round_robin(workloads.tp_groups(gpus, tp_old), reqs, 8)
     new = workloads.round_robin(workloads.tp_groups(gpus, tp_new), reqs, 8)
-    c = make(kv, gpus, units=160, reqs=8, blocks=20, fragmented=True, seed=tp_new)
+    c = make(kv, gpus, units=1024, reqs=8, blocks=20, fragmented=True, seed=tp_new)
     c.admit(old, seed=5)
     for a, b in ((old, new), (new, old)):
         before = c.snapshot()
