@@ -282,6 +282,7 @@ typedef struct tpr_switch_tables {
                               there on the stream (fused K3 store or a 4-byte D2H),
                               so a synchronous caller needs no separate read-back */
   void* k1_events[2];      /* nullable cudaEvent_t pair recorded around K1 (timing) */
+  int64_t n_records;       /* out: K3 records = the plan's + the release records */
 } tpr_switch_tables_t;
 
 /* tpr_switch_tables_t.mode: the planner of the switch.
@@ -298,7 +299,12 @@ typedef struct tpr_switch_tables {
  * migration.py:137-189, then tpr_kv_records and the capacity check).
  * `layouts` packs the old then the new KvLayouts as int64:
  *   n_old, n_new, then per layout: total_heads, tp, group[tp], count,
- *   (request id, context length) x count.
+ *   (request id, context length) x count,
+ * optionally followed by a release section: n_release, request id x n_release
+ * -- resident requests (not in the layouts) whose pages the same switch frees
+ * (destination KV-capacity eviction, engine.py:630-645). Their records (one per
+ * run of heads on one slot, dst = -1) follow the plan's in `records`;
+ * n_records counts both, n_plan the plan's transfers.
  * Returns TPR_ENOTFOUND when the switch needs the caller's general path: any
  * check the reference reports (GPU sets, head counts, carried requests,
  * context lengths, placement, capacity), a repeated old request id or an id

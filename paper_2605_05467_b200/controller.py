@@ -22,7 +22,7 @@ import torch
 from . import _native
 from .kvcache import MigrationStats, PagedKvCluster
 from .migration import KvLayout, MigrationPlan, plan_repartition
-from .placement import reuse_layouts
+from .placement import Arrival, KvBudget, enforce_kv_capacity, kv_capacity_decisions, reuse_layouts
 from .tracing import nvtx
 from .weights import ReshardStats, ShardedWeightStore
 
@@ -37,6 +37,7 @@ class SwitchResult:
     status: int = 0             # K3 status bits (0 = every head was where the plan said)
     events: dict = field(default_factory=dict)
     new_layouts: list | None = None  # the layouts the switch realised (reuse_order may reorder ranks)
+    evicted: list = field(default_factory=list)  # arrivals the destination could not hold (released)
 
     @property
     def bytes(self) -> int:
@@ -86,7 +87,8 @@ class ReconfigurationExecutor:
     def switch(self, old_layouts: list[KvLayout], new_layouts: list[KvLayout],
                new_weight_groups=None, parked=(), sync: bool = True,
                validate: bool = True, stream: torch.cuda.Stream | None = None,
-               trim: bool = False, reuse_order: bool = False) -> SwitchResult:
+               trim: bool = False, reuse_order: bool = False,
+               arrivals=None, kv_budget: KvBudget | None = None) -> SwitchResult:
         """Stop-and-migrate TP switch. With ``sync`` the call returns after the
         switch completed on the device and reports measured latencies; without
         it, work is only enqueued and ``stream`` (default: the device's default
@@ -95,10 +97,24 @@ class ReconfigurationExecutor:
         ``reuse_order`` re-ranks every new group to keep the most KV in place
         (placement.reuse_layouts); the realised layouts are in
         ``SwitchResult.new_layouts``. It changes the plan the reference would
-        produce, so it is off by default. Weight groups follow the new ranks."""
+        produce, so it is off by default. Weight groups follow the new ranks.
+
+        ``arrivals`` (placement.Arrival per migrating request): destination
+        KV-capacity admission inside the switch, as the reference's hook does
+        with ``kv_accounting`` (engine.py:600-601, 623-645). For every new
+        layout, its arrivals are decided against ``kv_budget`` bytes
+        ((gpu_memory_gb - weight_full_copy_gb) * 1e9 * tp, with the group's
+        other requests as ``used``) -- or, without a budget, against the
+        destination GPUs' free pages. Evicted requests leave both layout lists
+        and their pages are freed by the same native call; they are listed in
+        ``SwitchResult.evicted`` for the caller to re-queue."""
         t0 = time.perf_counter()
         if isinstance(new_layouts, KvLayout):
             new_layouts = [new_layouts]
+        evicted = []
+        if arrivals is not None:
+            old_layouts, new_layouts, evicted = self._admit(old_layouts, new_layouts, arrivals,
+                                                            kv_budget)
         if reuse_order:
             new_layouts = reuse_layouts(old_layouts, new_layouts,
                                         self.kv.kv.kv_bytes_per_token_per_head)
@@ -124,7 +140,8 @@ class ReconfigurationExecutor:
             with nvtx("plan+kv K3+K1"):
                 plan, kv_stats = self.kv.switch_layouts(
                     old_layouts, new_layouts, stream=ks, validate=validate,
-                    k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
+                    k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None,
+                    release=evicted)
         else:
             with nvtx("plan"):
                 plan = plan_repartition(old_layouts, new_layouts,
@@ -136,6 +153,8 @@ class ReconfigurationExecutor:
                 kv_stats = self.kv.migrate(
                     plan, stream=ks, validate=validate,
                     k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None)
+                if evicted:
+                    self.kv.release(evicted, stream=ks)
         w_stats = None
         if self.weights is not None and new_weight_groups is not None:
             ws = self.w_stream if self.overlap else main
@@ -150,8 +169,39 @@ class ReconfigurationExecutor:
         if ks is not main:
             main.wait_stream(ks)
         res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev,
-                           new_layouts=list(new_layouts))
+                           new_layouts=list(new_layouts), evicted=evicted)
         return self._finish(res, main, t0) if sync else res
+
+    def _admit(self, old_layouts, new_layouts, arrivals, kv_budget):
+        """(old, new, evicted): the layouts without the arrivals each new
+        group cannot hold (placement.kv_capacity_decisions per group)."""
+        kv = self.kv.kv
+        per_token = kv.kv_bytes_per_token_per_head * kv.total_heads
+        by_id = {a.request_id: a for a in arrivals}
+        gone, out_new = [], []
+        for lay in new_layouts:
+            ctx = dict(lay.requests)
+            arr = [Arrival(r, ctx[r], by_id[r].label, by_id[r].arrival_time)
+                   for r, _ in lay.requests if r in by_id]
+            if not arr:
+                out_new.append(lay)
+                continue
+            if kv_budget is not None:
+                used = sum(c for r, c in lay.requests if r not in by_id) * per_token
+                _, ev = kv_capacity_decisions(arr, kv_budget.bytes(lay.tp), used, per_token)
+            else:
+                _, ev = enforce_kv_capacity(self.kv, lay, arr)
+            drop = {a.request_id for a in ev}
+            gone.extend(a.request_id for a in ev)
+            out_new.append(KvLayout(lay.group, lay.tp, lay.total_heads,
+                                    tuple(rc for rc in lay.requests if rc[0] not in drop)))
+        if not gone:
+            return old_layouts, out_new, []
+        drop = set(gone)
+        out_old = [KvLayout(lay.group, lay.tp, lay.total_heads,
+                            tuple(rc for rc in lay.requests if rc[0] not in drop))
+                   for lay in old_layouts]
+        return out_old, out_new, gone
 
     def handoff(self, prefill: KvLayout, decode: KvLayout, sync: bool = True) -> SwitchResult:
         """Prefill->decode KV handoff between disjoint groups.

@@ -416,7 +416,8 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
     if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[0]), st)) != cudaSuccess)
       return cuda_fail(e, "tpr_kv_switch K31 start event");
     e = launch_k31(*geo, copy_params(geo), cp, h_xfers, n_xfers, filter_src, n_units, d_totals,
-                   d_status, status_mirror, st);
+                   d_status, status_mirror, st, cl->n_gpus,
+                   any_partial(h_xfers, n_xfers, geo->block_tokens));
     if (e == cudaSuccess) {
       g_k1_last.store(TPR_ENGINE_BULK);
       if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[1]), st)) != cudaSuccess)

@@ -662,9 +662,14 @@ __global__ void __launch_bounds__(64)
 // and leaves both scratch words zero for the next launch. A device-barrier
 // timeout already in *status aborts the call (nothing is touched, the bit stays).
 // ---------------------------------------------------------------------------
+// kTensor: partial pages move as TMA tensor boxes of the pools' maps (the
+// maps ride in the parameters too: > 4 KiB of parameters, CUDA >= 12.1); a
+// plan of full pages only takes the lean variant.
+template <bool kTensor>
 __global__ void __launch_bounds__(32)
     tpr_k31_switch(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo, KvCopyParams p,
-                   const __grid_constant__ KvClusterParams cl, int64_t* __restrict__ totals,
+                   const __grid_constant__ KvClusterParams cl,
+                   const __grid_constant__ KvTensorMaps tm, int64_t* __restrict__ totals,
                    int32_t* __restrict__ status, int32_t* status_mirror, int32_t stages,
                    uint32_t piece) {
   __shared__ int64_t s_off[4][kK31Xfers];  // mine, alloc, release offsets; units
@@ -737,16 +742,16 @@ __global__ void __launch_bounds__(32)
     if (bits) atomicOr(reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS),
                        (unsigned long long)bits);
     if (n_pages > 0) {
-      KvPieces<false> it;
+      KvPieces<kTensor> it;
       it.work = s_work;
       it.n_items = (int64_t)n_pages * p.items_per_unit;
       it.p = p;
       it.cl = &cl;
-      it.tm = nullptr;
+      it.tm = kTensor ? &tm : nullptr;
       it.piece = piece;
       it.stride = 1;
       it.start(0);
-      bulk_pipeline<false>(it, stages, nullptr);  // waits for its last store
+      bulk_pipeline<kTensor>(it, stages, kTensor ? &tm : nullptr);  // waits for its last store
     }
     // the last CTA publishes the status word and resets the scratch words
     __threadfence();
@@ -907,17 +912,26 @@ static const BulkConfig& k31_config() {
 cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
-                       cudaStream_t st) {
+                       cudaStream_t st, int n_gpus, bool partial) {
   if (n < 1 || n > kK31Xfers || n_units < 1) return cudaErrorNotSupported;
   const BulkConfig& c = k31_config();
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k31_switch), c, n_units, 32);
+  KvTensorMaps tm;
+  tm.enabled = 0;
+  if (partial) kv_tensor_maps(geo, cl, n_gpus, c.piece, &tm);
+  const void* fn = tm.enabled ? reinterpret_cast<const void*>(&tpr_k31_switch<true>)
+                              : reinterpret_cast<const void*>(&tpr_k31_switch<false>);
+  const int grid = bulk_grid(fn, c, n_units, 32);
   if ((n_units + grid - 1) / grid > kK31MaxPages) return cudaErrorNotSupported;
   K31Params rp;
   memcpy(rp.rec, h_rec, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n);
   rp.n = n;
   rp.filter = filter;
-  tpr_k31_switch<<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, totals, status, status_mirror,
-                                                     c.stages, c.piece);
+  if (tm.enabled)
+    tpr_k31_switch<true><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, status,
+                                                             status_mirror, c.stages, c.piece);
+  else
+    tpr_k31_switch<false><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, status,
+                                                              status_mirror, c.stages, c.piece);
   return cudaGetLastError();
 }
 

@@ -229,6 +229,16 @@ int tpr_switch_prepare(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
     }
     if (j < n_old) n_old_req += c;
   }
+  // optional release section: n_release, request ids (evicted requests whose
+  // pages are freed in the same switch, engine.py:630-645)
+  thread_local std::vector<int64_t> rel;
+  rel.clear();
+  if (pos < len) {
+    const int64_t n_rel = L[pos++];
+    if (n_rel < 0 || pos + n_rel != len) return set_error(TPR_EINVAL, "bad release section");
+    rel.assign(L + pos, L + pos + n_rel);
+    pos += n_rel;
+  }
   if (pos != len) return set_error(TPR_EINVAL, "layouts blob has trailing data");
   for (auto& m : members) {  // "GPU sets differ" (migration.py:150-155)
     std::sort(m.begin(), m.end());
@@ -240,7 +250,7 @@ int tpr_switch_prepare(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
   if (!heads_mode && members[0] != members[1])  // plan_repartition only (migration.py:150-155)
     return set_error(TPR_ENOTFOUND, "GPU sets differ");
   const int64_t n_plan_req = heads_mode ? n_old_req : (int64_t)req.size() - n_old_req;
-  const int64_t need = std::max<int64_t>(n_plan_req, 1) * H;
+  const int64_t need = (std::max<int64_t>(n_plan_req, 1) + (int64_t)rel.size()) * H;
   if (!t->plan || !t->records || t->plan_cap < need) {
     t->n_plan = need;
     return set_error(TPR_ECAPACITY, "plan capacity %lld < %lld", (long long)t->plan_cap,
@@ -284,6 +294,33 @@ int tpr_switch_prepare(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                       geo->block_tokens, t->kvb, t->validate, t->records, t->in_units,
                       t->out_units, &t->total_units);
   if (rc != TPR_OK) return set_error(TPR_ENOTFOUND, "records need the general path");
+  // release records after the plan's: one per run of heads on the same slot
+  // (dst = -1), in the order kvcache.release builds them
+  int64_t n_rec = n;
+  for (const int64_t rid : rel) {
+    const int64_t rs = (rid >= 0 && rid < t->req_lut_len) ? t->req_lut[rid] : -1;
+    if (rs < 0 || rs >= geo->n_req_slots) return set_error(TPR_ENOTFOUND, "released request not in table");
+    const int32_t* own = t->owner + (size_t)rs * H;
+    const int32_t ctx = t->slot_ctx[rs];
+    const int64_t nblk = ctx > 0 ? (ctx + geo->block_tokens - 1) / geo->block_tokens : 0;
+    for (int32_t h = 0; h < H;) {
+      int32_t e = h;
+      while (e < H && own[e] == own[h]) ++e;
+      if (own[h] < 0 || own[h] >= n_slots) return set_error(TPR_ENOTFOUND, "released request not placed");
+      int32_t* r = t->records + n_rec * 6;
+      r[0] = own[h];
+      r[1] = -1;
+      r[2] = (int32_t)rs;
+      r[3] = h;
+      r[4] = e;
+      r[5] = ctx;
+      t->out_units[own[h]] += (e - h) * nblk;
+      t->total_units += (e - h) * nblk;
+      ++n_rec;
+      h = e;
+    }
+  }
+  t->n_records = n_rec;
   for (int s = 0; s < n_slots; ++s)  // capacity (kvcache._check_capacity)
     if (t->in_units[s] > cl->ring_tail[s] - cl->ring_head[s])
       return set_error(TPR_ENOTFOUND, "slot %d out of KV units", s);
@@ -294,7 +331,7 @@ int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* 
                           const int64_t* L, int64_t len, tpr_switch_tables_t* t, void* stream) {
   int rc = tpr_switch_prepare(geo, cl, L, len, t);
   if (rc != TPR_OK) return rc;
-  const int64_t n = t->n_plan, units = t->total_units;
+  const int64_t n = t->n_records, units = t->total_units;  // plan + release records
   if (n > 0 && (n > t->xfers_cap || units + 1 > t->work_cap || !t->d_xfers || !t->d_meta ||
                 !t->d_totals || !t->d_status || (units > 0 && !t->d_work)))
     return tpr::set_error(TPR_ECAPACITY, "device scratch too small: %lld transfers, %lld units",

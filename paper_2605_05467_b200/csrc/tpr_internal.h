@@ -133,7 +133,7 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
 cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
-                       cudaStream_t st);
+                       cudaStream_t st, int n_gpus, bool partial);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

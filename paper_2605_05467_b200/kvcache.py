@@ -392,14 +392,7 @@ class PagedKvCluster:
         if not recs:
             return 0
         total = self._remap(np.asarray(recs, np.int64), stream, want_ext=False)
-        for rid in request_ids:
-            rs = self.req_slot.pop(rid)
-            if 0 <= rid < len(self._req_lut):
-                self._req_lut[rid] = -1
-            self.ctx_of.pop(rid, None)
-            self.owner[rs] = -1
-            self.slot_ctx[rs] = -1
-            self._free_req_slots.append(rs)
+        self._forget(request_ids)
         return total
 
     def fill_garbage(self, seed: int = 99, stream: torch.cuda.Stream | None = None) -> None:
@@ -577,7 +570,8 @@ class PagedKvCluster:
 
     def switch_layouts(self, old_layouts, new_layouts, stream: torch.cuda.Stream | None = None,
                        validate: bool = True, handshake_ms: float = 0.0,
-                       planner: str = "repartition", k1_events: tuple | None = None):
+                       planner: str = "repartition", k1_events: tuple | None = None,
+                       release=()):
         """``plan_repartition(old, new)`` + ``migrate(plan)`` in one native call
         (``tpr_kv_switch_layouts``): plan, records, capacity check, K3 + K1 and
         the placement update. Returns (MigrationPlan, MigrationStats) equal to
@@ -587,7 +581,10 @@ class PagedKvCluster:
 
         ``planner="head_transfers"``: one old and one new layout planned with
         ``head_transfers`` (any GPU sets: the prefill->decode handoff).
-        ``k1_events``: (start, end) CUDA events recorded around K1."""
+        ``k1_events``: (start, end) CUDA events recorded around K1.
+        ``release``: resident request ids (in neither layout list) whose pages
+        the same native call frees -- the destination's KV-capacity evictions
+        (engine.py:630-645); their records follow the plan's."""
         stream = stream or self._default_stream
         self.status_mirrored = False
         if planner not in ("repartition", "head_transfers"):
@@ -595,10 +592,18 @@ class PagedKvCluster:
         heads = planner == "head_transfers"
         if heads:
             old_layouts, new_layouts = [old_layouts], [new_layouts]
+        release = [int(r) for r in release]
+        if release:
+            carried = {r for lay in (*old_layouts, *new_layouts) for r, _ in lay.requests}
+            for rid in release:
+                if rid not in self.req_slot:
+                    raise MigrationError(f"request {rid} is not resident")
+                if rid in carried:
+                    raise MigrationError(f"request {rid} is both released and carried")
         if self._gpu_lut is None or not self._single_device:
             return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
-                                        heads)
-        blob = pack_layouts(old_layouts, new_layouts)
+                                        heads, release=release)
+        blob = pack_layouts(old_layouts, new_layouts, release)
         t = self._switch_tables(validate)
         t.mode = _native.TPR_SWITCH_HEAD_TRANSFERS if heads else _native.TPR_SWITCH_REPARTITION
         if k1_events:
@@ -629,13 +634,14 @@ class PagedKvCluster:
                 self._work.get((t.total_units + 1) * 4, stream)
         if rc == _native.TPR_ENOTFOUND:
             return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
-                                        heads, k1_events)
+                                        heads, k1_events, release)
         if rc != 0:
             raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
         n = t.n_plan
         self.status_mirrored = True
         plan = MigrationPlan.from_array(self._swt_plan[:n].copy(), handshake_ms=handshake_ms)
-        if n == 0:
+        self._forget(release)
+        if t.n_records == 0:
             return plan, MigrationStats(0, 0, 0, {}, {})
         self._staging.fence(stream)
         in_u, out_u = t.in_units, t.out_units
@@ -653,13 +659,27 @@ class PagedKvCluster:
                                     in_units=in_d, out_units=out_d)
 
     def _switch_general(self, old_layouts, new_layouts, stream, validate, handshake_ms,
-                        heads: bool = False, k1_events=None):
+                        heads: bool = False, k1_events=None, release=()):
         kvb = self.kv.kv_bytes_per_token_per_head
         if heads:
             plan = head_transfers_array(old_layouts[0], new_layouts[0], kvb)
         else:
             plan = plan_repartition(old_layouts, new_layouts, kvb, handshake_ms=handshake_ms)
-        return plan, self.migrate(plan, stream=stream, validate=validate, k1_events=k1_events)
+        stats = self.migrate(plan, stream=stream, validate=validate, k1_events=k1_events)
+        if release:
+            self.release(release, stream=stream)
+        return plan, stats
+
+    def _forget(self, request_ids) -> None:
+        """Host bookkeeping of requests whose pages a switch released."""
+        for rid in request_ids:
+            rs = self.req_slot.pop(rid)
+            if 0 <= rid < len(self._req_lut):
+                self._req_lut[rid] = -1
+            self.ctx_of.pop(rid, None)
+            self.owner[rs] = -1
+            self.slot_ctx[rs] = -1
+            self._free_req_slots.append(rs)
 
     # ------------------------------------------------------------ inspection
     def placement(self) -> dict:

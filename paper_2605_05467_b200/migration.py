@@ -343,9 +343,10 @@ def head_transfers_array(old: KvLayout, new: KvLayout, kvb: int) -> MigrationPla
         req, ctx, meta, np.asarray(table.ids, dtype=np.int64), old.total_heads, kvb))
 
 
-def pack_layouts(old_layouts, new_layouts):
+def pack_layouts(old_layouts, new_layouts, release=()):
     """Old and new layouts as one int64 array for ``tpr_switch_prepare``
-    (include/tpr.h): n_old, n_new, then every layout's ``packed()``."""
+    (include/tpr.h): n_old, n_new, then every layout's ``packed()``, then --
+    when ``release`` is not empty -- the ids of requests freed by the switch."""
     if isinstance(new_layouts, KvLayout):
         new_layouts = [new_layouts]
     flat = [len(old_layouts), len(new_layouts)]
@@ -353,6 +354,9 @@ def pack_layouts(old_layouts, new_layouts):
         flat.extend(lay.packed())
     for lay in new_layouts:
         flat.extend(lay.packed())
+    if release:
+        flat.append(len(release))
+        flat.extend(int(r) for r in release)
     return _array("q", flat)
 
 

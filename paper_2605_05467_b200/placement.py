@@ -9,12 +9,19 @@
   (rank r, gpu g) is the bytes of heads [r*H/N, (r+1)*H/N) already on g. It is
   opt-in, because it changes the plan the reference would produce.
 
-* ``enforce_kv_capacity`` -- destination admission/eviction on a real pool.
-  It follows engine.py:623-645: arrivals are taken feasible first, then by
-  arrival time. A best-effort arrival that does not fit is evicted (re-queued
-  by the caller); feasible ones are always kept. The budget is the
-  destination GPUs' actual free pages rather than
-  ``(gpu_memory_gb - weight_full_copy_gb) * tp`` bytes.
+* ``kv_capacity_decisions`` -- destination admission/eviction exactly as the
+  reference's controller hook decides it (``Simulator._enforce_kv_capacity``,
+  engine.py:623-645, with ``kv_accounting`` on, engine.py:600-601): the budget
+  is ``(gpu_memory_gb - weight_full_copy_gb) * 1e9 * tp`` bytes, ``used``
+  counts the requests already running on the group, arrivals are taken
+  feasible first, then by arrival time (a stable sort), and a best-effort
+  arrival that does not fit is evicted while a feasible one is always kept.
+  Pinned to the reference's own decisions (tests/golden/kv_capacity.json.gz).
+  ``ReconfigurationExecutor.switch(arrivals=...)`` applies it inside the switch
+  and frees the evicted requests' pages in the same native call.
+
+* ``enforce_kv_capacity`` -- the same rule against the destination GPUs'
+  actual free pages (the ring counters) instead of the byte budget.
 """
 
 from __future__ import annotations
@@ -84,6 +91,35 @@ class Arrival:
     context_len: int
     label: str = FEASIBLE
     arrival_time: float = 0.0
+
+
+@dataclass(frozen=True)
+class KvBudget:
+    """The reference's KV budget of a destination group (engine.py:623-628)."""
+
+    gpu_memory_gb: float
+    weight_full_copy_gb: float
+
+    def bytes(self, tp: int) -> float:
+        return (self.gpu_memory_gb - self.weight_full_copy_gb) * 1e9 * tp
+
+
+def kv_capacity_decisions(arrivals: Sequence[Arrival], budget_bytes: float, used_bytes: int,
+                          kv_bytes_per_token: int):
+    """(kept, evicted) of engine.py:629-645: ``need`` = context x total KV heads
+    x bytes per token per head (engine.py:246-251); kept in the decision order
+    (feasible first, then arrival time), evicted in the order they are
+    re-queued."""
+    kept, evicted = [], []
+    used = used_bytes
+    for a in sorted(arrivals, key=lambda a: (a.label == BEST_EFFORT, a.arrival_time)):
+        need = a.context_len * kv_bytes_per_token
+        if used + need > budget_bytes and a.label == BEST_EFFORT:
+            evicted.append(a)
+        else:
+            used += need
+            kept.append(a)
+    return kept, evicted
 
 
 def enforce_kv_capacity(cluster, layout: KvLayout, arrivals: Sequence[Arrival]):

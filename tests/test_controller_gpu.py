@@ -2,6 +2,7 @@
 streams), prefill->decode handoff over disjoint groups, capacity admission
 with eviction through release."""
 
+import numpy as np
 import pytest
 
 from oracle import check
@@ -190,3 +191,50 @@ def test_random_switch_walk_kv_and_weights(seed):
         check_against_oracle(store, pieces, groups)
         assert store.verify() == 0 and kv.placement() == M.layout_placement(new)
         cur = new
+
+
+def test_switch_evicts_inside_the_native_call():
+    # engine.py:600-601 + 623-645 executed: the destination group's byte budget
+    # keeps the feasible arrival and the oldest best-effort one; the other
+    # best-effort arrival is evicted, and its pages are freed by the same
+    # native call (release records after the plan's), bit-exact vs the oracle
+    from oracle import check
+    from paper_2605_05467_b200.placement import KvBudget
+    gpus = (0, 1, 2, 3)
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=256, max_requests=8, max_blocks=8, fragmented=True,
+                        seed=4)
+    kv.fill_garbage(seed=9)
+    reqs = ((1, 128), (2, 128), (3, 64))
+    old = [M.KvLayout((0, 1), 2, 8, reqs), M.KvLayout((2, 3), 2, 8, ())]
+    new = [M.KvLayout((2, 3), 2, 8, reqs), M.KvLayout((0, 1), 2, 8, ())]
+    kv.admit(old, seed=2)
+    kv.admit([M.KvLayout((2, 3), 2, 8, ((9, 40),))], seed=2)  # already running on (2, 3)
+    per_tok = KV.kv_bytes_per_token_per_head * 8
+    # room for request 9 (running) + 2 (feasible) + 3 (oldest best effort) + 10 tokens
+    budget = KvBudget(26.0 + (40 + 128 + 64 + 10) * per_tok / 2 / 1e9, 26.0)
+    arrivals = [Arrival(1, 128, BEST_EFFORT, 1.0), Arrival(2, 128, FEASIBLE, 2.0),
+                Arrival(3, 64, BEST_EFFORT, 0.5)]
+    new_all = [M.KvLayout((2, 3), 2, 8, reqs + ((9, 40),)), M.KvLayout((0, 1), 2, 8, ())]
+    old_all = old[:1] + [M.KvLayout((2, 3), 2, 8, ((9, 40),))]
+    kept_old = [M.KvLayout((0, 1), 2, 8, ((2, 128), (3, 64))), M.KvLayout((2, 3), 2, 8, ((9, 40),))]
+    kept_new = [M.KvLayout((2, 3), 2, 8, ((2, 128), (3, 64), (9, 40))), M.KvLayout((0, 1), 2, 8, ())]
+    plan = M.plan_repartition(kept_old, kept_new, KV.kv_bytes_per_token_per_head)
+    rs1 = kv.req_slot[1]
+    rec = np.concatenate([kv.records(plan), np.array([(0, -1, rs1, 0, 4, 128),
+                                                      (1, -1, rs1, 4, 8, 128)], np.int64)])
+    free0 = [kv.free_units(g) for g in gpus]
+    before = kv.snapshot()
+    ex = ReconfigurationExecutor(kv)
+    res = ex.switch(old_all, new_all, arrivals=arrivals, kv_budget=budget)
+    assert res.evicted == [1] and res.status == 0
+    assert np.array_equal(res.plan.as_array(), plan.as_array())
+    want = check.expected_after(kv, before, rec)
+    assert not any(check.compare(kv.snapshot(), want).values())
+    assert kv.placement() == M.layout_placement(kept_new) and 1 not in kv.req_slot
+    # GPUs 0 and 1 got back every page they held (request 1 released, 2 and 3 moved)
+    assert [kv.free_units(g) for g in gpus][:2] == [free0[0] + 80, free0[1] + 80]
+    v = kv.verify(seed=2)
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
+    # without a byte budget the same call decides against free pages
+    ex.switch(kept_new, kept_old, arrivals=[Arrival(2, 128, FEASIBLE, 0.0)])
+    assert kv.placement() == M.layout_placement(kept_old)

@@ -86,3 +86,26 @@ def test_capacity_keeps_everything_that_fits():
     c = _FakeCluster({0: 1000})
     kept, evicted = enforce_kv_capacity(c, lay([0], []), [Arrival(i, 100) for i in range(5)])
     assert len(kept) == 5 and not evicted
+
+
+def test_kv_capacity_decisions_match_the_reference_engine():
+    # every _enforce_kv_capacity call of the unmodified reference
+    # (tests/golden/gen_kv_capacity.py): its demo run with kv_accounting on,
+    # plus 300 random calls; same kept order, same evictions
+    import gzip
+    import json
+
+    from conftest import ROOT
+    from paper_2605_05467_b200.placement import KvBudget, kv_capacity_decisions
+    with gzip.open(ROOT / "tests" / "golden" / "kv_capacity.json.gz", "rt") as f:
+        doc = json.load(f)
+    n_ev = 0
+    for c in doc["demo"] + doc["random"]:
+        arr = [Arrival(r, ctx, label, t) for r, ctx, label, t in c["arrivals"]]
+        budget = KvBudget(c["gpu_memory_gb"], c["weight_full_copy_gb"]).bytes(c["tp"])
+        used = sum(c["running"]) * c["kv_bytes_per_token"]
+        kept, ev = kv_capacity_decisions(arr, budget, used, c["kv_bytes_per_token"])
+        assert [a.request_id for a in kept] == c["kept"]
+        assert [a.request_id for a in ev] == c["evicted"]
+        n_ev += len(ev)
+    assert len(doc["demo"]) >= 10 and n_ev > 100

@@ -127,9 +127,9 @@ def test_plan_capacity_is_reported():
 
 
 def test_struct_size_matches_header():
-    # tpr_switch_tables_t (include/tpr.h), 456 bytes: 24 pointer/int64 fields, two
+    # tpr_switch_tables_t (include/tpr.h), 464 bytes: 25 pointer/int64 fields, two
     # int32 and two [TPR_MAX_GPUS] int64 arrays
-    assert ctypes.sizeof(_native.SwitchTablesC) == 24 * 8 + 2 * 4 + 2 * 8 * _native.TPR_MAX_GPUS
+    assert ctypes.sizeof(_native.SwitchTablesC) == 25 * 8 + 2 * 4 + 2 * 8 * _native.TPR_MAX_GPUS
 
 
 def test_packed_layout_is_cached_and_exact():
@@ -138,6 +138,8 @@ def test_packed_layout_is_cached_and_exact():
     assert lay.packed() is lay.packed()
     blob = M.pack_layouts([lay], lay)
     assert list(blob) == [1, 1, *lay.packed(), *lay.packed()]
+    blob = M.pack_layouts([lay], lay, release=[11, 12])  # + the release section
+    assert list(blob) == [1, 1, *lay.packed(), *lay.packed(), 2, 11, 12]
 
 
 @pytest.mark.parametrize("src,dst", [((0, 1), (4, 5, 6, 7)), ((2,), (3,)), ((0, 1, 2, 3), (4, 5)),
