@@ -108,12 +108,14 @@ typedef struct tpr_kv_cluster {
 
 /* totals output of K3 (int64): [0] units processed by this caller,
  * [1+g] units allocated on slot g, [1+TPR_MAX_GPUS+g] units released on g;
- * [TPR_TOTALS_K31_DONE], [TPR_TOTALS_K31_STATUS] are scratch words of the
- * fused small-switch kernel. The caller zero-initialises d_totals once; the
- * kernels leave the scratch words zero between calls. */
+ * [TPR_TOTALS_K31_DONE], [TPR_TOTALS_K31_STATUS], [TPR_TOTALS_K31_EPOCH] are
+ * scratch words of the fused small-switch kernel. The caller zero-initialises
+ * d_totals once; the kernel leaves DONE and STATUS zero between calls and
+ * advances EPOCH (it tags the per-page reader counters K31 keeps in d_work). */
 #define TPR_TOTALS_K31_DONE (1 + 2 * TPR_MAX_GPUS)
 #define TPR_TOTALS_K31_STATUS (2 + 2 * TPR_MAX_GPUS)
-#define TPR_TOTALS_LEN (3 + 2 * TPR_MAX_GPUS)
+#define TPR_TOTALS_K31_EPOCH (3 + 2 * TPR_MAX_GPUS)
+#define TPR_TOTALS_LEN (4 + 2 * TPR_MAX_GPUS)
 
 /* ---- host utilities -------------------------------------------------- */
 /* Copy engine of K1 and K2 (process-wide): TPR_ENGINE_BULK (default) = TMA
@@ -126,17 +128,11 @@ int tpr_get_copy_engine(void);
 /* Launch-path knobs of tpr_kv_switch (process-wide; initial values from the
  * environment variables in brackets):
  *   "k3_fuse_units" [TPR_K3_FUSE_UNITS, 4096]: plans up to this many units
- *                   run K3 as one fused CTA (scan + remap), 0 = never;
- *   "pdl"           [TPR_PDL, 1]: programmatic dependent launch of K3b / K1:
- *                   0 never, 1 plans up to k3_fuse_units, 2 every plan
- *                   (neutral on large plans with dynamic claims);
- *   "zero_copy"     [TPR_ZERO_COPY, 1]: K3 reads pinned host records in place;
- *   "bulk_ws"       [TPR_BULK_WS, 0]: TMA engine with a producer and a consumer
- *                   warp per CTA instead of one issuing thread;
- *   "k1_dynamic"    [TPR_K1_DYNAMIC, 1]: K1 CTAs claim batches of items (1: 4 per
- *                   claim, n >= 2: n per claim, 0: static shares) from
- *                   the counter after the work list instead of a static
- *                   grid-stride share;
+ *                   run as one kernel (K31, below) or, when K31 does not
+ *                   apply, K3 as one fused CTA (scan + remap) with K1 launched
+ *                   behind it by programmatic dependent launch; 0 = never.
+ *                   Larger plans run K3 scan + remap and a normally launched
+ *                   K1 whose CTAs claim batches of 4 items dynamically;
  *   "tensor_partial" [TPR_TENSOR_PARTIAL, 1]: K1 (TMA engine) moves partial
  *                   pages as TMA tensor boxes (token x planes) instead of
  *                   one short copy per plane: 0 never, 1 when a page of the
@@ -146,7 +142,9 @@ int tpr_get_copy_engine(void);
  *                   ONE kernel, K31: every CTA redoes the keyed scan of the
  *                   records (kernel parameters) and owns whole pages, doing
  *                   their bookkeeping and their copy (ring TPR_BULK_K31
- *                   [6x32768]). The fused path leaves d_xfers unfilled.
+ *                   [6x32768]). The fused path leaves d_xfers unfilled and
+ *                   keeps epoch-tagged per-page counters in d_work (8 bytes
+ *                   per page): a freshly allocated d_work must be zeroed once.
  * tpr_get_tuning returns the current value, -1 for an unknown key. Two
  * read-only keys report the engine the last K1 / K2 launch used
  * ("k1_engine_last", "k2_engine_last": TPR_ENGINE_*, -1 before the first):
@@ -198,7 +196,7 @@ int tpr_plan_repartition(int32_t n_old, const int64_t* old_count, const int32_t*
  * g processes only transfers leaving slot g (one process per GPU, push
  * model) while allocation offsets still follow the whole plan.
  * d_work: int32x4 [n_units + 1] {src_unit, dst_unit, src|dst<<16, ntok}; the
- * extra last entry is K1's claim counter (K3 zeroes it; knob "k1_dynamic");
+ * extra last entry is K1's claim counter (K3 zeroes it);
  * d_work_ext (nullable): int32x4 {req_slot, head, block, xfer}.
  * n_units_hint: host-computed number of units this caller processes (the
  * expand grid is sized from it). d_status: int32 (device), OR-ed status bits. */

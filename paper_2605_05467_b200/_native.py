@@ -17,7 +17,7 @@ TPR_ABI_VERSION = 1
 TPR_MAX_GPUS = 16
 TPR_XFER_FIELDS = 6
 TPR_META_FIELDS = 4
-TPR_TOTALS_LEN = 3 + 2 * TPR_MAX_GPUS  # + 2 scratch words of the fused small switch
+TPR_TOTALS_LEN = 4 + 2 * TPR_MAX_GPUS  # + 3 scratch words of the fused small switch
 TPR_STATUS_WRONG_SOURCE = 1
 TPR_STATUS_DST_OCCUPIED = 2
 TPR_STATUS_BARRIER_TIMEOUT = 4
@@ -194,7 +194,7 @@ def k3_fuse_units() -> int:
     return int(load().tpr_get_tuning(b"k3_fuse_units"))
 
 
-TUNING_KEYS = ("k3_fuse_units", "pdl", "zero_copy", "tensor_partial", "bulk_ws", "k1_dynamic", "k31")
+TUNING_KEYS = ("k3_fuse_units", "tensor_partial", "k31")
 
 
 def set_tuning(key: str, value: int) -> None:

@@ -122,8 +122,7 @@ int64_t env_i64(const char* name, int64_t dflt);
 
 // Launch-path knobs (process-wide): initialised from the environment, changed
 // at run time with tpr_set_tuning (tests cover every combination).
-std::atomic<int64_t> g_zero_copy{-1}, g_pdl{-1}, g_fuse{-1}, g_tensor{-1}, g_ws{-1}, g_dyn{-1},
-    g_k31{-1};
+std::atomic<int64_t> g_fuse{-1}, g_tensor{-1}, g_k31{-1};
 
 int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
   int64_t v = k.load(std::memory_order_relaxed);
@@ -146,7 +145,6 @@ bool host_readable(const int32_t* h) {
 }
 
 const int32_t* device_view(const int32_t* h) {
-  if (!knob(g_zero_copy, "TPR_ZERO_COPY", 1)) return nullptr;  // 0: always copy H2D first
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
     cudaGetLastError();
@@ -178,26 +176,10 @@ cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_
 }  // namespace
 
 namespace tpr {
-bool pdl_enabled() { return knob(g_pdl, "TPR_PDL", 1) != 0; }
-
-// PDL pays for small plans (its launch overlap is worth a few us). Under the
-// static grid-stride schedule it cost ~2.5% on a large K1 (CTAs resident while
-// K3 still ran started their share late and left a tail); with dynamic claims
-// it is neutral there (profiles/ab/r01_pdl_dynamic_*). Large plans launch K1
-// normally.
 // knob "tensor_partial": 0 row copies, 1 tensor boxes when a page is partial
 // (default), 2 the tensor kernel for every plan (A/B measurements)
 bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) != 0; }
 bool tensor_kernel_always() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) >= 2; }
-bool bulk_ws() { return knob(g_ws, "TPR_BULK_WS", 0) != 0; }
-bool k1_dynamic() { return knob(g_dyn, "TPR_K1_DYNAMIC", 1) != 0; }
-// knob "k1_dynamic": 0 static shares, 1 dynamic claims of 4 items (default;
-// profiles/ab/r01_claimbatch_*: 2 contends on the counter, 4-6 best),
-// n >= 2 dynamic claims of n items
-int k1_claim_batch() {
-  const int64_t v = knob(g_dyn, "TPR_K1_DYNAMIC", 1);
-  return v <= 0 ? 0 : v == 1 ? 4 : (int)(v > 4096 ? 4096 : v);
-}
 
 // ---------------------------------------------------------------------------
 // TMA tensor maps of the KV pools (K1 partial pages, tpr_internal.h).
@@ -261,11 +243,11 @@ bool pool_map(const MapKey& k, CUtensorMap* out) {
   return true;
 }
 
-// knob "pdl": 0 off, 1 plans up to k3_fuse_units (default), 2 every plan
-bool pdl_for(int64_t n_units) {
-  const int64_t v = knob(g_pdl, "TPR_PDL", 1);
-  return v >= 2 || (v == 1 && n_units <= k3_fuse_units());
-}
+// Programmatic dependent launch of K3b / K1 pays for small plans (its launch
+// overlap is worth a few us); on a large K1 it was -2.5% under the static
+// schedule and is neutral with dynamic claims (profiles/ab/r01_pdl_*), so
+// large plans launch K1 normally.
+bool pdl_for(int64_t n_units) { return n_units <= k3_fuse_units(); }
 
 int64_t k3_fuse_units() {
   // one 1024-thread CTA expands up to 4 units per thread faster than a second
@@ -417,7 +399,7 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
       return cuda_fail(e, "tpr_kv_switch K31 start event");
     e = launch_k31(*geo, copy_params(geo), cp, h_xfers, n_xfers, filter_src, n_units, d_totals,
                    d_status, status_mirror, st, cl->n_gpus,
-                   any_partial(h_xfers, n_xfers, geo->block_tokens));
+                   any_partial(h_xfers, n_xfers, geo->block_tokens), d_work);
     if (e == cudaSuccess) {
       g_k1_last.store(TPR_ENGINE_BULK);
       if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[1]), st)) != cudaSuccess)
@@ -489,11 +471,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   if (!key) return fail(TPR_EINVAL, "null tuning key");
   if (value < 0) return fail(TPR_EINVAL, "tuning value must be >= 0");
   if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
-  else if (!strcmp(key, "pdl")) g_pdl.store(value > 2 ? 2 : value);
-  else if (!strcmp(key, "zero_copy")) g_zero_copy.store(value != 0);
   else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
-  else if (!strcmp(key, "bulk_ws")) g_ws.store(value != 0);
-  else if (!strcmp(key, "k1_dynamic")) g_dyn.store(value);
   else if (!strcmp(key, "k31")) g_k31.store(value != 0);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
@@ -502,11 +480,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
 int64_t tpr_get_tuning(const char* key) {
   if (!key) return -1;
   if (!strcmp(key, "k3_fuse_units")) return tpr::k3_fuse_units();
-  if (!strcmp(key, "pdl")) return knob(g_pdl, "TPR_PDL", 1);
-  if (!strcmp(key, "zero_copy")) return knob(g_zero_copy, "TPR_ZERO_COPY", 1);
   if (!strcmp(key, "tensor_partial")) return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1);
-  if (!strcmp(key, "bulk_ws")) return knob(g_ws, "TPR_BULK_WS", 0);
-  if (!strcmp(key, "k1_dynamic")) return knob(g_dyn, "TPR_K1_DYNAMIC", 1);
   if (!strcmp(key, "k31")) return knob(g_k31, "TPR_K31", 1);
   if (!strcmp(key, "k1_engine_last")) return g_k1_last.load();
   if (!strcmp(key, "k2_engine_last")) return g_k2_last.load();

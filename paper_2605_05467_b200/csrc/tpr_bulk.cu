@@ -107,7 +107,7 @@ struct Copy {
 // maps, one TMA box per (token, r_box planes): item g of the unit takes tokens
 // g, g + items_per_unit, ... (no strided short copies at all).
 // K1 items are handed out statically (grid-stride) or, with a claim counter,
-// dynamically in batches of `batch` consecutive items (knob k1_dynamic; 4 by
+// dynamically in batches of `batch` consecutive items (4 by
 // default) claimed one batch ahead: CTAs then stay on neighbouring items (a
 // small, shared working set of pages) and none drains late.
 
@@ -399,7 +399,7 @@ struct StageRing {
   int32_t dmap[kTensor ? kMaxStages : 1][kMaxSub];  // -1: linear store
   int32_t c1[kTensor ? kMaxStages : 1][kMaxSub];
   int32_t dc2[kTensor ? kMaxStages : 1][kMaxSub];
-  int cnt[kMaxStages];  // -1: end of work (warp-specialised pipeline)
+  int cnt[kMaxStages];
 
   // Stage t from its first copy `c` on; false when the source ran dry.
   template <class Source>
@@ -509,66 +509,8 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
   bulk_wait_all();
 }
 
-// Warp-specialised variant (64 threads): lane 0 of warp 0 produces (packs
-// copies, issues the loads), lane 0 of warp 1 consumes (issues the stores).
-// full[t] completes when stage t's loads have landed (tx bytes); empty[t] when
-// its stores have finished reading shared memory. The two issue streams no
-// longer serialise in one thread.
-__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <bool kTensor, class Source>
-__device__ __forceinline__ void bulk_pipeline_ws(Source& src_it, int stages,
-                                                 const KvTensorMaps* tm) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[kMaxStages];
-  __shared__ __align__(8) uint64_t empty[kMaxStages];
-  __shared__ StageRing<kTensor> ring;
-  const uint32_t piece = src_it.piece;
-  const uint32_t base = smem_u32(smem);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      bar_init(&full[s]);
-      bar_init(&empty[s]);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // ---------------------------------------- producer
-    pdl_wait();
-    src_it.start(blockIdx.x);
-    bool more = true;
-    for (int64_t k = 0;; ++k) {
-      const int t = (int)(k % stages);
-      if (k >= stages) bar_wait(&empty[t], (uint32_t)(((k / stages) - 1) & 1));
-      Copy c;
-      if (!more || src_it.next(c, piece, piece) != 1) {
-        ring.cnt[t] = -1;  // end of work
-        bar_arrive(&full[t]);
-        break;
-      }
-      more = ring.fill(src_it, c, t, base + (uint32_t)t * piece, piece, &full[t], tm);
-    }
-  } else if (threadIdx.x == 32) {  // ------------------------------- consumer
-    for (int64_t k = 0;; ++k) {
-      const int t = (int)(k % stages);
-      bar_wait(&full[t], (uint32_t)((k / stages) & 1));
-      if (ring.cnt[t] < 0) break;
-      ring.store(t, base + (uint32_t)t * piece, tm);
-      if (k >= 1) {  // stage k-1's stores have read shared memory: hand it back
-        bulk_wait_read_1();
-        bar_arrive(&empty[(k - 1) % stages]);
-      }
-    }
-    bulk_wait_all();  // every store has landed before the CTA exits
-  }
-}
-
 // K1 with partial pages as row copies (every page full: no tensor maps needed)
-template <bool kWS>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(32)
     tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
                            const __grid_constant__ KvClusterParams cl, int32_t stages,
                            uint32_t piece, int32_t dynamic) {
@@ -585,19 +527,14 @@ __global__ void __launch_bounds__(64)
   it.cl = &cl;
   it.tm = nullptr;
   it.piece = piece;
-  if (kWS) {
-    bulk_pipeline_ws<false>(it, stages, nullptr);
-    return;
-  }
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x != 0) return;  // one issuing thread per CTA
   pdl_wait();  // K3's work list (launched with programmatic serialization)
   it.start(blockIdx.x);
   bulk_pipeline<false>(it, stages, nullptr);
 }
 
 // K1 with partial pages as TMA tensor boxes of the pools' tensor maps
-template <bool kWS>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(32)
     tpr_k1_kv_migrate_tma(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
                           const __grid_constant__ KvClusterParams cl,
                           const __grid_constant__ KvTensorMaps tm, int32_t stages,
@@ -613,18 +550,13 @@ __global__ void __launch_bounds__(64)
   it.cl = &cl;
   it.tm = &tm;
   it.piece = piece;
-  if (kWS) {
-    bulk_pipeline_ws<true>(it, stages, &tm);
-    return;
-  }
   if (threadIdx.x != 0) return;
   pdl_wait();
   it.start(blockIdx.x);
   bulk_pipeline<true>(it, stages, &tm);
 }
 
-template <bool kWS>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(32)
     tpr_k2_copy_segments_bulk(const tpr_copy_seg_t* __restrict__ segs,
                               const int64_t* __restrict__ prefix, int32_t n_segs, int64_t n_items,
                               int64_t chunk, int64_t* claim, int32_t stages, uint32_t piece) {
@@ -636,11 +568,7 @@ __global__ void __launch_bounds__(64)
   it.n_items = n_items;
   it.chunk = chunk;
   it.piece = piece;
-  if (kWS) {
-    bulk_pipeline_ws<false>(it, stages, nullptr);  // the producer's start() claims work
-    return;
-  }
-  if (threadIdx.x != 0) return;  // one issuing thread: start() claims work
+  if (threadIdx.x != 0) return;  // one issuing thread: start() claims its first batch
   it.start(blockIdx.x);
   bulk_pipeline<false>(it, stages, nullptr);
 }
@@ -649,19 +577,30 @@ __global__ void __launch_bounds__(64)
 // K31: the whole switch of a small plan in ONE launch (K3 bookkeeping + K1
 // copy). The records ride in the kernel parameters (constant bank: every CTA
 // reads them without touching PCIe or L2). Every CTA redoes the keyed scan of
-// the plan (<= kK31Xfers records, one warp), then owns whole pages
-// p = blockIdx.x + j * gridDim.x: its lanes do those pages' block-table /
-// free-ring bookkeeping (k3_page, the same rules as K3), and its elected
-// thread moves them through the TMA ring. A page's bookkeeping and bytes stay
-// in one CTA, so no CTA ever waits for another (the source block-table entry
-// is read and cleared by the CTA that copies the page).
+// the plan (<= kK31Xfers records, one warp) and takes an equal contiguous
+// share of the ITEMS (32 KiB pieces of pages): CTA c copies items
+// [c*N/G, (c+1)*N/G). For each page its items touch, the CTA makes the page's
+// bookkeeping decision itself (k3_page_decide: the same three reads and the
+// same result in every CTA that shares the page, since nothing is written
+// before all of them have read) and counts itself in the page's reader
+// counter; the LAST reader applies the writes (source entry cleared, source
+// unit pushed, destination entry set). No CTA ever waits for another, and the
+// work is balanced to one item.
 //
-// The status word reports this call only: CTAs OR their bits into
-// totals[TPR_TOTALS_K31_STATUS]; the last CTA to finish (counter
-// totals[TPR_TOTALS_K31_DONE]) publishes them to *status (+ the pinned mirror)
-// and leaves both scratch words zero for the next launch. A device-barrier
-// timeout already in *status aborts the call (nothing is touched, the bit stays).
+// Reader counters live in the caller's work-list scratch (d_work, 8 bytes per
+// page), tagged with the launch epoch (totals[TPR_TOTALS_K31_EPOCH], advanced
+// by the last CTA), so they never need clearing (a freshly allocated d_work
+// must be zeroed once). The status word reports this
+// call only: CTAs OR their bits into totals[TPR_TOTALS_K31_STATUS]; the last
+// CTA to finish (counter totals[TPR_TOTALS_K31_DONE]) publishes them to
+// *status (+ the pinned mirror) and resets both scratch words. A
+// device-barrier timeout already in *status aborts the call (nothing is
+// touched, the bit stays).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t k31_cta_of(int64_t item, int64_t n_items, int64_t grid) {
+  return ((item + 1) * grid - 1) / n_items;  // the CTA whose share holds `item`
+}
+
 // kTensor: partial pages move as TMA tensor boxes of the pools' maps (the
 // maps ride in the parameters too: > 4 KiB of parameters, CUDA >= 12.1); a
 // plan of full pages only takes the lean variant.
@@ -670,14 +609,19 @@ __global__ void __launch_bounds__(32)
     tpr_k31_switch(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo, KvCopyParams p,
                    const __grid_constant__ KvClusterParams cl,
                    const __grid_constant__ KvTensorMaps tm, int64_t* __restrict__ totals,
-                   int32_t* __restrict__ status, int32_t* status_mirror, int32_t stages,
-                   uint32_t piece) {
+                   unsigned long long* __restrict__ readers, int32_t* __restrict__ status,
+                   int32_t* status_mirror, int32_t stages, uint32_t piece) {
   __shared__ int64_t s_off[4][kK31Xfers];  // mine, alloc, release offsets; units
   __shared__ int64_t s_carry[3][TPR_MAX_GPUS + 1];
   __shared__ __align__(16) int4 s_work[kK31MaxPages];
   const unsigned lane = threadIdx.x;
   const int32_t st0 = __ldcg(status);
   const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
+  const uint64_t epoch = (uint64_t)__ldcg(totals + TPR_TOTALS_K31_EPOCH);
+  // tags have the high bit set and are never 0xffffffff, so neither a work
+  // item K3 left in d_work ({unit >= 0 or -1, ...}) nor zeroed memory reads as
+  // a counter of this launch
+  const uint32_t tag = 0x80000000u | (uint32_t)((epoch + 1) % 0x7fffffffull);
   const int n = rp.n, B = geo.block_tokens;
   for (int i = lane; i < 3 * (TPR_MAX_GPUS + 1); i += 32) (&s_carry[0][0])[i] = 0;
   __syncwarp();
@@ -715,13 +659,15 @@ __global__ void __launch_bounds__(32)
     }
   }
   const int64_t n_mine = s_carry[0][0];
-  // this CTA's pages: bookkeeping, one lane per page
-  int n_pages = 0;
-  if (!abort && (int64_t)blockIdx.x < n_mine)
-    n_pages = (int)((n_mine - 1 - blockIdx.x) / gridDim.x) + 1;
+  const int64_t ipu = p.items_per_unit, n_items = n_mine * ipu, grid = gridDim.x;
+  // this CTA's share of the items and the pages they belong to
+  const int64_t i0 = (int64_t)blockIdx.x * n_items / grid;
+  const int64_t i1 = ((int64_t)blockIdx.x + 1) * n_items / grid;
+  const int64_t p0 = i0 / ipu;
+  const int n_pages = (abort || i1 <= i0) ? 0 : (int)((i1 - 1) / ipu - p0 + 1);
   int bits = 0;
   for (int j = lane; j < n_pages; j += 32) {
-    const int64_t pg = blockIdx.x + (int64_t)j * gridDim.x;
+    const int64_t pg = p0 + j;
     int lo = 0, hi = n;  // upper_bound(mine offsets, pg) - 1
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -733,8 +679,25 @@ __global__ void __launch_bounds__(32)
     const int h = r[3] + (int)(local / nblk);
     const int b = (int)(local - (int64_t)(h - r[3]) * nblk);
     const int ntok = (b == nblk - 1) ? ctx - b * B : B;
-    s_work[j] = k3_page(cl, geo, r[0], r[1], r[2], h, b, ntok, s_off[1][lo] + local,
-                        s_off[2][lo] + local, bits);
+    const PageOp op = k3_page_decide(cl, geo, r[0], r[1], r[2], h, b, ntok, s_off[1][lo] + local,
+                                     s_off[2][lo] + local);
+    s_work[j] = op.item;
+    bits |= op.bits;
+    // count this CTA among the page's readers; the last one writes
+    const uint32_t n_readers =
+        (uint32_t)(k31_cta_of((pg + 1) * ipu - 1, n_items, grid) - k31_cta_of(pg * ipu, n_items, grid) + 1);
+    __threadfence();  // this CTA's reads of the page's entries come first
+    unsigned long long old = __ldcg(readers + pg), assumed;
+    do {
+      assumed = old;
+      const uint32_t cnt = (uint32_t)(assumed >> 32) == tag ? (uint32_t)assumed + 1u : 1u;
+      old = atomicCAS(readers + pg, assumed, ((unsigned long long)tag << 32) | cnt);
+    } while (old != assumed);
+    const uint32_t before = (uint32_t)(old >> 32) == tag ? (uint32_t)old : 0u;
+    if (before + 1u == n_readers) {
+      __threadfence();  // every other reader's reads happened before its count
+      k3_page_write(cl, op);
+    }
   }
   bits = (int)__reduce_or_sync(0xffffffffu, (unsigned)bits);
   __syncwarp();
@@ -743,14 +706,14 @@ __global__ void __launch_bounds__(32)
                        (unsigned long long)bits);
     if (n_pages > 0) {
       KvPieces<kTensor> it;
-      it.work = s_work;
-      it.n_items = (int64_t)n_pages * p.items_per_unit;
+      it.work = s_work - p0;  // work[u] for the pages p0 .. p0 + n_pages - 1
+      it.n_items = i1;
       it.p = p;
       it.cl = &cl;
       it.tm = kTensor ? &tm : nullptr;
       it.piece = piece;
       it.stride = 1;
-      it.start(0);
+      it.start(i0);
       bulk_pipeline<kTensor>(it, stages, kTensor ? &tm : nullptr);  // waits for its last store
     }
     // the last CTA publishes the status word and resets the scratch words
@@ -763,6 +726,7 @@ __global__ void __launch_bounds__(32)
       const int32_t out = acc | (st0 & TPR_STATUS_BARRIER_TIMEOUT);
       *status = out;
       if (status_mirror) *reinterpret_cast<volatile int32_t*>(status_mirror) = out;
+      totals[TPR_TOTALS_K31_EPOCH] = (int64_t)(epoch + 1);
       *done = 0ull;
       if (!abort) totals[0] = n_mine;
     }
@@ -853,13 +817,12 @@ static int bulk_grid(const void* fn, const BulkConfig& c, int64_t items, int thr
   return grid < 1 ? 1 : (int)grid;
 }
 
-// schedulable units of a K1 launch: items, or claim batches when dynamic
-// items per dynamic claim for a K1 of `items` items: 0 (static grid-stride
-// shares) below 32 items per SM, where a copy is too short to drift and every
-// CTA should start at once
+// items per dynamic claim for a K1 of `items` items: 4 (profiles/ab/
+// r01_claimbatch_*: 2 contends on the counter, 4-6 best), or 0 (static
+// grid-stride shares) below 32 items per SM, where a copy is too short to
+// drift and every CTA should start at once
 static int64_t k1_batch_for(int64_t items) {
-  const int64_t b = k1_claim_batch();
-  return (b > 0 && items >= (int64_t)sm_count() * 32) ? b : 0;
+  return items >= (int64_t)sm_count() * 32 ? 4 : 0;
 }
 
 // schedulable units of a K1 launch: items, or claim batches when dynamic
@@ -868,25 +831,22 @@ static int64_t k1_grid_units(int64_t items) {
   return b > 0 ? (items + b - 1) / b : items;
 }
 
-// Warp-specialised pipelines (producer + consumer warps): TPR_BULK_WS / the
-// "bulk_ws" knob (0 = one issuing thread per CTA).
-template <bool kWS>
 static cudaError_t k1_launch(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
                              int64_t n_units, cudaStream_t st, bool pdl, const KvTensorMaps& tm,
                              const BulkConfig& c) {
-  const int threads = kWS ? 64 : 32;
+  const int64_t items = n_units * p.items_per_unit;
   if (tm.enabled) {
-    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma<kWS>), c,
-                               k1_grid_units(n_units * p.items_per_unit), threads);
-    return launch_ex(tpr_k1_kv_migrate_tma<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
-                     pdl, work, n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece,
-                     (int32_t)k1_batch_for(n_units * p.items_per_unit));
+    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma), c,
+                               k1_grid_units(items), 32);
+    return launch_ex(tpr_k1_kv_migrate_tma, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl, work,
+                     n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece,
+                     (int32_t)k1_batch_for(items));
   }
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk<kWS>), c,
-                             k1_grid_units(n_units * p.items_per_unit), threads);
-  return launch_ex(tpr_k1_kv_migrate_bulk<kWS>, dim3(grid), dim3(threads), (size_t)c.smem(), st,
-                   pdl, work, n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece,
-                   (int32_t)k1_batch_for(n_units * p.items_per_unit));
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
+                             k1_grid_units(items), 32);
+  return launch_ex(tpr_k1_kv_migrate_bulk, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl, work,
+                   n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece,
+                   (int32_t)k1_batch_for(items));
 }
 
 cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,
@@ -899,8 +859,7 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
   KvTensorMaps tm;
   tm.enabled = 0;
   if (geo && (partial || tensor_kernel_always())) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
-  return bulk_ws() ? k1_launch<true>(p, cl, work, n_units, st, pdl, tm, c)
-                   : k1_launch<false>(p, cl, work, n_units, st, pdl, tm, c);
+  return k1_launch(p, cl, work, n_units, st, pdl, tm, c);
 }
 
 // K31 ring: one CTA per SM owning ~1-28 whole pages; TPR_BULK_K31 overrides
@@ -912,26 +871,32 @@ static const BulkConfig& k31_config() {
 cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
-                       cudaStream_t st, int n_gpus, bool partial) {
-  if (n < 1 || n > kK31Xfers || n_units < 1) return cudaErrorNotSupported;
+                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work) {
+  if (n < 1 || n > kK31Xfers || n_units < 1 || !d_work) return cudaErrorNotSupported;
   const BulkConfig& c = k31_config();
   KvTensorMaps tm;
   tm.enabled = 0;
   if (partial) kv_tensor_maps(geo, cl, n_gpus, c.piece, &tm);
   const void* fn = tm.enabled ? reinterpret_cast<const void*>(&tpr_k31_switch<true>)
                               : reinterpret_cast<const void*>(&tpr_k31_switch<false>);
-  const int grid = bulk_grid(fn, c, n_units, 32);
-  if ((n_units + grid - 1) / grid > kK31MaxPages) return cudaErrorNotSupported;
+  const int64_t items = n_units * p.items_per_unit;
+  const int grid = bulk_grid(fn, c, items, 32);
+  // pages one CTA's share of the items touches
+  if (((items + grid - 1) / grid + p.items_per_unit - 1) / p.items_per_unit + 1 > kK31MaxPages)
+    return cudaErrorNotSupported;
+  unsigned long long* readers = reinterpret_cast<unsigned long long*>(d_work);
   K31Params rp;
   memcpy(rp.rec, h_rec, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n);
   rp.n = n;
   rp.filter = filter;
   if (tm.enabled)
-    tpr_k31_switch<true><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, status,
-                                                             status_mirror, c.stages, c.piece);
+    tpr_k31_switch<true><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
+                                                             status, status_mirror, c.stages,
+                                                             c.piece);
   else
-    tpr_k31_switch<false><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, status,
-                                                              status_mirror, c.stages, c.piece);
+    tpr_k31_switch<false><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
+                                                              status, status_mirror, c.stages,
+                                                              c.piece);
   return cudaGetLastError();
 }
 
@@ -941,17 +906,9 @@ cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, in
   const BulkConfig& c = k2_config();
   // dynamic claims hand out kClaimBatch items per CTA and batch
   const int64_t units = claim ? (n_items + kClaimBatch - 1) / kClaimBatch : n_items;
-  if (bulk_ws()) {
-    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk<true>), c,
-                               units, 64);
-    tpr_k2_copy_segments_bulk<true><<<grid, 64, c.smem(), st>>>(segs, prefix, n_segs, n_items,
-                                                                chunk, claim, c.stages, c.piece);
-    return cudaGetLastError();
-  }
-  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk<false>), c,
-                             units, 32);
-  tpr_k2_copy_segments_bulk<false><<<grid, 32, c.smem(), st>>>(segs, prefix, n_segs, n_items,
-                                                               chunk, claim, c.stages, c.piece);
+  const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k2_copy_segments_bulk), c, units, 32);
+  tpr_k2_copy_segments_bulk<<<grid, 32, c.smem(), st>>>(segs, prefix, n_segs, n_items, chunk, claim,
+                                                        c.stages, c.piece);
   return cudaGetLastError();
 }
 

@@ -65,9 +65,6 @@ void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int
                     uint32_t piece_bytes, KvTensorMaps* out);
 bool tensor_partial_enabled();
 bool tensor_kernel_always();
-bool bulk_ws();  // warp-specialised bulk pipelines (producer + consumer warps)
-bool k1_dynamic();  // K1 claims item batches from a counter after the work list
-int k1_claim_batch();  // items per claim, 0 = static shares
 
 int sm_count();
 
@@ -77,10 +74,9 @@ int ptr_device(uint64_t p);
 bool all_local(const uint64_t* ptrs, int n);
 void forget_ranges();
 
-// Programmatic dependent launch of K3b/K1 behind their producer (TPR_PDL=0
-// turns it off) and the plan size (units) up to which K3 runs as one fused
-// CTA (TPR_K3_FUSE_UNITS, 0 = never).
-bool pdl_enabled();
+// The plan size (units) up to which K3 runs as one fused CTA (or the whole
+// switch as K31; TPR_K3_FUSE_UNITS, 0 = never); programmatic dependent launch
+// of K3b / K1 behind their producer is used up to the same size.
 int64_t k3_fuse_units();
 bool pdl_for(int64_t n_units);
 
@@ -91,7 +87,7 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                    int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
                    int32_t* d_status, void* stream, int32_t* status_mirror,
-                   void* const* k1_events = nullptr);  // pdl_enabled() for plans up to k3_fuse_units()
+                   void* const* k1_events = nullptr);
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute when `pdl`.
 template <typename... KArgs, typename... Args>
@@ -133,7 +129,7 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
 cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
-                       cudaStream_t st, int n_gpus, bool partial);
+                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

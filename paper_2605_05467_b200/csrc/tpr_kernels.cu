@@ -664,7 +664,7 @@ cudaError_t launch_k1(const KvCopyParams& p, const KvClusterParams& cl, const in
   if (n_units <= 0) return cudaSuccess;
   const void* fn = reinterpret_cast<const void*>(&tpr_k1_kv_migrate<kCopyUnroll>);
   const int64_t items = n_units * p.items_per_unit;
-  const bool dyn = k1_dynamic() && items >= (int64_t)sm_count() * 32;  // as the bulk K1
+  const bool dyn = items >= (int64_t)sm_count() * 32;  // as the bulk K1
   const int grid = copy_grid(fn, kCopyThreads, dyn ? (items + kVecClaimBatch - 1) / kVecClaimBatch : items);
   return launch_ex(tpr_k1_kv_migrate<kCopyUnroll>, dim3(grid), dim3(kCopyThreads), 0, st, pdl,
                    work, n_units, p, cl, (int32_t)dyn);

@@ -210,7 +210,7 @@ class DistributedKvCluster:
 
     def _run_k3(self, rec: np.ndarray, filter_src: int, n_mine: int, want_ext: bool):
         st = self.stream
-        grow = lambda t, n: t if t.numel() >= n else torch.empty(max(n, 2 * t.numel()), dtype=t.dtype,
+        grow = lambda t, n: t if t.numel() >= n else torch.zeros(max(n, 2 * t.numel()), dtype=t.dtype,
                                                                  device=self.device)
         with torch.cuda.stream(st):
             self._xf = grow(self._xf, len(rec) * 6)
@@ -355,7 +355,7 @@ class DistributedKvCluster:
             k1_events[1].record(self.stream)
         elif n:
             st = self.stream
-            grow = lambda t_, k: t_ if t_.numel() >= k else torch.empty(  # noqa: E731
+            grow = lambda t_, k: t_ if t_.numel() >= k else torch.zeros(  # noqa: E731
                 max(k, 2 * t_.numel()), dtype=t_.dtype, device=self.device)
             with torch.cuda.stream(st):
                 self._xf = grow(self._xf, len(rec) * 6)

@@ -106,16 +106,17 @@ class _PinnedStaging:
 
 
 class _Scratch:
-    """Grow-only device buffer used on one stream."""
+    """Grow-only device buffer used on one stream (zeroed when it grows: the
+    work-list scratch holds K31's epoch-tagged reader counters)."""
 
     def __init__(self, dtype, device):
-        self.t = torch.empty(0, dtype=dtype, device=device)
+        self.t = torch.zeros(0, dtype=dtype, device=device)
 
     def get(self, n: int, stream: torch.cuda.Stream) -> torch.Tensor:
         if self.t.numel() < n:
-            self.t = torch.empty(max(n, 2 * self.t.numel(), 1024), dtype=self.t.dtype,
-                                 device=self.t.device)
-            self.t.record_stream(stream)
+            with torch.cuda.stream(stream):
+                self.t = torch.zeros(max(n, 2 * self.t.numel(), 1024), dtype=self.t.dtype,
+                                     device=self.t.device)
         return self.t
 
 

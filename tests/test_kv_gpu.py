@@ -93,17 +93,13 @@ def test_chain_of_switches_and_back():
 
 LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
     "k31_one_launch": dict(k31=1, k3_fuse_units=1 << 30),
+    "k31_rows_for_partial_pages": dict(k31=1, k3_fuse_units=1 << 30, tensor_partial=0),
     "k31_vector_engine_fallback": dict(k31=1, k3_fuse_units=1 << 30, engine="vector"),
-    "fused_k3_no_k31": dict(k31=0, k3_fuse_units=1 << 30, pdl=2, zero_copy=1, tensor_partial=1),
-    "split_plain_h2d_rows": dict(k3_fuse_units=0, pdl=0, zero_copy=0, tensor_partial=0),
-    "split_pdl_zero_copy": dict(k3_fuse_units=0, pdl=2, zero_copy=1, tensor_partial=1),
-    "fused_pdl_zero_copy": dict(k3_fuse_units=1 << 30, pdl=2, zero_copy=1, tensor_partial=1),
-    "fused_plain_h2d_rows": dict(k3_fuse_units=1 << 30, pdl=0, zero_copy=0, tensor_partial=0),
-    "ws_tensor": dict(bulk_ws=1, tensor_partial=1),
-    "ws_rows": dict(bulk_ws=1, tensor_partial=0, pdl=2),
-    "dynamic_split_tensor": dict(k1_dynamic=1, k3_fuse_units=0, tensor_partial=1),
-    "dynamic_fused_rows_pdl": dict(k1_dynamic=1, k3_fuse_units=1 << 30, tensor_partial=0, pdl=2),
-    "dynamic_ws": dict(k1_dynamic=1, bulk_ws=1),
+    "fused_k3_tensor": dict(k31=0, k3_fuse_units=1 << 30, tensor_partial=1),
+    "fused_k3_rows": dict(k31=0, k3_fuse_units=1 << 30, tensor_partial=0),
+    "split_k3_tensor": dict(k3_fuse_units=0, tensor_partial=1),
+    "split_k3_rows": dict(k3_fuse_units=0, tensor_partial=0),
+    "split_k3_tensor_kernel_always": dict(k3_fuse_units=0, tensor_partial=2),
 }
 
 

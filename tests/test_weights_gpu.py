@@ -151,25 +151,19 @@ def test_window_change_and_overflow():
     store.finish()
 
 
-@pytest.mark.parametrize("ws", [0, 1])
-def test_k2_pipelines_bit_exact(ws):
-    # one issuing thread vs producer + consumer warps (knob bulk_ws)
-    from paper_2605_05467_b200 import _native
-    saved = _native.get_tuning("bulk_ws")
-    _native.set_tuning("bulk_ws", ws)
-    try:
-        gpus = tuple(range(8))
-        for a, b in ((2, 8), (8, 4)):
-            store = ShardedWeightStore(MODEL, gpus)
-            store.load(workloads.tp_groups(gpus, a))
-            pieces = host_pieces(store)
-            store.reshard(workloads.tp_groups(gpus, b))
-            torch.cuda.synchronize()
-            check_against_oracle(store, pieces, workloads.tp_groups(gpus, b))
-            assert store.verify() == 0
-            store.finish()
-    finally:
-        _native.set_tuning("bulk_ws", saved)
+def test_k2_mixed_segments_bit_exact():
+    # TP2 -> TP8 (views + in-place fetches) and TP8 -> TP4 (in-place growth
+    # of every GPU): column- and row-parallel slices through one K2 launch
+    gpus = tuple(range(8))
+    for a, b in ((2, 8), (8, 4)):
+        store = ShardedWeightStore(MODEL, gpus)
+        store.load(workloads.tp_groups(gpus, a))
+        pieces = host_pieces(store)
+        store.reshard(workloads.tp_groups(gpus, b))
+        torch.cuda.synchronize()
+        check_against_oracle(store, pieces, workloads.tp_groups(gpus, b))
+        assert store.verify() == 0
+        store.finish()
 
 
 def test_device_matrix_fill_matches_numpy_pattern():

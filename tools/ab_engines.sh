@@ -5,7 +5,5 @@ set -x
 for i in 1 2; do
   [ -d exp_old ] && (cd exp_old && timeout 400 python bench.py --no-cpu --no-e2e --steps 20 > ../gpurun_out/ab_old_$i.json 2>&1)
   timeout 400 python bench.py --no-cpu --no-e2e --steps 20 > gpurun_out/ab_new_$i.json 2>&1
-  TPR_BULK_WS=1 timeout 400 python bench.py --no-cpu --no-e2e --steps 20 > gpurun_out/ab_ws_$i.json 2>&1
 done
 timeout 600 python tools/sweep.py --modes trace --max-seqs 1 --reps 2 --out gpurun_out/ab_sweep_new.jsonl > /dev/null 2>&1
-TPR_BULK_WS=1 timeout 600 python tools/sweep.py --modes trace --max-seqs 1 --reps 2 --out gpurun_out/ab_sweep_ws.jsonl > /dev/null 2>&1

@@ -5,7 +5,5 @@ timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool racecheck --error-exitc
 timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_kv_gpu.py tests/test_bulk_engine_gpu.py tests/test_weights_gpu.py -q -x -k "not full_size and not cfg" > gpurun_out/sanitize_memcheck_tests.log 2>&1; echo rc=$? >> gpurun_out/sanitize_memcheck_tests.log
 timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool synccheck --error-exitcode 9 python __graft_entry__.py > gpurun_out/sanitize_synccheck_smoke.log 2>&1; echo rc=$? >> gpurun_out/sanitize_synccheck_smoke.log
 # the warp-specialised pipeline (producer/consumer warps synchronised by mbarriers)
-TPR_BULK_WS=1 timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_kv_gpu.py -q -x -k "launch_paths and ws" > gpurun_out/sanitize_racecheck_ws.log 2>&1; echo rc=$? >> gpurun_out/sanitize_racecheck_ws.log
-TPR_BULK_WS=1 timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_kv_gpu.py tests/test_weights_gpu.py -q -x -k "launch_paths or k2_pipelines" > gpurun_out/sanitize_memcheck_ws.log 2>&1; echo rc=$? >> gpurun_out/sanitize_memcheck_ws.log
 # the fused K3's shared-memory scan and record copies, across plan sizes (one-warp blocks included)
 timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_kv_gpu.py -q -x -k "not full_size and not cfg and not large" > gpurun_out/sanitize_racecheck_k3.log 2>&1; echo rc=$? >> gpurun_out/sanitize_racecheck_k3.log

@@ -10,7 +10,7 @@ per switch, median over --reps:
   by a spin kernel while the host enqueues, so host stalls are excluded);
 * ``k1_roof_us``: 2 x bytes / measured copy peak.
 
-Run it with TPR_PDL=0 and/or TPR_K3_FUSE_UNITS=0 to compare the launch
+Run it with TPR_K31=0 and/or TPR_K3_FUSE_UNITS=0 to compare the launch
 variants (one JSON line per case, tagged with the environment).
 
     python tools/small_switch.py --out profiles/small_switch.jsonl
@@ -56,8 +56,8 @@ def main():
     args = ap.parse_args()
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
         if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
-    env = {k: os.environ.get(k, "") for k in ("TPR_PDL", "TPR_K3_FUSE_UNITS", "TPR_ZERO_COPY", "TPR_K31",
-                                              "TPR_BULK_K31")}
+    env = {k: os.environ.get(k, "") for k in ("TPR_K3_FUSE_UNITS", "TPR_K31", "TPR_BULK_K31",
+                                              "TPR_TENSOR_PARTIAL")}
     kv = LLAMA_3_1_8B.kv
     out = open(args.out, "a") if args.out else None
     torch.cuda.set_device(0)
