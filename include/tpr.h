@@ -281,6 +281,10 @@ typedef struct tpr_switch_tables {
                               so a synchronous caller needs no separate read-back */
   void* k1_events[2];      /* nullable cudaEvent_t pair recorded around K1 (timing) */
   int64_t n_records;       /* out: K3 records = the plan's + the release records */
+  int32_t records_async;   /* out: 1 when the device reads `records` after the call
+                              returns (keep them until the stream passes), 0 when
+                              the launch took them (K31: kernel parameters)   */
+  int32_t _pad2;
 } tpr_switch_tables_t;
 
 /* tpr_switch_tables_t.mode: the planner of the switch.

@@ -86,7 +86,8 @@ class SwitchTablesC(Structure):
         ("d_xfers", c_void_p), ("d_meta", c_void_p), ("xfers_cap", c_int64),
         ("d_totals", c_void_p), ("d_work", c_void_p), ("work_cap", c_int64),
         ("d_status", c_void_p), ("plan_bytes", c_int64), ("h_status", c_void_p),
-        ("k1_events", c_void_p * 2), ("n_records", c_int64),
+        ("k1_events", c_void_p * 2), ("n_records", c_int64), ("records_async", c_int32),
+        ("_pad2", c_int32),
     ]
 
 

@@ -134,14 +134,23 @@ int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
   return v;
 }
 
-// pinned or pageable host memory (the CPU can read it); not device memory
+// pinned or pageable host memory (the CPU can read it); not device memory.
+// Host answers are cached per address: under unified addressing a host
+// address is never a device address, so a cached "host" stays true.
 bool host_readable(const int32_t* h) {
+  thread_local const void* seen[8] = {nullptr};
+  thread_local int next = 0;
+  for (const void* s : seen)
+    if (s == h) return true;
   cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
-    cudaGetLastError();
-    return true;  // unregistered host memory
+  bool host = true;  // unregistered host memory fails the query
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) cudaGetLastError();
+  else host = a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+  if (host) {
+    seen[next] = h;
+    next = (next + 1) % 8;
   }
-  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+  return host;
 }
 
 const int32_t* device_view(const int32_t* h) {
@@ -377,7 +386,8 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                    int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
                    int32_t* d_status, void* stream, int32_t* status_mirror,
-                   void* const* k1_events) {
+                   void* const* k1_events, int32_t* records_async) {
+  if (records_async) *records_async = h_xfers != nullptr;
   int rc = check_geometry(geo);
   if (rc) return rc;
   KvClusterParams cp;
@@ -402,6 +412,7 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    any_partial(h_xfers, n_xfers, geo->block_tokens), d_work);
     if (e == cudaSuccess) {
       g_k1_last.store(TPR_ENGINE_BULK);
+      if (records_async) *records_async = 0;  // the launch copied them into its parameters
       if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[1]), st)) != cudaSuccess)
         return cuda_fail(e, "tpr_kv_switch K31 end event");
       return TPR_OK;

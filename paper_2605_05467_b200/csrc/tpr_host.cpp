@@ -336,10 +336,11 @@ int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* 
                 !t->d_totals || !t->d_status || (units > 0 && !t->d_work)))
     return tpr::set_error(TPR_ECAPACITY, "device scratch too small: %lld transfers, %lld units",
                           (long long)n, (long long)units);
+  t->records_async = 0;
   if (n == 0 && !t->h_status) return TPR_OK;
   rc = tpr::kv_switch_impl(geo, cl, t->records, t->d_xfers, (int32_t)n, -1, t->d_meta,
                            t->d_totals, units, t->d_work, t->d_status, stream, t->h_status,
-                           t->k1_events);
+                           t->k1_events, &t->records_async);
   if (rc != TPR_OK) return rc;
   if (n == 0) return TPR_OK;
   return tpr_kv_apply_owner(t->records, n, t->owner, geo->total_heads);

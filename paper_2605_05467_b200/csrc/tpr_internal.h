@@ -87,7 +87,7 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                    int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
                    int32_t* d_status, void* stream, int32_t* status_mirror,
-                   void* const* k1_events = nullptr);
+                   void* const* k1_events = nullptr, int32_t* records_async = nullptr);
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute when `pdl`.
 template <typename... KArgs, typename... Args>

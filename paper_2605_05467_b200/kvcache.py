@@ -644,7 +644,8 @@ class PagedKvCluster:
         self._forget(release)
         if t.n_records == 0:
             return plan, MigrationStats(0, 0, 0, {}, {})
-        self._staging.fence(stream)
+        if t.records_async:  # the device still reads the pinned records
+            self._staging.fence(stream)
         in_u, out_u = t.in_units, t.out_units
         ids = self.gpu_ids
         in_d, out_d = {}, {}

@@ -343,12 +343,30 @@ def head_transfers_array(old: KvLayout, new: KvLayout, kvb: int) -> MigrationPla
         req, ctx, meta, np.asarray(table.ids, dtype=np.int64), old.total_heads, kvb))
 
 
+_PACKED: list = []  # the last few (layout objects, blob): a controller alternates a few layout lists
+
+
 def pack_layouts(old_layouts, new_layouts, release=()):
     """Old and new layouts as one int64 array for ``tpr_switch_prepare``
     (include/tpr.h): n_old, n_new, then every layout's ``packed()``, then --
-    when ``release`` is not empty -- the ids of requests freed by the switch."""
+    when ``release`` is not empty -- the ids of requests freed by the switch.
+    Blobs of immutable layouts are remembered by identity."""
     if isinstance(new_layouts, KvLayout):
         new_layouts = [new_layouts]
+    if not release:
+        key = (*old_layouts, None, *new_layouts)
+        for k, blob in _PACKED:
+            if len(k) == len(key) and all(a is b for a, b in zip(k, key)):
+                return blob
+        if all(isinstance(lay.requests, tuple) for lay in key if lay is not None):
+            blob = _pack(old_layouts, new_layouts, ())
+            _PACKED.insert(0, (key, blob))
+            del _PACKED[8:]
+            return blob
+    return _pack(old_layouts, new_layouts, release)
+
+
+def _pack(old_layouts, new_layouts, release):
     flat = [len(old_layouts), len(new_layouts)]
     for lay in old_layouts:
         flat.extend(lay.packed())

@@ -509,13 +509,16 @@ def test_k31_reports_errors_per_call():
     from paper_2605_05467_b200.controller import ReconfigurationExecutor
     c = make(TINY, (0, 1))
     c.admit([M.KvLayout((0,), 1, 8, ((0, 10),))], seed=1)
+    # request 7 is admitted first: the bad switch below "releases" units GPU1
+    # never held, and the poisoned ring slots it pushes then land on positions
+    # request 7's pages were already popped from (a full ring would have them
+    # overwrite free slots -- a corrupted state that later pops report)
+    c.admit([M.KvLayout((0, 1), 2, 8, ((7, 33),))], seed=1)
     ex = ReconfigurationExecutor(c)
     lie = [M.KvLayout((1,), 1, 8, ((0, 10),)), M.KvLayout((0,), 1, 8, ())]
     bad = ex.switch(lie, [M.KvLayout((0, 1), 2, 8, ((0, 10),))], validate=False)
     assert bad.status & 1 and bad.status & 2
-    # the heads are now on GPU1 only as far as the host knows; a correct switch
-    # of another request reports a clean word
-    c.admit([M.KvLayout((0, 1), 2, 8, ((7, 33),))], seed=1)
+    # a correct switch of the other request reports a clean word
     ok = ex.switch([M.KvLayout((0, 1), 2, 8, ((7, 33),))],
                    [M.KvLayout((1, 0), 2, 8, ((7, 33),))], validate=False)
     assert ok.status == 0 and int(c.status.item()) == 0
