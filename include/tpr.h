@@ -145,6 +145,10 @@ int tpr_get_copy_engine(void);
  *                   [6x32768]). The fused path leaves d_xfers unfilled and
  *                   keeps epoch-tagged per-page counters in d_work (8 bytes
  *                   per page): a freshly allocated d_work must be zeroed once.
+ * Diagnostics: "k31_trace" = the device address of an int64 [grid][8] buffer
+ * (0 = off) where every K31 CTA stores globaltimer stamps of its phases
+ * (entry, scan, decisions, copies, exit), its SM, items and the grid size
+ * (tools/k31_trace.py).
  * tpr_get_tuning returns the current value, -1 for an unknown key. Two
  * read-only keys report the engine the last K1 / K2 launch used
  * ("k1_engine_last", "k2_engine_last": TPR_ENGINE_*, -1 before the first):

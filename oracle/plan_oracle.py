@@ -3,7 +3,7 @@
 Pure-Python restatement of the reference planner and cost models
 (pkg/src/tpsim/migration.py). Pinned against golden vectors produced by the
 reference itself (tests/golden/gen_golden.py, run in the build container where
-/root/reference exists); see tests/test_oracle_golden.py.
+/root/reference exists); see tests/test_oracle.py.
 
 Plain tuples, no classes: a layout is (group tuple, total_heads, requests).
 """

@@ -232,13 +232,29 @@ class ReconfigurationExecutor:
 def measured_switch_cost(executor: ReconfigurationExecutor):
     """Adapter with the signature of ``migration.switch_cost(mode, plan, params)``
     that executes ``plan`` (already in this cluster's placement) and returns the
-    measured pause in ms, for wiring into the reference engine."""
+    pause in ms, for wiring into the reference engine.
+
+    The modes keep the reference's meaning (migration.py:284-292): ``warm`` is
+    the measured switch plus the metadata handshake ``params.handshake_ms``
+    (the reference's warm cost is handshake + the pipelined copy model);
+    ``naive_reload`` / ``naive_kernel_init`` add ``params.reload_ms`` /
+    ``params.kernel_init_ms`` to the measured KV move, since a naive switch
+    also reloads weights / re-initialises kernels, which this data path does
+    not execute. Any other mode raises the reference's MigrationError."""
+    from .migration import NAIVE_KERNEL_INIT, NAIVE_RELOAD, WARM, MigrationError
 
     def cost(mode, plan: MigrationPlan, params) -> float:
+        if mode not in (WARM, NAIVE_RELOAD, NAIVE_KERNEL_INIT):
+            raise MigrationError(f"unknown switch mode {mode!r}")
         t0 = time.perf_counter()
         executor.kv.migrate(plan, stream=executor.kv_stream)
         executor.kv_stream.synchronize()
-        return (time.perf_counter() - t0) * 1e3
+        measured = (time.perf_counter() - t0) * 1e3
+        if mode == WARM:
+            return params.handshake_ms + measured
+        if mode == NAIVE_RELOAD:
+            return params.reload_ms + measured
+        return params.kernel_init_ms + measured
 
     return cost
 

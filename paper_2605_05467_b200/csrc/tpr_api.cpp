@@ -122,7 +122,7 @@ int64_t env_i64(const char* name, int64_t dflt);
 
 // Launch-path knobs (process-wide): initialised from the environment, changed
 // at run time with tpr_set_tuning (tests cover every combination).
-std::atomic<int64_t> g_fuse{-1}, g_tensor{-1}, g_k31{-1};
+std::atomic<int64_t> g_fuse{-1}, g_tensor{-1}, g_k31{-1}, g_k31_trace{0};
 
 int64_t knob(std::atomic<int64_t>& k, const char* env, int64_t dflt) {
   int64_t v = k.load(std::memory_order_relaxed);
@@ -257,6 +257,8 @@ bool pool_map(const MapKey& k, CUtensorMap* out) {
 // schedule and is neutral with dynamic claims (profiles/ab/r01_pdl_*), so
 // large plans launch K1 normally.
 bool pdl_for(int64_t n_units) { return n_units <= k3_fuse_units(); }
+
+int64_t k31_trace_buffer() { return g_k31_trace.load(std::memory_order_relaxed); }
 
 int64_t k3_fuse_units() {
   // one 1024-thread CTA expands up to 4 units per thread faster than a second
@@ -484,6 +486,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
   else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
   else if (!strcmp(key, "k31")) g_k31.store(value != 0);
+  else if (!strcmp(key, "k31_trace")) g_k31_trace.store(value);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;
 }
@@ -493,6 +496,7 @@ int64_t tpr_get_tuning(const char* key) {
   if (!strcmp(key, "k3_fuse_units")) return tpr::k3_fuse_units();
   if (!strcmp(key, "tensor_partial")) return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1);
   if (!strcmp(key, "k31")) return knob(g_k31, "TPR_K31", 1);
+  if (!strcmp(key, "k31_trace")) return g_k31_trace.load();
   if (!strcmp(key, "k1_engine_last")) return g_k1_last.load();
   if (!strcmp(key, "k2_engine_last")) return g_k2_last.load();
   return -1;

@@ -615,6 +615,15 @@ __global__ void __launch_bounds__(32)
   __shared__ int64_t s_carry[3][TPR_MAX_GPUS + 1];
   __shared__ __align__(16) int4 s_work[kK31MaxPages];
   const unsigned lane = threadIdx.x;
+  // phase stamps for tools/k31_trace.py: entry, scan, decisions, copies, exit
+  auto stamp = [&](int k) {
+    if (rp.trace != nullptr && lane == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      rp.trace[blockIdx.x * 8 + k] = t;
+    }
+  };
+  stamp(0);
   const int32_t st0 = __ldcg(status);
   const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
   const uint64_t epoch = (uint64_t)__ldcg(totals + TPR_TOTALS_K31_EPOCH);
@@ -659,6 +668,7 @@ __global__ void __launch_bounds__(32)
     }
   }
   const int64_t n_mine = s_carry[0][0];
+  stamp(1);
   const int64_t ipu = p.items_per_unit, n_items = n_mine * ipu, grid = gridDim.x;
   // this CTA's share of the items and the pages they belong to
   const int64_t i0 = (int64_t)blockIdx.x * n_items / grid;
@@ -701,6 +711,7 @@ __global__ void __launch_bounds__(32)
   }
   bits = (int)__reduce_or_sync(0xffffffffu, (unsigned)bits);
   __syncwarp();
+  stamp(2);
   if (lane == 0) {
     if (bits) atomicOr(reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS),
                        (unsigned long long)bits);
@@ -716,6 +727,7 @@ __global__ void __launch_bounds__(32)
       it.start(i0);
       bulk_pipeline<kTensor>(it, stages, kTensor ? &tm : nullptr);  // waits for its last store
     }
+    stamp(3);
     // the last CTA publishes the status word and resets the scratch words
     __threadfence();
     unsigned long long* done = reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_DONE);
@@ -729,6 +741,14 @@ __global__ void __launch_bounds__(32)
       totals[TPR_TOTALS_K31_EPOCH] = (int64_t)(epoch + 1);
       *done = 0ull;
       if (!abort) totals[0] = n_mine;
+    }
+    stamp(4);
+    if (rp.trace != nullptr) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      rp.trace[blockIdx.x * 8 + 5] = smid;
+      rp.trace[blockIdx.x * 8 + 6] = (uint64_t)(i1 - i0);
+      rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
     }
   }
 }
@@ -889,6 +909,7 @@ cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
   memcpy(rp.rec, h_rec, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n);
   rp.n = n;
   rp.filter = filter;
+  rp.trace = reinterpret_cast<uint64_t*>(k31_trace_buffer());
   if (tm.enabled)
     tpr_k31_switch<true><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
                                                              status, status_mirror, c.stages,

@@ -57,7 +57,9 @@ struct K31Params {
   int32_t rec[kK31Xfers][TPR_XFER_FIELDS];
   int32_t n;
   int32_t filter;
+  uint64_t* trace;  // nullable: per-CTA globaltimer stamps (knob "k31_trace")
 };
+int64_t k31_trace_buffer();
 
 // Tensor maps for the pools of `cl` (cached per pool); out->enabled = 0 when
 // the geometry does not fit TMA's limits or the driver entry point is missing.

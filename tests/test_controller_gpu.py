@@ -142,9 +142,16 @@ def test_measured_switch_cost_adapter():
     new = M.KvLayout((0, 1), 2, 8, ((0, 50), (1, 50)))
     kv.admit(old, seed=1)
     cost = measured_switch_cost(ex)
-    ms = cost(M.WARM, M.plan_repartition(old, new, KV.kv_bytes_per_token_per_head), M.CostModelParams())
-    assert ms > 0
+    params = M.CostModelParams()
+    ms = cost(M.WARM, M.plan_repartition(old, new, KV.kv_bytes_per_token_per_head), params)
+    assert ms > params.handshake_ms
     assert kv.placement() == M.layout_placement(new)
+    # the naive modes add the reference's fixed reload / kernel-init cost
+    back = M.plan_repartition([new], old, KV.kv_bytes_per_token_per_head)
+    assert cost(M.NAIVE_RELOAD, back, params) > params.reload_ms
+    assert kv.placement() == M.layout_placement(old)
+    with pytest.raises(M.MigrationError, match="unknown switch mode"):
+        cost("bogus", back, params)
 
 
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TPR_FUZZ_SEEDS", "3"))))

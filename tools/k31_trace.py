@@ -1,0 +1,83 @@
+"""Where the time of a small switch goes inside K31 (knob "k31_trace"): every
+CTA stamps %globaltimer at its entry, after the keyed scan, after its page
+decisions, after its copies and at its exit. Prints, per phase, the
+min / median / max over CTAs relative to the first CTA's entry (ns), plus the
+spread of CTA entry times (launch ramp).
+
+    python tools/k31_trace.py [--case 1seq|cfg1|1seq4096] [--engine bulk]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+CASES = {"1seq": (8, 1, 2, 1, 463), "cfg1": (2, 1, 2, 4, 512), "1seq4096": (8, 8, 1, 1, 4096)}
+
+
+def main():
+    import torch
+
+    from paper_2605_05467_b200 import _native, workloads
+    from paper_2605_05467_b200.controller import ReconfigurationExecutor
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
+    from paper_2605_05467_b200.kvcache import PagedKvCluster
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="1seq", choices=sorted(CASES))
+    ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    slots, a, b, n, ctx = CASES[args.case]
+    kv = LLAMA_3_1_8B.kv
+    gpus = tuple(range(slots))
+    reqs = [(i, ctx) for i in range(n)]
+    la = workloads.round_robin(workloads.tp_groups(gpus, a), reqs, kv.total_heads)
+    lb = workloads.round_robin(workloads.tp_groups(gpus, b), reqs, kv.total_heads)
+    units = 2 * n * kv.total_heads * kv.blocks(ctx) + 64
+    cl = PagedKvCluster(kv, gpus, units_per_gpu=units, max_requests=n, max_blocks=kv.blocks(ctx),
+                        fragmented=True, seed=0)
+    cl.admit(la, seed=5)
+    ex = ReconfigurationExecutor(cl)
+    buf = torch.zeros(2048 * 8, dtype=torch.int64, device="cuda")
+    _native.set_tuning("k31_trace", buf.data_ptr())
+    rows = []
+    try:
+        for i in range(args.reps):
+            buf.zero_()
+            torch.cuda._sleep(200_000)  # the launch waits on the stream, not the host
+            ex.switch(*((la, lb) if i % 2 == 0 else (lb, la)), validate=False)
+            t = buf.view(-1, 8).cpu().numpy()
+            grid = int(t[0, 7])
+            if grid <= 0:
+                raise SystemExit("no K31 launch (plan outside the fused path?)")
+            t = t[:grid]
+            base = t[:, 0].min()
+            rows.append({k: (t[:, j] - base) for j, k in enumerate(("entry", "scan", "decide",
+                                                                      "copies", "exit"))})
+    finally:
+        _native.set_tuning("k31_trace", 0)
+    last = rows[len(rows) // 2:]
+    out = {"case": args.case, "grid": grid, "items_per_cta": [int(x) for x in
+                                                              np.unique(t[:, 6])]}
+    for k in ("entry", "scan", "decide", "copies", "exit"):
+        v = np.concatenate([r[k] for r in last])
+        out[k] = {"min": int(v.min()), "median": int(np.median(v)), "max": int(v.max())}
+    out["copy_phase_median_ns"] = int(np.median(np.concatenate(
+        [r["copies"] - r["decide"] for r in last])))
+    out["kernel_span_median_ns"] = int(np.median([r["exit"].max() for r in last]))
+    print(json.dumps(out))
+    if args.out:
+        with open(args.out, "a") as f:
+            f.write(json.dumps(out) + "\n")
+
+
+if __name__ == "__main__":
+    main()
