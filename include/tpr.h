@@ -414,10 +414,8 @@ int tpr_matrix_verify(uint64_t buf, int64_t rows, int64_t cols, int64_t pitch_el
 /* ---- library baselines (measurement only) ------------------------------ */
 /* The paper's straw-man ("cudaMemcpyAsync ... issue a
  * separate request for each memory page"): copy n (src, dst, bytes) pages with
- * one cudaMemcpyAsync each (method 0) or one cudaMemcpyBatchAsync (method 1).
- * Arrays are host memory. */
+ * one cudaMemcpyAsync each (method 0, the only method). Arrays are host memory. */
 #define TPR_BASELINE_MEMCPY 0
-#define TPR_BASELINE_MEMCPY_BATCH 1
 int tpr_baseline_copy_pages(const uint64_t* src, const uint64_t* dst, const uint64_t* bytes,
                             int64_t n, int32_t method, void* stream);
 

@@ -808,30 +808,6 @@ int tpr_baseline_copy_pages(const uint64_t* src, const uint64_t* dst, const uint
     }
     return TPR_OK;
   }
-  if (method == TPR_BASELINE_MEMCPY_BATCH) {
-#if CUDART_VERSION >= 12080
-    if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread)
-      return fail(TPR_EINVAL, "cudaMemcpyBatchAsync needs an explicitly created stream");
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0;
-    size_t fail_idx = 0;
-    const int64_t kMax = 1 << 20;  // the API takes size_t counts; chunk very long lists
-    for (int64_t off = 0; off < n; off += kMax) {
-      const size_t cnt = (size_t)std::min<int64_t>(kMax, n - off);
-      cudaError_t e = cudaMemcpyBatchAsync(
-          reinterpret_cast<void**>(const_cast<uint64_t*>(dst + off)),
-          reinterpret_cast<void**>(const_cast<uint64_t*>(src + off)),
-          reinterpret_cast<size_t*>(const_cast<uint64_t*>(bytes + off)), cnt, &attr, &attr_idx, 1,
-          &fail_idx, st);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyBatchAsync");
-    }
-    return TPR_OK;
-#else
-    return fail(TPR_EINVAL, "cudaMemcpyBatchAsync needs CUDA >= 12.8");
-#endif
-  }
   return fail(TPR_EINVAL, "unknown baseline method %d", method);
 }
 

@@ -8,7 +8,6 @@ One request of 4096..40960 tokens moves all 8 KV heads between two GPU slots
 
 * per-plane cudaMemcpyAsync: one call per (page, layer, K|V) plane, 4 KiB each;
   this is the "separate request for each memory page" straw-man;
-* per-plane cudaMemcpyBatchAsync: the same planes in one CUDA 12.8+ batch call;
 * per-page cudaMemcpyAsync: one call per 256 KiB page (all layers);
 * K3 + K1 (this repo): one ABI call.
 
@@ -118,7 +117,7 @@ def main():
     args = ap.parse_args()
     kv = LLAMA_3_1_8B.kv
     H = kv.total_heads
-    st = torch.cuda.Stream()  # explicit stream: cudaMemcpyBatchAsync refuses the legacy one
+    st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
     out = open(args.out, "w")
     for fragmented in (True, False):
@@ -164,7 +163,6 @@ def main():
             res = {"fragmented": fragmented, "tokens": tokens, "bytes": nbytes,
                    "k3_k1_ms": k1_ms}
             for name, gran, method in (("memcpy_per_plane", "plane", 0),
-                                       ("memcpy_batch_per_plane", "plane", 1),
                                        ("memcpy_per_page", "page", 0)):
                 if gran == "page":
                     s = p0 + su * U
@@ -185,7 +183,7 @@ def main():
                     torch.cuda.synchronize()
                     ts.append((time.perf_counter() - t0) * 1e3)
                 res[name + "_ms"] = min(ts)
-                res[name + "_calls"] = int(len(s)) if method == 0 else 1
+                res[name + "_calls"] = int(len(s))
             res["aggregate_pipelined_ms"] = aggregate_pipelined(c, su, du, st)
             res["speedup_vs_memcpy_per_plane"] = res["memcpy_per_plane_ms"] / k1_ms
             print(json.dumps(res))
