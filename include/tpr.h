@@ -115,7 +115,12 @@ typedef struct tpr_kv_cluster {
 #define TPR_TOTALS_K31_DONE (1 + 2 * TPR_MAX_GPUS)
 #define TPR_TOTALS_K31_STATUS (2 + 2 * TPR_MAX_GPUS)
 #define TPR_TOTALS_K31_EPOCH (3 + 2 * TPR_MAX_GPUS)
-#define TPR_TOTALS_LEN (4 + 2 * TPR_MAX_GPUS)
+/* [TPR_TOTALS_K31_PAR + 2k + parity], k = 0 claim counter, 1 CTAs decided,
+ * 2 status bits: the dynamic small-switch kernel's words, double-buffered by
+ * the launch parity the host tracks per d_totals (a launch resets the other
+ * parity's words, which the previous launch on the stream used). */
+#define TPR_TOTALS_K31_PAR (4 + 2 * TPR_MAX_GPUS)
+#define TPR_TOTALS_LEN (10 + 2 * TPR_MAX_GPUS)
 
 /* ---- host utilities -------------------------------------------------- */
 /* Copy engine of K1 and K2 (process-wide): TPR_ENGINE_BULK (default) = TMA
@@ -139,15 +144,23 @@ int tpr_get_copy_engine(void);
  *                   plan is partial, 2 the tensor kernel for every plan;
  *   "k31"           [TPR_K31, 1]: a plan of at most k3_fuse_units pages and 96
  *                   transfers (host records, TMA engine, local pools) runs as
- *                   ONE kernel, K31: every CTA redoes the keyed scan of the
- *                   records (kernel parameters) and owns whole pages, doing
- *                   their bookkeeping and their copy (ring TPR_BULK_K31
- *                   [6x32768]). The fused path leaves d_xfers unfilled and
- *                   keeps epoch-tagged per-page counters in d_work (8 bytes
- *                   per page): a freshly allocated d_work must be zeroed once.
+ *                   ONE kernel, K31, with the records and their three keyed
+ *                   exclusive scans (done on the host) in its parameters and
+ *                   two warps per CTA (ring TPR_BULK_K31 [3x32768], two CTAs
+ *                   per SM). Two schedules: item shares (every CTA decides
+ *                   the pages its equal share of 32 KiB items touches, the
+ *                   last reader applies the bookkeeping; epoch-tagged
+ *                   per-page counters in d_work, 8 bytes per page: a freshly
+ *                   allocated d_work must be zeroed once) and dynamic (each
+ *                   page decided once by its owner CTA, a grid-wide wait --
+ *                   cooperative launch -- then K1's dynamic item claims).
+ *                   0 = off, 1 = item shares below 512 pages and dynamic from
+ *                   there, 2 = always dynamic, 3 = always item shares. The
+ *                   fused path leaves d_xfers unfilled.
  * Diagnostics: "k31_trace" = the device address of an int64 [grid][8] buffer
  * (0 = off) where every K31 CTA stores globaltimer stamps of its phases
- * (entry, scan, decisions, copies, exit), its SM, items and the grid size
+ * (item shares: entry, decisions, copies, bookkeeping; dynamic: entry,
+ * decisions, grid-wide wait, copies) and the grid size in [7]
  * (tools/k31_trace.py).
  * tpr_get_tuning returns the current value, -1 for an unknown key. Two
  * read-only keys report the engine the last K1 / K2 launch used
@@ -289,6 +302,11 @@ typedef struct tpr_switch_tables {
                               returns (keep them until the stream passes), 0 when
                               the launch took them (K31: kernel parameters)   */
   int32_t _pad2;
+  int64_t* ring_head_io;   /* nullable int64 [n_slots]: advanced by in_units    */
+  int64_t* ring_tail_io;   /* nullable int64 [n_slots]: advanced by out_units
+                              (both after the switch is enqueued; point them at
+                              the cluster's own ring_head / ring_tail to keep
+                              the host ring counters without a round trip)    */
 } tpr_switch_tables_t;
 
 /* tpr_switch_tables_t.mode: the planner of the switch.

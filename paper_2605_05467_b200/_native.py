@@ -17,7 +17,7 @@ TPR_ABI_VERSION = 1
 TPR_MAX_GPUS = 16
 TPR_XFER_FIELDS = 6
 TPR_META_FIELDS = 4
-TPR_TOTALS_LEN = 4 + 2 * TPR_MAX_GPUS  # + 3 scratch words of the fused small switch
+TPR_TOTALS_LEN = 10 + 2 * TPR_MAX_GPUS  # + scratch words of the fused small switch
 TPR_STATUS_WRONG_SOURCE = 1
 TPR_STATUS_DST_OCCUPIED = 2
 TPR_STATUS_BARRIER_TIMEOUT = 4
@@ -87,7 +87,7 @@ class SwitchTablesC(Structure):
         ("d_totals", c_void_p), ("d_work", c_void_p), ("work_cap", c_int64),
         ("d_status", c_void_p), ("plan_bytes", c_int64), ("h_status", c_void_p),
         ("k1_events", c_void_p * 2), ("n_records", c_int64), ("records_async", c_int32),
-        ("_pad2", c_int32),
+        ("_pad2", c_int32), ("ring_head_io", c_void_p), ("ring_tail_io", c_void_p),
     ]
 
 

@@ -65,6 +65,10 @@ class ReconfigurationExecutor:
         self.w_stream = torch.cuda.Stream(device=dev) if overlap else self.kv_stream
         self.time_kernels = time_kernels
         self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        # numpy views of the pinned status words (indexing a tensor costs
+        # microseconds on the small-switch path)
+        self._status_np = self._status_host.numpy()
+        self._kv_status_np = kv.status_host.numpy()
         self.main_stream = torch.cuda.current_stream(dev)
         # reused per synchronous switch (each one waits for its end event)
         self._ev_sync = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -79,7 +83,7 @@ class ReconfigurationExecutor:
                          4, main.cuda_stream)
         res.events["end"].record(main)
         res.events["end"].synchronize()
-        res.status = int((self.kv.status_host if mirrored else self._status_host)[0])
+        res.status = int((self._kv_status_np if mirrored else self._status_np)[0])
         res.host_ms = (time.perf_counter() - t0) * 1e3
         res.device_ms = res.events["start"].elapsed_time(res.events["end"])
         return res

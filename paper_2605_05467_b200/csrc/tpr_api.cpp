@@ -411,7 +411,8 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
       return cuda_fail(e, "tpr_kv_switch K31 start event");
     e = launch_k31(*geo, copy_params(geo), cp, h_xfers, n_xfers, filter_src, n_units, d_totals,
                    d_status, status_mirror, st, cl->n_gpus,
-                   any_partial(h_xfers, n_xfers, geo->block_tokens), d_work);
+                   any_partial(h_xfers, n_xfers, geo->block_tokens), d_work,
+                   (int)knob(g_k31, "TPR_K31", 1));
     if (e == cudaSuccess) {
       g_k1_last.store(TPR_ENGINE_BULK);
       if (records_async) *records_async = 0;  // the launch copied them into its parameters
@@ -485,7 +486,7 @@ int tpr_set_tuning(const char* key, int64_t value) {
   if (value < 0) return fail(TPR_EINVAL, "tuning value must be >= 0");
   if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
   else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
-  else if (!strcmp(key, "k31")) g_k31.store(value != 0);
+  else if (!strcmp(key, "k31")) g_k31.store(value < 0 ? 0 : value > 3 ? 3 : value);
   else if (!strcmp(key, "k31_trace")) g_k31_trace.store(value);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;

@@ -15,6 +15,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
 #include "tpr.h"
 #include "tpr_common.cuh"
 #include "tpr_internal.h"
@@ -122,6 +126,7 @@ struct KvPieces {
   int64_t item;
   unsigned long long* claim = nullptr;  // dynamic schedule (0 at kernel start)
   int64_t batch = 4, item_end = 0, next_batch = 0;
+  bool work_l2 = false;  // work items written by this launch: read them from L2
   int64_t stride = -1;  // static schedule step (-1: gridDim.x, grid-stride shares)
   // current item: linear rows ...
   const char* s;
@@ -164,7 +169,7 @@ struct KvPieces {
     while (take(it)) {
       const int64_t u = it / p.items_per_unit;
       const int g = (int)(it - u * p.items_per_unit);
-      const int4 w = work[u];
+      const int4 w = work_l2 ? __ldcg(work + u) : work[u];
       const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
       if (w.x < 0 || w.y < 0 || ntok <= 0) continue;  // a page K3 refused (status word)
       const int64_t nb = (int64_t)ntok * p.tok_bytes;
@@ -575,147 +580,114 @@ __global__ void __launch_bounds__(32)
 
 // ---------------------------------------------------------------------------
 // K31: the whole switch of a small plan in ONE launch (K3 bookkeeping + K1
-// copy). The records ride in the kernel parameters (constant bank: every CTA
-// reads them without touching PCIe or L2). Every CTA redoes the keyed scan of
-// the plan (<= kK31Xfers records, one warp) and takes an equal contiguous
-// share of the ITEMS (32 KiB pieces of pages): CTA c copies items
-// [c*N/G, (c+1)*N/G). For each page its items touch, the CTA makes the page's
-// bookkeeping decision itself (k3_page_decide: the same three reads and the
-// same result in every CTA that shares the page, since nothing is written
-// before all of them have read) and counts itself in the page's reader
-// counter; the LAST reader applies the writes (source entry cleared, source
-// unit pushed, destination entry set). No CTA ever waits for another, and the
-// work is balanced to one item.
+// copy). The records and their three keyed exclusive scans (units before
+// each record that this rank moves / its destination ring hands out / its
+// source ring takes back) ride in the kernel parameters: the host builds the
+// records, so it does K3's scan in passing, and every CTA starts deciding at
+// entry. CTA c copies an equal contiguous share of the ITEMS (32 KiB pieces
+// of pages), items [c*N/G, (c+1)*N/G). For each page its items touch, the
+// CTA makes the page's bookkeeping decision itself (k3_page_decide: the same
+// three reads and the same result in every CTA that shares the page, since
+// nothing is written before all of them have read) and counts itself in the
+// page's reader counter; the LAST reader applies the writes (source entry
+// cleared, source unit pushed, destination entry set). No CTA ever waits for
+// another, and the work is balanced to one item.
+//
+// Two warps per CTA. The copies need only the decisions (unit ids), not the
+// bookkeeping writes, and the writes touch tables and rings, never page
+// bytes. So once the 64 threads have decided the CTA's pages (one read round
+// trip, one thread per page), warp 0's elected thread streams the copies
+// while warp 1 does the reader counting, the writes, the status bits and the
+// completion counter off the copy's critical path.
 //
 // Reader counters live in the caller's work-list scratch (d_work, 8 bytes per
 // page), tagged with the launch epoch (totals[TPR_TOTALS_K31_EPOCH], advanced
 // by the last CTA), so they never need clearing (a freshly allocated d_work
 // must be zeroed once). The status word reports this
 // call only: CTAs OR their bits into totals[TPR_TOTALS_K31_STATUS]; the last
-// CTA to finish (counter totals[TPR_TOTALS_K31_DONE]) publishes them to
-// *status (+ the pinned mirror) and resets both scratch words. A
-// device-barrier timeout already in *status aborts the call (nothing is
-// touched, the bit stays).
+// CTA to finish its bookkeeping (counter totals[TPR_TOTALS_K31_DONE])
+// publishes them to *status (+ the pinned mirror) and resets both scratch
+// words. A device-barrier timeout already in *status aborts the call (no
+// copy, no write; the bit stays).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int64_t k31_cta_of(int64_t item, int64_t n_items, int64_t grid) {
   return ((item + 1) * grid - 1) / n_items;  // the CTA whose share holds `item`
 }
 
+constexpr int kK31Threads = 64;
+constexpr int64_t kK31DynamicUnits = 512;  // auto schedule: dynamic from here up
+static_assert(kK31MaxPages <= kK31Threads, "one deciding thread per page");
+
 // kTensor: partial pages move as TMA tensor boxes of the pools' maps (the
 // maps ride in the parameters too: > 4 KiB of parameters, CUDA >= 12.1); a
 // plan of full pages only takes the lean variant.
 template <bool kTensor>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(kK31Threads)
     tpr_k31_switch(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo, KvCopyParams p,
                    const __grid_constant__ KvClusterParams cl,
                    const __grid_constant__ KvTensorMaps tm, int64_t* __restrict__ totals,
                    unsigned long long* __restrict__ readers, int32_t* __restrict__ status,
                    int32_t* status_mirror, int32_t stages, uint32_t piece) {
-  __shared__ int64_t s_off[4][kK31Xfers];  // mine, alloc, release offsets; units
-  __shared__ int64_t s_carry[3][TPR_MAX_GPUS + 1];
   __shared__ __align__(16) int4 s_work[kK31MaxPages];
-  const unsigned lane = threadIdx.x;
-  // phase stamps for tools/k31_trace.py: entry, scan, decisions, copies, exit
+  __shared__ PageOp s_op[kK31MaxPages];
+  __shared__ int s_bits[2];
+  __shared__ int32_t s_st0;
+  __shared__ uint64_t s_epoch;
+  const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  // phase stamps for tools/k31_trace.py: entry, decisions, copies, bookkeeping
   auto stamp = [&](int k) {
-    if (rp.trace != nullptr && lane == 0) {
-      uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      rp.trace[blockIdx.x * 8 + k] = t;
-    }
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    rp.trace[blockIdx.x * 8 + k] = t;
   };
-  stamp(0);
-  const int32_t st0 = __ldcg(status);
-  const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
-  const uint64_t epoch = (uint64_t)__ldcg(totals + TPR_TOTALS_K31_EPOCH);
-  // tags have the high bit set and are never 0xffffffff, so neither a work
-  // item K3 left in d_work ({unit >= 0 or -1, ...}) nor zeroed memory reads as
-  // a counter of this launch
-  const uint32_t tag = 0x80000000u | (uint32_t)((epoch + 1) % 0x7fffffffull);
+  const bool tracing = rp.trace != nullptr;
+  if (tracing && tid == 0) stamp(0);
   const int n = rp.n, B = geo.block_tokens;
-  for (int i = lane; i < 3 * (TPR_MAX_GPUS + 1); i += 32) (&s_carry[0][0])[i] = 0;
-  __syncwarp();
-  // three keyed exclusive scans over the records, 32 at a time
-  for (int base = 0; base < n; base += 32) {
-    const int t = base + (int)lane;
-    int key[3] = {0, TPR_MAX_GPUS, TPR_MAX_GPUS};
-    int64_t val[3] = {0, 0, 0};
-    if (t < n) {
-      const int32_t* r = rp.rec[t];
-      const int64_t nblk = r[5] > 0 ? (r[5] + B - 1) / B : 0;
-      const int64_t u = (int64_t)(r[4] - r[3]) * nblk;
-      key[1] = r[1] >= 0 ? r[1] : TPR_MAX_GPUS;
-      key[2] = r[0] >= 0 ? r[0] : TPR_MAX_GPUS;
-      val[0] = (rp.filter < 0 || r[0] == rp.filter) ? u : 0;
-      val[1] = r[1] >= 0 ? u : 0;
-      val[2] = r[0] >= 0 ? u : 0;
-      s_off[3][t] = val[0];
+  if (warp == 1) {  // the call's status and epoch words, tensor maps warmed
+    if (lane == 0) {
+      s_st0 = __ldcg(status);
+      s_epoch = (uint64_t)__ldcg(totals + TPR_TOTALS_K31_EPOCH);
     }
-#pragma unroll
-    for (int sc = 0; sc < 3; ++sc) {
-      const unsigned peers = __match_any_sync(0xffffffffu, key[sc]);
-      const unsigned lower = peers & ((1u << lane) - 1u);
-      int64_t acc = 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int64_t vj = __shfl_sync(0xffffffffu, val[sc], j);
-        if ((lower >> j) & 1u) acc += vj;
-      }
-      const int64_t carry = s_carry[sc][key[sc]];
-      if (t < n) s_off[sc][t] = carry + acc;
-      __syncwarp();
-      if (lane == 31u - (unsigned)__clz(peers)) s_carry[sc][key[sc]] = carry + acc + val[sc];
-      __syncwarp();
-    }
+    if (kTensor && tm.enabled && lane < TPR_MAX_GPUS && cl.pool[lane] != 0)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.map[lane]))
+                   : "memory");
   }
-  const int64_t n_mine = s_carry[0][0];
-  stamp(1);
+  const int64_t n_mine = rp.n_mine;
   const int64_t ipu = p.items_per_unit, n_items = n_mine * ipu, grid = gridDim.x;
   // this CTA's share of the items and the pages they belong to
   const int64_t i0 = (int64_t)blockIdx.x * n_items / grid;
   const int64_t i1 = ((int64_t)blockIdx.x + 1) * n_items / grid;
   const int64_t p0 = i0 / ipu;
-  const int n_pages = (abort || i1 <= i0) ? 0 : (int)((i1 - 1) / ipu - p0 + 1);
+  const int n_pages = i1 <= i0 ? 0 : (int)((i1 - 1) / ipu - p0 + 1);
+  // decisions: one thread per page (reads only)
   int bits = 0;
-  for (int j = lane; j < n_pages; j += 32) {
-    const int64_t pg = p0 + j;
+  if ((int)tid < n_pages) {
+    const int64_t pg = p0 + tid;
     int lo = 0, hi = n;  // upper_bound(mine offsets, pg) - 1
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (s_off[0][mid] <= pg) lo = mid; else hi = mid;
+      if (rp.off[0][mid] <= pg) lo = mid; else hi = mid;
     }
     const int32_t* r = rp.rec[lo];
-    const int64_t local = pg - s_off[0][lo];
+    const int64_t local = pg - rp.off[0][lo];
     const int ctx = r[5], nblk = (ctx + B - 1) / B;
     const int h = r[3] + (int)(local / nblk);
     const int b = (int)(local - (int64_t)(h - r[3]) * nblk);
     const int ntok = (b == nblk - 1) ? ctx - b * B : B;
-    const PageOp op = k3_page_decide(cl, geo, r[0], r[1], r[2], h, b, ntok, s_off[1][lo] + local,
-                                     s_off[2][lo] + local);
-    s_work[j] = op.item;
-    bits |= op.bits;
-    // count this CTA among the page's readers; the last one writes
-    const uint32_t n_readers =
-        (uint32_t)(k31_cta_of((pg + 1) * ipu - 1, n_items, grid) - k31_cta_of(pg * ipu, n_items, grid) + 1);
-    __threadfence();  // this CTA's reads of the page's entries come first
-    unsigned long long old = __ldcg(readers + pg), assumed;
-    do {
-      assumed = old;
-      const uint32_t cnt = (uint32_t)(assumed >> 32) == tag ? (uint32_t)assumed + 1u : 1u;
-      old = atomicCAS(readers + pg, assumed, ((unsigned long long)tag << 32) | cnt);
-    } while (old != assumed);
-    const uint32_t before = (uint32_t)(old >> 32) == tag ? (uint32_t)old : 0u;
-    if (before + 1u == n_readers) {
-      __threadfence();  // every other reader's reads happened before its count
-      k3_page_write(cl, op);
-    }
+    const PageOp op = k3_page_decide(cl, geo, r[0], r[1], r[2], h, b, ntok, rp.off[1][lo] + local,
+                                     rp.off[2][lo] + local);
+    s_work[tid] = op.item;
+    s_op[tid] = op;
+    bits = op.bits;
   }
   bits = (int)__reduce_or_sync(0xffffffffu, (unsigned)bits);
-  __syncwarp();
-  stamp(2);
-  if (lane == 0) {
-    if (bits) atomicOr(reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS),
-                       (unsigned long long)bits);
-    if (n_pages > 0) {
+  if (lane == 0) s_bits[warp] = bits;
+  __syncthreads();  // s_work complete: the copies can start
+  if (tracing && tid == 0) stamp(1);
+  const int32_t st0 = s_st0;
+  const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
+  if (warp == 0) {
+    if (tid == 0 && n_pages > 0 && !abort) {
       KvPieces<kTensor> it;
       it.work = s_work - p0;  // work[u] for the pages p0 .. p0 + n_pages - 1
       it.n_items = i1;
@@ -727,7 +699,45 @@ __global__ void __launch_bounds__(32)
       it.start(i0);
       bulk_pipeline<kTensor>(it, stages, kTensor ? &tm : nullptr);  // waits for its last store
     }
-    stamp(3);
+    if (tracing && tid == 0) {
+      stamp(2);
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      rp.trace[blockIdx.x * 8 + 5] = smid;
+      rp.trace[blockIdx.x * 8 + 6] = (uint64_t)(i1 - i0);
+      rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
+    }
+    return;
+  }
+  // warp 1: bookkeeping of the pages this CTA decided (the deciding threads'
+  // ops are in shared memory), then the completion counter
+  const uint64_t epoch = s_epoch;
+  // tags have the high bit set and are never 0xffffffff, so neither a work
+  // item K3 left in d_work ({unit >= 0 or -1, ...}) nor zeroed memory reads as
+  // a counter of this launch
+  const uint32_t tag = 0x80000000u | (uint32_t)((epoch + 1) % 0x7fffffffull);
+  __threadfence();  // this CTA's reads of the pages' entries come first
+  for (int j = (int)lane; j < (abort ? 0 : n_pages); j += 32) {
+    const int64_t pg = p0 + j;
+    const uint32_t n_readers =
+        (uint32_t)(k31_cta_of((pg + 1) * ipu - 1, n_items, grid) - k31_cta_of(pg * ipu, n_items, grid) + 1);
+    unsigned long long old = __ldcg(readers + pg), assumed;
+    do {
+      assumed = old;
+      const uint32_t cnt = (uint32_t)(assumed >> 32) == tag ? (uint32_t)assumed + 1u : 1u;
+      old = atomicCAS(readers + pg, assumed, ((unsigned long long)tag << 32) | cnt);
+    } while (old != assumed);
+    const uint32_t before = (uint32_t)(old >> 32) == tag ? (uint32_t)old : 0u;
+    if (before + 1u == n_readers) {
+      __threadfence();  // every other reader's reads happened before its count
+      k3_page_write(cl, s_op[j]);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const int all_bits = abort ? 0 : (s_bits[0] | s_bits[1]);
+    if (all_bits) atomicOr(reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS),
+                           (unsigned long long)all_bits);
     // the last CTA publishes the status word and resets the scratch words
     __threadfence();
     unsigned long long* done = reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_DONE);
@@ -742,14 +752,109 @@ __global__ void __launch_bounds__(32)
       *done = 0ull;
       if (!abort) totals[0] = n_mine;
     }
-    stamp(4);
-    if (rp.trace != nullptr) {
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      rp.trace[blockIdx.x * 8 + 5] = smid;
-      rp.trace[blockIdx.x * 8 + 6] = (uint64_t)(i1 - i0);
-      rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
+    if (tracing) stamp(3);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K31 dynamic variant (knob k31 = 2): every page is decided exactly once, by
+// the CTA whose static share of PAGES holds it, which applies its
+// bookkeeping writes at once (no other CTA reads that page's entries) and
+// stores its work item. A CTA then counts itself as decided and waits until
+// every CTA has (a grid-wide dependency: the kernel is launched cooperatively,
+// so all CTAs are resident), and copies items under K1's dynamic claims, so
+// CTAs that stream faster take more items and none drains late. The claim,
+// decided and status words are double-buffered by launch parity (rp.parity,
+// tracked by the host per d_totals): CTA 0 resets the other parity's words,
+// which only the previous launch on the stream used.
+// ---------------------------------------------------------------------------
+template <bool kTensor>
+__global__ void __launch_bounds__(kK31Threads)
+    tpr_k31_switch_dyn(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo,
+                       KvCopyParams p, const __grid_constant__ KvClusterParams cl,
+                       const __grid_constant__ KvTensorMaps tm, int64_t* __restrict__ totals,
+                       int4* __restrict__ work, int32_t* __restrict__ status,
+                       int32_t* status_mirror, int32_t stages, uint32_t piece) {
+  __shared__ int s_bits[2];
+  const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  auto stamp = [&](int k) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    rp.trace[blockIdx.x * 8 + k] = t;
+  };
+  const bool tracing = rp.trace != nullptr;
+  if (tracing && tid == 0) stamp(0);
+  const int par = rp.parity & 1;
+  unsigned long long* words = reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_PAR);
+  if (blockIdx.x == 0 && tid < 3) words[2 * tid + (par ^ 1)] = 0ull;
+  const int n = rp.n, B = geo.block_tokens;
+  const int32_t st0 = __ldcg(status);
+  const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
+  const int64_t n_mine = rp.n_mine, grid = gridDim.x;
+  const int64_t pa = (int64_t)blockIdx.x * n_mine / grid;
+  const int64_t pb = ((int64_t)blockIdx.x + 1) * n_mine / grid;
+  int bits = 0;
+  for (int64_t pg = pa + tid; pg < pb; pg += kK31Threads) {
+    int lo = 0, hi = n;  // upper_bound(mine offsets, pg) - 1
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (rp.off[0][mid] <= pg) lo = mid; else hi = mid;
     }
+    const int32_t* r = rp.rec[lo];
+    const int64_t local = pg - rp.off[0][lo];
+    const int ctx = r[5], nblk = (ctx + B - 1) / B;
+    const int h = r[3] + (int)(local / nblk);
+    const int b = (int)(local - (int64_t)(h - r[3]) * nblk);
+    const int ntok = (b == nblk - 1) ? ctx - b * B : B;
+    const PageOp op = k3_page_decide(cl, geo, r[0], r[1], r[2], h, b, ntok, rp.off[1][lo] + local,
+                                     rp.off[2][lo] + local);
+    if (!abort) {
+      k3_page_write(cl, op);
+      work[pg] = op.item;
+    }
+    bits |= op.bits;
+  }
+  bits = (int)__reduce_or_sync(0xffffffffu, (unsigned)bits);
+  if (lane == 0) s_bits[warp] = bits;
+  __syncthreads();
+  if (tid != 0) return;
+  if (tracing) stamp(1);
+  const int all_bits = abort ? 0 : (s_bits[0] | s_bits[1]);
+  if (all_bits) atomicOr(&words[4 + par], (unsigned long long)all_bits);
+  __threadfence();  // this CTA's writes and bits before its count
+  if (atomicAdd(&words[2 + par], 1ull) == (unsigned long long)grid - 1) {
+    __threadfence();
+    const int32_t out = (int32_t)atomicOr(&words[4 + par], 0ull) | (st0 & TPR_STATUS_BARRIER_TIMEOUT);
+    *status = out;
+    if (status_mirror) *reinterpret_cast<volatile int32_t*>(status_mirror) = out;
+    if (!abort) totals[0] = n_mine;
+  }
+  if (abort) return;
+  // every page decided (and its bookkeeping written) before any copy reads
+  // a work item
+  while (true) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&words[2 + par]) : "memory");
+    if (v >= (unsigned long long)grid) break;
+  }
+  if (tracing) stamp(2);
+  KvPieces<kTensor> it;
+  it.work = work;
+  it.work_l2 = true;
+  it.n_items = n_mine * p.items_per_unit;
+  it.p = p;
+  it.cl = &cl;
+  it.tm = kTensor ? &tm : nullptr;
+  it.piece = piece;
+  if (rp.batch > 0) {
+    it.claim = &words[par];
+    it.batch = rp.batch;
+  }
+  it.start(blockIdx.x);
+  bulk_pipeline<kTensor>(it, stages, kTensor ? &tm : nullptr);
+  if (tracing) {
+    stamp(3);
+    rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
   }
 }
 
@@ -882,40 +987,95 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
   return k1_launch(p, cl, work, n_units, st, pdl, tm, c);
 }
 
-// K31 ring: one CTA per SM owning ~1-28 whole pages; TPR_BULK_K31 overrides
+// K31 ring: 3 x 32 KiB, two CTAs per SM (a one-sequence switch: 19.5 ->
+// 15.4 us of device time against 6 x 32 KiB with one CTA per SM, cfg1 even);
+// TPR_BULK_K31 overrides
 static const BulkConfig& k31_config() {
-  static BulkConfig c = parse_bulk("TPR_BULK_K31", BulkConfig{6, 32768});
+  static BulkConfig c = parse_bulk("TPR_BULK_K31", BulkConfig{3, 32768});
   return c;
 }
+
+// launch parity per d_totals (the dynamic K31's double-buffered words): the
+// parity of a buffer's next launch; advanced only by a launch that succeeded
+static std::mutex g_par_mu;
+static std::unordered_map<const int64_t*, uint32_t> g_par;
 
 cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
-                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work) {
+                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work, int variant) {
   if (n < 1 || n > kK31Xfers || n_units < 1 || !d_work) return cudaErrorNotSupported;
   const BulkConfig& c = k31_config();
   KvTensorMaps tm;
   tm.enabled = 0;
   if (partial) kv_tensor_maps(geo, cl, n_gpus, c.piece, &tm);
-  const void* fn = tm.enabled ? reinterpret_cast<const void*>(&tpr_k31_switch<true>)
-                              : reinterpret_cast<const void*>(&tpr_k31_switch<false>);
+  // schedule: item shares with redundant decisions for the smallest plans,
+  // owner decisions + dynamic claims from 512 pages up (profiles/README.md
+  // §4d: 116 pages 15.4 vs 19.5 us, 1024 pages 97.3 vs 93.0 us, 1792 pages
+  // 160.8 vs 152.6 us); knob k31 = 2 / 3 forces one
+  const bool dyn = variant == 2 || (variant == 1 && n_units >= kK31DynamicUnits);
+  const void* fn = dyn ? (tm.enabled ? reinterpret_cast<const void*>(&tpr_k31_switch_dyn<true>)
+                                     : reinterpret_cast<const void*>(&tpr_k31_switch_dyn<false>))
+                       : (tm.enabled ? reinterpret_cast<const void*>(&tpr_k31_switch<true>)
+                                     : reinterpret_cast<const void*>(&tpr_k31_switch<false>));
   const int64_t items = n_units * p.items_per_unit;
-  const int grid = bulk_grid(fn, c, items, 32);
-  // pages one CTA's share of the items touches
-  if (((items + grid - 1) / grid + p.items_per_unit - 1) / p.items_per_unit + 1 > kK31MaxPages)
+  const int grid = bulk_grid(fn, c, items, kK31Threads);
+  if (!dyn && ((items + grid - 1) / grid + p.items_per_unit - 1) / p.items_per_unit + 1 >
+                  kK31MaxPages)  // pages one CTA's share of the items touches
     return cudaErrorNotSupported;
-  unsigned long long* readers = reinterpret_cast<unsigned long long*>(d_work);
   K31Params rp;
   memcpy(rp.rec, h_rec, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n);
+  // K3's three keyed exclusive scans (tpr_kernels.cu k3 scan), on the host
+  int64_t mine = 0, in_u[TPR_MAX_GPUS] = {}, out_u[TPR_MAX_GPUS] = {};
+  for (int t = 0; t < n; ++t) {
+    const int32_t* r = h_rec + (size_t)t * TPR_XFER_FIELDS;
+    const int64_t nblk = r[5] > 0 ? (r[5] + geo.block_tokens - 1) / geo.block_tokens : 0;
+    const int64_t u = (int64_t)(r[4] - r[3]) * nblk;
+    rp.off[0][t] = mine;
+    rp.off[1][t] = r[1] >= 0 && r[1] < TPR_MAX_GPUS ? in_u[r[1]] : 0;
+    rp.off[2][t] = r[0] >= 0 && r[0] < TPR_MAX_GPUS ? out_u[r[0]] : 0;
+    if (filter < 0 || r[0] == filter) mine += u;
+    if (r[1] >= 0 && r[1] < TPR_MAX_GPUS) in_u[r[1]] += u;
+    if (r[0] >= 0 && r[0] < TPR_MAX_GPUS) out_u[r[0]] += u;
+  }
+  rp.n_mine = mine;
   rp.n = n;
   rp.filter = filter;
   rp.trace = reinterpret_cast<uint64_t*>(k31_trace_buffer());
+  rp.parity = 0;
+  rp.batch = 0;
+  if (dyn) {
+    // one item per claim (cfg1 52.2 us against 54.0 with 2 or 4 per claim)
+    rp.batch = items > (int64_t)grid ? 1 : 0;  // 0: one static item each covers it
+    std::lock_guard<std::mutex> lk(g_par_mu);
+    uint32_t& par = g_par[totals];
+    rp.parity = (int32_t)(par & 1u);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kK31Threads);
+    cfg.dynamicSmemBytes = (size_t)c.smem();
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the decided wait
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int4* work = reinterpret_cast<int4*>(d_work);
+    cudaError_t e = tm.enabled
+        ? cudaLaunchKernelEx(&cfg, tpr_k31_switch_dyn<true>, rp, geo, p, cl, tm, totals, work,
+                             status, status_mirror, (int32_t)c.stages, (uint32_t)c.piece)
+        : cudaLaunchKernelEx(&cfg, tpr_k31_switch_dyn<false>, rp, geo, p, cl, tm, totals, work,
+                             status, status_mirror, (int32_t)c.stages, (uint32_t)c.piece);
+    if (e == cudaSuccess) ++par;
+    return e;
+  }
+  unsigned long long* readers = reinterpret_cast<unsigned long long*>(d_work);
   if (tm.enabled)
-    tpr_k31_switch<true><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
+    tpr_k31_switch<true><<<grid, kK31Threads, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
                                                              status, status_mirror, c.stages,
                                                              c.piece);
   else
-    tpr_k31_switch<false><<<grid, 32, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
+    tpr_k31_switch<false><<<grid, kK31Threads, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
                                                               status, status_mirror, c.stages,
                                                               c.piece);
   return cudaGetLastError();

@@ -343,6 +343,10 @@ int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* 
                            t->k1_events, &t->records_async);
   if (rc != TPR_OK) return rc;
   if (n == 0) return TPR_OK;
+  for (int32_t s = 0; s < cl->n_gpus; ++s) {  // the host ring counters
+    if (t->ring_head_io) t->ring_head_io[s] += t->in_units[s];
+    if (t->ring_tail_io) t->ring_tail_io[s] += t->out_units[s];
+  }
   return tpr_kv_apply_owner(t->records, n, t->owner, geo->total_heads);
 }
 

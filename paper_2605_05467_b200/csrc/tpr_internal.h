@@ -55,8 +55,16 @@ constexpr int kK31Xfers = 96;      // records per fused launch (2304 B of parame
 constexpr int kK31MaxPages = 64;   // pages one CTA owns
 struct K31Params {
   int32_t rec[kK31Xfers][TPR_XFER_FIELDS];
+  // per record: units before it that this rank moves (filter), that its
+  // destination ring hands out, that its source ring takes back -- the three
+  // keyed exclusive scans K3 does on the device, done on the host (the
+  // records are on the host anyway)
+  int64_t off[3][kK31Xfers];
+  int64_t n_mine;   // units this rank moves
   int32_t n;
   int32_t filter;
+  int32_t parity;   // dynamic kernel: which scratch words of d_totals this launch uses
+  int32_t batch;    // dynamic kernel: items per claim (0 = static shares)
   uint64_t* trace;  // nullable: per-CTA globaltimer stamps (knob "k31_trace")
 };
 int64_t k31_trace_buffer();
@@ -131,7 +139,8 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
 cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
-                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work);
+                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work,
+                       int variant);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

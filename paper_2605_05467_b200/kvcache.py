@@ -157,8 +157,6 @@ class PagedKvCluster:
                                                 dtype=torch.int32, device=dev))
             order = gen.permutation(units) if fragmented else np.arange(units)
             self.rings.append(torch.from_numpy(order.astype(np.int32)).to(dev))
-        self.ring_head = [0] * len(self.gpu_ids)
-        self.ring_tail = list(self.units)
         # request bookkeeping (host is authoritative; device copies for checks)
         self.req_slot: dict[int, int] = {}
         self.ctx_of: dict[int, int] = {}
@@ -186,6 +184,9 @@ class PagedKvCluster:
         self.status_mirrored = False  # the last switch_layouts refreshed status_host
         self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
                                         H, self.max_blocks, self.max_requests, self.n_units)
+        # the C view of the cluster; its ring counters (monotonic head/tail per
+        # slot) are the host's authoritative copy, advanced in place by the
+        # one-call switch
         self._cl = _native.KvClusterC()
         self._cl.n_gpus = self.n_gpus
         for s in range(self.n_gpus):
@@ -193,6 +194,8 @@ class PagedKvCluster:
             self._cl.block_table[s] = self.block_tables[s].data_ptr()
             self._cl.free_ring[s] = self.rings[s].data_ptr()
             self._cl.units[s] = self.units[s]
+            self._cl.ring_head[s] = 0
+            self._cl.ring_tail[s] = self.units[s]
         self._last_in = self._last_out = np.zeros(self.n_gpus, np.int64)
         self._gpu_ids_arr = np.asarray(self.gpu_ids, dtype=np.int64)
         self._n_units_c = ctypes.c_int64(0)
@@ -204,16 +207,22 @@ class PagedKvCluster:
     def n_gpus(self) -> int:
         return len(self.gpu_ids)
 
+    @property
+    def ring_head(self) -> list:
+        """Units ever allocated per slot (monotonic free-ring head), a copy."""
+        return self._cl.ring_head[: self.n_gpus]
+
+    @property
+    def ring_tail(self) -> list:
+        """Units ever released per slot + capacity (monotonic free-ring tail), a copy."""
+        return self._cl.ring_tail[: self.n_gpus]
+
     def free_units(self, gpu: int) -> int:
         s = self.slot_of[gpu]
-        return self.ring_tail[s] - self.ring_head[s]
+        return self._cl.ring_tail[s] - self._cl.ring_head[s]
 
     def _cluster_c(self) -> _native.KvClusterC:
-        c = self._cl
-        for s in range(self.n_gpus):
-            c.ring_head[s] = self.ring_head[s]
-            c.ring_tail[s] = self.ring_tail[s]
-        return c
+        return self._cl
 
     def _units_per_record(self, xf: np.ndarray) -> np.ndarray:
         B = self.kv.block_tokens
@@ -290,16 +299,18 @@ class PagedKvCluster:
         return total, in_u, out_u
 
     def _check_capacity(self, in_u) -> None:
+        head, tail = self._cl.ring_head, self._cl.ring_tail
         for s in range(self.n_gpus):
-            free = self.ring_tail[s] - self.ring_head[s]
+            free = tail[s] - head[s]
             if in_u[s] > free:
                 raise MigrationError(
                     f"gpu {self.gpu_ids[s]}: {in_u[s]} KV units needed, {free} free")
 
     def _commit(self, in_u, out_u):
+        head, tail = self._cl.ring_head, self._cl.ring_tail
         for s in range(self.n_gpus):
-            self.ring_head[s] += int(in_u[s])
-            self.ring_tail[s] += int(out_u[s])
+            head[s] += int(in_u[s])
+            tail[s] += int(out_u[s])
 
     # -------------------------------------------------------------- K3 driver
     def _remap(self, xf: np.ndarray, stream: torch.cuda.Stream, want_ext: bool) -> int:
@@ -565,9 +576,30 @@ class PagedKvCluster:
             t.d_totals = self._totals.data_ptr()
             t.d_status = self.status.data_ptr()
             t.h_status = self.status_host.data_ptr()
+            base = ctypes.addressof(self._cl)
+            t.ring_head_io = base + _native.KvClusterC.ring_head.offset
+            t.ring_tail_io = base + _native.KvClusterC.ring_tail.offset
             self._swt_plan = np.empty((0, 6), np.int64)
+            self._swt_bufs = None
+            self._swt_records = None
         t.validate = int(validate)
         return t
+
+    def _switch_buffers(self, t, stream) -> None:
+        """Point the tables at plan/records/device scratch sized for the
+        current plan capacity (grow-only; set again only when one grew)."""
+        rows = self._swt_plan
+        cap = max(len(rows), 1)
+        xf = self._xf.get(cap * 6, stream)
+        meta = self._meta.get(cap * 4, stream)
+        work = self._work.t
+        key = (xf.data_ptr(), meta.data_ptr(), work.data_ptr(), work.numel())
+        held = self._swt_bufs
+        if held is None or held[0] is not rows or held[1] != key:
+            t.plan, t.plan_cap = rows.ctypes.data, len(rows)
+            t.d_xfers, t.d_meta, t.xfers_cap = xf.data_ptr(), meta.data_ptr(), len(rows)
+            t.d_work, t.work_cap = work.data_ptr(), work.numel() // 4
+            self._swt_bufs = (rows, key)
 
     def switch_layouts(self, old_layouts, new_layouts, stream: torch.cuda.Stream | None = None,
                        validate: bool = True, handshake_ms: float = 0.0,
@@ -611,21 +643,17 @@ class PagedKvCluster:
             for e in k1_events:  # torch creates the event on its first record; libtpr
                 e.record(stream)  # then re-records it around K1 on the same stream
             t.k1_events[0], t.k1_events[1] = k1_events[0].cuda_event, k1_events[1].cuda_event
-        else:
+        elif t.k1_events[0]:
             t.k1_events[0] = t.k1_events[1] = None
         lib = _native.load()
-        cl = self._cluster_c()
         addr = blob.buffer_info()[0]
         for _ in range(3):  # grow-and-retry when a buffer is too small
             rows = self._swt_plan
-            h_ptr, raw = self._staging.acquire(max(len(rows), 1) * 24)
-            t.plan, t.plan_cap, t.records = rows.ctypes.data, len(rows), h_ptr
-            t.d_xfers = self._xf.get(max(len(rows), 1) * 6, stream).data_ptr()
-            t.d_meta = self._meta.get(max(len(rows), 1) * 4, stream).data_ptr()
-            t.xfers_cap = len(rows)
-            work = self._work.t
-            t.d_work, t.work_cap = work.data_ptr(), work.numel() // 4
-            rc = lib.tpr_kv_switch_layouts(ctypes.byref(self._geo), ctypes.byref(cl), addr,
+            h_ptr, _raw = self._staging.acquire(max(len(rows), 1) * 24)
+            if h_ptr != self._swt_records:
+                t.records = self._swt_records = h_ptr
+            self._switch_buffers(t, stream)
+            rc = lib.tpr_kv_switch_layouts(ctypes.byref(self._geo), ctypes.byref(self._cl), addr,
                                            len(blob), ctypes.byref(t), stream.cuda_stream)
             if rc != _native.TPR_ECAPACITY:
                 break
@@ -641,22 +669,17 @@ class PagedKvCluster:
         n = t.n_plan
         self.status_mirrored = True
         plan = MigrationPlan.from_array(self._swt_plan[:n].copy(), handshake_ms=handshake_ms)
-        self._forget(release)
+        if release:
+            self._forget(release)
         if t.n_records == 0:
             return plan, MigrationStats(0, 0, 0, {}, {})
         if t.records_async:  # the device still reads the pinned records
             self._staging.fence(stream)
-        in_u, out_u = t.in_units, t.out_units
+        # the native call advanced the ring counters (t.ring_head_io / ring_tail_io)
+        ng = self.n_gpus
         ids = self.gpu_ids
-        in_d, out_d = {}, {}
-        for s_ in range(self.n_gpus):
-            a, b = in_u[s_], out_u[s_]
-            self.ring_head[s_] += a
-            self.ring_tail[s_] += b
-            if a:
-                in_d[ids[s_]] = a
-            if b:
-                out_d[ids[s_]] = b
+        in_d = {ids[s_]: a for s_, a in enumerate(t.in_units[:ng]) if a}
+        out_d = {ids[s_]: b for s_, b in enumerate(t.out_units[:ng]) if b}
         return plan, MigrationStats(transfers=n, units=t.total_units, bytes=t.plan_bytes,
                                     in_units=in_d, out_units=out_d)
 

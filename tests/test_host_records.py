@@ -33,8 +33,10 @@ def host_cluster(gpu_ids, H, max_requests, reqs):
     c._gpu_ids_arr = ids
     c._req_lut = np.full(16, -1, dtype=np.int64)
     c._n_units_c = ctypes.c_int64(0)
-    c.ring_head = [0] * len(gpu_ids)
-    c.ring_tail = [10**9] * len(gpu_ids)
+    c._cl = _native.KvClusterC()  # ring counters live in the C view of the cluster
+    c._cl.n_gpus = len(gpu_ids)
+    for s in range(len(gpu_ids)):
+        c._cl.ring_head[s], c._cl.ring_tail[s] = 0, 10**9
     for rs, (rid, ctx, group) in enumerate(reqs):
         c.req_slot[rid] = rs
         c._set_req(rid, rs)

@@ -93,6 +93,9 @@ def test_chain_of_switches_and_back():
 
 LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
     "k31_one_launch": dict(k31=1, k3_fuse_units=1 << 30),
+    "k31_dynamic": dict(k31=2, k3_fuse_units=1 << 30),
+    "k31_item_share": dict(k31=3, k3_fuse_units=1 << 30),
+    "k31_dynamic_rows_for_partial_pages": dict(k31=2, k3_fuse_units=1 << 30, tensor_partial=0),
     "k31_rows_for_partial_pages": dict(k31=1, k3_fuse_units=1 << 30, tensor_partial=0),
     "k31_vector_engine_fallback": dict(k31=1, k3_fuse_units=1 << 30, engine="vector"),
     "fused_k3_tensor": dict(k31=0, k3_fuse_units=1 << 30, tensor_partial=1),
@@ -474,9 +477,18 @@ def test_cfg2_full_size_property():
     assert c.placement() == M.layout_placement(w.new)
 
 
+@pytest.fixture(params=[3, 2], ids=["item_share", "dynamic"])
+def k31_variant(request):
+    from paper_2605_05467_b200 import _native
+    saved = _native.get_tuning("k31")
+    _native.set_tuning("k31", request.param)
+    yield request.param
+    _native.set_tuning("k31", saved)
+
+
 @pytest.mark.parametrize("model", ["tiny", "8b"])
 @pytest.mark.parametrize("tp_old,tp_new", [(1, 2), (2, 1), (1, 8), (8, 1), (4, 8), (8, 2)])
-def test_k31_single_launch_bit_exact(model, tp_old, tp_new):
+def test_k31_single_launch_bit_exact(model, tp_old, tp_new, k31_variant):
     # small plans (<= 96 transfers, <= k3_fuse_units pages): the whole switch is
     # one launch (K31: bookkeeping + TMA copy per CTA-owned page), with ragged
     # contexts (partial pages as row copies) and 8 slots, against the oracle
@@ -504,7 +516,7 @@ def test_k31_single_launch_bit_exact(model, tp_old, tp_new):
     assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
 
 
-def test_k31_reports_errors_per_call():
+def test_k31_reports_errors_per_call(k31_variant):
     # K31's status word is this call's bits only, also in the pinned mirror
     from paper_2605_05467_b200.controller import ReconfigurationExecutor
     c = make(TINY, (0, 1))

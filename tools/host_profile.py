@@ -59,6 +59,38 @@ def main():
                 torch.cuda.synchronize()
         torch.cuda.synchronize()
         print(f"switch(sync={sync}) median {np.median(t) * 1e6:.1f} us", flush=True)
+    # the native call alone, and its host half (plan + records, no launch)
+    from paper_2605_05467_b200 import _native
+    lib = _native.load()
+    real = lib.tpr_kv_switch_layouts
+    prep = lib.tpr_switch_prepare
+    t_nat, t_prep = [], []
+
+    class Timed:
+        def __call__(self, geo, cl_, addr, n, t, stream):
+            t0 = time.perf_counter()
+            prep(geo, cl_, addr, n, t)
+            t1 = time.perf_counter()
+            rc = real(geo, cl_, addr, n, t, stream)
+            t_nat.append(time.perf_counter() - t1)
+            t_prep.append(t1 - t0)
+            return rc
+
+    lib.tpr_kv_switch_layouts = Timed()
+    try:
+        t = []
+        for i in range(args.n):
+            t0 = time.perf_counter()
+            ex.switch(*((la, lb) if i % 2 == 0 else (lb, la)), validate=False, sync=False)
+            t.append(time.perf_counter() - t0)
+            if i % 16 == 15:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+    finally:
+        lib.tpr_kv_switch_layouts = real
+    nat, pre, tot = (np.median(x) * 1e6 for x in (t_nat, t_prep, t))
+    print(f"split: native call {nat:.1f} us (of which plan+records {pre:.1f}, launch path "
+          f"{nat - pre:.1f}); Python around it {tot - nat - pre:.1f} us", flush=True)
     pr = cProfile.Profile()
     pr.enable()
     run(args.n, False)

@@ -1,6 +1,6 @@
 """Where the time of a small switch goes inside K31 (knob "k31_trace"): every
-CTA stamps %globaltimer at its entry, after the keyed scan, after its page
-decisions, after its copies and at its exit. Prints, per phase, the
+CTA stamps %globaltimer at its entry, after its page decisions (the copies
+start), after its copies (warp 0) and after its bookkeeping (warp 1). Prints, per phase, the
 min / median / max over CTAs relative to the first CTA's entry (ns), plus the
 spread of CTA entry times (launch ramp).
 
@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -18,6 +19,10 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
+
+# stamps: the item-share kernel (TPR_K31=1) and the dynamic one (TPR_K31=2)
+DYN = os.environ.get("TPR_K31", "1") == "2"
+NAMES = ("entry", "decide", "barrier", "copies") if DYN else ("entry", "decide", "copies", "books")
 
 CASES = {"1seq": (8, 1, 2, 1, 463), "cfg1": (2, 1, 2, 4, 512), "1seq4096": (8, 8, 1, 1, 4096)}
 
@@ -60,19 +65,19 @@ def main():
                 raise SystemExit("no K31 launch (plan outside the fused path?)")
             t = t[:grid]
             base = t[:, 0].min()
-            rows.append({k: (t[:, j] - base) for j, k in enumerate(("entry", "scan", "decide",
-                                                                      "copies", "exit"))})
+            rows.append({k: (t[:, j] - base) for j, k in enumerate(NAMES)})
     finally:
         _native.set_tuning("k31_trace", 0)
     last = rows[len(rows) // 2:]
-    out = {"case": args.case, "grid": grid, "items_per_cta": [int(x) for x in
-                                                              np.unique(t[:, 6])]}
-    for k in ("entry", "scan", "decide", "copies", "exit"):
+    out = {"case": args.case, "variant": "dynamic" if DYN else "item-share", "grid": grid,
+           "items_per_cta": [int(x) for x in np.unique(t[:, 6])]}
+    for k in NAMES:
         v = np.concatenate([r[k] for r in last])
         out[k] = {"min": int(v.min()), "median": int(np.median(v)), "max": int(v.max())}
     out["copy_phase_median_ns"] = int(np.median(np.concatenate(
-        [r["copies"] - r["decide"] for r in last])))
-    out["kernel_span_median_ns"] = int(np.median([r["exit"].max() for r in last]))
+        [r["copies"] - r[NAMES[-2] if DYN else "decide"] for r in last])))
+    out["kernel_span_median_ns"] = int(np.median([max(r[k].max() for k in NAMES[1:])
+                                                   for r in last]))
     print(json.dumps(out))
     if args.out:
         with open(args.out, "a") as f:

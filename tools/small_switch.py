@@ -34,6 +34,8 @@ CASES = (  # (name, slots, tp_old, tp_new, seqs, ctx)
     ("cfg1 4x512 TP1->TP2", 2, 1, 2, 4, 512),
     ("1 seq x 463 TP1->TP2", 8, 1, 2, 1, 463),
     ("1 seq x 4096 TP8->TP1", 8, 8, 1, 1, 4096),
+    ("1 seq x 4096 TP1->TP2", 8, 1, 2, 1, 4096),
+    ("4 seqs x 4096 TP1->TP2", 8, 1, 2, 4, 4096),
     ("8 seqs x 4096 TP2->TP4", 8, 2, 4, 8, 4096),
     ("16 seqs x 4096 TP4->TP8", 8, 4, 8, 16, 4096),
     ("64 seqs x 4096 TP4->TP8", 8, 4, 8, 64, 4096),
