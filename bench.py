@@ -205,14 +205,14 @@ def setup_ours(w, device, overlap=None, weights_mode="sharded", fragmented=True)
 
 
 def k1_kernel_name(w) -> str:
-    """The K1 kernel this workload launches (bulk engine): the lean kernel when
-    every context is a whole number of pages, else the tensor-box kernel."""
+    """The K1 kernel this workload launches: the TMA bulk kernel (partial pages
+    as tensor boxes), or the vector engine's when that is selected."""
     from paper_2605_05467_b200 import _native
     if _native.copy_engine() != "bulk":
         return "tpr_k1_kv_migrate<8> (vector engine)"
     B = w.model.kv.block_tokens
     full = all(c % B == 0 for _, c in w.requests)
-    return "tpr_k1_kv_migrate_bulk<0>" if full else "tpr_k1_kv_migrate_tma<0>"
+    return "tpr_k1_kv_migrate_bulk" + ("" if full else " (tensor boxes for partial pages)")
 
 
 def weights_note(w, w_bytes) -> str:

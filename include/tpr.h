@@ -138,10 +138,10 @@ int tpr_get_copy_engine(void);
  *                   behind it by programmatic dependent launch; 0 = never.
  *                   Larger plans run K3 scan + remap and a normally launched
  *                   K1 whose CTAs claim batches of 4 items dynamically;
- *   "tensor_partial" [TPR_TENSOR_PARTIAL, 1]: K1 (TMA engine) moves partial
- *                   pages as TMA tensor boxes (token x planes) instead of
- *                   one short copy per plane: 0 never, 1 when a page of the
- *                   plan is partial, 2 the tensor kernel for every plan;
+ *   "tensor_partial" [TPR_TENSOR_PARTIAL, 1]: K1 / K31 (TMA engine) move
+ *                   partial pages as TMA tensor boxes (token x planes)
+ *                   instead of one short copy per plane: 0 never, 1 when a
+ *                   page of the plan is partial (one K1 kernel either way);
  *   "k31"           [TPR_K31, 1]: a plan of at most k3_fuse_units pages and 96
  *                   transfers (host records, TMA engine, local pools) runs as
  *                   ONE kernel, K31, with the records and their three keyed
@@ -229,7 +229,8 @@ int tpr_kv_migrate(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* d_work, int64_t n_units, void* stream);
 /* tpr_kv_migrate with flags: TPR_MIGRATE_FULL_PAGES = the caller knows every
  * page of the plan is full (all context lengths are multiples of the page
- * size), so K1 needs no tensor maps for partial pages (the lean kernel). */
+ * size), so K1 launches without encoding the pools' tensor maps (the same
+ * kernel; partial pages would then move as row copies). */
 #define TPR_MIGRATE_FULL_PAGES 1
 int tpr_kv_migrate_ex(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                       const int32_t* d_work, int64_t n_units, int32_t flags, void* stream);

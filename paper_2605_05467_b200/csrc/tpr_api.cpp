@@ -186,9 +186,8 @@ cudaError_t run_k2(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_
 
 namespace tpr {
 // knob "tensor_partial": 0 row copies, 1 tensor boxes when a page is partial
-// (default), 2 the tensor kernel for every plan (A/B measurements)
+// (default)
 bool tensor_partial_enabled() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) != 0; }
-bool tensor_kernel_always() { return knob(g_tensor, "TPR_TENSOR_PARTIAL", 1) >= 2; }
 
 // ---------------------------------------------------------------------------
 // TMA tensor maps of the KV pools (K1 partial pages, tpr_internal.h).
@@ -485,8 +484,8 @@ int tpr_set_tuning(const char* key, int64_t value) {
   if (!key) return fail(TPR_EINVAL, "null tuning key");
   if (value < 0) return fail(TPR_EINVAL, "tuning value must be >= 0");
   if (!strcmp(key, "k3_fuse_units")) g_fuse.store(value);
-  else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 2 ? 2 : value);
-  else if (!strcmp(key, "k31")) g_k31.store(value < 0 ? 0 : value > 3 ? 3 : value);
+  else if (!strcmp(key, "tensor_partial")) g_tensor.store(value > 1 ? 1 : value);
+  else if (!strcmp(key, "k31")) g_k31.store(value > 3 ? 3 : value);
   else if (!strcmp(key, "k31_trace")) g_k31_trace.store(value);
   else return fail(TPR_EINVAL, "unknown tuning key '%s'", key);
   return TPR_OK;

@@ -113,9 +113,10 @@ struct Copy {
 // K1 items are handed out statically (grid-stride) or, with a claim counter,
 // dynamically in batches of `batch` consecutive items (4 by
 // default) claimed one batch ahead: CTAs then stay on neighbouring items (a
-// small, shared working set of pages) and none drains late.
+// small, shared working set of pages) and none drains late. One kernel serves
+// every plan: with tm->enabled = 0 (a plan of full pages, or tensor boxes
+// switched off) partial pages fall back to row copies.
 
-template <bool kTensor>
 struct KvPieces {
   const int4* work;
   int64_t n_items;
@@ -135,10 +136,12 @@ struct KvPieces {
   // ... or tensor boxes
   int32_t t_src, t_dst, t_tok, t_ntok, t_step, t_pb, t_sc2, t_dc2;
   bool tensor;
+  bool boxes;  // partial pages as tensor boxes (the pools' maps are enabled)
 
   __device__ void start(int64_t first) {
     rows_left = 0;
     tensor = false;
+    boxes = tm != nullptr && tm->enabled;
     if (claim) {
       item = first * batch;
       item_end = min(item + batch, n_items);
@@ -173,7 +176,7 @@ struct KvPieces {
       const int src_slot = w.z & 0xffff, dst_slot = (w.z >> 16) & 0xffff, ntok = w.w;
       if (w.x < 0 || w.y < 0 || ntok <= 0) continue;  // a page K3 refused (status word)
       const int64_t nb = (int64_t)ntok * p.tok_bytes;
-      if (kTensor && nb != p.pitch) {  // partial page: tensor boxes
+      if (boxes && nb != p.pitch) {  // partial page: tensor boxes
         if (g >= ntok) continue;            // no token for this item slot
         tensor = true;
         t_src = src_slot;
@@ -209,8 +212,8 @@ struct KvPieces {
   // or one tensor box when it fits avail_box), 2 = the next copy is a box
   // that does not fit this stage (nothing consumed), 0 = no work left.
   __device__ int next(Copy& c, uint32_t avail_linear, uint32_t avail_box) {
-    if (!(kTensor && tensor) && rows_left == 0 && !load_item()) return 0;
-    if (kTensor && tensor) {
+    if (!tensor && rows_left == 0 && !load_item()) return 0;
+    if (tensor) {
       const uint32_t bb = (uint32_t)(tm->r_box * p.tok_bytes);
       if (bb > avail_box) return 2;
       c.smap = t_src;
@@ -384,7 +387,7 @@ constexpr int kMaxSub = 16;  // copies packed into one shared-memory stage
 // moving one stage: fill() packs copies into stage t and issues their loads,
 // store() issues the stage's stores. A stage is `piece` bytes of shared
 // memory filled with up to kMaxSub consecutive copies (one 32 KiB page chunk,
-// many short rows of row-parallel weight slices, or -- K1 with kTensor -- TMA
+// many short rows of row-parallel weight slices, or -- K1, kTensor -- TMA
 // tensor boxes of partial pages, 128-byte aligned). The stage's loads all
 // complete on one mbarrier; its stores form one bulk group, so small copies
 // still keep a full stage of bytes in flight.
@@ -393,9 +396,10 @@ constexpr int kMaxSub = 16;  // copies packed into one shared-memory stage
 // path stays in registers and each load is issued as soon as its copy is
 // produced; the stage's single arrive.expect_tx follows (the tx-count may go
 // transiently negative; the phase cannot complete before the arrival). Only
-// the lean pipelines (no tensor boxes) take the fast path for a full linear
-// stage, expect_tx before the load: that order is +1.4% on full pages but
-// costs 4-20% when tensor-box stages use it or mix with it.
+// K2's pipeline (linear copies only, kTensor = false) takes the fast path for
+// a full linear stage, expect_tx before the load: that order costs 4-20% when
+// tensor-box stages use it or mix with it; with dynamic claims
+// K1 runs full pages as fast without it (7.649 vs 7.657 ms on cfg2).
 template <bool kTensor>
 struct StageRing {
   char* dst[kMaxStages][kMaxSub];
@@ -514,12 +518,14 @@ __device__ __forceinline__ void bulk_pipeline(Source& src_it, int stages,
   bulk_wait_all();
 }
 
-// K1 with partial pages as row copies (every page full: no tensor maps needed)
+// K1: the work list K3 wrote -> page copies (partial pages as TMA tensor
+// boxes of the pools' maps when tm.enabled, else as row copies)
 __global__ void __launch_bounds__(32)
     tpr_k1_kv_migrate_bulk(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
-                           const __grid_constant__ KvClusterParams cl, int32_t stages,
+                           const __grid_constant__ KvClusterParams cl,
+                           const __grid_constant__ KvTensorMaps tm, int32_t stages,
                            uint32_t piece, int32_t dynamic) {
-  KvPieces<false> it;
+  KvPieces it;
   // the claim counter is the int4 slot after the work list (zeroed by K3);
   // `dynamic` = items per claim, 0 = static grid-stride shares
   if (dynamic > 0) {
@@ -530,33 +536,10 @@ __global__ void __launch_bounds__(32)
   it.n_items = n_units * p.items_per_unit;
   it.p = p;
   it.cl = &cl;
-  it.tm = nullptr;
+  it.tm = &tm;
   it.piece = piece;
   if (threadIdx.x != 0) return;  // one issuing thread per CTA
   pdl_wait();  // K3's work list (launched with programmatic serialization)
-  it.start(blockIdx.x);
-  bulk_pipeline<false>(it, stages, nullptr);
-}
-
-// K1 with partial pages as TMA tensor boxes of the pools' tensor maps
-__global__ void __launch_bounds__(32)
-    tpr_k1_kv_migrate_tma(const int4* __restrict__ work, int64_t n_units, KvCopyParams p,
-                          const __grid_constant__ KvClusterParams cl,
-                          const __grid_constant__ KvTensorMaps tm, int32_t stages,
-                          uint32_t piece, int32_t dynamic) {
-  KvPieces<true> it;
-  if (dynamic > 0) {
-    it.claim = reinterpret_cast<unsigned long long*>(const_cast<int4*>(work + n_units));
-    it.batch = dynamic;
-  }
-  it.work = work;
-  it.n_items = n_units * p.items_per_unit;
-  it.p = p;
-  it.cl = &cl;
-  it.tm = &tm;
-  it.piece = piece;
-  if (threadIdx.x != 0) return;
-  pdl_wait();
   it.start(blockIdx.x);
   bulk_pipeline<true>(it, stages, &tm);
 }
@@ -618,10 +601,8 @@ constexpr int kK31Threads = 64;
 constexpr int64_t kK31DynamicUnits = 512;  // auto schedule: dynamic from here up
 static_assert(kK31MaxPages <= kK31Threads, "one deciding thread per page");
 
-// kTensor: partial pages move as TMA tensor boxes of the pools' maps (the
-// maps ride in the parameters too: > 4 KiB of parameters, CUDA >= 12.1); a
-// plan of full pages only takes the lean variant.
-template <bool kTensor>
+// Partial pages move as TMA tensor boxes of the pools' maps when tm.enabled
+// (the maps ride in the parameters too: > 4 KiB of parameters, CUDA >= 12.1).
 __global__ void __launch_bounds__(kK31Threads)
     tpr_k31_switch(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo, KvCopyParams p,
                    const __grid_constant__ KvClusterParams cl,
@@ -648,7 +629,7 @@ __global__ void __launch_bounds__(kK31Threads)
       s_st0 = __ldcg(status);
       s_epoch = (uint64_t)__ldcg(totals + TPR_TOTALS_K31_EPOCH);
     }
-    if (kTensor && tm.enabled && lane < TPR_MAX_GPUS && cl.pool[lane] != 0)
+    if (tm.enabled && lane < TPR_MAX_GPUS && cl.pool[lane] != 0)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.map[lane]))
                    : "memory");
   }
@@ -688,16 +669,16 @@ __global__ void __launch_bounds__(kK31Threads)
   const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
   if (warp == 0) {
     if (tid == 0 && n_pages > 0 && !abort) {
-      KvPieces<kTensor> it;
+      KvPieces it;
       it.work = s_work - p0;  // work[u] for the pages p0 .. p0 + n_pages - 1
       it.n_items = i1;
       it.p = p;
       it.cl = &cl;
-      it.tm = kTensor ? &tm : nullptr;
+      it.tm = &tm;
       it.piece = piece;
       it.stride = 1;
       it.start(i0);
-      bulk_pipeline<kTensor>(it, stages, kTensor ? &tm : nullptr);  // waits for its last store
+      bulk_pipeline<true>(it, stages, &tm);  // waits for its last store
     }
     if (tracing && tid == 0) {
       stamp(2);
@@ -768,7 +749,6 @@ __global__ void __launch_bounds__(kK31Threads)
 // tracked by the host per d_totals): CTA 0 resets the other parity's words,
 // which only the previous launch on the stream used.
 // ---------------------------------------------------------------------------
-template <bool kTensor>
 __global__ void __launch_bounds__(kK31Threads)
     tpr_k31_switch_dyn(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo,
                        KvCopyParams p, const __grid_constant__ KvClusterParams cl,
@@ -838,20 +818,20 @@ __global__ void __launch_bounds__(kK31Threads)
     if (v >= (unsigned long long)grid) break;
   }
   if (tracing) stamp(2);
-  KvPieces<kTensor> it;
+  KvPieces it;
   it.work = work;
   it.work_l2 = true;
   it.n_items = n_mine * p.items_per_unit;
   it.p = p;
   it.cl = &cl;
-  it.tm = kTensor ? &tm : nullptr;
+  it.tm = &tm;
   it.piece = piece;
   if (rp.batch > 0) {
     it.claim = &words[par];
     it.batch = rp.batch;
   }
   it.start(blockIdx.x);
-  bulk_pipeline<kTensor>(it, stages, kTensor ? &tm : nullptr);
+  bulk_pipeline<true>(it, stages, &tm);
   if (tracing) {
     stamp(3);
     rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
@@ -960,17 +940,10 @@ static cudaError_t k1_launch(const KvCopyParams& p, const KvClusterParams& cl, c
                              int64_t n_units, cudaStream_t st, bool pdl, const KvTensorMaps& tm,
                              const BulkConfig& c) {
   const int64_t items = n_units * p.items_per_unit;
-  if (tm.enabled) {
-    const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_tma), c,
-                               k1_grid_units(items), 32);
-    return launch_ex(tpr_k1_kv_migrate_tma, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl, work,
-                     n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece,
-                     (int32_t)k1_batch_for(items));
-  }
   const int grid = bulk_grid(reinterpret_cast<const void*>(&tpr_k1_kv_migrate_bulk), c,
                              k1_grid_units(items), 32);
   return launch_ex(tpr_k1_kv_migrate_bulk, dim3(grid), dim3(32), (size_t)c.smem(), st, pdl, work,
-                   n_units, p, cl, (int32_t)c.stages, (uint32_t)c.piece,
+                   n_units, p, cl, tm, (int32_t)c.stages, (uint32_t)c.piece,
                    (int32_t)k1_batch_for(items));
 }
 
@@ -982,8 +955,8 @@ cudaError_t launch_k1_bulk(const KvCopyParams& p, const KvClusterParams& cl, con
   const BulkConfig& c = n_units * p.items_per_unit <= k1_small_items() ? k1_small_config()
                                                                         : k1_config();
   KvTensorMaps tm;
-  tm.enabled = 0;
-  if (geo && (partial || tensor_kernel_always())) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
+  tm.enabled = 0;  // a plan of full pages needs no tensor map
+  if (geo && partial) kv_tensor_maps(*geo, cl, n_gpus, c.piece, &tm);
   return k1_launch(p, cl, work, n_units, st, pdl, tm, c);
 }
 
@@ -1014,10 +987,8 @@ cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
   // §4d: 116 pages 15.4 vs 19.5 us, 1024 pages 97.3 vs 93.0 us, 1792 pages
   // 160.8 vs 152.6 us); knob k31 = 2 / 3 forces one
   const bool dyn = variant == 2 || (variant == 1 && n_units >= kK31DynamicUnits);
-  const void* fn = dyn ? (tm.enabled ? reinterpret_cast<const void*>(&tpr_k31_switch_dyn<true>)
-                                     : reinterpret_cast<const void*>(&tpr_k31_switch_dyn<false>))
-                       : (tm.enabled ? reinterpret_cast<const void*>(&tpr_k31_switch<true>)
-                                     : reinterpret_cast<const void*>(&tpr_k31_switch<false>));
+  const void* fn = dyn ? reinterpret_cast<const void*>(&tpr_k31_switch_dyn)
+                       : reinterpret_cast<const void*>(&tpr_k31_switch);
   const int64_t items = n_units * p.items_per_unit;
   const int grid = bulk_grid(fn, c, items, kK31Threads);
   if (!dyn && ((items + grid - 1) / grid + p.items_per_unit - 1) / p.items_per_unit + 1 >
@@ -1061,21 +1032,13 @@ cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int4* work = reinterpret_cast<int4*>(d_work);
-    cudaError_t e = tm.enabled
-        ? cudaLaunchKernelEx(&cfg, tpr_k31_switch_dyn<true>, rp, geo, p, cl, tm, totals, work,
-                             status, status_mirror, (int32_t)c.stages, (uint32_t)c.piece)
-        : cudaLaunchKernelEx(&cfg, tpr_k31_switch_dyn<false>, rp, geo, p, cl, tm, totals, work,
-                             status, status_mirror, (int32_t)c.stages, (uint32_t)c.piece);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tpr_k31_switch_dyn, rp, geo, p, cl, tm, totals, work,
+                                       status, status_mirror, (int32_t)c.stages, (uint32_t)c.piece);
     if (e == cudaSuccess) ++par;
     return e;
   }
   unsigned long long* readers = reinterpret_cast<unsigned long long*>(d_work);
-  if (tm.enabled)
-    tpr_k31_switch<true><<<grid, kK31Threads, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
-                                                             status, status_mirror, c.stages,
-                                                             c.piece);
-  else
-    tpr_k31_switch<false><<<grid, kK31Threads, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
+  tpr_k31_switch<<<grid, kK31Threads, (size_t)c.smem(), st>>>(rp, geo, p, cl, tm, totals, readers,
                                                               status, status_mirror, c.stages,
                                                               c.piece);
   return cudaGetLastError();

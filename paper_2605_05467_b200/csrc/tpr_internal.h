@@ -74,7 +74,6 @@ int64_t k31_trace_buffer();
 void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
                     uint32_t piece_bytes, KvTensorMaps* out);
 bool tensor_partial_enabled();
-bool tensor_kernel_always();
 
 int sm_count();
 

@@ -102,7 +102,6 @@ LAUNCH_PATHS = {  # tpr_kv_switch launch variants: all must give the same bytes
     "fused_k3_rows": dict(k31=0, k3_fuse_units=1 << 30, tensor_partial=0),
     "split_k3_tensor": dict(k3_fuse_units=0, tensor_partial=1),
     "split_k3_rows": dict(k3_fuse_units=0, tensor_partial=0),
-    "split_k3_tensor_kernel_always": dict(k3_fuse_units=0, tensor_partial=2),
 }
 
 

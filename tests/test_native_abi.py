@@ -29,11 +29,13 @@ def test_tuning_knobs_roundtrip():
     lib = _native.load()
     saved = {k: _native.get_tuning(k) for k in _native.TUNING_KEYS}
     try:
-        assert saved["k3_fuse_units"] >= 0 and saved["k31"] in (0, 1)
+        assert saved["k3_fuse_units"] >= 0 and saved["k31"] in (0, 1, 2, 3)
         _native.set_tuning("k3_fuse_units", 0)
         assert _native.get_tuning("k3_fuse_units") == 0
         _native.set_tuning("tensor_partial", 5)
-        assert _native.get_tuning("tensor_partial") == 2
+        assert _native.get_tuning("tensor_partial") == 1
+        _native.set_tuning("k31", 9)
+        assert _native.get_tuning("k31") == 3
         assert lib.tpr_set_tuning(b"nope", 1) == -1 and b"unknown tuning key" in lib.tpr_last_error()
         assert lib.tpr_set_tuning(b"k31", -1) == -1
         assert lib.tpr_set_tuning(b"pdl", 1) == -1  # retired knobs are unknown keys

@@ -18,4 +18,4 @@ timeout 1500 python tools/sweep.py --out $O/${T}_sweep.jsonl > $O/${T}_sweep.log
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tpr_k[0-9] -c 200 --csv --log-file $O/${T}_launches_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tpr_k[0-9] -c 200 --csv --log-file $O/${T}_launches_cfg1.csv python bench.py --config 0 --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:tpr_k1_kv_migrate_bulk --launch-skip 1 -c 1 -o $O/${T}_k1_lean_cfg2 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:tpr_k1_kv_migrate_tma --launch-skip 2 -c 1 -o $O/${T}_k1_tensor_trace python tools/sweep.py --modes trace --only 4:8:256 --reps 1 --k1-reps 1 --out /dev/null > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:tpr_k1_kv_migrate_bulk --launch-skip 2 -c 1 -o $O/${T}_k1_tensor_trace python tools/sweep.py --modes trace --only 4:8:256 --reps 1 --k1-reps 1 --out /dev/null > /dev/null 2>&1
