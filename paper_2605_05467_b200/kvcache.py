@@ -111,12 +111,16 @@ class _Scratch:
 
     def __init__(self, dtype, device):
         self.t = torch.zeros(0, dtype=dtype, device=device)
+        self.n = 0
+        self.version = 0  # bumped on every reallocation
 
     def get(self, n: int, stream: torch.cuda.Stream) -> torch.Tensor:
-        if self.t.numel() < n:
+        if self.n < n:
             with torch.cuda.stream(stream):
-                self.t = torch.zeros(max(n, 2 * self.t.numel(), 1024), dtype=self.t.dtype,
+                self.t = torch.zeros(max(n, 2 * self.n, 1024), dtype=self.t.dtype,
                                      device=self.t.device)
+            self.n = self.t.numel()
+            self.version += 1
         return self.t
 
 
@@ -589,17 +593,18 @@ class PagedKvCluster:
         """Point the tables at plan/records/device scratch sized for the
         current plan capacity (grow-only; set again only when one grew)."""
         rows = self._swt_plan
-        cap = max(len(rows), 1)
-        xf = self._xf.get(cap * 6, stream)
-        meta = self._meta.get(cap * 4, stream)
-        work = self._work.t
-        key = (xf.data_ptr(), meta.data_ptr(), work.data_ptr(), work.numel())
         held = self._swt_bufs
-        if held is None or held[0] is not rows or held[1] != key:
-            t.plan, t.plan_cap = rows.ctypes.data, len(rows)
-            t.d_xfers, t.d_meta, t.xfers_cap = xf.data_ptr(), meta.data_ptr(), len(rows)
-            t.d_work, t.work_cap = work.data_ptr(), work.numel() // 4
-            self._swt_bufs = (rows, key)
+        xf, meta, work = self._xf, self._meta, self._work
+        if (held is not None and held[0] is rows and held[1] == xf.version
+                and held[2] == meta.version and held[3] == work.version):
+            return
+        cap = max(len(rows), 1)
+        xf.get(cap * 6, stream)
+        meta.get(cap * 4, stream)
+        t.plan, t.plan_cap = rows.ctypes.data, len(rows)
+        t.d_xfers, t.d_meta, t.xfers_cap = xf.t.data_ptr(), meta.t.data_ptr(), len(rows)
+        t.d_work, t.work_cap = work.t.data_ptr(), work.n // 4
+        self._swt_bufs = (rows, xf.version, meta.version, work.version)
 
     def switch_layouts(self, old_layouts, new_layouts, stream: torch.cuda.Stream | None = None,
                        validate: bool = True, handshake_ms: float = 0.0,
@@ -668,7 +673,7 @@ class PagedKvCluster:
             raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
         n = t.n_plan
         self.status_mirrored = True
-        plan = MigrationPlan.from_array(self._swt_plan[:n].copy(), handshake_ms=handshake_ms)
+        plan = MigrationPlan.from_rows(self._swt_plan[:n].copy(), handshake_ms)
         if release:
             self._forget(release)
         if t.n_records == 0:

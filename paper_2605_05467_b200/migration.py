@@ -141,6 +141,17 @@ class MigrationPlan:
         plan.predicted_latency_ms = {}
         return plan
 
+    @classmethod
+    def from_rows(cls, arr: np.ndarray, handshake_ms: float = 0.0) -> "MigrationPlan":
+        """from_array for an array that is already C-contiguous int64 [n, 6]
+        and owned by the plan (the one-call switch's copy of its plan rows)."""
+        plan = cls.__new__(cls)
+        plan._list = None
+        plan._arr = arr
+        plan.handshake_ms = handshake_ms
+        plan.predicted_latency_ms = {}
+        return plan
+
     def _get_transfers(self) -> list[Transfer]:
         if self._list is None:
             self._list = [Transfer(*map(int, row)) for row in self._arr]
