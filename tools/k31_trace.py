@@ -20,9 +20,10 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-# stamps: the item-share kernel (TPR_K31=1) and the dynamic one (TPR_K31=2)
-DYN = os.environ.get("TPR_K31", "1") == "2"
-NAMES = ("entry", "decide", "barrier", "copies") if DYN else ("entry", "decide", "copies", "books")
+# stamps of the item-share schedule and of the dynamic one (TPR_K31: 1 = by
+# plan size, dynamic from 512 pages; 2 = dynamic; 3 = item shares)
+NAMES_ITEM = ("entry", "decide", "copies", "books")
+NAMES_DYN = ("entry", "decide", "barrier", "copies")
 
 CASES = {"1seq": (8, 1, 2, 1, 463), "cfg1": (2, 1, 2, 4, 512), "1seq4096": (8, 8, 1, 1, 4096)}
 
@@ -53,29 +54,34 @@ def main():
     ex = ReconfigurationExecutor(cl)
     buf = torch.zeros(2048 * 8, dtype=torch.int64, device="cuda")
     _native.set_tuning("k31_trace", buf.data_ptr())
+    knob = os.environ.get("TPR_K31", "1") or "1"
     rows = []
+    dyn = False
     try:
         for i in range(args.reps):
             buf.zero_()
             torch.cuda._sleep(200_000)  # the launch waits on the stream, not the host
-            ex.switch(*((la, lb) if i % 2 == 0 else (lb, la)), validate=False)
+            r = ex.switch(*((la, lb) if i % 2 == 0 else (lb, la)), validate=False)
+            dyn = knob == "2" or (knob == "1" and r.kv.units >= 512)
             t = buf.view(-1, 8).cpu().numpy()
             grid = int(t[0, 7])
             if grid <= 0:
                 raise SystemExit("no K31 launch (plan outside the fused path?)")
             t = t[:grid]
             base = t[:, 0].min()
-            rows.append({k: (t[:, j] - base) for j, k in enumerate(NAMES)})
+            rows.append({k: (t[:, j] - base) for j, k in enumerate(NAMES_DYN if dyn else NAMES_ITEM)})
     finally:
         _native.set_tuning("k31_trace", 0)
     last = rows[len(rows) // 2:]
-    out = {"case": args.case, "variant": "dynamic" if DYN else "item-share", "grid": grid,
-           "items_per_cta": [int(x) for x in np.unique(t[:, 6])]}
+    NAMES = NAMES_DYN if dyn else NAMES_ITEM
+    out = {"case": args.case, "variant": "dynamic" if dyn else "item-share", "grid": grid}
+    if not dyn:
+        out["items_per_cta"] = [int(x) for x in np.unique(t[:, 6])]
     for k in NAMES:
         v = np.concatenate([r[k] for r in last])
         out[k] = {"min": int(v.min()), "median": int(np.median(v)), "max": int(v.max())}
     out["copy_phase_median_ns"] = int(np.median(np.concatenate(
-        [r["copies"] - r[NAMES[-2] if DYN else "decide"] for r in last])))
+        [r["copies"] - r["barrier" if dyn else "decide"] for r in last])))
     out["kernel_span_median_ns"] = int(np.median([max(r[k].max() for k in NAMES[1:])
                                                    for r in last]))
     print(json.dumps(out))

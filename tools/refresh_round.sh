@@ -14,8 +14,8 @@ timeout 300 python tools/small_switch.py --out $O/${T}_small_switch.jsonl > $O/$
 timeout 900 python tools/weight_sweep.py --out $O/${T}_weight_sweep.jsonl > $O/${T}_weight_sweep.log 2>&1
 timeout 900 python tools/weight_sweep.py --model 70b --layers 20 --sets 8:4,8 --sets 4:2,4 --out $O/${T}_weight_sweep_70b.jsonl > $O/${T}_weight_sweep_70b.log 2>&1
 # ncu: launch lists (cfg2, cfg1) and full captures of K1 (cfg2; trace contexts), K2 (cfg2) and K31
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tpr_ -c 200 --csv --log-file $O/${T}_launches_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-headline > /dev/null 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tpr_ -c 200 --csv --log-file $O/${T}_launches_cfg1.csv python bench.py --config 0 --steps 4 --warmup 3 --no-cpu --no-e2e --no-headline > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tpr_k[0-9] -c 200 --csv --log-file $O/${T}_launches_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-headline > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tpr_k[0-9] -c 200 --csv --log-file $O/${T}_launches_cfg1.csv python bench.py --config 0 --steps 4 --warmup 3 --no-cpu --no-e2e --no-headline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:tpr_k1_kv_migrate_bulk --launch-skip 1 -c 1 -o $O/${T}_k1_cfg2 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-headline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:tpr_k2 --launch-skip 1 -c 1 -o $O/${T}_k2_cfg2 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-headline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:tpr_k1_kv_migrate_bulk --launch-skip 2 -c 1 -o $O/${T}_k1_tensor_trace python tools/sweep.py --modes trace --only 4:8:256 --reps 1 --k1-reps 1 --out /dev/null > /dev/null 2>&1

@@ -152,7 +152,7 @@ def main():
             cpu_ms = cpu_point(la, lb, reqs, gpus, kv) if n <= args.cpu_max_seqs else None
             row = {
                 "mode": mode, "tp_old": a, "tp_new": b, "seqs": n,
-                "ctx_total": int(sum(ctxs)), "transfers": len(fwd), "bytes": nbytes,
+                "ctx_total": int(sum(ctxs)), "transfers": fwd.n_transfers, "bytes": nbytes,
                 "device_ms": d, "host_ms": float(np.median(host_ms)),
                 "gbs": nbytes / (d * 1e-3) / 1e9 if d > 0 else None,
                 "hbm_frac": (2 * nbytes / (peak * 1e9)) / (d * 1e-3) if d > 0 else None,
