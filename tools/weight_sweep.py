@@ -32,7 +32,7 @@ def main():
     from paper_2605_05467_b200 import workloads
     import dataclasses
 
-    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B, LLAMA_3_1_70B
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B, LLAMA_3_1_70B, MAX_TP
     from paper_2605_05467_b200.weights import ShardedWeightStore
 
     ap = argparse.ArgumentParser()
@@ -66,7 +66,9 @@ def main():
                 # a->b timed, b->a untimed, repeated; the first pair is warm-up
                 # (the first touch of freshly cudaMalloc'd arenas costs ~0.1
                 # ms/GB once per process; the caching allocator reuses them)
-                store = ShardedWeightStore(model, gpus)
+                # arena window: the larger of the two shards (slices), the least
+                # HBM that still lets a growing shard stay in place
+                store = ShardedWeightStore(model, gpus, max_slices=max(MAX_TP // a, MAX_TP // b))
                 store.load(workloads.tp_groups(gpus, a))
                 torch.cuda.synchronize()
                 st = torch.cuda.current_stream()
