@@ -260,6 +260,16 @@ int tpr_kv_records(const int64_t* plan, int64_t n, const int64_t* gpu_lut, int64
                    int32_t validate, int32_t* records, int64_t* in_units, int64_t* out_units,
                    int64_t* total_units);
 
+/* K3's three keyed exclusive scans over n records, on the host (what the
+ * one-launch small switch K31 passes in its parameters): meta[t] =
+ * {units before t this caller moves (records with src == filter, or all when
+ * filter < 0), units before t its destination ring hands out, units before t
+ * its source ring takes back, units of t this caller moves} -- the int64 x 4
+ * rows K3 writes to d_meta (TPR_META_FIELDS). *n_mine (nullable) = the total
+ * this caller moves. */
+int tpr_record_offsets(const int32_t* records, int64_t n, int32_t filter, int32_t block_tokens,
+                       int64_t* meta, int64_t* n_mine);
+
 /* After a switch is enqueued: owner[req slot][h] = dst slot for every head of
  * every record (apply_plan, migration.py:192-207, on the host placement). */
 int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads);

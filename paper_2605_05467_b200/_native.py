@@ -29,7 +29,8 @@ TPR_ENOTFOUND = -4  # an id outside the caller's lookup tables (use the Python m
 EXPORTS = (
     "tpr_set_copy_engine", "tpr_get_copy_engine", "tpr_set_tuning", "tpr_get_tuning",
     "tpr_version", "tpr_last_error", "tpr_device_info", "tpr_plan_heads", "tpr_plan_repartition",
-    "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_migrate_ex", "tpr_kv_records", "tpr_kv_apply_owner", "tpr_kv_switch",
+    "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_migrate_ex", "tpr_kv_records", "tpr_record_offsets",
+    "tpr_kv_apply_owner", "tpr_kv_switch",
     "tpr_switch_prepare", "tpr_kv_switch_layouts",
     "tpr_memcpy_h2d", "tpr_memcpy_d2h",
     "tpr_copy_prepare", "tpr_weight_reshard", "tpr_reshard_buffer_bytes", "tpr_weight_reshard_host",
@@ -123,6 +124,7 @@ _SIGNATURES = {
                                  c_int64, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64,
                                  c_int32, c_void_p, c_void_p, c_void_p, _P64]),
     "tpr_kv_apply_owner": (c_int32, [c_void_p, c_int64, c_void_p, c_int32]),
+    "tpr_record_offsets": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "tpr_kv_switch": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                 c_void_p]),

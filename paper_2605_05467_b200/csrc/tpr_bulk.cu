@@ -996,19 +996,12 @@ cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
     return cudaErrorNotSupported;
   K31Params rp;
   memcpy(rp.rec, h_rec, sizeof(int32_t) * TPR_XFER_FIELDS * (size_t)n);
-  // K3's three keyed exclusive scans (tpr_kernels.cu k3 scan), on the host
-  int64_t mine = 0, in_u[TPR_MAX_GPUS] = {}, out_u[TPR_MAX_GPUS] = {};
-  for (int t = 0; t < n; ++t) {
-    const int32_t* r = h_rec + (size_t)t * TPR_XFER_FIELDS;
-    const int64_t nblk = r[5] > 0 ? (r[5] + geo.block_tokens - 1) / geo.block_tokens : 0;
-    const int64_t u = (int64_t)(r[4] - r[3]) * nblk;
-    rp.off[0][t] = mine;
-    rp.off[1][t] = r[1] >= 0 && r[1] < TPR_MAX_GPUS ? in_u[r[1]] : 0;
-    rp.off[2][t] = r[0] >= 0 && r[0] < TPR_MAX_GPUS ? out_u[r[0]] : 0;
-    if (filter < 0 || r[0] == filter) mine += u;
-    if (r[1] >= 0 && r[1] < TPR_MAX_GPUS) in_u[r[1]] += u;
-    if (r[0] >= 0 && r[0] < TPR_MAX_GPUS) out_u[r[0]] += u;
-  }
+  // K3's three keyed exclusive scans (tpr_kernels.cu k3_scan_body), on the
+  // host: the per-record offsets K3 would write to d_meta
+  int64_t meta[kK31Xfers * TPR_META_FIELDS], mine = 0;
+  tpr_record_offsets(h_rec, n, filter, geo.block_tokens, meta, &mine);
+  for (int t = 0; t < n; ++t)
+    for (int k = 0; k < 3; ++k) rp.off[k][t] = meta[t * TPR_META_FIELDS + k];
   rp.n_mine = mine;
   rp.n = n;
   rp.filter = filter;

@@ -350,6 +350,30 @@ int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* 
   return tpr_kv_apply_owner(t->records, n, t->owner, geo->total_heads);
 }
 
+int tpr_record_offsets(const int32_t* records, int64_t n, int32_t filter, int32_t block_tokens,
+                       int64_t* meta, int64_t* n_mine) {
+  if (n < 0 || (n > 0 && (!records || !meta)) || block_tokens < 1)
+    return tpr::set_error(TPR_EINVAL, "bad tpr_record_offsets arguments");
+  int64_t mine = 0, in_u[TPR_MAX_GPUS] = {}, out_u[TPR_MAX_GPUS] = {};
+  for (int64_t t = 0; t < n; ++t) {
+    const int32_t* r = records + t * TPR_XFER_FIELDS;
+    const int64_t nblk = r[5] > 0 ? (r[5] + block_tokens - 1) / block_tokens : 0;
+    const int64_t u = (int64_t)(r[4] - r[3]) * nblk;
+    const bool has_dst = r[1] >= 0 && r[1] < TPR_MAX_GPUS, has_src = r[0] >= 0 && r[0] < TPR_MAX_GPUS;
+    const int64_t m = (filter < 0 || r[0] == filter) ? u : 0;
+    int64_t* o = meta + t * TPR_META_FIELDS;
+    o[0] = mine;
+    o[1] = has_dst ? in_u[r[1]] : 0;
+    o[2] = has_src ? out_u[r[0]] : 0;
+    o[3] = m;
+    mine += m;
+    if (has_dst) in_u[r[1]] += u;
+    if (has_src) out_u[r[0]] += u;
+  }
+  if (n_mine) *n_mine = mine;
+  return TPR_OK;
+}
+
 int tpr_kv_apply_owner(const int32_t* records, int64_t n, int32_t* owner, int32_t total_heads) {
   if (n < 0 || (n > 0 && (!records || !owner)) || total_heads < 1)
     return tpr::set_error(TPR_EINVAL, "bad tpr_kv_apply_owner arguments");

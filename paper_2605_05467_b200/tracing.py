@@ -11,11 +11,12 @@ import contextlib
 import os
 
 ENABLED = os.environ.get("TPR_NVTX", "0") == "1"
+_OFF = contextlib.nullcontext()  # reusable: nothing is allocated per range when off
 
 
 def nvtx(name: str):
     if not ENABLED:
-        return contextlib.nullcontext()
+        return _OFF
     import torch
 
     return torch.cuda.nvtx.range(f"tpr:{name}")

@@ -533,3 +533,34 @@ def test_k31_reports_errors_per_call(k31_variant):
     ok = ex.switch([M.KvLayout((0, 1), 2, 8, ((7, 33),))],
                    [M.KvLayout((1, 0), 2, 8, ((7, 33),))], validate=False)
     assert ok.status == 0 and int(c.status.item()) == 0
+
+
+def test_host_record_offsets_equal_the_device_scan():
+    # K31 takes K3's keyed scans from the host (tpr_record_offsets); the split
+    # K3 writes the same rows to d_meta on the device: they must agree
+    import ctypes
+    from paper_2605_05467_b200 import _native
+    gpus = tuple(range(8))
+    rng = np.random.default_rng(5)
+    reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 400, size=40))]
+    old = workloads.round_robin(workloads.tp_groups(gpus, 2), reqs, 8)
+    new = workloads.round_robin(workloads.tp_groups(gpus, 8), reqs, 8)
+    c = make(TINY, gpus, units=4096, reqs=48, blocks=32, fragmented=True, seed=2)
+    c.admit(old, seed=3)
+    plan = M.plan_repartition(old, new, TINY.kv_bytes_per_token_per_head)
+    rec = c.records(plan, validate=False).astype(np.int32)
+    saved = {k: _native.get_tuning(k) for k in ("k31", "k3_fuse_units")}
+    try:
+        _native.set_tuning("k31", 0)
+        _native.set_tuning("k3_fuse_units", 0)
+        c.migrate(plan)
+        torch.cuda.synchronize()
+    finally:
+        for k, v in saved.items():
+            _native.set_tuning(k, v)
+    n = len(rec)
+    dev = c._meta.t[: n * 4].cpu().numpy().reshape(n, 4)
+    host = np.zeros((n, 4), np.int64)
+    _native.call("tpr_record_offsets", rec.ctypes.data, n, -1, TINY.block_tokens,
+                 host.ctypes.data, None)
+    assert np.array_equal(dev, host)

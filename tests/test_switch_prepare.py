@@ -166,3 +166,44 @@ def test_head_transfers_mode_takes_one_layout_each():
     tab = Tables(gpus, [a])
     rc, _ = tab.prepare([a, b], [b], mode=_native.TPR_SWITCH_HEAD_TRANSFERS)
     assert rc == -1
+
+
+def _offsets_restated(rec: np.ndarray, filt: int, B: int) -> np.ndarray:
+    """K3's three keyed exclusive scans (tpr_kernels.cu k3_scan_body) as plain
+    loops: per record, units before it this caller moves, units before it its
+    destination ring hands out, units before it its source ring takes back,
+    and its own units this caller moves."""
+    out = np.zeros((len(rec), 4), np.int64)
+    mine, into, outof = 0, {}, {}
+    for t, (s, d, _, lo, hi, ctx) in enumerate(rec.tolist()):
+        u = (hi - lo) * (-(-ctx // B) if ctx > 0 else 0)
+        m = u if (filt < 0 or s == filt) else 0
+        out[t] = (mine, into.get(d, 0) if d >= 0 else 0, outof.get(s, 0) if s >= 0 else 0, m)
+        mine += m
+        if d >= 0:
+            into[d] = into.get(d, 0) + u
+        if s >= 0:
+            outof[s] = outof.get(s, 0) + u
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("filt", [-1, 0, 3])
+def test_record_offsets_match_the_k3_scan_restated(seed, filt):
+    # tpr_record_offsets: the host-side scan K31 carries in its parameters
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 97))
+    rec = np.empty((n, 6), np.int32)
+    rec[:, 0] = rng.integers(-1, 8, n)
+    rec[:, 1] = rng.integers(-1, 8, n)
+    rec[:, 2] = rng.integers(0, 50, n)
+    rec[:, 3] = rng.integers(0, 4, n)
+    rec[:, 4] = rec[:, 3] + rng.integers(1, 5, n)
+    rec[:, 5] = rng.integers(0, 3000, n)
+    meta = np.full((n, 4), -7, np.int64)
+    total = ctypes.c_int64(-1)
+    _native.call("tpr_record_offsets", rec.ctypes.data, n, filt, 16, meta.ctypes.data,
+                 ctypes.byref(total))
+    want = _offsets_restated(rec, filt, 16)
+    assert np.array_equal(meta, want)
+    assert total.value == int(want[:, 3].sum())
