@@ -116,11 +116,12 @@ typedef struct tpr_kv_cluster {
 #define TPR_TOTALS_K31_STATUS (2 + 2 * TPR_MAX_GPUS)
 #define TPR_TOTALS_K31_EPOCH (3 + 2 * TPR_MAX_GPUS)
 /* [TPR_TOTALS_K31_PAR + 2k + parity], k = 0 claim counter, 1 CTAs decided,
- * 2 status bits: the dynamic small-switch kernel's words, double-buffered by
- * the launch parity the host tracks per d_totals (a launch resets the other
- * parity's words, which the previous launch on the stream used). */
+ * 2 status bits, 3 CTAs finished: the dynamic small-switch kernel's words,
+ * double-buffered by the launch parity the host tracks per d_totals (a launch
+ * resets the other parity's words, which the previous launch on the stream
+ * used). */
 #define TPR_TOTALS_K31_PAR (4 + 2 * TPR_MAX_GPUS)
-#define TPR_TOTALS_LEN (10 + 2 * TPR_MAX_GPUS)
+#define TPR_TOTALS_LEN (12 + 2 * TPR_MAX_GPUS)
 
 /* ---- host utilities -------------------------------------------------- */
 /* Copy engine of K1 and K2 (process-wide): TPR_ENGINE_BULK (default) = TMA
@@ -304,7 +305,7 @@ typedef struct tpr_switch_tables {
   int64_t work_cap;
   int32_t* d_status;       /* device int32                                     */
   int64_t plan_bytes;      /* out: the plan's total bytes (MigrationPlan.total_bytes) */
-  int32_t* h_status;       /* nullable pinned host int32: the status word is mirrored
+  int32_t* h_status;       /* nullable pinned host int32 [2]: the status word is mirrored
                               there on the stream (fused K3 store or a 4-byte D2H),
                               so a synchronous caller needs no separate read-back */
   void* k1_events[2];      /* nullable cudaEvent_t pair recorded around K1 (timing) */
@@ -312,12 +313,20 @@ typedef struct tpr_switch_tables {
   int32_t records_async;   /* out: 1 when the device reads `records` after the call
                               returns (keep them until the stream passes), 0 when
                               the launch took them (K31: kernel parameters)   */
-  int32_t _pad2;
+  int32_t ticket;          /* in: nonzero asks for a completion ticket;
+                              out: nonzero when the switch ran as K31 with h_status:
+                              the kernel writes it to h_status[1] (h_status must
+                              then hold 2 int32) after the status word, once every
+                              copy and table write of the switch is done; a
+                              synchronous caller may spin on it instead of an
+                              event. 0: wait for the stream.                   */
   int64_t* ring_head_io;   /* nullable int64 [n_slots]: advanced by in_units    */
   int64_t* ring_tail_io;   /* nullable int64 [n_slots]: advanced by out_units
                               (both after the switch is enqueued; point them at
                               the cluster's own ring_head / ring_tail to keep
                               the host ring counters without a round trip)    */
+  void* start_event;       /* nullable cudaEvent_t recorded on the stream right
+                              before the switch's first launch (after planning) */
 } tpr_switch_tables_t;
 
 /* tpr_switch_tables_t.mode: the planner of the switch.
@@ -376,6 +385,10 @@ int tpr_kv_switch(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
 int tpr_memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes, void* stream);
 /* Stream-ordered device->host copy (pinned destination), e.g. the status word. */
 int tpr_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, void* stream);
+
+/* cudaEventRecord(event, stream) for a caller without its own CUDA binding
+ * (the executor's end-of-switch event, ~0.5 us through ctypes). */
+int tpr_event_record(void* event, void* stream);
 
 /* ---- K2: weight reshard = batched 2-D strided copy (device) ------------ */
 typedef struct tpr_copy_seg {

@@ -17,7 +17,7 @@ TPR_ABI_VERSION = 1
 TPR_MAX_GPUS = 16
 TPR_XFER_FIELDS = 6
 TPR_META_FIELDS = 4
-TPR_TOTALS_LEN = 10 + 2 * TPR_MAX_GPUS  # + scratch words of the fused small switch
+TPR_TOTALS_LEN = 12 + 2 * TPR_MAX_GPUS  # + scratch words of the fused small switch
 TPR_STATUS_WRONG_SOURCE = 1
 TPR_STATUS_DST_OCCUPIED = 2
 TPR_STATUS_BARRIER_TIMEOUT = 4
@@ -32,7 +32,7 @@ EXPORTS = (
     "tpr_kv_remap", "tpr_kv_migrate", "tpr_kv_migrate_ex", "tpr_kv_records", "tpr_record_offsets",
     "tpr_kv_apply_owner", "tpr_kv_switch",
     "tpr_switch_prepare", "tpr_kv_switch_layouts",
-    "tpr_memcpy_h2d", "tpr_memcpy_d2h",
+    "tpr_memcpy_h2d", "tpr_memcpy_d2h", "tpr_event_record",
     "tpr_copy_prepare", "tpr_weight_reshard", "tpr_reshard_buffer_bytes", "tpr_weight_reshard_host",
     "tpr_kv_fill", "tpr_pool_fill", "tpr_kv_verify", "tpr_matrix_fill",
     "tpr_matrix_verify", "tpr_baseline_copy_pages", "tpr_device_barrier", "tpr_device_alloc",
@@ -88,7 +88,8 @@ class SwitchTablesC(Structure):
         ("d_totals", c_void_p), ("d_work", c_void_p), ("work_cap", c_int64),
         ("d_status", c_void_p), ("plan_bytes", c_int64), ("h_status", c_void_p),
         ("k1_events", c_void_p * 2), ("n_records", c_int64), ("records_async", c_int32),
-        ("_pad2", c_int32), ("ring_head_io", c_void_p), ("ring_tail_io", c_void_p),
+        ("ticket", c_int32), ("ring_head_io", c_void_p), ("ring_tail_io", c_void_p),
+        ("start_event", c_void_p),
     ]
 
 
@@ -125,6 +126,7 @@ _SIGNATURES = {
                                  c_int32, c_void_p, c_void_p, c_void_p, _P64]),
     "tpr_kv_apply_owner": (c_int32, [c_void_p, c_int64, c_void_p, c_int32]),
     "tpr_record_offsets": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    "tpr_event_record": (c_int32, [c_void_p, c_void_p]),
     "tpr_kv_switch": (c_int32, [POINTER(KvGeometryC), POINTER(KvClusterC), c_void_p, c_void_p,
                                 c_int32, c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                 c_void_p]),

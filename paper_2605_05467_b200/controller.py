@@ -15,6 +15,7 @@ returns the measured pause, which replaces ``switch_cost`` in the engine
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import torch
@@ -33,15 +34,37 @@ class SwitchResult:
     kv: MigrationStats
     weights: ReshardStats | None
     host_ms: float = 0.0        # pause -> resume wall time (only when synced)
-    device_ms: float = 0.0      # CUDA-event time of the whole switch (only when synced)
     status: int = 0             # K3 status bits (0 = every head was where the plan said)
     events: dict = field(default_factory=dict)
     new_layouts: list | None = None  # the layouts the switch realised (reuse_order may reorder ranks)
     evicted: list = field(default_factory=list)  # arrivals the destination could not hold (released)
+    _device_ms: float | None = field(default=None, repr=False)
+    _timed: bool = field(default=False, repr=False)
 
     @property
     def bytes(self) -> int:
         return self.kv.bytes + (self.weights.bytes if self.weights else 0)
+
+    @property
+    def device_ms(self) -> float:
+        """CUDA-event time of the switch on the device, from its first launch
+        to the end of its last kernel (only when synced; 0.0 otherwise). Read
+        from the switch's events on first access: cudaEventElapsedTime costs
+        ~6 us of host time, which a synchronous switch does not pay."""
+        if self._device_ms is None:
+            if self._timed:
+                self.events["end"].synchronize()  # a ticket-waited switch may still be retiring
+                self._device_ms = self.events["start"].elapsed_time(self.events["end"])
+            else:
+                self._device_ms = 0.0
+        return self._device_ms
+
+    @device_ms.setter
+    def device_ms(self, value: float) -> None:
+        self._device_ms = float(value)
+
+
+_SYNC_EVENT_PAIRS = 64  # event pairs an executor cycles through for synchronous switches
 
 
 class ReconfigurationExecutor:
@@ -70,10 +93,37 @@ class ReconfigurationExecutor:
         self._status_np = self._status_host.numpy()
         self._kv_status_np = kv.status_host.numpy()
         self.main_stream = torch.cuda.current_stream(dev)
-        # reused per synchronous switch (each one waits for its end event)
-        self._ev_sync = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        # synchronous switches cycle through a ring of event pairs; a result
+        # reads its device time lazily, and a pair is re-used only after the
+        # result that last held it (if still alive and unread) has read it
+        self._ev_ring = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                         for _ in range(_SYNC_EVENT_PAIRS)]
+        for pair in self._ev_ring:  # create the CUDA events now; libtpr records them by handle
+            for e in pair:
+                e.record(self.main_stream)
+        self._ev_handles = [(e0.cuda_event, e1.cuda_event) for e0, e1 in self._ev_ring]
+        self._ev_users = [None] * _SYNC_EVENT_PAIRS
+        self._ev_next = 0
+        self._record = _native.load().tpr_event_record
 
-    def _finish(self, res: SwitchResult, main: torch.cuda.Stream, t0: float) -> SwitchResult:
+    @property
+    def _ev_sync(self):
+        """The event pair the next synchronous switch records (tools use it)."""
+        return self._ev_ring[self._ev_next]
+
+    def _take_sync_events(self):
+        i = self._ev_next
+        self._ev_next = (i + 1) % _SYNC_EVENT_PAIRS
+        prev = self._ev_users[i]
+        if prev is not None:
+            r = prev()
+            if r is not None and r._device_ms is None:
+                r.device_ms  # noqa: B018 -- read before the pair is re-recorded
+            self._ev_users[i] = None
+        return i, self._ev_ring[i]
+
+    def _finish(self, res: SwitchResult, main: torch.cuda.Stream, t0: float,
+                slot: int | None = None) -> SwitchResult:
         """Synchronous tail: the step's result (K3's status word) read back,
         then the host waits for the end event. After the one-call switch the
         word is already mirrored into pinned memory on the stream."""
@@ -81,11 +131,31 @@ class ReconfigurationExecutor:
         if not mirrored:
             _native.call("tpr_memcpy_d2h", self._status_host.data_ptr(), self.kv.status.data_ptr(),
                          4, main.cuda_stream)
-        res.events["end"].record(main)
-        res.events["end"].synchronize()
+        end = res.events["end"]
+        if slot is not None:
+            if self._record(self._ev_handles[slot][1], main.cuda_stream):
+                raise _native.NativeError(_native.load().tpr_last_error().decode(errors="replace"))
+        else:
+            end.record(main)
+        no_k2 = res.weights is None or res.weights.segments == 0
+        ticket = self.kv.last_ticket if mirrored and no_k2 else 0
+        if ticket:
+            # the one-launch switch writes its ticket into pinned memory once
+            # every copy and table write is done: spin on it instead of
+            # waiting for the end event (which completes a few us later)
+            word = self._kv_status_np
+            spins = 0
+            while word[1] != ticket:
+                spins += 1
+                if not spins & 0xfff and end.query() and word[1] != ticket:
+                    raise _native.NativeError("switch kernel finished without its ticket")
+        else:
+            end.synchronize()
         res.status = int((self._kv_status_np if mirrored else self._status_np)[0])
         res.host_ms = (time.perf_counter() - t0) * 1e3
-        res.device_ms = res.events["start"].elapsed_time(res.events["end"])
+        res._timed = True  # device_ms: read on first access
+        if slot is not None:
+            self._ev_users[slot] = weakref.ref(res)
         return res
 
     def switch(self, old_layouts: list[KvLayout], new_layouts: list[KvLayout],
@@ -127,25 +197,33 @@ class ReconfigurationExecutor:
                 new_weight_groups = [ranked.get(frozenset(g), tuple(g)) for g in new_weight_groups]
         main = stream or self.main_stream
         ev = {}
-        if sync:
-            ev = {"start": self._ev_sync[0], "end": self._ev_sync[1]}
-            ev["start"].record(main)
-        if self.time_kernels:
-            for k in ("k1_start", "k1_end", "k2_start", "k2_end"):
-                ev[k] = torch.cuda.Event(enable_timing=True)
+        slot = None
         # one stream unless K1 and K2 overlap: no cross-stream event waits on
         # the (latency-bound) small-switch path
         ks = self.kv_stream if self.overlap else main
+        one_call = self.handshake is None
+        start_handle = None
+        if sync:
+            slot, (e0, e1) = self._take_sync_events()
+            ev = {"start": e0, "end": e1}
+            if one_call and ks is main:  # recorded by libtpr right before the first launch
+                start_handle = self._ev_handles[slot][0]
+            else:
+                e0.record(main)
+        if self.time_kernels:
+            for k in ("k1_start", "k1_end", "k2_start", "k2_end"):
+                ev[k] = torch.cuda.Event(enable_timing=True)
         if ks is not main:
             ks.wait_stream(main)
-        if self.handshake is None:
+        if one_call:
             # plan + records + K3 + K1 in one native call (K1 bracketed by events
             # when the kernels are timed)
             with nvtx("plan+kv K3+K1"):
                 plan, kv_stats = self.kv.switch_layouts(
                     old_layouts, new_layouts, stream=ks, validate=validate,
                     k1_events=(ev["k1_start"], ev["k1_end"]) if self.time_kernels else None,
-                    release=evicted)
+                    release=evicted, start_event=start_handle,
+                    want_ticket=sync and (self.weights is None or new_weight_groups is None))
         else:
             with nvtx("plan"):
                 plan = plan_repartition(old_layouts, new_layouts,
@@ -174,7 +252,7 @@ class ReconfigurationExecutor:
             main.wait_stream(ks)
         res = SwitchResult(plan=plan, kv=kv_stats, weights=w_stats, events=ev,
                            new_layouts=list(new_layouts), evicted=evicted)
-        return self._finish(res, main, t0) if sync else res
+        return self._finish(res, main, t0, slot) if sync else res
 
     def _admit(self, old_layouts, new_layouts, arrivals, kv_budget):
         """(old, new, evicted): the layouts without the arrivals each new
@@ -216,19 +294,24 @@ class ReconfigurationExecutor:
         exactly what runs here, through K3 + K1."""
         t0 = time.perf_counter()
         main = torch.cuda.current_stream(self.device)
-        ev = ({"start": self._ev_sync[0], "end": self._ev_sync[1]} if sync else
-              {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")})
+        slot = None
+        if sync:
+            slot, (e0, e1) = self._take_sync_events()
+            ev = {"start": e0, "end": e1}
+        else:
+            ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "end")}
         ev["start"].record(main)
         ks = self.kv_stream if self.overlap else main
         if ks is not main:
             ks.wait_event(ev["start"])
         # head_transfers + records + K3 + K1 in one native call
-        plan, stats = self.kv.switch_layouts(prefill, decode, stream=ks, planner="head_transfers")
+        plan, stats = self.kv.switch_layouts(prefill, decode, stream=ks, planner="head_transfers",
+                                             want_ticket=sync)
         if ks is not main:
             main.wait_stream(ks)
         res = SwitchResult(plan=plan, kv=stats, weights=None, events=ev)
         if sync:
-            return self._finish(res, main, t0)
+            return self._finish(res, main, t0, slot)
         ev["end"].record(main)
         return res
 

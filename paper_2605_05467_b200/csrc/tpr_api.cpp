@@ -387,8 +387,9 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                    int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
                    int32_t* d_status, void* stream, int32_t* status_mirror,
-                   void* const* k1_events, int32_t* records_async) {
+                   void* const* k1_events, int32_t* records_async, int32_t* ticket) {
   if (records_async) *records_async = h_xfers != nullptr;
+  if (ticket) *ticket = 0;
   int rc = check_geometry(geo);
   if (rc) return rc;
   KvClusterParams cp;
@@ -408,11 +409,17 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
     const bool timed = k1_events && k1_events[0] && k1_events[1];
     if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[0]), st)) != cudaSuccess)
       return cuda_fail(e, "tpr_kv_switch K31 start event");
+    int32_t tk = 0;
+    if (ticket && status_mirror) {  // nonzero, distinct from the last few calls
+      static std::atomic<int32_t> g_ticket{0};
+      tk = g_ticket.fetch_add(1) % 0x3fffffff + 1;
+    }
     e = launch_k31(*geo, copy_params(geo), cp, h_xfers, n_xfers, filter_src, n_units, d_totals,
                    d_status, status_mirror, st, cl->n_gpus,
                    any_partial(h_xfers, n_xfers, geo->block_tokens), d_work,
-                   (int)knob(g_k31, "TPR_K31", 1));
+                   (int)knob(g_k31, "TPR_K31", 1), tk);
     if (e == cudaSuccess) {
+      if (ticket) *ticket = tk;
       g_k1_last.store(TPR_ENGINE_BULK);
       if (records_async) *records_async = 0;  // the launch copied them into its parameters
       if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[1]), st)) != cudaSuccess)
@@ -646,6 +653,12 @@ int tpr_memcpy_d2h(void* dst, uint64_t src, uint64_t bytes, void* stream) {
   cudaError_t e = cudaMemcpyAsync(dst, reinterpret_cast<const void*>(src), bytes,
                                   cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_memcpy_d2h");
+}
+
+int tpr_event_record(void* event, void* stream) {
+  if (!event) return fail(TPR_EINVAL, "null event");
+  cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TPR_OK : cuda_fail(e, "tpr_event_record");
 }
 
 int tpr_copy_prepare(tpr_copy_seg_t* segs, int32_t n, int64_t chunk, int64_t* prefix,

@@ -597,6 +597,38 @@ __device__ __forceinline__ int64_t k31_cta_of(int64_t item, int64_t n_items, int
   return ((item + 1) * grid - 1) / n_items;  // the CTA whose share holds `item`
 }
 
+// The item-share kernel's completion: each CTA counts itself after its
+// bookkeeping and status bits (warp 1) and, when the caller asked for a
+// ticket, after its copies too (warp 0); the last count publishes the status
+// word (device + pinned mirror), then the ticket into mirror[1] -- a host
+// that spins on the ticket knows every copy and every table write of the call
+// is done -- and resets the scratch words and advances the epoch (every CTA
+// read it at entry).
+__device__ __forceinline__ void k31_item_share_done(int64_t* totals, int32_t* status,
+                                                    int32_t* status_mirror, int32_t st0,
+                                                    uint64_t epoch, bool abort, int64_t n_mine,
+                                                    int32_t ticket) {
+  __threadfence();
+  unsigned long long* done = reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_DONE);
+  const unsigned long long counts = (ticket ? 2ull : 1ull) * gridDim.x;
+  if (atomicAdd(done, 1ull) != counts - 1) return;
+  __threadfence();
+  const int32_t acc = (int32_t)atomicExch(
+      reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS), 0ull);
+  const int32_t out = acc | (st0 & TPR_STATUS_BARRIER_TIMEOUT);
+  *status = out;
+  if (status_mirror) {
+    *reinterpret_cast<volatile int32_t*>(status_mirror) = out;
+    if (ticket) {
+      __threadfence_system();  // the status word lands first
+      *reinterpret_cast<volatile int32_t*>(status_mirror + 1) = ticket;
+    }
+  }
+  totals[TPR_TOTALS_K31_EPOCH] = (int64_t)(epoch + 1);
+  *done = 0ull;
+  if (!abort) totals[0] = n_mine;
+}
+
 constexpr int kK31Threads = 64;
 constexpr int64_t kK31DynamicUnits = 512;  // auto schedule: dynamic from here up
 static_assert(kK31MaxPages <= kK31Threads, "one deciding thread per page");
@@ -680,13 +712,17 @@ __global__ void __launch_bounds__(kK31Threads)
       it.start(i0);
       bulk_pipeline<true>(it, stages, &tm);  // waits for its last store
     }
-    if (tracing && tid == 0) {
-      stamp(2);
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      rp.trace[blockIdx.x * 8 + 5] = smid;
-      rp.trace[blockIdx.x * 8 + 6] = (uint64_t)(i1 - i0);
-      rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
+    if (tid == 0) {
+      if (tracing) {
+        stamp(2);
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        rp.trace[blockIdx.x * 8 + 5] = smid;
+        rp.trace[blockIdx.x * 8 + 6] = (uint64_t)(i1 - i0);
+        rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
+      }
+      if (rp.ticket)  // with a ticket, the copies count too: it is published after them
+        k31_item_share_done(totals, status, status_mirror, st0, s_epoch, abort, n_mine, rp.ticket);
     }
     return;
   }
@@ -719,20 +755,7 @@ __global__ void __launch_bounds__(kK31Threads)
     const int all_bits = abort ? 0 : (s_bits[0] | s_bits[1]);
     if (all_bits) atomicOr(reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS),
                            (unsigned long long)all_bits);
-    // the last CTA publishes the status word and resets the scratch words
-    __threadfence();
-    unsigned long long* done = reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_DONE);
-    if (atomicAdd(done, 1ull) == gridDim.x - 1) {
-      __threadfence();
-      const int32_t acc = (int32_t)atomicExch(
-          reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_STATUS), 0ull);
-      const int32_t out = acc | (st0 & TPR_STATUS_BARRIER_TIMEOUT);
-      *status = out;
-      if (status_mirror) *reinterpret_cast<volatile int32_t*>(status_mirror) = out;
-      totals[TPR_TOTALS_K31_EPOCH] = (int64_t)(epoch + 1);
-      *done = 0ull;
-      if (!abort) totals[0] = n_mine;
-    }
+    k31_item_share_done(totals, status, status_mirror, st0, epoch, abort, n_mine, rp.ticket);
     if (tracing) stamp(3);
   }
 }
@@ -749,6 +772,21 @@ __global__ void __launch_bounds__(kK31Threads)
 // tracked by the host per d_totals): CTA 0 resets the other parity's words,
 // which only the previous launch on the stream used.
 // ---------------------------------------------------------------------------
+// The dynamic kernel's completion: the last CTA to finish its copies writes
+// the status (already final: every CTA counted itself decided, bits first,
+// before any copy) and then the caller's ticket into the pinned mirror.
+__device__ __forceinline__ void k31_dyn_done(unsigned long long* words, int par, int64_t grid,
+                                             int32_t* status_mirror, int32_t st0, int32_t ticket) {
+  if (!ticket || !status_mirror) return;
+  __threadfence();
+  if (atomicAdd(&words[6 + par], 1ull) != (unsigned long long)grid - 1) return;
+  __threadfence();
+  const int32_t out = (int32_t)atomicOr(&words[4 + par], 0ull) | (st0 & TPR_STATUS_BARRIER_TIMEOUT);
+  *reinterpret_cast<volatile int32_t*>(status_mirror) = out;
+  __threadfence_system();  // the status word lands first
+  *reinterpret_cast<volatile int32_t*>(status_mirror + 1) = ticket;
+}
+
 __global__ void __launch_bounds__(kK31Threads)
     tpr_k31_switch_dyn(const __grid_constant__ K31Params rp, tpr_kv_geometry_t geo,
                        KvCopyParams p, const __grid_constant__ KvClusterParams cl,
@@ -766,7 +804,7 @@ __global__ void __launch_bounds__(kK31Threads)
   if (tracing && tid == 0) stamp(0);
   const int par = rp.parity & 1;
   unsigned long long* words = reinterpret_cast<unsigned long long*>(totals + TPR_TOTALS_K31_PAR);
-  if (blockIdx.x == 0 && tid < 3) words[2 * tid + (par ^ 1)] = 0ull;
+  if (blockIdx.x == 0 && tid < 4) words[2 * tid + (par ^ 1)] = 0ull;
   const int n = rp.n, B = geo.block_tokens;
   const int32_t st0 = __ldcg(status);
   const bool abort = (st0 & TPR_STATUS_BARRIER_TIMEOUT) != 0;
@@ -809,7 +847,10 @@ __global__ void __launch_bounds__(kK31Threads)
     if (status_mirror) *reinterpret_cast<volatile int32_t*>(status_mirror) = out;
     if (!abort) totals[0] = n_mine;
   }
-  if (abort) return;
+  if (abort) {
+    k31_dyn_done(words, par, grid, status_mirror, st0, rp.ticket);
+    return;
+  }
   // every page decided (and its bookkeeping written) before any copy reads
   // a work item
   while (true) {
@@ -836,6 +877,7 @@ __global__ void __launch_bounds__(kK31Threads)
     stamp(3);
     rp.trace[blockIdx.x * 8 + 7] = (uint64_t)gridDim.x;
   }
+  k31_dyn_done(words, par, grid, status_mirror, st0, rp.ticket);
 }
 
 // Ring shape per kernel (shared memory = stages x piece per CTA). Measured on
@@ -976,7 +1018,8 @@ static std::unordered_map<const int64_t*, uint32_t> g_par;
 cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
-                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work, int variant) {
+                       cudaStream_t st, int n_gpus, bool partial, int32_t* d_work, int variant,
+                       int32_t ticket) {
   if (n < 1 || n > kK31Xfers || n_units < 1 || !d_work) return cudaErrorNotSupported;
   const BulkConfig& c = k31_config();
   KvTensorMaps tm;
@@ -1008,6 +1051,7 @@ cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
   rp.trace = reinterpret_cast<uint64_t*>(k31_trace_buffer());
   rp.parity = 0;
   rp.batch = 0;
+  rp.ticket = ticket;
   if (dyn) {
     // one item per claim (cfg1 52.2 us against 54.0 with 2 or 4 per claim)
     rp.batch = items > (int64_t)grid ? 1 : 0;  // 0: one static item each covers it

@@ -9,6 +9,8 @@
 #include <utility>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "tpr.h"
 #include "tpr_internal.h"
 
@@ -337,10 +339,17 @@ int tpr_kv_switch_layouts(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* 
     return tpr::set_error(TPR_ECAPACITY, "device scratch too small: %lld transfers, %lld units",
                           (long long)n, (long long)units);
   t->records_async = 0;
+  const bool want_ticket = t->ticket != 0;  // in: the caller will spin on a ticket
+  t->ticket = 0;
+  if (t->start_event) {  // the switch's device interval starts at its first launch
+    cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(t->start_event),
+                                    static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return tpr::set_error(TPR_ECUDA, "start event: %s", cudaGetErrorString(e));
+  }
   if (n == 0 && !t->h_status) return TPR_OK;
   rc = tpr::kv_switch_impl(geo, cl, t->records, t->d_xfers, (int32_t)n, -1, t->d_meta,
                            t->d_totals, units, t->d_work, t->d_status, stream, t->h_status,
-                           t->k1_events, &t->records_async);
+                           t->k1_events, &t->records_async, want_ticket ? &t->ticket : nullptr);
   if (rc != TPR_OK) return rc;
   if (n == 0) return TPR_OK;
   for (int32_t s = 0; s < cl->n_gpus; ++s) {  // the host ring counters

@@ -65,6 +65,7 @@ struct K31Params {
   int32_t filter;
   int32_t parity;   // dynamic kernel: which scratch words of d_totals this launch uses
   int32_t batch;    // dynamic kernel: items per claim (0 = static shares)
+  int32_t ticket;   // != 0: written to status_mirror[1] once every copy and write is done
   uint64_t* trace;  // nullable: per-CTA globaltimer stamps (knob "k31_trace")
 };
 int64_t k31_trace_buffer();
@@ -92,11 +93,15 @@ bool pdl_for(int64_t n_units);
 // tpr_kv_switch with an optional pinned host mirror of the status word, kept
 // current on the stream (fused K3 store, else a 4-byte D2H after K1)
 // k1_events (nullable): cudaEvent_t pair recorded on the stream around K1.
+// ticket (nullable, out): when the switch ran as K31 with a status mirror, a
+// nonzero number the kernel writes to status_mirror[1] once every copy and
+// table write is done (the caller may spin on it); 0 otherwise.
 int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
                    const int32_t* h_xfers, int32_t* d_xfers, int32_t n_xfers, int32_t filter_src,
                    int64_t* d_meta, int64_t* d_totals, int64_t n_units, int32_t* d_work,
                    int32_t* d_status, void* stream, int32_t* status_mirror,
-                   void* const* k1_events = nullptr, int32_t* records_async = nullptr);
+                   void* const* k1_events = nullptr, int32_t* records_async = nullptr,
+                   int32_t* ticket = nullptr);
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute when `pdl`.
 template <typename... KArgs, typename... Args>
@@ -139,7 +144,7 @@ cudaError_t launch_k31(const tpr_kv_geometry_t& geo, const KvCopyParams& p,
                        const KvClusterParams& cl, const int32_t* h_rec, int32_t n, int32_t filter,
                        int64_t n_units, int64_t* totals, int32_t* status, int32_t* status_mirror,
                        cudaStream_t st, int n_gpus, bool partial, int32_t* d_work,
-                       int variant);
+                       int variant, int32_t ticket = 0);
 cudaError_t launch_k2_bulk(const tpr_copy_seg_t* segs, const int64_t* prefix, int32_t n_segs,
                            int64_t n_items, int64_t chunk, int64_t* claim, cudaStream_t st);
 cudaError_t launch_kv_fill(const KvCopyParams& p, const KvClusterParams& cl, const int4* work,

@@ -184,8 +184,10 @@ class PagedKvCluster:
         self.status = torch.zeros(1, dtype=torch.int32, device=self.home)
         # pinned host mirror of the status word, kept current by the one-call
         # switch on its stream (no separate read-back for a synchronous caller)
-        self.status_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        # [status word, completion ticket] (tpr_switch_tables_t.h_status / .ticket)
+        self.status_host = torch.zeros(2, dtype=torch.int32, pin_memory=True)
         self.status_mirrored = False  # the last switch_layouts refreshed status_host
+        self.last_ticket = 0  # nonzero: the last switch_layouts' kernel writes it to status_host[1]
         self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
                                         H, self.max_blocks, self.max_requests, self.n_units)
         # the C view of the cluster; its ring counters (monotonic head/tail per
@@ -609,7 +611,7 @@ class PagedKvCluster:
     def switch_layouts(self, old_layouts, new_layouts, stream: torch.cuda.Stream | None = None,
                        validate: bool = True, handshake_ms: float = 0.0,
                        planner: str = "repartition", k1_events: tuple | None = None,
-                       release=()):
+                       release=(), start_event: int | None = None, want_ticket: bool = False):
         """``plan_repartition(old, new)`` + ``migrate(plan)`` in one native call
         (``tpr_kv_switch_layouts``): plan, records, capacity check, K3 + K1 and
         the placement update. Returns (MigrationPlan, MigrationStats) equal to
@@ -622,9 +624,16 @@ class PagedKvCluster:
         ``k1_events``: (start, end) CUDA events recorded around K1.
         ``release``: resident request ids (in neither layout list) whose pages
         the same native call frees -- the destination's KV-capacity evictions
-        (engine.py:630-645); their records follow the plan's."""
+        (engine.py:630-645); their records follow the plan's.
+        ``start_event``: a CUDA event handle recorded on ``stream`` right
+        before the switch's first launch (on every path).
+        ``want_ticket``: ask the one-launch kernel for a completion ticket
+        (``last_ticket``, written to ``status_host[1]`` when the switch is
+        done) for a caller that spins on it; it delays the kernel's exit by
+        the ticket's host write, so asynchronous callers leave it off."""
         stream = stream or self._default_stream
         self.status_mirrored = False
+        self.last_ticket = 0
         if planner not in ("repartition", "head_transfers"):
             raise MigrationError(f"unknown planner {planner!r}")
         heads = planner == "head_transfers"
@@ -639,6 +648,8 @@ class PagedKvCluster:
                 if rid in carried:
                     raise MigrationError(f"request {rid} is both released and carried")
         if self._gpu_lut is None or not self._single_device:
+            if start_event:
+                _native.call("tpr_event_record", start_event, stream.cuda_stream)
             return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
                                         heads, release=release)
         blob = pack_layouts(old_layouts, new_layouts, release)
@@ -650,6 +661,9 @@ class PagedKvCluster:
             t.k1_events[0], t.k1_events[1] = k1_events[0].cuda_event, k1_events[1].cuda_event
         elif t.k1_events[0]:
             t.k1_events[0] = t.k1_events[1] = None
+        if start_event != t.start_event:
+            t.start_event = start_event
+        t.ticket = 1 if want_ticket else 0
         lib = _native.load()
         addr = blob.buffer_info()[0]
         for _ in range(3):  # grow-and-retry when a buffer is too small
@@ -662,17 +676,21 @@ class PagedKvCluster:
                                            len(blob), ctypes.byref(t), stream.cuda_stream)
             if rc != _native.TPR_ECAPACITY:
                 break
+            t.ticket = 1 if want_ticket else 0
             if t.n_plan > len(rows):
                 self._swt_plan = np.empty((max(t.n_plan, 2 * len(rows)), 6), np.int64)
             if t.total_units + 1 > t.work_cap:
                 self._work.get((t.total_units + 1) * 4, stream)
-        if rc == _native.TPR_ENOTFOUND:
+        if rc == _native.TPR_ENOTFOUND:  # nothing was enqueued
+            if start_event:
+                _native.call("tpr_event_record", start_event, stream.cuda_stream)
             return self._switch_general(old_layouts, new_layouts, stream, validate, handshake_ms,
                                         heads, k1_events, release)
         if rc != 0:
             raise MigrationError(lib.tpr_last_error().decode(errors="replace"))
         n = t.n_plan
         self.status_mirrored = True
+        self.last_ticket = t.ticket
         plan = MigrationPlan.from_rows(self._swt_plan[:n].copy(), handshake_ms)
         if release:
             self._forget(release)

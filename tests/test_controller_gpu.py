@@ -245,3 +245,68 @@ def test_switch_evicts_inside_the_native_call():
     # without a byte budget the same call decides against free pages
     ex.switch(kept_new, kept_old, arrivals=[Arrival(2, 128, FEASIBLE, 0.0)])
     assert kv.placement() == M.layout_placement(kept_old)
+
+
+def test_device_ms_is_read_lazily_and_survives_event_reuse():
+    # a synchronous switch does not pay cudaEventElapsedTime; its result reads
+    # the device time on first access, also after the executor has cycled its
+    # event ring past it (the pair is read before it is re-recorded)
+    import torch
+    from paper_2605_05467_b200 import controller
+    gpus = (0, 1)
+    reqs = [(0, 300)]
+    a = workloads.round_robin(workloads.tp_groups(gpus, 1), reqs, 8)
+    b = workloads.round_robin(workloads.tp_groups(gpus, 2), reqs, 8)
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=256, max_requests=1, max_blocks=32)
+    kv.admit(a, seed=1)
+    ex = ReconfigurationExecutor(kv)
+    first = ex.switch(a, b)
+    assert first._device_ms is None and first.host_ms > 0
+    cur = b
+    for i in range(controller._SYNC_EVENT_PAIRS + 6):
+        nxt = a if cur is b else b
+        r = ex.switch(cur, nxt)
+        cur = nxt
+        assert r.device_ms > 0  # read right away
+    assert first._device_ms is not None and 0 < first.device_ms < 1e3
+    nosync = ex.switch(cur, a if cur is b else b, sync=False)
+    assert nosync.device_ms == 0.0
+    torch.cuda.synchronize()
+
+
+def test_sync_small_switch_waits_on_the_kernel_ticket():
+    # a synchronous one-launch switch returns when K31's ticket reaches pinned
+    # memory (written after every copy and table write); asynchronous and
+    # multi-kernel switches carry no ticket
+    from paper_2605_05467_b200 import _native
+    gpus = tuple(range(4))
+    reqs = [(i, 20 + 37 * i) for i in range(5)]
+    lay = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2, 4)}
+    kv = PagedKvCluster(KV, gpus, units_per_gpu=512, max_requests=8, max_blocks=16, fragmented=True)
+    kv.admit(lay[1], seed=4)
+    ex = ReconfigurationExecutor(kv)
+    seen = set()
+    for k31, (a, b) in zip((1, 2, 3, 1), ((1, 2), (2, 4), (4, 1), (1, 4))):
+        saved = _native.get_tuning("k31")
+        _native.set_tuning("k31", k31)
+        try:
+            before = kv.snapshot()
+            plan = M.plan_repartition(lay[a], lay[b], KV.kv_bytes_per_token_per_head)
+            rec = kv.records(plan, validate=False)
+            res = ex.switch(lay[a], lay[b])
+        finally:
+            _native.set_tuning("k31", saved)
+        t = kv.last_ticket
+        assert t != 0 and t not in seen and int(kv.status_host[1]) == t and res.status == 0
+        seen.add(t)
+        diff = check.compare(kv.snapshot(), check.expected_after(kv, before, rec))
+        assert not any(diff.values()), diff
+        assert res.device_ms > 0
+    r = ex.switch(lay[4], lay[2], sync=False)
+    assert kv.last_ticket == 0 and r.kv.units > 0
+    _native.set_tuning("k31", 0)
+    try:
+        r = ex.switch(lay[2], lay[1])  # fused K3 + K1: the end event, no ticket
+        assert kv.last_ticket == 0 and r.status == 0
+    finally:
+        _native.set_tuning("k31", 1)

@@ -127,9 +127,9 @@ def test_plan_capacity_is_reported():
 
 
 def test_struct_size_matches_header():
-    # tpr_switch_tables_t (include/tpr.h), 488 bytes: 27 pointer/int64 fields, four
+    # tpr_switch_tables_t (include/tpr.h), 496 bytes: 28 pointer/int64 fields, four
     # int32 and two [TPR_MAX_GPUS] int64 arrays
-    assert ctypes.sizeof(_native.SwitchTablesC) == 27 * 8 + 4 * 4 + 2 * 8 * _native.TPR_MAX_GPUS
+    assert ctypes.sizeof(_native.SwitchTablesC) == 28 * 8 + 4 * 4 + 2 * 8 * _native.TPR_MAX_GPUS
 
 
 def test_packed_layout_is_cached_and_exact():
