@@ -923,13 +923,7 @@ static const BulkConfig& k1_small_config() {
   static BulkConfig c = parse_bulk("TPR_BULK_K1_SMALL", BulkConfig{3, 32768});
   return c;
 }
-static int64_t k1_small_items() {
-  static const int64_t v = [] {
-    const char* e = getenv("TPR_K1_SMALL_ITEMS_PER_SM");
-    return (int64_t)(e ? atoll(e) : 24) * sm_count();
-  }();
-  return v;
-}
+static int64_t k1_small_items() { return (int64_t)24 * sm_count(); }  // 24 items per SM
 static const BulkConfig& k2_config() {
   static BulkConfig c = parse_bulk("TPR_BULK_K2", BulkConfig{3, 32768});
   return c;

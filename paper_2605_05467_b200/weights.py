@@ -33,7 +33,6 @@ switch is then views only (the paper's zero-overhead weight switching).
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -44,7 +43,7 @@ from . import _native
 from .geometry import MAX_TP, ModelGeometry
 from .migration import MigrationError
 
-CHUNK_BYTES = int(os.environ.get("TPR_K2_CHUNK", 32 * 1024))  # K2 work-item size (bytes)
+CHUNK_BYTES = 32 * 1024  # K2 work-item size (bytes): one ring stage
 
 
 @dataclass
