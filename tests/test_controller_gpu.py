@@ -200,11 +200,21 @@ def test_random_switch_walk_kv_and_weights(seed):
         cur = new
 
 
-def test_switch_evicts_inside_the_native_call():
+@pytest.fixture(params=[0, 2, 3], ids=["k3_then_k1", "k31_dynamic", "k31_item_share"])
+def k31_mode(request):
+    from paper_2605_05467_b200 import _native
+    saved = _native.get_tuning("k31")
+    _native.set_tuning("k31", request.param)
+    yield request.param
+    _native.set_tuning("k31", saved)
+
+
+def test_switch_evicts_inside_the_native_call(k31_mode):
     # engine.py:600-601 + 623-645 executed: the destination group's byte budget
     # keeps the feasible arrival and the oldest best-effort one; the other
     # best-effort arrival is evicted, and its pages are freed by the same
     # native call (release records after the plan's), bit-exact vs the oracle
+    # -- through K3 + K1 and through both K31 schedules
     from oracle import check
     from paper_2605_05467_b200.placement import KvBudget
     gpus = (0, 1, 2, 3)

@@ -152,7 +152,7 @@ def test_large_plan_takes_split_k3_and_matches_oracle():
     assert _native.kv_switch_launches(stats.units) == 3
 
 
-@pytest.mark.parametrize("n_reqs", [1, 31, 512, 513, 900])
+@pytest.mark.parametrize("n_reqs", [1, 31, 96, 97, 512, 513, 900])
 def test_fused_k3_record_counts_bit_exact(n_reqs):
     # fused K3 (<= k3_fuse_units pages) keeps up to 512 records in shared
     # memory and reads larger plans from global: both sides of the boundary,
@@ -564,3 +564,29 @@ def test_host_record_offsets_equal_the_device_scan():
     _native.call("tpr_record_offsets", rec.ctypes.data, n, -1, TINY.block_tokens,
                  host.ctypes.data, None)
     assert np.array_equal(dev, host)
+
+
+@pytest.mark.parametrize("pages", [504, 508, 512, 516])
+def test_k31_schedule_boundary_bit_exact(pages):
+    # the auto K31 schedule switches from item shares to the dynamic one at
+    # 512 pages: plans on both sides, ragged contexts, the one-call path
+    from paper_2605_05467_b200 import _native
+    assert _native.get_tuning("k31") == 1
+    gpus = (0, 1)
+    # TP1 -> TP2 moves 4 heads of every request: pages = 4 * sum(blocks)
+    blocks = pages // 4
+    ctxs = [16 * 9] * (blocks // 9) + ([16 * (blocks % 9) - 3] if blocks % 9 else [])
+    reqs = [(i, c) for i, c in enumerate(ctxs)]
+    lay = {tp: workloads.round_robin(workloads.tp_groups(gpus, tp), reqs, 8) for tp in (1, 2)}
+    c = make(TINY, gpus, units=16 * pages, reqs=len(reqs), blocks=16, seed=pages)
+    c.admit(lay[1], seed=6)
+    for a, b in ((1, 2), (2, 1)):
+        before = c.snapshot()
+        plan = M.plan_repartition(lay[a], lay[b], TINY.kv_bytes_per_token_per_head)
+        rec = c.records(plan, validate=False)
+        got, st = c.switch_layouts(lay[a], lay[b])
+        assert st.units == pages and _native.kv_switch_launches(st.units, st.transfers) == 1
+        want = check.expected_after(c, before, rec)
+        assert not any(check.compare(c.snapshot(), want).values())
+    v = c.verify(seed=6)
+    assert v["placement_errors"] == 0 and v["word_mismatches"] == 0
