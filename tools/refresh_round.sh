@@ -1,6 +1,6 @@
 # Re-measure everything the docs cite (one B200). Outputs under gpurun_out/.
 #   bash tools/refresh_round.sh [tag]     (default tag: final); then tools/refresh_extra.sh [tag]
-#   and, back in the container, python tools/apply_refresh.py <tag>
+#   then copy the outputs the docs cite into profiles/rNN/
 T=${1:-final}
 O=gpurun_out
 set -x
