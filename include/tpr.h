@@ -171,7 +171,7 @@ int tpr_get_copy_engine(void);
  * of another GPU take the vector engine, and no tensor map is ever encoded
  * over a peer mapping.
  * Read once from the environment (TMA engine ring shapes, "<stages>x<bytes>"):
- *   TPR_BULK_K1 [6x32768], TPR_BULK_K2 [3x32768], TPR_BULK_K1_SMALL [3x32768]
+ *   TPR_BULK_K1 [3x65536], TPR_BULK_K2 [3x32768], TPR_BULK_K1_SMALL [3x32768]
  *   for K1s of at most 24 items per SM, TPR_BULK_K31 [3x32768]. */
 int tpr_set_tuning(const char* key, int64_t value);
 int64_t tpr_get_tuning(const char* key);

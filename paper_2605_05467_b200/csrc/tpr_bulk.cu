@@ -881,9 +881,9 @@ __global__ void __launch_bounds__(kK31Threads)
 }
 
 // Ring shape per kernel (shared memory = stages x piece per CTA). Measured on
-// B200 (profiles/README.md): K1 streams whole 32 KiB page chunks and is
-// fastest with one CTA per SM and 32 KiB pieces (6 x 32 KiB = 192 KiB, at the
-// measured copy peak); K2's row-parallel slices are 1-7 KiB rows, so it wants
+// B200 (profiles/README.md): K1 streams 32 KiB page items with one CTA per SM
+// and a 192 KiB ring; 3 stages of 64 KiB (two items per stage) beat 6 x 32 KiB
+// by 0.3% on cfg2 and 0.4% on the 70B switch, even on trace contexts; K2's row-parallel slices are 1-7 KiB rows, so it wants
 // more issuing CTAs per SM: 3 x 32 KiB = 96 KiB, 2 CTAs/SM (with dynamic
 // claims; 4 x 16 KiB / 3 CTAs/SM is within 1%, >= 128 KiB rings lose 25-45%,
 // profiles/README.md). Override with TPR_BULK_K1 / TPR_BULK_K2 =
@@ -912,7 +912,7 @@ static BulkConfig parse_bulk(const char* env, BulkConfig c) {
 }
 
 static const BulkConfig& k1_config() {
-  static BulkConfig c = parse_bulk("TPR_BULK_K1", BulkConfig{6, 32768});
+  static BulkConfig c = parse_bulk("TPR_BULK_K1", BulkConfig{3, 65536});
   return c;
 }
 // Short K1s (up to 24 items per SM, ~110 MiB) finish sooner with more,
