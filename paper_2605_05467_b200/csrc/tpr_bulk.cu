@@ -588,10 +588,11 @@ __global__ void __launch_bounds__(32)
 // by the last CTA), so they never need clearing (a freshly allocated d_work
 // must be zeroed once). The status word reports this
 // call only: CTAs OR their bits into totals[TPR_TOTALS_K31_STATUS]; the last
-// CTA to finish its bookkeeping (counter totals[TPR_TOTALS_K31_DONE])
-// publishes them to *status (+ the pinned mirror) and resets both scratch
-// words. A device-barrier timeout already in *status aborts the call (no
-// copy, no write; the bit stays).
+// count of the completion counter totals[TPR_TOTALS_K31_DONE]
+// (k31_item_share_done) publishes them to *status (+ the pinned mirror and
+// the caller's ticket) and resets both scratch words. A device-barrier
+// timeout already in *status aborts the call (no copy, no write; the bit
+// stays).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int64_t k31_cta_of(int64_t item, int64_t n_items, int64_t grid) {
   return ((item + 1) * grid - 1) / n_items;  // the CTA whose share holds `item`
