@@ -314,7 +314,8 @@ typedef struct tpr_switch_tables {
                               returns (keep them until the stream passes), 0 when
                               the launch took them (K31: kernel parameters)   */
   int32_t ticket;          /* in: nonzero asks for a completion ticket;
-                              out: nonzero when the switch ran as K31 with h_status:
+                              out: nonzero when the switch ran as K31 with h_status
+                              and at most 2048 pages:
                               the kernel writes it to h_status[1] (h_status must
                               then hold 2 int32) after the status word, once every
                               copy and table write of the switch is done; a

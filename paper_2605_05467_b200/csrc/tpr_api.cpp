@@ -410,7 +410,9 @@ int kv_switch_impl(const tpr_kv_geometry_t* geo, const tpr_kv_cluster_t* cl,
     if (timed && (e = cudaEventRecord(static_cast<cudaEvent_t>(k1_events[0]), st)) != cudaSuccess)
       return cuda_fail(e, "tpr_kv_switch K31 start event");
     int32_t tk = 0;
-    if (ticket && status_mirror) {  // nonzero, distinct from the last few calls
+    // a ticket is for a host that spins on it: only switches short enough to
+    // spin through (<= 2048 pages, ~0.2 ms); longer ones wait on the stream
+    if (ticket && status_mirror && n_units <= 2048) {  // nonzero, distinct from the last few calls
       static std::atomic<int32_t> g_ticket{0};
       tk = g_ticket.fetch_add(1) % 0x3fffffff + 1;
     }
