@@ -113,3 +113,15 @@ def test_copy_prepare_rejects_bad_chunk():
     n = ctypes.c_int64()
     with pytest.raises(_native.NativeError, match="multiple of 16"):
         _native.call("tpr_copy_prepare", None, 0, 100, prefix.ctypes.data, ctypes.byref(n))
+
+
+def test_small_switch_entries_check_arguments_without_a_gpu():
+    # argument checks that return before any CUDA call: a null event, bad
+    # record-offset arguments; and tpr_record_offsets on an empty plan
+    import ctypes
+    lib = _native.load()
+    assert lib.tpr_event_record(None, None) == -1 and b"null event" in lib.tpr_last_error()
+    assert lib.tpr_record_offsets(None, 3, -1, 16, None, None) == -1
+    assert lib.tpr_record_offsets(None, 0, -1, 0, None, None) == -1  # block_tokens < 1
+    total = ctypes.c_int64(7)
+    assert lib.tpr_record_offsets(None, 0, -1, 16, None, ctypes.byref(total)) == 0 and total.value == 0
