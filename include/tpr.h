@@ -40,7 +40,10 @@
 extern "C" {
 #endif
 
-#define TPR_ABI_VERSION 1
+/* ABI 2 (round 2): tpr_switch_tables_t gained ring_head_io / ring_tail_io /
+ * start_event and the ticket field; TPR_TOTALS_LEN grew by the small-switch
+ * kernel's words; tpr_record_offsets and tpr_event_record are new. */
+#define TPR_ABI_VERSION 2
 #define TPR_MAX_GPUS 16
 
 enum tpr_status {

@@ -13,7 +13,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libtpr.so"
 
-TPR_ABI_VERSION = 1
+TPR_ABI_VERSION = 2
 TPR_MAX_GPUS = 16
 TPR_XFER_FIELDS = 6
 TPR_META_FIELDS = 4
