@@ -8,7 +8,9 @@ output/2, i.e. mid-decode). Llama-3.1-8B KV geometry.
 On one B200 the 8 slots are logical (all pools in one HBM). So each switch is
 bounded by HBM: t_roof = 2 * bytes / measured copy peak. Every point reports:
 
-* the measured switch latency (device events and host wall, synchronous);
+* the measured switch latency (device events and host wall, synchronous), the
+  device work alone (stream held while the host enqueues), and the public
+  synchronous call ``ReconfigurationExecutor.switch`` end to end;
 * GB/s and the fraction of that roofline;
 * the reference cost model's prediction for the same plan (default
   CostModelParams, migration.py:77-98);
@@ -36,6 +38,7 @@ def main():
     import torch
 
     from paper_2605_05467_b200 import migration as M, workloads
+    from paper_2605_05467_b200.controller import ReconfigurationExecutor
     from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
     from paper_2605_05467_b200.kvcache import PagedKvCluster
 
@@ -97,6 +100,7 @@ def main():
             max_ctx, max_n = max(max_ctx, max(ctxs)), max(max_n, n)
         cluster = PagedKvCluster(kv, gpus, units_per_gpu=units + 256, max_requests=max_n,
                                  max_blocks=kv.blocks(max_ctx), fragmented=True, seed=0)
+        ex = ReconfigurationExecutor(cluster)
         # touch every pool page once: first writes to fresh cudaMalloc memory
         # are slower, and which points would pay for them depends on the order
         cluster.fill_garbage(seed=1)
@@ -135,6 +139,11 @@ def main():
                 e1.record(stream)
                 e1.synchronize()
                 exec_ms.append(e0.elapsed_time(e1))
+            e2e_ms = []  # the public synchronous call (ReconfigurationExecutor.switch)
+            for r in range(2 * reps):  # fwd/back pairs: ends in layout A
+                res = ex.switch(*((la, lb) if r % 2 == 0 else (lb, la)), validate=False)
+                if r % 2 == 0:
+                    e2e_ms.append(res.host_ms)
             k1_ms = []
             for r in range(2 * args.k1_reps):  # fwd/back pairs: ends in layout A
                 k0, k1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
@@ -159,6 +168,9 @@ def main():
                 # the planner alone on the host; the switch's device work alone
                 "plan_host_ms": float(np.median(plan_ms)), "exec_device_ms": x,
                 "exec_hbm_frac": (2 * nbytes / (peak * 1e9)) / (x * 1e-3) if x > 0 else None,
+                # end to end through the public synchronous call (host wall time)
+                "e2e_ms": float(np.median(e2e_ms)),
+                "e2e_hbm_frac": (2 * nbytes / (peak * 1e9)) / (float(np.median(e2e_ms)) * 1e-3),
                 "k1_ms": float(np.median(k1_ms)) if k1_ms else None,
                 "k1_hbm_frac": (2 * nbytes / (peak * 1e9)) / (float(np.median(k1_ms)) * 1e-3)
                 if k1_ms else None,
