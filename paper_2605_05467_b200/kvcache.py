@@ -187,6 +187,7 @@ class PagedKvCluster:
         # [status word, completion ticket] (tpr_switch_tables_t.h_status / .ticket)
         self.status_host = torch.zeros(2, dtype=torch.int32, pin_memory=True)
         self.status_mirrored = False  # the last switch_layouts refreshed status_host
+        self._swt = self._swt_lut = None  # the cached tpr_switch_tables_t (_switch_tables)
         self.last_ticket = 0  # nonzero: the last switch_layouts' kernel writes it to status_host[1]
         self._geo = _native.KvGeometryC(kv.layers, kv.head_dim, kv.dtype_bytes, kv.block_tokens,
                                         H, self.max_blocks, self.max_requests, self.n_units)
@@ -567,8 +568,8 @@ class PagedKvCluster:
     def _switch_tables(self, validate: bool) -> _native.SwitchTablesC:
         """The cached tpr_switch_tables_t of this cluster (lookup tables, host
         outputs, device scratch); pointers refreshed when a table grows."""
-        t = self.__dict__.get("_swt")
-        if t is None or self.__dict__.get("_swt_lut") is not self._req_lut:
+        t = self._swt
+        if t is None or self._swt_lut is not self._req_lut:
             t = self._swt = _native.SwitchTablesC()
             self._swt_lut = self._req_lut
             t.gpu_lut = self._gpu_lut.ctypes.data

@@ -361,13 +361,15 @@ def pack_layouts(old_layouts, new_layouts, release=()):
     """Old and new layouts as one int64 array for ``tpr_switch_prepare``
     (include/tpr.h): n_old, n_new, then every layout's ``packed()``, then --
     when ``release`` is not empty -- the ids of requests freed by the switch.
-    Blobs of immutable layouts are remembered by identity."""
+    Blobs of immutable layouts are remembered (looked up by equality)."""
     if isinstance(new_layouts, KvLayout):
         new_layouts = [new_layouts]
     if not release:
         key = (*old_layouts, None, *new_layouts)
         for k, blob in _PACKED:
-            if len(k) == len(key) and all(a is b for a, b in zip(k, key)):
+            # tuple equality: identical layouts short-circuit in C; equal ones
+            # (frozen dataclasses) pack to the same blob anyway
+            if k == key:
                 return blob
         if all(isinstance(lay.requests, tuple) for lay in key if lay is not None):
             blob = _pack(old_layouts, new_layouts, ())
