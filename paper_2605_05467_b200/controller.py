@@ -124,9 +124,11 @@ class ReconfigurationExecutor:
 
     def _finish(self, res: SwitchResult, main: torch.cuda.Stream, t0: float,
                 slot: int | None = None) -> SwitchResult:
-        """Synchronous tail: the step's result (K3's status word) read back,
-        then the host waits for the end event. After the one-call switch the
-        word is already mirrored into pinned memory on the stream."""
+        """Synchronous tail: the end event is recorded, the host waits -- on the
+        one-launch kernel's completion ticket in pinned memory when it has one
+        (no weight copy followed), else on the end event -- and reads the
+        status word, which the one-call switch mirrors into pinned memory on
+        the stream (other paths: a 4-byte D2H here)."""
         mirrored = self.kv.status_mirrored
         if not mirrored:
             _native.call("tpr_memcpy_d2h", self._status_host.data_ptr(), self.kv.status.data_ptr(),
