@@ -244,3 +244,34 @@ def test_random_reshard_walk(seed):
         torch.cuda.synchronize()
         check_against_oracle(store, pieces, groups)
         assert store.verify() == 0, step
+
+
+def _real_shape_layer(base):
+    """One decoder layer with the model's real matrix shapes (q/k/v, o,
+    gate/up, down), vocab cut to 1024 so the host oracle stays small."""
+    import dataclasses
+    return dataclasses.replace(base, name=f"{base.name} (1 layer, vocab 1024)", layers=1, vocab=1024,
+                               matrices=())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("base,tp_old,tp_new", [
+    ("8b", 8, 1), ("8b", 1, 2), ("8b", 2, 8), ("8b", 4, 2), ("8b", 8, 4), ("8b", 2, 4),
+    ("70b", 8, 1), ("70b", 8, 4), ("70b", 4, 8), ("70b", 4, 2)])
+def test_real_matrix_shapes_bit_exact(base, tp_old, tp_new):
+    # the Llama-3.1-8B / 70B matrix shapes (row-parallel rows of 1-7 KiB,
+    # 14336 / 28672-wide gate/up/down) through K2, against the narrow/concat
+    # oracle, with the arena window of the larger shard
+    model = _real_shape_layer(geometry.LLAMA_3_1_8B if base == "8b" else geometry.LLAMA_3_1_70B)
+    gpus = tuple(range(8))
+    store = ShardedWeightStore(model, gpus, max_slices=max(8 // tp_old, 8 // tp_new))
+    store.load(workloads.tp_groups(gpus, tp_old))
+    pieces = host_pieces(store)
+    new_groups = workloads.tp_groups(gpus, tp_new)
+    stats = store.reshard(new_groups)
+    torch.cuda.synchronize()
+    check_against_oracle(store, pieces, new_groups)
+    assert store.verify() == 0
+    assert (stats.local_bytes, stats.remote_bytes) == expected_volume(
+        workloads.tp_groups(gpus, tp_old), new_groups, store.bytes_per_slice)[:2]
+    store.finish()
