@@ -485,21 +485,23 @@ def k31_variant(request):
     _native.set_tuning("k31", saved)
 
 
-@pytest.mark.parametrize("model", ["tiny", "8b"])
+@pytest.mark.parametrize("model", ["tiny", "8b", "70b"])
 @pytest.mark.parametrize("tp_old,tp_new", [(1, 2), (2, 1), (1, 8), (8, 1), (4, 8), (8, 2)])
 def test_k31_single_launch_bit_exact(model, tp_old, tp_new, k31_variant):
     # small plans (<= 96 transfers, <= k3_fuse_units pages): the whole switch is
-    # one launch (K31: bookkeeping + TMA copy per CTA-owned page), with ragged
-    # contexts (partial pages as row copies) and 8 slots, against the oracle
+    # one launch (K31), with ragged contexts (partial pages as TMA tensor boxes:
+    # 64 planes per box on 8B pages, 80 on 70B pages) and 8 slots, against the
+    # oracle
     from paper_2605_05467_b200 import _native
-    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B
-    kv = TINY if model == "tiny" else LLAMA_3_1_8B.kv
+    from paper_2605_05467_b200.geometry import LLAMA_3_1_8B, LLAMA_3_1_70B
+    kv = {"tiny": TINY, "8b": LLAMA_3_1_8B.kv, "70b": LLAMA_3_1_70B.kv}[model]
     gpus = tuple(range(8))
     rng = np.random.default_rng(tp_old * 31 + tp_new)
     reqs = [(i, int(c)) for i, c in enumerate(rng.integers(1, 300, size=6))]
     old = workloads.round_robin(workloads.tp_groups(gpus, tp_old), reqs, 8)
     new = workloads.round_robin(workloads.tp_groups(gpus, tp_new), reqs, 8)
-    c = make(kv, gpus, units=1024, reqs=8, blocks=20, fragmented=True, seed=tp_new)
+    units = 400 if model == "70b" else 1024  # 640 KiB pages: keep the host snapshots small
+    c = make(kv, gpus, units=units, reqs=8, blocks=20, fragmented=True, seed=tp_new)
     c.admit(old, seed=5)
     for a, b in ((old, new), (new, old)):
         before = c.snapshot()
