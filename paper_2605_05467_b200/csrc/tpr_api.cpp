@@ -328,17 +328,36 @@ int ptr_device(uint64_t p) {
   return dev;
 }
 
+std::atomic<uint64_t> g_range_gen{0};  // bumped when allocations go away (memos below)
+
 void forget_ranges() {
   std::lock_guard<std::mutex> lock(g_range_mu);
   g_ranges.clear();
+  g_range_gen.fetch_add(1);
 }
 
 bool all_local(const uint64_t* ptrs, int n) {
   int cur = 0;
   cudaGetDevice(&cur);
-  for (int i = 0; i < n; ++i)
-    if (ptrs[i] && ptr_device(ptrs[i]) != cur) return false;
-  return true;
+  // the last answer per thread: a switch asks about the same pools every call
+  thread_local int last_dev = -1, last_n = -1;
+  thread_local uint64_t last_ptrs[TPR_MAX_GPUS], last_gen = ~0ull;
+  thread_local bool last_local = false;
+  const uint64_t gen = g_range_gen.load(std::memory_order_relaxed);
+  if (n >= 0 && n <= TPR_MAX_GPUS && cur == last_dev && n == last_n && gen == last_gen &&
+      memcmp(ptrs, last_ptrs, sizeof(uint64_t) * (size_t)n) == 0)
+    return last_local;
+  bool local = true;
+  for (int i = 0; i < n && local; ++i)
+    if (ptrs[i] && ptr_device(ptrs[i]) != cur) local = false;
+  if (n >= 0 && n <= TPR_MAX_GPUS) {
+    last_dev = cur;
+    last_n = n;
+    last_gen = gen;
+    memcpy(last_ptrs, ptrs, sizeof(uint64_t) * (size_t)n);
+    last_local = local;
+  }
+  return local;
 }
 
 int sm_count() {
@@ -357,6 +376,45 @@ int sm_count() {
 
 void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
                     uint32_t piece_bytes, KvTensorMaps* out) {
+  // the last result per thread and ring piece (K1 and K31 ask with different
+  // pieces): a switch asks about the same pools every call
+  struct Memo {
+    int dev = -1, n = -1, tok = 0, rows = 0, bt = 0, enabled_knob = -1;
+    uint32_t piece = 0;
+    uint64_t pool[TPR_MAX_GPUS];
+    int64_t units[TPR_MAX_GPUS];
+    KvTensorMaps tm;
+  };
+  thread_local Memo memo[2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int knob_now = tensor_partial_enabled() ? 1 : 0;
+  for (Memo& m : memo)
+    if (m.dev == dev && m.n == n_gpus && m.piece == piece_bytes && m.enabled_knob == knob_now &&
+        m.tok == geo.head_dim * geo.dtype_bytes && m.rows == 2 * geo.layers &&
+        m.bt == geo.block_tokens && n_gpus >= 0 && n_gpus <= TPR_MAX_GPUS &&
+        memcmp(m.pool, cl.pool, sizeof(uint64_t) * (size_t)n_gpus) == 0 &&
+        memcmp(m.units, cl.units, sizeof(int64_t) * (size_t)n_gpus) == 0) {
+      *out = m.tm;
+      return;
+    }
+  kv_tensor_maps_uncached(geo, cl, n_gpus, piece_bytes, out);
+  if (n_gpus < 0 || n_gpus > TPR_MAX_GPUS) return;
+  Memo& m = memo[memo[0].piece == piece_bytes || memo[0].dev < 0 ? 0 : 1];
+  m.dev = dev;
+  m.n = n_gpus;
+  m.piece = piece_bytes;
+  m.enabled_knob = knob_now;
+  m.tok = geo.head_dim * geo.dtype_bytes;
+  m.rows = 2 * geo.layers;
+  m.bt = geo.block_tokens;
+  memcpy(m.pool, cl.pool, sizeof(uint64_t) * (size_t)n_gpus);
+  memcpy(m.units, cl.units, sizeof(int64_t) * (size_t)n_gpus);
+  m.tm = *out;
+}
+
+void kv_tensor_maps_uncached(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
+                             uint32_t piece_bytes, KvTensorMaps* out) {
   out->enabled = 0;
   const int32_t tok = geo.head_dim * geo.dtype_bytes;
   const int32_t rows = 2 * geo.layers;

@@ -74,6 +74,8 @@ int64_t k31_trace_buffer();
 // the geometry does not fit TMA's limits or the driver entry point is missing.
 void kv_tensor_maps(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
                     uint32_t piece_bytes, KvTensorMaps* out);
+void kv_tensor_maps_uncached(const tpr_kv_geometry_t& geo, const KvClusterParams& cl, int n_gpus,
+                             uint32_t piece_bytes, KvTensorMaps* out);
 bool tensor_partial_enabled();
 
 int sm_count();
